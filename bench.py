@@ -1,0 +1,354 @@
+"""Benchmark: matrix-free neo-Hookean K.p on one B200 (BASELINE config 2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): 64^3 hexahedra on [0,1]^3, P=4 SDME_M,
+m=5 Gauss points per direction, 50,923,779 DOFs, FP64, neo-Hookean
+E=1e7 nu=0.3 rho=1e3; u = 0.02 sin(2 pi (x+y+z)) on vertex modes + U(-a, a)
+noise with a = 1e-3 h, p ~ N(0,1) (seed 1).  A *step* is one
+K(u).p over the whole mesh.  Inputs (u, p: 407 MB each) exceed the 126 MB L2,
+so no explicit flush is needed between steps.
+
+``value`` is device-timed (CUDA events on the library's stream, inputs
+resident in HBM); ``e2e`` goes through the reference-facing API
+(GpuFemProblem.apply_tangent with host numpy vectors in the reference free-DOF
+order, H2D + permutation + K.p + D2H inside the timed region).
+
+``--impl reference`` times the reference algorithm's CPU path (the oracle
+restatement of element_tangent(...) @ p_e, oracle/fem.py, kind "port") on a
+bounded sample of same-size elements, on all host cores.
+N > 1: replicas only (the path does not shard in this tier).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+P, M, NEL = 4, 5, 64
+E_MOD, NU, RHO = 1.0e7, 0.3, 1.0e3
+METRIC = "matrix-free K.p GDOF/s (FP64), 64^3 hex P=4 SDME"
+UNIT = "GDOF/s"
+
+
+def sf_macs(n, m):
+    """Sum-factorisation MACs per scalar field."""
+    return 2 * m * n ** 3 + 3 * m * m * n * n + 3 * m ** 3 * n
+
+
+def kp_flops(n_elem, n, m):
+    """Algorithmic FP64 flops of one K.p (recompute variant):
+    E (2*9*SF(n,m) + 411 m^3)."""
+    return n_elem * (2 * 9 * sf_macs(n, m) + 411 * m ** 3)
+
+
+def fint_flops(n_elem, n, m):
+    return n_elem * (2 * 6 * sf_macs(n, m) + 170 * m ** 3)
+
+
+def measured_peaks():
+    out = {}
+    try:
+        out.update(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))))
+    except Exception:
+        pass
+    try:
+        fp = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+        out["fp64_tflops"] = fp["fp64_tflops"]
+    except Exception:
+        out["fp64_tflops"] = None
+    return out
+
+
+def config2_fields(pb, seed_u=0, seed_p=1):
+    """Lattice-order inputs of config 2/3: smooth part on vertex
+    modes (all lattice nodes for the nodal basis), uniform noise of amplitude
+    1e-3 h on every coefficient, p ~ N(0, 1)."""
+    from paper_2104_13466_b200.basis import gll_rule
+
+    mesh, Pp = pb.mesh, pb.P
+    h = min(mesh.h)
+    shape = pb.lattice_shape
+    nodal = pb.basis.kind.is_nodal
+    if nodal:
+        nodes = gll_rule(Pp + 1).points
+        xi = np.concatenate(([nodes[0]], [nodes[-1]], nodes[1:-1]))
+        xs = mesh.lattice_coords(Pp, xi)
+    else:
+        xs = mesh.lattice_coords(Pp)
+    sx = np.sin(2 * np.pi * xs[0])
+    cx = np.cos(2 * np.pi * xs[0])
+    sy, cy = np.sin(2 * np.pi * xs[1]), np.cos(2 * np.pi * xs[1])
+    sz, cz = np.sin(2 * np.pi * xs[2]), np.cos(2 * np.pi * xs[2])
+    # sin(a+b+c) by separable products (no 3D temporaries beyond the output)
+    smooth = (np.einsum("z,y,x->zyx", cz, cy, sx) + np.einsum("z,y,x->zyx", cz, sy, cx)
+              + np.einsum("z,y,x->zyx", sz, cy, cx) - np.einsum("z,y,x->zyx", sz, sy, sx))
+    smooth *= 0.02
+    if not nodal:
+        vert = [np.arange(n) % Pp == 0 for n in (shape[3], shape[2], shape[1])]
+        mask = np.einsum("z,y,x->zyx", vert[2], vert[1], vert[0])
+        smooth *= mask
+    rng = np.random.default_rng(seed_u)
+    u = 1e-3 * h * rng.uniform(-1.0, 1.0, size=shape)
+    u += smooth[None]
+    p = np.random.default_rng(seed_p).standard_normal(shape)
+    return u, p
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.rows = []
+        self.proc = None
+        self.index = index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thr = threading.Thread(target=self._read, daemon=True)
+            self.thr.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def dist_max(val, ws):
+    """Max over ranks (torch.distributed plumbing for N>1 replicas)."""
+    if ws == 1:
+        return val
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([val], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def dist_barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def cpu_sample_kp(n_elem_sample=None, threads=None, reps=1):
+    """Reference algorithm on the host: element_tangent(...) @ p_e over a
+    sample of h=1/64 P=4 elements (oracle restatement, dense B^T D B +
+    geometric, femcore.py:130-146).  Returns (seconds per element, cores, elems)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import basis as ob
+    from oracle import fem as of
+
+    threads = threads or os.cpu_count() or 1
+    n_elem_sample = n_elem_sample or max(8, 2 * threads)
+    h = 1.0 / NEL
+    div = (2, 2, 2)
+    pb = of.Problem(of.Mesh(div, (2 * h,) * 3), ob.Basis("SDME_M", P), of.Material(E_MOD, NU, RHO), M)
+    rng = np.random.default_rng(0)
+    u = 1e-3 * h * rng.uniform(-1, 1, pb.n_free)
+    p = rng.standard_normal(pb.n_free)
+    ue = [pb.gather(e, u) for e in range(pb.mesh.ne)]
+    pe = [pb.gather(e, p).reshape(-1) for e in range(pb.mesh.ne)]
+
+    def one(k):
+        e = k % pb.mesh.ne
+        _, grad, wdet = pb.tab.per_elem[e]
+        return of.elem_tangent(pb.mat, grad, wdet, ue[e], e) @ pe[e]
+
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(one, range(threads)))  # warm
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            list(ex.map(one, range(n_elem_sample)))
+        dt = time.perf_counter() - t0
+    return dt / (reps * n_elem_sample), threads, n_elem_sample
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    n_dof = 3 * (P * NEL + 1) ** 3
+    n_elem = NEL ** 3
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_sample_kp(threads, threads)
+    per = []
+    for _ in range(args.steps):
+        s, cores, ns = cpu_sample_kp(2 * threads, threads)
+        per.append(s)
+    s_elem = float(np.mean(per))
+    t_step = s_elem * n_elem  # one full-mesh K.p, extrapolated from the sample
+    value = n_dof / t_step / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": "config2: 64^3 hex, P=4 SDME_M, m=5, K.p",
+                                        "n_dofs": n_dof, "elements": n_elem},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{2 * threads} elements of h=1/64 per step (dense element_tangent@p_e, "
+                                   f"oracle/fem.py), scaled by 262144 elements"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+        os.environ["CUDA_VISIBLE_DEVICES_RANK"] = str(local)
+    from paper_2104_13466_b200 import BoxMesh, GpuFemProblem, NeoHookean, build_basis
+    from paper_2104_13466_b200.basis import BasisKind, gauss_rule
+
+    mat = NeoHookean.from_engineering(E_MOD, NU, RHO)
+    basis = build_basis(P, BasisKind("SDME_M"))
+    pb = GpuFemProblem(BoxMesh((NEL,) * 3, (1.0,) * 3), basis, mat, gauss_rule(M), reference_order=True)
+    n_dof = pb.n_lattice
+    u_lat, p_lat = config2_fields(pb)
+    u = pb.vector().set_lattice(u_lat)
+    p = pb.vector().set_lattice(p_lat)
+    y = pb.vector()
+    # admissibility log (D4): min J and max |du/dX| are checked by the kernel's inversion flag
+    pb.fint_(u, y)
+
+    for _ in range(args.warmup):
+        pb.apply_(u, p, y)
+    pb.sync()
+    dist_barrier(ws)
+    l0 = pb.launch_count()
+    with ClockSampler(local) as clk:
+        ms_total = pb.time_op("apply", u, p, y, 0.0, args.steps) * args.steps
+    launches = pb.launch_count() - l0
+    pb.sync()
+    ms_total = dist_max(ms_total, ws)
+    t_step = ms_total / 1e3 / args.steps
+    value = ws * n_dof / t_step / 1e9
+
+    # roofline of the dominant kernel (the 8 colour passes of K.p)
+    flops = kp_flops(NEL ** 3, P + 1, M)
+    bytes_alg = 3 * 8 * n_dof
+    peaks = measured_peaks()
+    fp64_peak = peaks.get("fp64_tflops")
+    achieved = flops / t_step / 1e12
+    roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": achieved / fp64_peak if fp64_peak else None, "traffic": None,
+            "peak_source": "profiles/fp64_peak.json (measured DFMA chain on this pool's B200)",
+            "hbm": {"achieved_gbs": bytes_alg / t_step / 1e9, "peak_gbs": peaks.get("hbm_gbs"),
+                    "frac": bytes_alg / t_step / 1e9 / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None},
+            "algorithmic_flops_per_step": flops, "algorithmic_bytes_per_step": bytes_alg}
+    t_fint = pb.time_op("fint", u, p, y, 0.0, max(3, args.steps // 2)) / 1e3
+
+    # e2e through the reference-facing API with host buffers (free order)
+    u_free = pb.to_free(u_lat)
+    p_free = pb.to_free(p_lat)
+    del u_lat, p_lat
+    pb.apply_tangent(u_free, p_free)
+    e2e_steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        out = pb.apply_tangent(u_free, p_free)
+    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    t_e2e = dist_max(t_e2e, ws)
+    e2e = {"value": ws * n_dof / t_e2e / 1e9, "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * pb.n_free,
+           "d2h_bytes_per_step": 8 * pb.n_free, "ms_per_step": t_e2e * 1e3,
+           "api": "GpuFemProblem.apply_tangent(u_free, p_free) -> ndarray"}
+    del out
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        s, cores, ns = cpu_sample_kp(None, None)
+        cpu_val = n_dof / (s * NEL ** 3) / 1e9
+        cpu = {"value": cpu_val, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{ns} elements (h=1/64, P=4, m=5) dense element_tangent@p_e per timing, "
+                         f"scaled to 262144 elements"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config2: 64^3 hex on [0,1]^3, P=4 SDME_M, m=5 Gauss, K(u).p",
+                       "n_dofs": n_dof, "elements": NEL ** 3, "parallelism": f"replicas{ws}",
+                       "l2": "inputs (2 x 407 MB) exceed the 126 MB L2; no flush"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "fint_ms": t_fint * 1e3,
+            "fint_gdofs": n_dof / t_fint / 1e9,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,140 @@
+/* sdme.h -- C ABI of the B200 matrix-free neo-Hookean path (sm_100a, FP64).
+ *
+ * Drop-in boundary for the hot path of the reference package `sdmefem`
+ * (arXiv 2104.13466).  The reference has no FFI: its seams are duck-typed
+ * Python calls.  Each entry point below names the reference
+ * interface it replaces; the Python mirror `paper_2104_13466_b200` binds these
+ * with ctypes (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *  - every function returns an sdme_status; details via sdme_last_error().
+ *  - all device memory is owned by the context; host buffers are only read or
+ *    written during the call (nothing retained).
+ *  - one CUDA stream per context; calls are blocking unless named *_async;
+ *    a context is not re-entrant.
+ *  - vectors are opaque integer ids of device-resident lattice vectors
+ *    (3 * Lx*Ly*Lz doubles, component-major, x fastest; Dirichlet points 0).
+ *  - "free" vectors are host arrays in the reference free-DOF order
+ *    (meshdof.py:345-370), length n_free.
+ *  - deterministic: no floating-point atomics; fixed reduction trees; reruns
+ *    are bit-identical.
+ */
+#ifndef SDME_H
+#define SDME_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SDME_OK = 0,
+  SDME_INVERSION = 1,      /* det F <= 0: ElementInversionError (femcore.py:36-42)     */
+  SDME_INDEFINITE = 2,     /* p^T A p <= 0: PCGError (solver.py:151-155)               */
+  SDME_MAXIT = 3,          /* PCG iteration cap: PCGError (solver.py:166-170)          */
+  SDME_BAD_DIAGONAL = 4,   /* non-positive Jacobi diagonal: ValueError (solver.py:107) */
+  SDME_BAD_ARGUMENT = 5,   /* invalid argument / unsupported (P, m)                    */
+  SDME_CUDA_ERROR = 6      /* CUDA runtime error (message in sdme_last_error)          */
+} sdme_status;
+
+typedef struct sdme_ctx sdme_ctx;
+
+/* Problem descriptor: FemProblem(mesh, element, dmap, mat, rule)
+ * (femcore.py:276-295) restricted to axis-aligned gen_box_mesh meshes
+ * (meshdof.py:146-193).  B, D are m x (P+1) row-major in the REFERENCE
+ * function order [left, right, internal 2..P] (basis1d.py:83); the library
+ * permutes them to lattice order. */
+typedef struct {
+  int P;                 /* polynomial order, 1..8                          */
+  int m;                 /* Gauss points per direction (femcore.py:289-292) */
+  int nx, ny, nz;        /* elements per axis                               */
+  double hx, hy, hz;     /* element edge lengths                            */
+  double origin[3];      /* mesh origin                                     */
+  const double* B;       /* m x (P+1) values                                */
+  const double* D;       /* m x (P+1) derivatives                           */
+  const double* w;       /* m weights                                       */
+  double mu, lambda_lame, rho0;      /* NeoHookean (material.py:32-46)      */
+  int dirichlet_mask[3]; /* per component bits: 1 xmin 2 xmax 4 ymin 8 ymax 16 zmin 32 zmax */
+  const int32_t* perm;   /* optional: 3*Lx*Ly*Lz lattice -> free index or -1; NULL = none */
+  int64_t n_free;        /* reference free-DOF count (required with perm)   */
+} sdme_desc;
+
+/* lifecycle ------------------------------------------------------------- */
+int sdme_create(const sdme_desc* desc, sdme_ctx** out);
+int sdme_destroy(sdme_ctx* ctx);
+/* 3*Lx*Ly*Lz (lattice vector length) */
+int sdme_lattice_size(const sdme_ctx* ctx, int64_t* n);
+/* Last error: code, element id and quadrature point (inversion), message. */
+int sdme_last_error(const sdme_ctx* ctx, int64_t* elem, int* qp, char* msg, size_t n);
+
+/* vectors --------------------------------------------------------------- */
+int sdme_vec_alloc(sdme_ctx* ctx, int* id);              /* zero-filled */
+int sdme_vec_free(sdme_ctx* ctx, int id);
+int sdme_vec_upload(sdme_ctx* ctx, int id, const double* host);     /* lattice order */
+int sdme_vec_download(sdme_ctx* ctx, int id, double* host);
+int sdme_vec_upload_free(sdme_ctx* ctx, int id, const double* host);    /* reference order */
+int sdme_vec_download_free(sdme_ctx* ctx, int id, double* host);
+int sdme_vec_fill(sdme_ctx* ctx, int id, double value);  /* Dirichlet points stay 0 */
+int sdme_vec_copy(sdme_ctx* ctx, int dst, int src);
+/* y = sum_t c[t] * x[t]  (nterms <= 6; y may alias an x) -- the axpys of
+ * dynamics.py:219, 246-248 */
+int sdme_vec_lincomb(sdme_ctx* ctx, int y, int nterms, const double* c, const int* x);
+/* out = a * b elementwise (Jacobi apply, lumped-mass scaling) */
+int sdme_vec_mul(sdme_ctx* ctx, int out, int a, int b);
+/* deterministic dot product (solver.py:150, 159, 163 `@` / norm) */
+int sdme_vec_dot(sdme_ctx* ctx, int a, int b, double* out);
+/* dst = 1/src on free points, 0 on Dirichlet points; SDME_BAD_DIAGONAL if a
+ * free entry is <= 0 (lumped-mass inverse, Jacobi preconditioner) */
+int sdme_vec_reciprocal(sdme_ctx* ctx, int dst, int src);
+
+/* operators (problem-level, femcore.py:346-372) ------------------------- */
+/* r = f_int(u)   -- FemProblem.internal_force (femcore.py:346-349)            */
+int sdme_fint(sdme_ctx* ctx, int u, int r);
+/* y = c_k K_T(u) p + c_m M p -- element_tangent(...)@p + mass (femcore.py:130-156,
+ * consumer solver.py:149 `a @ p`, Newmark eff = kt + b1 m, dynamics.py:236-237) */
+int sdme_apply(sdme_ctx* ctx, int u, int p, int y, double c_k, double c_m);
+/* y = M a -- mass_full @ a_trial (dynamics.py:198) */
+int sdme_mass(sdme_ctx* ctx, int a, int y);
+/* d = diag(c_k K_T(u) + c_m M) on free points -- a.diagonal() (solver.py:106) */
+int sdme_diag(sdme_ctx* ctx, int u, double c_k, double c_m, int d);
+
+/* Jacobi-PCG on A = K_T(u_lin) + c_m M (solver.py:129-170 with
+ * precond "diagonal" (1) or "none" (0)); x0 = 0.  On SDME_INDEFINITE /
+ * SDME_MAXIT, *iters and *relres carry the PCGError stats. */
+int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, double tol,
+             int maxit, int precond, int* iters, double* relres);
+
+/* explicit central difference with lumped mass (D6, dynamics.py:152-164):
+ * psi = s_load*load - f_int(u) + f_c ; u_next = 2u - u_prev + dt^2 psi / m_L ;
+ * v = (u_next - u_prev)/(2 dt).  load / fc may be -1 (absent).  inv_ml is the
+ * reciprocal lumped mass vector (0 on Dirichlet points). */
+int sdme_explicit_step(sdme_ctx* ctx, int u, int u_prev, int v, int load, double s_load,
+                       int fc, int inv_ml, double dt, int scratch);
+
+/* penalty contact against a rigid plane on a box side (contact.py:87-128):
+ * fc = sum_q warea t_N N_f n, gaps (optional, host) = gap per face point in the
+ * reference face/point order; side = 0..5 (xmin..zmax); qf = face rule points
+ * (default P+1) with Bf (qf x (P+1), reference function order), points xf and
+ * weights wf of the 1D face rule; stats[0] = penetration max(-g, 0), stats[1] = min active
+ * pressure (0 if none), stats[2] = active point count. */
+int sdme_contact(sdme_ctx* ctx, int u, int side, int qf, const double* Bf, const double* xf,
+                 const double* wf, const double* point,
+                 const double* normal, double eps, int fc, double* gaps_host,
+                 double* stats);
+/* number of face points of a side for the given qf */
+int sdme_contact_points(const sdme_ctx* ctx, int side, int qf, int64_t* n);
+
+/* timing (CUDA events on the context stream) ----------------------------- */
+/* op: 0 = apply (K p, c_m), 1 = fint, 2 = mass, 3 = diag, 4 = pcg iteration vector
+ * kernels; returns mean milliseconds per call over `reps` back-to-back calls. */
+int sdme_time_op(sdme_ctx* ctx, int op, int u, int p, int y, double c_m, int reps, double* ms);
+int sdme_sync(sdme_ctx* ctx);
+/* kernel launches issued by this context since creation (evidence for bench) */
+int sdme_launch_count(const sdme_ctx* ctx, int64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDME_H */

@@ -1,0 +1,187 @@
+"""Penalty contact against a rigid plane, GPU force evaluation.
+
+Mirrors ``sdmefem.contact`` (``contact.py:25-204``): :class:`RigidObstacle`,
+:class:`ContactParams`, and :class:`GpuPenaltyContact` with
+``evaluate_forces`` (force, pressures, gaps, active set, settled flag),
+``accept_step`` (penalty stepping + history) and ``penalty_energy``.  The
+contact *stiffness* matrix (implicit contact) is the next row;
+``evaluate_forces`` returns ``stiffness=None``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import native
+from .basis import gauss_rule
+from .lattice import FACE_TAGS
+from .problem import DeviceVector, GpuFemProblem
+
+__all__ = ["RigidObstacle", "ContactParams", "ContactForces", "GpuPenaltyContact", "gap"]
+
+
+@dataclass(frozen=True)
+class RigidObstacle:
+    """Plane through ``point`` with unit ``outward_normal`` (``contact.py:25-39``)."""
+
+    point: np.ndarray
+    outward_normal: np.ndarray
+
+    def __post_init__(self):
+        object.__setattr__(self, "point", np.asarray(self.point, dtype=float))
+        n = np.asarray(self.outward_normal, dtype=float)
+        nrm = np.linalg.norm(n)
+        if abs(nrm - 1.0) > 1e-12:
+            n = n / nrm
+        object.__setattr__(self, "outward_normal", n)
+
+
+def gap(obstacle: RigidObstacle, x: np.ndarray) -> np.ndarray:
+    """``contact.py:42-45``."""
+    return (np.asarray(x, dtype=float) - obstacle.point) @ obstacle.outward_normal
+
+
+@dataclass
+class ContactParams:
+    """``contact.py:48-59``."""
+
+    eps_n: float
+    deps_n: float = 0.0
+    gap_tol: float = 1e-3
+    stress_tol: float = 1e-2
+
+    def __post_init__(self):
+        if self.eps_n <= 0.0:
+            raise ValueError("penalty stiffness must be positive")
+        if self.gap_tol <= 0.0 or self.stress_tol <= 0.0:
+            raise ValueError("tolerances must be positive")
+
+
+@dataclass
+class ContactForces:
+    force: np.ndarray
+    stiffness: object
+    pressures: np.ndarray
+    gaps: np.ndarray
+    active: np.ndarray
+    settled: bool
+
+
+class GpuPenaltyContact:
+    """Penalty contact of one box side against a rigid plane (``contact.py:72-204``)."""
+
+    def __init__(self, problem: GpuFemProblem, obstacle: RigidObstacle, params: ContactParams,
+                 surface_tag: str, quad_order: int | None = None):
+        if surface_tag not in FACE_TAGS:
+            raise KeyError(f"unknown boundary tag {surface_tag!r}")
+        self.problem = problem
+        self.obstacle = obstacle
+        self.params = params
+        self.surface_tag = surface_tag
+        self.side = FACE_TAGS.index(surface_tag)
+        self.qf = quad_order if quad_order is not None else problem.P + 1  # contact.py:81-83
+        rule = gauss_rule(self.qf)
+        v, _ = problem.basis.eval(rule.points)
+        self.Bf = np.ascontiguousarray(v.T)
+        self.xf = np.ascontiguousarray(rule.points)
+        self.wf = np.ascontiguousarray(rule.weights)
+        n = C.c_int64(0)
+        native.lib().sdme_contact_points(problem._ctx, self.side, self.qf, C.byref(n))
+        self.n_points = n.value
+        self._last_pressures = None
+        self.history = []
+        self._fc = None
+        self._u = None
+
+    def forces_(self, u: DeviceVector, fc: DeviceVector, record: bool = False):
+        """Device path: fc = contact nodal force at u (no host traffic unless
+        ``record`` asks for the gap statistics)."""
+        pb = self.problem
+        gaps = np.empty(self.n_points) if record else None
+        stats = np.zeros(3) if record else None
+        rc = native.lib().sdme_contact(
+            pb._ctx, u.vid, self.side, self.qf, native.dptr(self.Bf), native.dptr(self.xf),
+            native.dptr(self.wf), native.dptr(self.obstacle.point), native.dptr(self.obstacle.outward_normal),
+            float(self.params.eps_n), fc.vid,
+            native.dptr(gaps) if record else None, native.dptr(stats) if record else None)
+        native.check(pb._ctx, rc, "contact")
+        if record:
+            self.history.append((self.params.eps_n, float(stats[0]), float(stats[1]), int(stats[2])))
+        return gaps
+
+    def _gaps(self, u: DeviceVector, fc: DeviceVector):
+        gaps = np.empty(self.n_points)
+        rc = native.lib().sdme_contact(
+            self.problem._ctx, u.vid, self.side, self.qf, native.dptr(self.Bf), native.dptr(self.xf),
+            native.dptr(self.wf), native.dptr(self.obstacle.point), native.dptr(self.obstacle.outward_normal),
+            float(self.params.eps_n), fc.vid, native.dptr(gaps), None)
+        native.check(self.problem._ctx, rc, "contact")
+        return gaps
+
+    def _scratch(self):
+        if self._fc is None:
+            self._fc = DeviceVector(self.problem)
+            self._u = DeviceVector(self.problem)
+        return self._u, self._fc
+
+    def evaluate_forces(self, u_free: np.ndarray) -> ContactForces:
+        """``contact.py:103-151`` (force, pressures per face point, gaps, active, settled)."""
+        u, fc = self._scratch()
+        u.set_free(u_free)
+        g = self._gaps(u, fc)
+        act = g < 0.0
+        pressures = np.where(act, -self.params.eps_n * g, 0.0)
+        settled = self._pressure_settled(pressures)
+        self._last_pressures = pressures
+        return ContactForces(fc.free(), None, pressures, g, act, settled)
+
+    def _pressure_settled(self, pressures):
+        """``contact.py:153-160``."""
+        prev = self._last_pressures
+        if prev is None or prev.shape != pressures.shape:
+            return not pressures.any()
+        scale = max(np.abs(pressures).max(), np.abs(prev).max())
+        if scale == 0.0:
+            return True
+        return float(np.abs(pressures - prev).max()) / scale <= self.params.stress_tol
+
+    def accept_step(self, u_free: np.ndarray):
+        """``contact.py:162-176``: history row and penalty stepping."""
+        u, fc = self._scratch()
+        u.set_free(u_free)
+        g = self._gaps(u, fc)
+        pen = max(float(-g.min()), 0.0) if g.size else 0.0
+        act = g < 0.0
+        tn = np.where(act, -self.params.eps_n * g, 0.0)
+        t_min = float(tn[act].min()) if act.any() else 0.0
+        self.history.append((self.params.eps_n, pen, t_min, int(act.sum())))
+        if pen > self.params.gap_tol and self.params.deps_n > 0.0:
+            self.params.eps_n += self.params.deps_n
+        self._last_pressures = None
+
+    def penalty_energy(self, u_free: np.ndarray) -> float:
+        """``contact.py:178-184``: sum over points of eps/2 warea min(g,0)^2."""
+        u, fc = self._scratch()
+        u.set_free(u_free)
+        g = self._gaps(u, fc).reshape(-1, self.qf, self.qf)
+        ax = self.side // 2
+        d1, d2 = [d for d in range(3) if d != ax]
+        h = self.problem.mesh.h
+        warea = np.outer(self.wf, self.wf) * 0.25 * h[d1] * h[d2]
+        pen = np.minimum(g, 0.0)
+        return float(0.5 * self.params.eps_n * (warea[None] * pen ** 2).sum())
+
+    def stiffness_bound(self) -> float:
+        """Gershgorin bound of the contact stiffness rows, all points active:
+        eps * max_f sum_q warea |N_f| sum_g |N_g| (for the CFL estimate, D7)."""
+        ax = self.side // 2
+        d1, d2 = [d for d in range(3) if d != ax]
+        h = self.problem.mesh.h
+        a1 = np.abs(self.Bf)  # (qf, n)
+        w = self.wf * 0.5
+        # 1D factors: s[l] = sum_a w_a |phi_l(a)| sum_k |phi_k(a)|; neighbours double up
+        s = (w[:, None] * a1 * a1.sum(axis=1)[:, None]).sum(axis=0)
+        return float(self.params.eps_n * 4.0 * s.max() ** 2 * h[d1] * h[d2])

@@ -1,0 +1,771 @@
+// C-ABI implementation: context, device vectors, operator dispatch over (P, m),
+// the Jacobi-PCG driver (solver.py:129-170), explicit step and contact.
+// Build: see paper_2104_13466_b200/build.py (nvcc -gencode arch=compute_100a,code=sm_100a).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sdme.h"
+#include "contact_kernels.cuh"
+#include "element_kernels.cuh"
+#include "vector_kernels.cuh"
+
+using namespace sdme;
+
+namespace {
+
+constexpr unsigned long long kNoFlag = ~0ull;
+
+struct Ops;
+
+}  // namespace
+
+struct sdme_ctx {
+  int P = 0, m = 0, n = 0;
+  Geo geo{};
+  double h[3]{}, origin[3]{};
+  std::vector<double> Bl, Dl, w;  // lattice-local order, m x n
+  cudaStream_t st = nullptr;
+  long long nvec = 0;             // 3 * Ns
+  std::vector<double*> vecs;
+  int* d_perm = nullptr;
+  int64_t n_free = 0;
+  unsigned char* d_free = nullptr;  // 1 on free lattice dofs
+  double* d_fbuf = nullptr;         // staging for free-order vectors
+  double* d_partial = nullptr;
+  double* d_scal = nullptr;
+  double* h_scal = nullptr;         // pinned
+  unsigned long long* d_flag = nullptr;
+  unsigned long long* h_flag = nullptr;
+  double* d_gaps = nullptr;
+  long long gaps_cap = 0;
+  double* h_gaps = nullptr;
+  // PCG scratch vectors (lazily allocated ids)
+  int v_r = -1, v_p = -1, v_ap = -1, v_dinv = -1, v_tmp = -1;
+  const Ops* ops = nullptr;
+  int err_code = 0;
+  int64_t err_elem = -1;
+  int err_qp = -1;
+  std::string err_msg;
+  int64_t launches = 0;
+};
+
+namespace {
+
+struct Ops {
+  void (*element)(sdme_ctx*, int mode, const double* u, const double* p, double* y, double ck, double cm);
+  void (*diag)(sdme_ctx*, const double* u, double* d, double ck, double cm);
+};
+
+int set_err(sdme_ctx* c, int code, const std::string& msg, int64_t elem = -1, int qp = -1) {
+  if (c) {
+    c->err_code = code;
+    c->err_msg = msg;
+    c->err_elem = elem;
+    c->err_qp = qp;
+  }
+  return code;
+}
+
+#define CK(call)                                                                  \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess)                                                        \
+      return set_err(ctx, SDME_CUDA_ERROR, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+int check_launch(sdme_ctx* ctx) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(ctx, SDME_CUDA_ERROR, std::string("launch: ") + cudaGetErrorString(e));
+  return SDME_OK;
+}
+
+inline int grid_for(long long n, int threads = 256) {
+  long long g = (n + threads - 1) / threads;
+  return (int)std::max<long long>(1, std::min<long long>(g, 148LL * 16));
+}
+
+template <int N, int M>
+struct Conf {
+  static constexpr int bytes = Smem<N, M>::per_elem * 8;
+  static constexpr int EB = bytes > 100000 ? 1 : (100000 / bytes > 8 ? 8 : 100000 / bytes);
+};
+
+template <int N, int M>
+Tab<N, M> make_tab(const sdme_ctx* c) {
+  Tab<N, M> t;
+  for (int a = 0; a < M; ++a) {
+    for (int l = 0; l < N; ++l) {
+      t.B[a][l] = c->Bl[a * N + l];
+      t.D[a][l] = c->Dl[a * N + l];
+    }
+    t.W[a] = c->w[a];
+  }
+  return t;
+}
+
+template <int N, int M, int MODE>
+void launch_mode(sdme_ctx* c, const Tab<N, M>& tb, OpArgs a) {
+  constexpr int EB = Conf<N, M>::EB;
+  constexpr int smem = Conf<N, M>::bytes * EB;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(element_op<N, M, EB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_done = true;
+  }
+  for (int col = 0; col < 8; ++col) {
+    const long long cnt = colour_count(c->geo, col);
+    if (cnt == 0) continue;
+    a.colour = col;
+    const long long grid = (cnt + EB - 1) / EB;
+    element_op<N, M, EB, MODE><<<(unsigned)grid, 128, smem, c->st>>>(tb, c->geo, a);
+    ++c->launches;
+  }
+}
+
+template <int N, int M>
+void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, double* y, double ck, double cm) {
+  const Tab<N, M> tb = make_tab<N, M>(c);
+  OpArgs a{u, p, y, ck, cm, 0, c->d_flag};
+  if (mode == MODE_FINT) launch_mode<N, M, MODE_FINT>(c, tb, a);
+  else if (mode == MODE_APPLY) launch_mode<N, M, MODE_APPLY>(c, tb, a);
+  else launch_mode<N, M, MODE_MASS>(c, tb, a);
+}
+
+template <int N, int M>
+void diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm) {
+  constexpr int EB = Conf<N, M>::EB;
+  constexpr int smem = Conf<N, M>::bytes * EB;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(element_diag<N, M, EB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_done = true;
+  }
+  const Tab<N, M> tb = make_tab<N, M>(c);
+  OpArgs a{u, nullptr, d, ck, cm, 0, c->d_flag};
+  for (int col = 0; col < 8; ++col) {
+    const long long cnt = colour_count(c->geo, col);
+    if (cnt == 0) continue;
+    a.colour = col;
+    element_diag<N, M, EB><<<(unsigned)((cnt + EB - 1) / EB), 128, smem, c->st>>>(tb, c->geo, a);
+    ++c->launches;
+  }
+}
+
+template <int N, int M>
+const Ops* ops_for() {
+  static const Ops o{&element_impl<N, M>, &diag_impl<N, M>};
+  return &o;
+}
+
+const Ops* select_ops(int P, int m) {
+#define SDME_CASE(PP, MM) \
+  if (P == PP && m == MM) return ops_for<PP + 1, MM>();
+#define SDME_P(PP) SDME_CASE(PP, PP + 1) SDME_CASE(PP, PP + 2)
+  SDME_P(1) SDME_P(2) SDME_P(3) SDME_P(4) SDME_P(5) SDME_P(6) SDME_P(7) SDME_P(8)
+#undef SDME_P
+#undef SDME_CASE
+  return nullptr;
+}
+
+double* vec(sdme_ctx* c, int id) {
+  if (id < 0 || id >= (int)c->vecs.size()) return nullptr;
+  return c->vecs[id];
+}
+
+int alloc_vec(sdme_ctx* ctx, int* id) {
+  double* p = nullptr;
+  CK(cudaMalloc(&p, ctx->nvec * sizeof(double)));
+  CK(cudaMemsetAsync(p, 0, ctx->nvec * sizeof(double), ctx->st));
+  for (size_t i = 0; i < ctx->vecs.size(); ++i)
+    if (!ctx->vecs[i]) {
+      ctx->vecs[i] = p;
+      *id = (int)i;
+      return SDME_OK;
+    }
+  ctx->vecs.push_back(p);
+  *id = (int)ctx->vecs.size() - 1;
+  return SDME_OK;
+}
+
+int ensure(sdme_ctx* ctx, int& id) {
+  if (id >= 0) return SDME_OK;
+  return alloc_vec(ctx, &id);
+}
+
+// deterministic dot into d_scal[slot]
+int dot_into(sdme_ctx* ctx, const double* a, const double* b, int slot) {
+  DotArgs<1> da{{a}, {b}};
+  k_dots<1><<<kRedBlocks, kRedThreads, 0, ctx->st>>>(da, ctx->nvec, ctx->d_partial);
+  k_finish<1><<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal + slot);
+  ctx->launches += 2;
+  return check_launch(ctx);
+}
+
+int read_scalars(sdme_ctx* ctx) {
+  CK(cudaMemcpyAsync(ctx->h_scal, ctx->d_scal, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return SDME_OK;
+}
+
+int reset_flag(sdme_ctx* ctx) {
+  CK(cudaMemcpyAsync(ctx->d_flag, &kNoFlag, sizeof(kNoFlag), cudaMemcpyHostToDevice, ctx->st));
+  return SDME_OK;
+}
+
+int check_flag(sdme_ctx* ctx) {
+  CK(cudaMemcpyAsync(ctx->h_flag, ctx->d_flag, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  const unsigned long long f = *ctx->h_flag;
+  if (f != kNoFlag) {
+    const long long nq = (long long)ctx->m * ctx->m * ctx->m;
+    const int64_t e = (int64_t)(f / nq);
+    const int q = (int)(f % nq);
+    char buf[128];
+    snprintf(buf, sizeof buf, "element %lld inverted at quadrature point %d", (long long)e, q);
+    return set_err(ctx, SDME_INVERSION, buf, e, q);
+  }
+  return SDME_OK;
+}
+
+// y = A p  with A = c_k K(u) + c_m M (y zeroed first)
+int apply_raw(sdme_ctx* ctx, const double* u, const double* p, double* y, double ck, double cm) {
+  CK(cudaMemsetAsync(y, 0, ctx->nvec * sizeof(double), ctx->st));
+  if (ck != 0.0)
+    ctx->ops->element(ctx, MODE_APPLY, u, p, y, ck, cm);
+  else
+    ctx->ops->element(ctx, MODE_MASS, nullptr, p, y, 0.0, cm);
+  return check_launch(ctx);
+}
+
+}  // namespace
+
+// =========================================================================
+extern "C" {
+
+int sdme_create(const sdme_desc* d, sdme_ctx** out) {
+  if (!d || !out) return SDME_BAD_ARGUMENT;
+  *out = nullptr;
+  const Ops* ops = select_ops(d->P, d->m);
+  if (!ops || d->nx < 1 || d->ny < 1 || d->nz < 1 || !(d->hx > 0) || !(d->hy > 0) || !(d->hz > 0) ||
+      !d->B || !d->D || !d->w)
+    return SDME_BAD_ARGUMENT;
+  sdme_ctx* ctx = new sdme_ctx();
+  ctx->ops = ops;
+  ctx->P = d->P;
+  ctx->m = d->m;
+  ctx->n = d->P + 1;
+  const int n = ctx->n, m = ctx->m, P = d->P;
+  // reference function order [left, right, internal 2..P] -> lattice offset l
+  auto func_of = [&](int l) { return l == 0 ? 0 : (l == P ? 1 : l + 1); };
+  ctx->Bl.resize(m * n);
+  ctx->Dl.resize(m * n);
+  ctx->w.assign(d->w, d->w + m);
+  for (int a = 0; a < m; ++a)
+    for (int l = 0; l < n; ++l) {
+      ctx->Bl[a * n + l] = d->B[a * n + func_of(l)];
+      ctx->Dl[a * n + l] = d->D[a * n + func_of(l)];
+    }
+  Geo& g = ctx->geo;
+  g.nx = d->nx; g.ny = d->ny; g.nz = d->nz;
+  g.Lx = P * d->nx + 1; g.Ly = P * d->ny + 1; g.Lz = P * d->nz + 1;
+  g.Ns = (long long)g.Lx * g.Ly * g.Lz;
+  g.s[0] = 2.0 / d->hx; g.s[1] = 2.0 / d->hy; g.s[2] = 2.0 / d->hz;
+  g.detJ = d->hx * d->hy * d->hz / 8.0;
+  g.mu = d->mu; g.lam = d->lambda_lame; g.rho = d->rho0;
+  for (int c = 0; c < 3; ++c) g.dmask[c] = d->dirichlet_mask[c];
+  ctx->h[0] = d->hx; ctx->h[1] = d->hy; ctx->h[2] = d->hz;
+  for (int c = 0; c < 3; ++c) ctx->origin[c] = d->origin[c];
+  ctx->nvec = 3 * g.Ns;
+  ctx->n_free = d->n_free;
+
+  auto fail = [&](int code) {
+    sdme_destroy(ctx);
+    return code;
+  };
+  if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+  if (cudaMalloc(&ctx->d_partial, kRedBlocks * 4 * sizeof(double)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+  if (cudaMalloc(&ctx->d_scal, 16 * sizeof(double)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+  if (cudaMallocHost(&ctx->h_scal, 16 * sizeof(double)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+  if (cudaMalloc(&ctx->d_flag, sizeof(unsigned long long)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+  if (cudaMallocHost(&ctx->h_flag, sizeof(unsigned long long)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+  // free mask from the Dirichlet planes
+  {
+    std::vector<unsigned char> fm(ctx->nvec, 1);
+    for (int c = 0; c < 3; ++c) {
+      const int mk = g.dmask[c];
+      if (!mk) continue;
+      for (int Z = 0; Z < g.Lz; ++Z)
+        for (int Y = 0; Y < g.Ly; ++Y)
+          for (int X = 0; X < g.Lx; ++X) {
+            const bool cons = ((mk & 1) && X == 0) || ((mk & 2) && X == g.Lx - 1) || ((mk & 4) && Y == 0) ||
+                              ((mk & 8) && Y == g.Ly - 1) || ((mk & 16) && Z == 0) || ((mk & 32) && Z == g.Lz - 1);
+            if (cons) fm[c * g.Ns + ((long long)Z * g.Ly + Y) * g.Lx + X] = 0;
+          }
+    }
+    if (cudaMalloc(&ctx->d_free, ctx->nvec) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+    if (cudaMemcpy(ctx->d_free, fm.data(), ctx->nvec, cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(SDME_CUDA_ERROR);
+  }
+  if (d->perm) {
+    if (d->n_free <= 0) return fail(SDME_BAD_ARGUMENT);
+    if (cudaMalloc(&ctx->d_perm, ctx->nvec * sizeof(int)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+    if (cudaMemcpy(ctx->d_perm, d->perm, ctx->nvec * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(SDME_CUDA_ERROR);
+    if (cudaMalloc(&ctx->d_fbuf, d->n_free * sizeof(double)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+  }
+  *out = ctx;
+  return SDME_OK;
+}
+
+int sdme_destroy(sdme_ctx* ctx) {
+  if (!ctx) return SDME_OK;
+  if (ctx->st) cudaStreamSynchronize(ctx->st);
+  for (double* p : ctx->vecs)
+    if (p) cudaFree(p);
+  cudaFree(ctx->d_perm);
+  cudaFree(ctx->d_free);
+  cudaFree(ctx->d_fbuf);
+  cudaFree(ctx->d_partial);
+  cudaFree(ctx->d_scal);
+  cudaFree(ctx->d_flag);
+  cudaFree(ctx->d_gaps);
+  if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
+  if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
+  if (ctx->h_gaps) cudaFreeHost(ctx->h_gaps);
+  if (ctx->st) cudaStreamDestroy(ctx->st);
+  delete ctx;
+  return SDME_OK;
+}
+
+int sdme_lattice_size(const sdme_ctx* ctx, int64_t* n) {
+  if (!ctx || !n) return SDME_BAD_ARGUMENT;
+  *n = ctx->nvec;
+  return SDME_OK;
+}
+
+int sdme_last_error(const sdme_ctx* ctx, int64_t* elem, int* qp, char* msg, size_t n) {
+  if (!ctx) return SDME_BAD_ARGUMENT;
+  if (elem) *elem = ctx->err_elem;
+  if (qp) *qp = ctx->err_qp;
+  if (msg && n) {
+    strncpy(msg, ctx->err_msg.c_str(), n - 1);
+    msg[n - 1] = 0;
+  }
+  return ctx->err_code;
+}
+
+int sdme_vec_alloc(sdme_ctx* ctx, int* id) {
+  if (!ctx || !id) return SDME_BAD_ARGUMENT;
+  return alloc_vec(ctx, id);
+}
+
+int sdme_vec_free(sdme_ctx* ctx, int id) {
+  double* p = ctx ? vec(ctx, id) : nullptr;
+  if (!p) return SDME_BAD_ARGUMENT;
+  CK(cudaStreamSynchronize(ctx->st));
+  cudaFree(p);
+  ctx->vecs[id] = nullptr;
+  return SDME_OK;
+}
+
+int sdme_vec_upload(sdme_ctx* ctx, int id, const double* host) {
+  double* p = ctx ? vec(ctx, id) : nullptr;
+  if (!p || !host) return SDME_BAD_ARGUMENT;
+  CK(cudaMemcpyAsync(p, host, ctx->nvec * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return SDME_OK;
+}
+
+int sdme_vec_download(sdme_ctx* ctx, int id, double* host) {
+  double* p = ctx ? vec(ctx, id) : nullptr;
+  if (!p || !host) return SDME_BAD_ARGUMENT;
+  CK(cudaMemcpyAsync(host, p, ctx->nvec * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return SDME_OK;
+}
+
+int sdme_vec_upload_free(sdme_ctx* ctx, int id, const double* host) {
+  double* p = ctx ? vec(ctx, id) : nullptr;
+  if (!p || !host || !ctx->d_perm) return set_err(ctx, SDME_BAD_ARGUMENT, "no permutation / bad vector");
+  CK(cudaMemcpyAsync(ctx->d_fbuf, host, ctx->n_free * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  k_free_to_lattice<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, ctx->d_fbuf, ctx->d_perm, ctx->nvec);
+  ++ctx->launches;
+  CK(cudaStreamSynchronize(ctx->st));
+  return check_launch(ctx);
+}
+
+int sdme_vec_download_free(sdme_ctx* ctx, int id, double* host) {
+  double* p = ctx ? vec(ctx, id) : nullptr;
+  if (!p || !host || !ctx->d_perm) return set_err(ctx, SDME_BAD_ARGUMENT, "no permutation / bad vector");
+  k_lattice_to_free<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(ctx->d_fbuf, p, ctx->d_perm, ctx->nvec);
+  ++ctx->launches;
+  CK(cudaMemcpyAsync(host, ctx->d_fbuf, ctx->n_free * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return check_launch(ctx);
+}
+
+int sdme_vec_fill(sdme_ctx* ctx, int id, double value) {
+  double* p = ctx ? vec(ctx, id) : nullptr;
+  if (!p) return SDME_BAD_ARGUMENT;
+  // value on free points, 0 on Dirichlet points
+  k_fill_masked<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, ctx->d_free, value, ctx->nvec);
+  ++ctx->launches;
+  return check_launch(ctx);
+}
+
+int sdme_vec_copy(sdme_ctx* ctx, int dst, int src) {
+  double* a = ctx ? vec(ctx, dst) : nullptr;
+  double* b = ctx ? vec(ctx, src) : nullptr;
+  if (!a || !b) return SDME_BAD_ARGUMENT;
+  CK(cudaMemcpyAsync(a, b, ctx->nvec * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
+  return SDME_OK;
+}
+
+int sdme_vec_lincomb(sdme_ctx* ctx, int y, int nterms, const double* c, const int* x) {
+  double* py = ctx ? vec(ctx, y) : nullptr;
+  if (!py || nterms < 0 || nterms > 6) return SDME_BAD_ARGUMENT;
+  LinComb lc{};
+  lc.nt = nterms;
+  for (int t = 0; t < nterms; ++t) {
+    lc.x[t] = vec(ctx, x[t]);
+    if (!lc.x[t]) return SDME_BAD_ARGUMENT;
+    lc.c[t] = c[t];
+  }
+  k_lincomb<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(lc, py, ctx->nvec);
+  ++ctx->launches;
+  return check_launch(ctx);
+}
+
+int sdme_vec_mul(sdme_ctx* ctx, int out, int a, int b) {
+  double* po = ctx ? vec(ctx, out) : nullptr;
+  double* pa = ctx ? vec(ctx, a) : nullptr;
+  double* pb = ctx ? vec(ctx, b) : nullptr;
+  if (!po || !pa || !pb) return SDME_BAD_ARGUMENT;
+  k_mul<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(po, pa, pb, ctx->nvec);
+  ++ctx->launches;
+  return check_launch(ctx);
+}
+
+int sdme_vec_dot(sdme_ctx* ctx, int a, int b, double* out) {
+  double* pa = ctx ? vec(ctx, a) : nullptr;
+  double* pb = ctx ? vec(ctx, b) : nullptr;
+  if (!pa || !pb || !out) return SDME_BAD_ARGUMENT;
+  int rc = dot_into(ctx, pa, pb, S_NB);
+  if (rc) return rc;
+  rc = read_scalars(ctx);
+  if (rc) return rc;
+  *out = ctx->h_scal[S_NB];
+  return SDME_OK;
+}
+
+int sdme_vec_reciprocal(sdme_ctx* ctx, int dst, int src) {
+  double* a = ctx ? vec(ctx, dst) : nullptr;
+  double* b = ctx ? vec(ctx, src) : nullptr;
+  if (!a || !b) return SDME_BAD_ARGUMENT;
+  CK(cudaMemcpyAsync(ctx->d_flag, &kNoFlag, sizeof(kNoFlag), cudaMemcpyHostToDevice, ctx->st));
+  k_invert_diag<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(a, b, ctx->d_free, ctx->nvec, ctx->d_flag);
+  ++ctx->launches;
+  CK(cudaMemcpyAsync(ctx->h_flag, ctx->d_flag, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  if (*ctx->h_flag != kNoFlag)
+    return set_err(ctx, SDME_BAD_DIAGONAL, "diagonal preconditioner needs positive diagonal entries",
+                   (int64_t)*ctx->h_flag, -1);
+  return check_launch(ctx);
+}
+
+int sdme_fint(sdme_ctx* ctx, int u, int r) {
+  double* pu = ctx ? vec(ctx, u) : nullptr;
+  double* pr = ctx ? vec(ctx, r) : nullptr;
+  if (!pu || !pr) return SDME_BAD_ARGUMENT;
+  int rc = reset_flag(ctx);
+  if (rc) return rc;
+  CK(cudaMemsetAsync(pr, 0, ctx->nvec * sizeof(double), ctx->st));
+  ctx->ops->element(ctx, MODE_FINT, pu, nullptr, pr, 1.0, 0.0);
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  return check_flag(ctx);
+}
+
+int sdme_apply(sdme_ctx* ctx, int u, int p, int y, double c_k, double c_m) {
+  double* pu = ctx ? vec(ctx, u) : nullptr;
+  double* pp = ctx ? vec(ctx, p) : nullptr;
+  double* py = ctx ? vec(ctx, y) : nullptr;
+  if ((!pu && c_k != 0.0) || !pp || !py || py == pp) return SDME_BAD_ARGUMENT;
+  int rc = reset_flag(ctx);
+  if (rc) return rc;
+  rc = apply_raw(ctx, pu, pp, py, c_k, c_m);
+  if (rc) return rc;
+  return c_k != 0.0 ? check_flag(ctx) : SDME_OK;
+}
+
+int sdme_mass(sdme_ctx* ctx, int a, int y) {
+  double* pa = ctx ? vec(ctx, a) : nullptr;
+  double* py = ctx ? vec(ctx, y) : nullptr;
+  if (!pa || !py || pa == py) return SDME_BAD_ARGUMENT;
+  return apply_raw(ctx, nullptr, pa, py, 0.0, 1.0);
+}
+
+int sdme_diag(sdme_ctx* ctx, int u, double c_k, double c_m, int d) {
+  double* pu = ctx ? vec(ctx, u) : nullptr;
+  double* pd = ctx ? vec(ctx, d) : nullptr;
+  if ((!pu && c_k != 0.0) || !pd) return SDME_BAD_ARGUMENT;
+  int rc = reset_flag(ctx);
+  if (rc) return rc;
+  CK(cudaMemsetAsync(pd, 0, ctx->nvec * sizeof(double), ctx->st));
+  ctx->ops->diag(ctx, pu, pd, c_k, c_m);
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  return c_k != 0.0 ? check_flag(ctx) : SDME_OK;
+}
+
+int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, double tol, int maxit,
+             int precond, int* iters, double* relres) {
+  if (!ctx) return SDME_BAD_ARGUMENT;
+  double* pu = vec(ctx, u_lin);
+  double* pb = vec(ctx, b);
+  double* px = vec(ctx, x);
+  if ((!pu && c_k != 0.0) || !pb || !px || pb == px || maxit < 0)
+    return set_err(ctx, SDME_BAD_ARGUMENT, "bad vector id");
+  if (!(tol > 0.0 && tol < 1.0)) return set_err(ctx, SDME_BAD_ARGUMENT, "tolerance must lie in (0, 1)");
+  int rc;
+  if ((rc = ensure(ctx, ctx->v_r)) || (rc = ensure(ctx, ctx->v_p)) || (rc = ensure(ctx, ctx->v_ap)) ||
+      (rc = ensure(ctx, ctx->v_dinv)))
+    return rc;
+  double* r = vec(ctx, ctx->v_r);
+  double* p = vec(ctx, ctx->v_p);
+  double* ap = vec(ctx, ctx->v_ap);
+  double* dinv = vec(ctx, ctx->v_dinv);
+  if (iters) *iters = 0;
+  if (relres) *relres = 0.0;
+  // preconditioner (solver.py:102-126): built before the ||b|| short-circuit
+  if (precond == 1) {
+    if ((rc = sdme_diag(ctx, u_lin, c_k, c_m, ctx->v_ap))) return rc;
+    if ((rc = sdme_vec_reciprocal(ctx, ctx->v_dinv, ctx->v_ap))) return rc;
+  } else if (precond == 0) {
+    k_fill_masked<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(dinv, ctx->d_free, 1.0, ctx->nvec);
+    ++ctx->launches;
+  } else {
+    return set_err(ctx, SDME_BAD_ARGUMENT, "unknown preconditioner (out of scope: sgs)");
+  }
+  // ||b||
+  if ((rc = dot_into(ctx, pb, pb, S_NB)) || (rc = read_scalars(ctx))) return rc;
+  const double nb = std::sqrt(ctx->h_scal[S_NB]);
+  CK(cudaMemsetAsync(px, 0, ctx->nvec * sizeof(double), ctx->st));
+  if (nb == 0.0) {
+    CK(cudaStreamSynchronize(ctx->st));
+    return SDME_OK;
+  }
+  // r = b ; p = z = dinv r ; rz = r.z
+  CK(cudaMemcpyAsync(r, pb, ctx->nvec * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
+  k_mul<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, dinv, r, ctx->nvec);
+  ++ctx->launches;
+  if ((rc = dot_into(ctx, r, p, S_RZ))) return rc;
+  double rel_prev = 1.0;
+  for (int it = 1; it <= maxit; ++it) {
+    if ((rc = apply_raw(ctx, pu, p, ap, c_k, c_m))) return rc;
+    if ((rc = dot_into(ctx, p, ap, S_PAP))) return rc;
+    k_alpha<<<1, 32, 0, ctx->st>>>(ctx->d_scal);
+    k_pcg_update<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(px, r, p, ap, dinv, ctx->d_scal, ctx->nvec,
+                                                          ctx->d_partial);
+    k_finish<2><<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal + S_RR);
+    k_beta<<<1, 32, 0, ctx->st>>>(ctx->d_scal);
+    ctx->launches += 4;
+    if ((rc = check_launch(ctx)) || (rc = read_scalars(ctx))) return rc;
+    const double pap = ctx->h_scal[S_PAP];
+    if (!(pap > 0.0)) {
+      if (iters) *iters = it;
+      if (relres) *relres = rel_prev;
+      char buf[128];
+      snprintf(buf, sizeof buf, "indefinite operator detected at iteration %d (p^T A p = %.3e)", it, pap);
+      return set_err(ctx, SDME_INDEFINITE, buf);
+    }
+    const double rel = std::sqrt(ctx->h_scal[S_RR]) / nb;
+    if (rel <= tol) {
+      if (iters) *iters = it;
+      if (relres) *relres = rel;
+      return SDME_OK;
+    }
+    rel_prev = rel;
+    k_pcg_p<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, r, dinv, ctx->d_scal, ctx->nvec);
+    k_roll<<<1, 32, 0, ctx->st>>>(ctx->d_scal);
+    ctx->launches += 2;
+  }
+  // maxit: true residual ||b - A x|| / ||b||  (solver.py:166)
+  if ((rc = apply_raw(ctx, pu, px, ap, c_k, c_m))) return rc;
+  {
+    LinComb lc{};
+    lc.nt = 2;
+    lc.x[0] = pb;
+    lc.x[1] = ap;
+    lc.c[0] = 1.0;
+    lc.c[1] = -1.0;
+    k_lincomb<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(lc, r, ctx->nvec);
+    ++ctx->launches;
+  }
+  if ((rc = dot_into(ctx, r, r, S_RR)) || (rc = read_scalars(ctx))) return rc;
+  const double rel = std::sqrt(ctx->h_scal[S_RR]) / nb;
+  if (iters) *iters = maxit;
+  if (relres) *relres = rel;
+  char buf[128];
+  snprintf(buf, sizeof buf, "PCG did not converge in %d iterations (relative residual %.3e)", maxit, rel);
+  return set_err(ctx, SDME_MAXIT, buf);
+}
+
+int sdme_explicit_step(sdme_ctx* ctx, int u, int u_prev, int v, int load, double s_load, int fc,
+                       int inv_ml, double dt, int scratch) {
+  if (!ctx) return SDME_BAD_ARGUMENT;
+  double *pu = vec(ctx, u), *pup = vec(ctx, u_prev), *pv = vec(ctx, v), *pm = vec(ctx, inv_ml),
+         *ps = vec(ctx, scratch);
+  const double* pl = load >= 0 ? vec(ctx, load) : nullptr;
+  const double* pf = fc >= 0 ? vec(ctx, fc) : nullptr;
+  if (!pu || !pup || !pv || !pm || !ps || (load >= 0 && !pl) || (fc >= 0 && !pf) || !(dt > 0.0))
+    return set_err(ctx, SDME_BAD_ARGUMENT, "bad explicit-step argument");
+  int rc = sdme_fint(ctx, u, scratch);
+  if (rc) return rc;
+  k_explicit_step<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(pu, pup, pv, pl, s_load, ps, pf, pm, dt, ctx->nvec);
+  ++ctx->launches;
+  return check_launch(ctx);
+}
+
+int sdme_contact_points(const sdme_ctx* ctx, int side, int qf, int64_t* n) {
+  if (!ctx || side < 0 || side > 5 || qf < 1 || !n) return SDME_BAD_ARGUMENT;
+  const int axis = side / 2;
+  const int ne[3] = {ctx->geo.nx, ctx->geo.ny, ctx->geo.nz};
+  const int d1 = axis == 0 ? 1 : 0, d2 = axis == 2 ? 1 : 2;
+  *n = (int64_t)ne[d1] * ne[d2] * qf * qf;
+  return SDME_OK;
+}
+
+int sdme_contact(sdme_ctx* ctx, int u, int side, int qf, const double* Bf, const double* xf, const double* wf,
+                 const double* point, const double* normal, double eps, int fc, double* gaps_host,
+                 double* stats) {
+  if (!ctx) return SDME_BAD_ARGUMENT;
+  double* pu = vec(ctx, u);
+  double* pf = vec(ctx, fc);
+  if (!pu || !pf || side < 0 || side > 5 || qf < 1 || qf > kMaxQF || ctx->n > kMaxN || !Bf || !xf || !wf ||
+      !point || !normal)
+    return set_err(ctx, SDME_BAD_ARGUMENT, "bad contact argument");
+  int64_t npts = 0;
+  sdme_contact_points(ctx, side, qf, &npts);
+  if (npts > ctx->gaps_cap) {
+    cudaFree(ctx->d_gaps);
+    if (ctx->h_gaps) cudaFreeHost(ctx->h_gaps);
+    CK(cudaMalloc(&ctx->d_gaps, npts * sizeof(double)));
+    CK(cudaMallocHost(&ctx->h_gaps, npts * sizeof(double)));
+    ctx->gaps_cap = npts;
+  }
+  FaceTab ft{};
+  ft.n = ctx->n;
+  ft.qf = qf;
+  const int P = ctx->P;
+  auto func_of = [&](int l) { return l == 0 ? 0 : (l == P ? 1 : l + 1); };
+  for (int a = 0; a < qf; ++a) {
+    for (int l = 0; l < ctx->n; ++l) ft.B[a][l] = Bf[a * ctx->n + func_of(l)];
+    ft.W[a] = wf[a];
+    ft.X[a] = xf[a];
+  }
+  ContactArgs ca{};
+  ca.axis = side / 2;
+  ca.side = side % 2;
+  const double nrm = std::sqrt(normal[0] * normal[0] + normal[1] * normal[1] + normal[2] * normal[2]);
+  for (int c = 0; c < 3; ++c) {
+    ca.origin[c] = ctx->origin[c];
+    ca.h[c] = ctx->h[c];
+    ca.point[c] = point[c];
+    ca.normal[c] = std::fabs(nrm - 1.0) > 1e-12 ? normal[c] / nrm : normal[c];
+  }
+  ca.eps = eps;
+  ca.u = pu;
+  ca.fc = pf;
+  ca.gaps = ctx->d_gaps;
+  CK(cudaMemsetAsync(pf, 0, ctx->nvec * sizeof(double), ctx->st));
+  const int ne[3] = {ctx->geo.nx, ctx->geo.ny, ctx->geo.nz};
+  const int d1 = ca.axis == 0 ? 1 : 0, d2 = ca.axis == 2 ? 1 : 2;
+  for (int col = 0; col < 4; ++col) {
+    const int m1 = (ne[d1] - (col & 1) + 1) >> 1, m2 = (ne[d2] - ((col >> 1) & 1) + 1) >> 1;
+    if (m1 <= 0 || m2 <= 0) continue;
+    ca.colour = col;
+    k_contact<<<m1 * m2, 128, 0, ctx->st>>>(ft, ctx->geo, ca);
+    ++ctx->launches;
+  }
+  int rc = check_launch(ctx);
+  if (rc) return rc;
+  if (gaps_host || stats) {
+    CK(cudaMemcpyAsync(ctx->h_gaps, ctx->d_gaps, npts * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    if (gaps_host) memcpy(gaps_host, ctx->h_gaps, npts * sizeof(double));
+    if (stats) {
+      double pen = 0.0, tmin = 0.0;
+      long long act = 0;
+      bool any = false;
+      for (int64_t i = 0; i < npts; ++i) {
+        const double gp = ctx->h_gaps[i];
+        pen = std::max(pen, -gp);
+        if (gp < 0.0) {
+          const double tn = -eps * gp;
+          tmin = any ? std::min(tmin, tn) : tn;
+          any = true;
+          ++act;
+        }
+      }
+      stats[0] = std::max(pen, 0.0);
+      stats[1] = any ? tmin : 0.0;
+      stats[2] = (double)act;
+    }
+  }
+  return SDME_OK;
+}
+
+int sdme_time_op(sdme_ctx* ctx, int op, int u, int p, int y, double c_m, int reps, double* ms) {
+  if (!ctx || reps < 1 || !ms) return SDME_BAD_ARGUMENT;
+  double *pu = vec(ctx, u), *pp = vec(ctx, p), *py = vec(ctx, y);
+  if (!pu || !pp || !py) return SDME_BAD_ARGUMENT;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaStreamSynchronize(ctx->st));
+  CK(cudaEventRecord(e0, ctx->st));
+  for (int r = 0; r < reps; ++r) {
+    switch (op) {
+      case 0: apply_raw(ctx, pu, pp, py, 1.0, c_m); break;
+      case 1:
+        cudaMemsetAsync(py, 0, ctx->nvec * sizeof(double), ctx->st);
+        ctx->ops->element(ctx, MODE_FINT, pu, nullptr, py, 1.0, 0.0);
+        break;
+      case 2: apply_raw(ctx, nullptr, pp, py, 0.0, 1.0); break;
+      case 3:
+        cudaMemsetAsync(py, 0, ctx->nvec * sizeof(double), ctx->st);
+        ctx->ops->diag(ctx, pu, py, 1.0, c_m);
+        break;
+      default: return SDME_BAD_ARGUMENT;
+    }
+  }
+  CK(cudaEventRecord(e1, ctx->st));
+  CK(cudaEventSynchronize(e1));
+  float t = 0.f;
+  CK(cudaEventElapsedTime(&t, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms = (double)t / reps;
+  return check_launch(ctx);
+}
+
+int sdme_sync(sdme_ctx* ctx) {
+  if (!ctx) return SDME_BAD_ARGUMENT;
+  CK(cudaStreamSynchronize(ctx->st));
+  return SDME_OK;
+}
+
+int sdme_launch_count(const sdme_ctx* ctx, int64_t* n) {
+  if (!ctx || !n) return SDME_BAD_ARGUMENT;
+  *n = ctx->launches;
+  return SDME_OK;
+}
+
+}  // extern "C"

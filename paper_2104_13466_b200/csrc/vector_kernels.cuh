@@ -1,0 +1,230 @@
+// HBM-bound vector kernels: deterministic reductions, fused PCG updates,
+// explicit central-difference update, boundary permutations.
+//
+// Replaces solver.py:140-165 (norms, dots, axpys and the Jacobi apply of the
+// reference PCG loop) and dynamics.py:158-164 (central-difference update).
+// Reductions are two-level with a FIXED grid (kRedBlocks) and fixed in-block
+// trees, so every dot product is bit-reproducible run to run.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sdme {
+
+constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed -> deterministic partials
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum of NV values in fixed order; result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* out) {
+  __shared__ double red[NV][kRedThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double s = warp_sum(v[k]);
+    if (lane == 0) red[k][wid] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = 0.0;
+      for (int w = 0; w < kRedThreads / 32; ++w) s += red[k][w];
+      out[k] = s;
+    }
+  }
+}
+
+template <int NV>
+struct DotArgs {
+  const double* a[NV];
+  const double* b[NV];
+};
+
+// partial[blk*NV + k] for dots (a_k . b_k)
+template <int NV>
+__global__ void __launch_bounds__(kRedThreads) k_dots(const DotArgs<NV> da, long long n, double* partial) {
+  const double* const* a = da.a;
+  const double* const* b = da.b;
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] = fma(a[k][i], b[k][i], acc[k]);
+  }
+  double out[NV];
+  block_sum<NV>(acc, out);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) partial[blockIdx.x * NV + k] = out[k];
+  }
+}
+
+// Sum kRedBlocks partials (fixed order) into res[k].
+template <int NV>
+__global__ void __launch_bounds__(kRedThreads) k_finish(const double* partial, double* res) {
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+  for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] += partial[i * NV + k];
+  }
+  double out[NV];
+  block_sum<NV>(acc, out);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) res[k] = out[k];
+  }
+}
+
+// y = sum_t c_t x_t (up to 6 terms; y may alias an x)
+struct LinComb {
+  const double* x[6];
+  double c[6];
+  int nt;
+};
+__global__ void k_lincomb(LinComb lc, double* y, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int t = 0; t < lc.nt; ++t) s = fma(lc.c[t], lc.x[t][i], s);
+    y[i] = s;
+  }
+}
+
+// ---------------------------------------------------------------- PCG pieces
+// Device scalar block (solver.py:143-165 state):
+//   s[0] = rz, s[1] = pap, s[2] = alpha, s[3] = rr, s[4] = rz_new, s[5] = beta,
+//   s[6] = ||b||
+enum { S_RZ = 0, S_PAP, S_ALPHA, S_RR, S_RZN, S_BETA, S_NB, S_COUNT };
+
+// alpha = rz / pap  (after pap reduced into s[S_PAP])
+__global__ void k_alpha(double* s) {
+  if (threadIdx.x == 0) s[S_ALPHA] = s[S_RZ] / s[S_PAP];
+}
+
+// x += alpha p ; r -= alpha ap ; partial (r.r, r.(dinv r))
+__global__ void __launch_bounds__(kRedThreads) k_pcg_update(double* __restrict__ x, double* __restrict__ r,
+                                                            const double* __restrict__ p,
+                                                            const double* __restrict__ ap,
+                                                            const double* __restrict__ dinv,
+                                                            const double* __restrict__ s, long long n,
+                                                            double* partial) {
+  const double alpha = s[S_ALPHA];
+  double acc[2] = {0.0, 0.0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, ap[i], r[i]);
+    r[i] = ri;
+    acc[0] = fma(ri, ri, acc[0]);
+    acc[1] = fma(ri, dinv[i] * ri, acc[1]);
+  }
+  double out[2];
+  block_sum<2>(acc, out);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x * 2 + 0] = out[0];
+    partial[blockIdx.x * 2 + 1] = out[1];
+  }
+}
+
+// after finishing (rr, rz_new) into s[S_RR], s[S_RZN]: beta, rz <- rz_new
+__global__ void k_beta(double* s) {
+  if (threadIdx.x == 0) {
+    s[S_BETA] = s[S_RZN] / s[S_RZ];
+  }
+}
+__global__ void k_roll(double* s) {
+  if (threadIdx.x == 0) s[S_RZ] = s[S_RZN];
+}
+
+// p = dinv r + beta p
+__global__ void k_pcg_p(double* __restrict__ p, const double* __restrict__ r, const double* __restrict__ dinv,
+                        const double* __restrict__ s, long long n) {
+  const double beta = s[S_BETA];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], dinv[i] * r[i]);
+}
+
+// x = value on free points, 0 on constrained
+__global__ void k_fill_masked(double* __restrict__ x, const unsigned char* __restrict__ freemask, double value,
+                              long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = freemask[i] ? value : 0.0;
+}
+
+// z = dinv r  (initial p)
+__global__ void k_mul(double* __restrict__ z, const double* __restrict__ d, const double* __restrict__ r, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    z[i] = d[i] * r[i];
+}
+
+// dinv = 1/d on free points, 0 on constrained; count non-positive free entries
+__global__ void k_invert_diag(double* __restrict__ dinv, const double* __restrict__ d,
+                              const unsigned char* __restrict__ freemask, long long n,
+                              unsigned long long* bad) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (freemask[i]) {
+      const double v = d[i];
+      if (!(v > 0.0)) atomicMin(bad, (unsigned long long)i);
+      dinv[i] = 1.0 / v;
+    } else {
+      dinv[i] = 0.0;
+    }
+  }
+}
+
+// ------------------------------------------------------- boundary permutation
+// lattice -> reference free order and back (perm[i] = free index or -1)
+__global__ void k_free_to_lattice(double* __restrict__ lat, const double* __restrict__ fr,
+                                  const int* __restrict__ perm, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int k = perm[i];
+    lat[i] = k >= 0 ? fr[k] : 0.0;
+  }
+}
+__global__ void k_lattice_to_free(double* __restrict__ fr, const double* __restrict__ lat,
+                                  const int* __restrict__ perm, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int k = perm[i];
+    if (k >= 0) fr[k] = lat[i];
+  }
+}
+
+// ------------------------------------------------------------ explicit update
+// psi = s_load*load - fint + fc ; u_next = 2u - u_prev + dt^2 psi / m_L ;
+// v = (u_next - u_prev)/(2 dt) ; u_prev <- u ; u <- u_next     (D6 / A13)
+__global__ void k_explicit_step(double* __restrict__ u, double* __restrict__ u_prev, double* __restrict__ v,
+                                const double* __restrict__ load, double s_load,
+                                const double* __restrict__ fint, const double* __restrict__ fc,
+                                const double* __restrict__ inv_ml, double dt, long long n) {
+  const double dt2 = dt * dt, i2dt = 1.0 / (2.0 * dt);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double psi = -fint[i];
+    if (load) psi = fma(s_load, load[i], psi);
+    if (fc) psi += fc[i];
+    const double ui = u[i], up = u_prev[i];
+    const double un = (2.0 * ui - up) + dt2 * psi * inv_ml[i];
+    v[i] = (un - up) * i2dt;
+    u_prev[i] = ui;
+    u[i] = un;
+  }
+}
+
+}  // namespace sdme

@@ -1,0 +1,300 @@
+"""Time integration drivers on device-resident vectors.
+
+``newmark_run`` follows ``sdmefem.dynamics.newmark_run`` (``dynamics.py:173-257``)
+step for step -- trial acceleration, residual psi = P - R(u) - M a, Newton
+stop relative to the first ||psi|| of the step, effective operator
+K_T + b1 M, Newmark v/a update -- with every vector operation on the GPU and
+the linear solves done by matrix-free Jacobi-PCG.
+
+``explicit_run`` is the central-difference scheme of ``dynamics.py:130-170``
+with the row-sum lumped mass and penalty contact against a rigid plane
+(SURVEY D6): m_L = M 1, w = dt^2 psi / m_L, u+ = 2u - u_prev + w,
+v = (u+ - u_prev) / (2 dt).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import NewtonDivergenceError
+from .problem import DeviceVector, GpuFemProblem
+from .solver import SolverConfig, StatsLog, pcg_gpu
+
+__all__ = ["NewmarkCoeffs", "TimeState", "Trajectory", "ScaledLoad", "cfl_dt", "newmark_run",
+           "explicit_run", "estimate_lambda_max"]
+
+
+@dataclass
+class NewmarkCoeffs:
+    """``dynamics.py:46-59``."""
+
+    dt: float
+    gamma: float = 0.5
+    beta: float = 0.25
+
+    def __post_init__(self):
+        if self.dt <= 0.0:
+            raise ValueError("time step must be positive")
+        self.b1 = 1.0 / (self.beta * self.dt ** 2)
+        self.b2 = 1.0 / (self.beta * self.dt)
+        self.b3 = (1.0 - 2.0 * self.beta) / (2.0 * self.beta)
+
+
+@dataclass
+class TimeState:
+    t: float
+    u: np.ndarray
+    v: np.ndarray
+    a: np.ndarray
+    u_prev: np.ndarray | None = None
+
+
+@dataclass
+class Trajectory:
+    times: list = field(default_factory=list)
+    snapshots: list = field(default_factory=list)
+    energy: list = field(default_factory=list)
+    state: TimeState | None = None
+    stats: StatsLog = field(default_factory=StatsLog)
+    newton_iters: list = field(default_factory=list)
+    contact_history: list = field(default_factory=list)
+
+
+class ScaledLoad:
+    """external_load(t) = scale(t) * base, kept on the device (one upload).
+
+    Any plain callable returning a free vector is accepted by the drivers too
+    (uploaded every evaluation); this form avoids the per-step transfer.
+    """
+
+    def __init__(self, base_free: np.ndarray, scale=lambda t: 1.0):
+        self.base = np.asarray(base_free, dtype=float)
+        self.scale = scale
+
+    def __call__(self, t):
+        return self.scale(t) * self.base
+
+
+def cfl_dt(mesh, mat, delta: float, mode: str = "AsPrinted") -> float:
+    """``dynamics.py:81-101`` (host arithmetic only)."""
+    if not 0.2 < delta < 0.9:
+        raise ValueError(f"delta should lie in (0.2, 0.9), got {delta}")
+    mu, lam, rho = mat.mu, mat.lambda_lame, mat.rho0
+    e_mod = mu * (3.0 * lam + 2.0 * mu) / (lam + mu)
+    nu = lam / (2.0 * (lam + mu))
+    bulk = e_mod / (3.0 * (1.0 - 2.0 * nu))
+    c = 3.0 * bulk * (1.0 - nu) / (rho * (1.0 + nu))
+    if mode == "PhysicalSqrt":
+        c = np.sqrt(c)
+    elif mode != "AsPrinted":
+        raise ValueError(f"unknown CFL mode {mode!r}")
+    return delta * mesh.min_edge_length() / c
+
+
+class _Load:
+    """Evaluates external_load(t) into a device vector."""
+
+    def __init__(self, problem: GpuFemProblem, external_load):
+        self.pb = problem
+        self.fn = external_load
+        self.vec = DeviceVector(problem)
+        self.scaled = isinstance(external_load, ScaledLoad)
+        if self.scaled:
+            self.base = DeviceVector(problem).set_free(external_load.base)
+        self._last = None
+
+    def at(self, t: float) -> DeviceVector:
+        if self.scaled:
+            s = float(self.fn.scale(t))
+            if self._last != s:
+                self.vec.assign(s, self.base)
+                self._last = s
+        else:
+            self.vec.set_free(np.asarray(self.fn(t), dtype=float))
+        return self.vec
+
+
+def _dev(problem, x) -> DeviceVector:
+    v = DeviceVector(problem)
+    if x is not None:
+        v.set_free(np.asarray(x, dtype=float))
+    return v
+
+
+def newmark_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
+                newton_tol: float = 1e-8, newton_maxit: int = 25, u0=None, v0=None,
+                cfg: SolverConfig | None = None, gamma: float = 0.5, beta: float = 0.25,
+                contact=None, snapshot_stride: int = 0, track_energy: bool = False) -> Trajectory:
+    """Implicit Newmark with Newton-Raphson (``dynamics.py:173-257``)."""
+    if contact is not None:
+        raise NotImplementedError("implicit penalty contact (contact stiffness) is the next row "
+                                  "(SURVEY F3); use explicit_run(..., contact=...)")
+    if track_energy:
+        raise NotImplementedError("energy tracking is not on the GPU path")
+    cfg = cfg or SolverConfig(precond="diagonal", tol=1e-10, condense=False)
+    cfg.validate()
+    nm = NewmarkCoeffs(dt, gamma, beta)
+    pb = problem
+    u = _dev(pb, u0)
+    v = _dev(pb, v0)
+    load = _Load(pb, external_load)
+    traj = Trajectory()
+    uk, atr, psi, tmp, du, a = (DeviceVector(pb) for _ in range(6))
+
+    def residual(uk_, atr_, t_next):
+        # psi = P(t) - R(uk) - M a_trial   (dynamics.py:197-203)
+        pb.fint_(uk_, tmp)
+        pb.mass_(atr_, psi)
+        return psi.assign(1.0, load.at(t_next), -1.0, tmp, -1.0, psi)
+
+    # a0 = M^-1 psi0 (mass-only PCG, short-circuits for psi0 = 0)
+    atr.fill(0.0)
+    residual(u, atr, 0.0)
+    _, st = pcg_gpu(pb, None, psi, c_m=1.0, precond=cfg.precond, tol=cfg.tol, maxit=cfg.maxit,
+                    c_k=0.0, x=a)
+    traj.stats.add(-1, 0, "newmark-init", st)
+
+    t = 0.0
+    for step in range(n_steps):
+        t_next = t + dt
+        uk.copy_from(u)
+        psi_ref = None
+        n_newton = 0
+        for k in range(newton_maxit):
+            # a_trial = b1 (uk - u) - b2 v - b3 a  (difference first, as dynamics.py:219)
+            tmp.assign(1.0, uk, -1.0, u)
+            atr.assign(nm.b1, tmp, -nm.b2, v, -nm.b3, a)
+            residual(uk, atr, t_next)
+            rnorm = psi.norm()
+            if psi_ref is None:
+                psi_ref = rnorm
+            if psi_ref == 0.0:
+                break
+            if rnorm <= newton_tol * psi_ref:
+                break
+            if k == newton_maxit - 1:
+                raise NewtonDivergenceError(
+                    f"Newton did not converge in {newton_maxit} iterations at t={t_next:.6g} "
+                    f"(residual {rnorm / psi_ref:.3e} relative)", rnorm)
+            _, st = pcg_gpu(pb, uk, psi, c_m=nm.b1, precond=cfg.precond, tol=cfg.tol,
+                            maxit=cfg.maxit, x=du)
+            traj.stats.add(step, k, "newmark", st)
+            uk.assign(1.0, uk, 1.0, du)
+            n_newton += 1
+        traj.newton_iters.append(n_newton)
+        # a_next = b1(uk-u) - b2 v - b3 a ; v += dt((1-g) a + g a_next) ; u = uk
+        tmp.assign(1.0, uk, -1.0, u)
+        atr.assign(nm.b1, tmp, -nm.b2, v, -nm.b3, a)
+        v.assign(1.0, v, dt * (1.0 - gamma), a, dt * gamma, atr)
+        a.copy_from(atr)
+        u.copy_from(uk)
+        t = t_next
+        if snapshot_stride and (step + 1) % snapshot_stride == 0:
+            traj.times.append(t)
+            traj.snapshots.append(u.free())
+    traj.state = TimeState(t, u.free(), v.free(), a.free())
+    return traj
+
+
+def lumped_mass(problem: GpuFemProblem) -> tuple[DeviceVector, DeviceVector]:
+    """(m_L, 1/m_L): row sums of the consistent mass over free columns,
+    ``mass().sum(axis=1)``, computed as M 1 on the device."""
+    ones = DeviceVector(problem).fill(1.0)
+    ml = problem.mass_(ones, DeviceVector(problem))
+    inv = DeviceVector(problem)
+    from . import native
+
+    native.check(problem._ctx, native.lib().sdme_vec_reciprocal(problem._ctx, inv.vid, ml.vid),
+                 "lumped mass")
+    return ml, inv
+
+
+def estimate_lambda_max(problem: GpuFemProblem, inv_ml: DeviceVector, contact=None,
+                        iters: int = 30, seed: int = 0) -> float:
+    """Power iteration for lambda_max(M_L^-1 (K_0 + K_c)) at u = 0.
+
+    Contact stiffness is bounded by eps * sum_q warea N_f^2 on the contact
+    plane; it is included as a diagonal upper bound when ``contact`` is given.
+    """
+    pb = problem
+    rng = np.random.default_rng(seed)
+    x = DeviceVector(pb).set_free(rng.standard_normal(pb.n_free))
+    y = DeviceVector(pb)
+    z = DeviceVector(pb)
+    u0 = DeviceVector(pb)
+    lam = 0.0
+    # symmetric form: A = M^-1/2 K M^-1/2 ; iterate on y = M^-1 K x (same spectrum)
+    for _ in range(iters):
+        nrm = x.norm()
+        x.assign(1.0 / nrm, x)
+        pb.apply_(u0, x, y, 1.0, 0.0)
+        _mul(pb, z, inv_ml, y)
+        lam = z.norm()
+        x.copy_from(z)
+    if contact is not None:
+        lam += contact.stiffness_bound() * max(inv_ml.lattice().max(), 0.0)
+    return float(lam)
+
+
+def _mul(pb, out, a, b):
+    from . import native
+
+    native.check(pb._ctx, native.lib().sdme_vec_mul(pb._ctx, out.vid, a.vid, b.vid), "vec_mul")
+    return out
+
+
+def explicit_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int, u0=None, v0=None,
+                 cfg: SolverConfig | None = None, snapshot_stride: int = 0, contact=None,
+                 record_every: int = 0) -> Trajectory:
+    """Central difference with lumped mass (+ penalty contact) on the GPU.
+
+    ``external_load`` may be None (no load), a :class:`ScaledLoad`, or any
+    callable of t returning a free vector.  Startup a0 = M_L^-1 psi0,
+    u_-1 = u0 - dt v0 + dt^2/2 a0 (``dynamics.py:152-155``).
+    """
+    pb = problem
+    u = _dev(pb, u0)
+    v = _dev(pb, v0)
+    traj = Trajectory()
+    _, inv_ml = lumped_mass(pb)
+    load = _Load(pb, external_load) if external_load is not None else None
+    fint = DeviceVector(pb)
+    fc = DeviceVector(pb) if contact is not None else None
+    u_prev = DeviceVector(pb)
+    a0 = DeviceVector(pb)
+    # psi0 = P(0) - f_int(u0) + f_c(u0)
+    pb.fint_(u, fint)
+    terms = [-1.0, fint]
+    if load is not None:
+        terms += [1.0, load.at(0.0)]
+    if contact is not None:
+        contact.forces_(u, fc)
+        terms += [1.0, fc]
+    psi = DeviceVector(pb).assign(*terms)
+    _mul(pb, a0, inv_ml, psi)
+    u_prev.assign(1.0, u, -dt, v, 0.5 * dt * dt, a0)
+    del psi
+    t = 0.0
+    from . import native
+
+    lib = native.lib()
+    for step in range(n_steps):
+        lid = -1
+        if load is not None:
+            lid = load.at(t).vid
+        fid = -1
+        if contact is not None:
+            contact.forces_(u, fc, record=(record_every and step % record_every == 0))
+            fid = fc.vid
+        native.check(pb._ctx, lib.sdme_explicit_step(pb._ctx, u.vid, u_prev.vid, v.vid, lid, 1.0, fid,
+                                                     inv_ml.vid, dt, fint.vid), "explicit_step")
+        t += dt
+        if snapshot_stride and (step + 1) % snapshot_stride == 0:
+            traj.times.append(t)
+            traj.snapshots.append(u.free())
+    traj.state = TimeState(t, u.free(), v.free(), a0.free(), u_prev.free())
+    if contact is not None:
+        traj.contact_history = list(contact.history)
+    return traj

@@ -1,0 +1,143 @@
+"""Jacobi-PCG on the GPU: drop-in for ``sdmefem.solver.pcg`` / ``LinearSolver``.
+
+The reference's ``pcg(a, b, precond, tol, maxit)`` (``solver.py:129-170``)
+needs an assembled matrix (``a @ p`` and ``a.diagonal()``), so the drop-in
+replaces the *solver*, not just the operator.  The operator is
+A = c_k K_T(u_lin) + c_m M, applied matrix-free on the device; the iteration,
+its order of checks (pAp <= 0 -> PCGError; recursive-residual stop; maxit ->
+PCGError with the true residual) and :class:`SolveStats` are the reference's.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import native
+from .errors import PCGError
+from .problem import DeviceVector, GpuFemProblem
+
+__all__ = ["SolveStats", "StatsLog", "PCGError", "SolverConfig", "pcg_gpu", "GpuLinearSolver",
+           "make_solver"]
+
+_PRECOND = {"diagonal": 1, "none": 0, None: 0}
+
+
+@dataclass
+class SolveStats:
+    """``solver.py:41-47``."""
+
+    iterations: int
+    residual: float
+    seconds: float
+    preconditioner: str
+    converged: bool = True
+
+
+@dataclass
+class StatsLog:
+    """``solver.py:50-75``: per-linear-solve records of the drivers."""
+
+    rows: list = field(default_factory=list)
+
+    def add(self, step: int, newton_iter: int, solver: str, stats: SolveStats):
+        self.rows.append({"step": step, "newton_iter": newton_iter, "solver": solver,
+                          "preconditioner": stats.preconditioner, "iterations": stats.iterations,
+                          "residual": stats.residual, "seconds": stats.seconds})
+
+    def mean_iterations(self) -> float:
+        return float(np.mean([r["iterations"] for r in self.rows])) if self.rows else 0.0
+
+    def total_seconds(self) -> float:
+        return float(sum(r["seconds"] for r in self.rows))
+
+
+@dataclass
+class SolverConfig:
+    """``dynamics.py:38-43``.  The GPU path solves the full (uncondensed)
+    system with the Jacobi preconditioner; ``precond="sgs"`` and
+    ``condense=True`` need the assembled CSR and are rejected."""
+
+    precond: str = "diagonal"
+    tol: float = 1e-12
+    maxit: int = 200000
+    condense: bool = False
+
+    def validate(self):
+        if self.condense:
+            raise ValueError("condense=True (Schur on dense element matrices) is not available on the "
+                             "matrix-free GPU path; use condense=False")
+        if self.precond not in _PRECOND:
+            raise ValueError(f"preconditioner {self.precond!r} is not available on the GPU path "
+                             "(Jacobi 'diagonal' or 'none')")
+
+
+def pcg_gpu(problem: GpuFemProblem, u_lin, b, c_m: float = 0.0, precond: str = "diagonal",
+            tol: float = 1e-8, maxit: int = 10000, c_k: float = 1.0, x: DeviceVector | None = None):
+    """Solve (c_k K_T(u_lin) + c_m M) x = b on the device.
+
+    ``u_lin`` / ``b``: free-order ndarrays or :class:`DeviceVector`.  Returns
+    (x, SolveStats) with x of the same kind as ``b``.  Raises ``ValueError``
+    for a bad tol or non-positive diagonal and :class:`PCGError` exactly where
+    the reference does.
+    """
+    if not 0.0 < tol < 1.0:
+        raise ValueError(f"tolerance must lie in (0, 1), got {tol}")
+    if precond not in _PRECOND:
+        raise ValueError(f"unknown preconditioner {precond!r}")
+    tag = "diagonal" if _PRECOND[precond] == 1 else "none"
+    t0 = time.perf_counter()
+    host = not isinstance(b, DeviceVector)
+    bv = problem._scratch("pcg_b").set_free(b) if host else b
+    if u_lin is None or c_k == 0.0:
+        uv = None
+    elif isinstance(u_lin, DeviceVector):
+        uv = u_lin
+    else:
+        uv = problem._scratch("pcg_u").set_free(u_lin)
+    xv = x if x is not None else (problem._scratch("pcg_x") if host else DeviceVector(problem))
+    its = C.c_int(0)
+    rel = C.c_double(0.0)
+    rc = native.lib().sdme_pcg(problem._ctx, uv.vid if uv is not None else -1, c_k, c_m, bv.vid, xv.vid,
+                               tol, maxit, _PRECOND[precond], C.byref(its), C.byref(rel))
+    secs = time.perf_counter() - t0
+    if rc in (native.INDEFINITE, native.MAXIT):
+        _, _, _, msg = native.last_error(problem._ctx)
+        raise PCGError(msg, SolveStats(its.value, rel.value, secs, tag, False))
+    native.check(problem._ctx, rc, "pcg")
+    stats = SolveStats(its.value, rel.value, secs, tag)
+    return (xv.free() if host else xv), stats
+
+
+@dataclass
+class GpuLinearSolver:
+    """``LinearSolver`` (solver.py:302-322) for A = c_k K_T(u_lin) + c_m M."""
+
+    problem: GpuFemProblem
+    u_lin: DeviceVector | None
+    c_m: float = 0.0
+    precond: str = "diagonal"
+    tol: float = 1e-8
+    maxit: int = 50000
+    c_k: float = 1.0
+
+    @property
+    def condensed(self) -> bool:
+        return False
+
+    def solve(self, rhs, x: DeviceVector | None = None):
+        return pcg_gpu(self.problem, self.u_lin, rhs, self.c_m, self.precond, self.tol, self.maxit,
+                       self.c_k, x=x)
+
+
+def make_solver(problem: GpuFemProblem, u_lin, c_m: float, cfg: SolverConfig,
+                c_k: float = 1.0) -> GpuLinearSolver:
+    """``make_solver`` (dynamics.py:111-127) without element matrices: the
+    operator is defined by its linearisation point and mass coefficient."""
+    cfg.validate()
+    if u_lin is not None and not isinstance(u_lin, DeviceVector):
+        u_lin = problem.vector(np.asarray(u_lin, dtype=float))
+    return GpuLinearSolver(problem, u_lin, c_m, cfg.precond, cfg.tol, cfg.maxit, c_k)

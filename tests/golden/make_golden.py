@@ -1,0 +1,212 @@
+"""Generate golden vectors from the REAL reference package (sdmefem).
+
+Run in the build container, where the reference tree exists:
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_golden.py
+
+Writes small compressed .npz fixtures next to this file.  Nothing at test or
+bench time reads /root/reference; the fixtures are the pin for both the oracle
+(tests/test_oracle_golden.py) and the GPU path (tests/test_gpu_parity.py).
+All inputs are seeded (numpy default_rng) and stored alongside the outputs.
+"""
+
+from __future__ import annotations
+
+import os
+import time
+
+import numpy as np
+
+from sdmefem.basis1d import BasisKind, build_basis
+from sdmefem.contact import ContactParams, PenaltyContact, RigidObstacle
+from sdmefem.dynamics import SolverConfig, newmark_run
+from sdmefem.femcore import (FemProblem, build_face_tables, element_internal_force,
+                             element_mass, element_tangent)
+from sdmefem.material import NeoHookean
+from sdmefem.meshdof import build_dofmap, gen_box_mesh
+from sdmefem.quadrature import gauss_rule
+from sdmefem.solver import pcg
+from sdmefem.tensorelem import TensorElement
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+KINDS = ("LagrangeGLL", "ModalJacobi", "SDME_M", "SDME_K", "SDME_H")
+MAT = NeoHookean.from_engineering(1.0e7, 0.3, 1.0e3)
+
+
+def problem(tag, P, div, lengths, m, dirichlet=None, origin=None):
+    mesh = gen_box_mesh(div, lengths, origin)
+    el = TensorElement.create(3, build_basis(P, BasisKind(tag)))
+    dm = build_dofmap(mesh, el, dirichlet)
+    return FemProblem(mesh, el, dm, MAT, rule=gauss_rule(m))
+
+
+def smooth_plus_noise(prob, amp, noise, seed):
+    """Seeded admissible displacement: L2 projection of a smooth field plus
+    small i.i.d. coefficient noise (keeps det F > 0)."""
+    rng = np.random.default_rng(seed)
+    u = prob.l2_project(lambda x: amp * np.column_stack(
+        [np.sin(2 * np.pi * (x[:, 0] + x[:, 1] + x[:, 2])),
+         np.cos(2 * np.pi * (x[:, 0] - 0.5 * x[:, 2])),
+         x[:, 0] * x[:, 1]]))
+    return u + noise * rng.uniform(-1.0, 1.0, prob.n_free)
+
+
+def gen_basis():
+    out = {}
+    for tag in KINDS:
+        for P in (1, 2, 3, 4, 6, 8):
+            if P == 1 and tag.startswith("SDME"):
+                continue
+            b = build_basis(P, BasisKind(tag))
+            out[f"{tag}_P{P}_T"] = b.transform
+            for m in (P + 1, P + 2):
+                bb = b.with_rule(gauss_rule(m))
+                out[f"{tag}_P{P}_m{m}_B"] = bb.values.T
+                out[f"{tag}_P{P}_m{m}_D"] = bb.derivs.T
+    np.savez_compressed(os.path.join(HERE, "basis.npz"), **out)
+
+
+def gen_elements():
+    """Single-element meshes: the global vector is the element vector in
+    reference local order (function-major, component fastest)."""
+    out = {}
+    cases = []
+    for tag in KINDS:
+        for P in (2, 3, 4, 6, 8):
+            for m in (P + 1, P + 2):
+                cases.append((tag, P, m, (1 / 64,) * 3))
+    cases += [("SDME_M", 4, 5, (0.5, 0.3, 0.7)), ("LagrangeGLL", 3, 5, (0.2, 1.0, 0.4)),
+              ("ModalJacobi", 2, 3, (1.0, 1.0, 1.0))]
+    for ci, (tag, P, m, h) in enumerate(cases):
+        prob = problem(tag, P, (1, 1, 1), h, m)
+        rng = np.random.default_rng(100 + ci)
+        nf = prob.n_free
+        scale = 0.05 * min(h) / P
+        u = scale * rng.uniform(-1, 1, nf)
+        p = rng.standard_normal(nf)
+        tab = prob.tables[0]
+        ue = prob.gather(0, u)
+        r = element_internal_force(tab, MAT, ue, 0)
+        k = element_tangent(tab, MAT, ue, 0)
+        mm = element_mass(tab, MAT, 3)
+        c_m = 1.0 / (0.25 * 1e-4 ** 2)
+        key = f"c{ci}"
+        out[key + "_meta"] = np.array([KINDS.index(tag), P, m, *h])
+        out[key + "_u"] = u
+        out[key + "_p"] = p
+        out[key + "_fint"] = r
+        pe = prob.gather(0, p).reshape(-1)
+        out[key + "_kp"] = k @ pe
+        out[key + "_mp"] = mm @ pe
+        out[key + "_diag"] = np.diag(k + c_m * mm)
+        out[key + "_cm"] = np.array(c_m)
+    np.savez_compressed(os.path.join(HERE, "elements.npz"), **out)
+
+
+def gen_global():
+    """Multi-element meshes with Dirichlet faces, reference free order."""
+    out = {}
+    cases = [("SDME_M", 4, 5, (2, 3, 2), (1.0, 1.5, 1.0), [("xmin", (0, 1, 2))]),
+             ("LagrangeGLL", 3, 5, (3, 2, 2), (1.0, 1.0, 0.5), [("xmin", (0, 1, 2)), ("zmax", (2,))]),
+             ("ModalJacobi", 2, 3, (2, 2, 3), (0.5, 0.5, 1.0), None),
+             ("SDME_H", 3, 4, (2, 2, 2), (1.0, 1.0, 1.0), [("ymin", (1,))])]
+    for ci, (tag, P, m, div, L, dr) in enumerate(cases):
+        prob = problem(tag, P, div, L, m, dr)
+        u = smooth_plus_noise(prob, 0.01, 1e-4, 7 + ci)
+        rng = np.random.default_rng(50 + ci)
+        p = rng.standard_normal(prob.n_free)
+        c_m = 3.0e4
+        kt = prob.tangent(u)
+        mass = prob.mass()
+        eff = kt + c_m * mass
+        key = f"g{ci}"
+        out[key + "_meta"] = np.array([KINDS.index(tag), P, m, *div, *L])
+        out[key + "_dir"] = np.array([[["xmin", "xmax", "ymin", "ymax", "zmin", "zmax"].index(t), c]
+                                      for t, cs in (dr or []) for c in cs]).reshape(-1, 2)
+        out[key + "_u"] = u
+        out[key + "_p"] = p
+        out[key + "_fint"] = prob.internal_force(u)
+        out[key + "_kp"] = kt @ p
+        out[key + "_mp"] = mass @ p
+        out[key + "_diag"] = eff.diagonal()
+        out[key + "_cm"] = np.array(c_m)
+        b = prob.internal_force(u) + 1e3 * p
+        x, st = pcg(eff, b, precond="diagonal", tol=1e-10, maxit=100000)
+        out[key + "_pcg_b"] = b
+        out[key + "_pcg_x"] = x
+        out[key + "_pcg_iters"] = np.array(st.iterations)
+    np.savez_compressed(os.path.join(HERE, "global.npz"), **out)
+
+
+def gen_config1():
+    """BASELINE config 1: 4^3 P=4 SDME, (P+2)^3 Gauss, Newmark 10 steps,
+    Jacobi-PCG 1e-10 full system."""
+    P, m = 4, 6
+    prob = problem("SDME_M", P, (4, 4, 4), (1.0, 1.0, 1.0), m, [("xmin", (0, 1, 2))])
+    faces = build_face_tables(prob.mesh, prob.element, "xmax", prob.rule)
+    base = prob.traction_vector(faces, lambda f: np.tile([0.0, 0.0, 1.0e5], (len(f.pts), 1)))
+    dt = 1e-4
+    ramp = 10 * dt
+    load = lambda t: base * min(t / ramp, 1.0)
+    cfg = SolverConfig(precond="diagonal", tol=1e-10, maxit=200000, condense=False)
+    t0 = time.perf_counter()
+    traj = newmark_run(prob, load, dt, 10, newton_tol=1e-8, cfg=cfg)
+    wall = time.perf_counter() - t0
+    rows = [(r["step"], r["newton_iter"], r["iterations"]) for r in traj.stats.rows]
+    np.savez_compressed(os.path.join(HERE, "config1.npz"), u=traj.state.u, v=traj.state.v,
+                        a=traj.state.a, load=base, newton_iters=np.array(traj.newton_iters),
+                        pcg_rows=np.array(rows), wall_s=np.array(wall))
+    print("config1", wall, "s", traj.newton_iters, [r[2] for r in rows])
+
+
+def gen_contact():
+    """Contact force + D6 explicit restatement loop from reference pieces."""
+    out = {}
+    P = 3
+    prob = problem("SDME_M", P, (3, 2, 2), (0.3, 0.2, 0.2), P + 1, None,
+                   origin=(0.0, 0.0, 0.0))
+    obst = RigidObstacle(np.array([-1e-3, 0.0, 0.0]), np.array([1.0, 0.0, 0.0]))
+    cont = PenaltyContact(prob, obst, ContactParams(1e10), "xmin")
+    rng = np.random.default_rng(3)
+    u = prob.l2_project(lambda x: MAT.rho0 * np.tile([-2e-3, 0.0, 0.0], (len(x), 1)))
+    u = u + 1e-4 * rng.uniform(-1, 1, prob.n_free)
+    fc = cont.evaluate_forces(u)
+    out["u"] = u
+    out["force"] = fc.force
+    out["gaps"] = fc.gaps
+    # D6 explicit loop: lumped mass, contact, v0 = -10 m/s in x
+    ml = np.asarray(prob.mass().sum(axis=1)).ravel()
+    v0 = prob.l2_project(lambda x: MAT.rho0 * np.tile([-10.0, 0.0, 0.0], (len(x), 1)))
+    dt = 2e-7
+    n_steps = 40
+    uu = np.zeros(prob.n_free)
+    obst2 = RigidObstacle(np.array([-2e-5, 0.0, 0.0]), np.array([1.0, 0.0, 0.0]))
+    cont2 = PenaltyContact(prob, obst2, ContactParams(1e10), "xmin")
+
+    def psi(uk):
+        return -prob.internal_force(uk) + cont2.evaluate_forces(uk).force
+
+    a0 = psi(uu) / ml
+    up = uu - dt * v0 + 0.5 * dt * dt * a0
+    for _ in range(n_steps):
+        un = 2 * uu - up + dt * dt * psi(uu) / ml
+        vv = (un - up) / (2 * dt)
+        up, uu = uu, un
+    out["v0"] = v0
+    out["explicit_u"] = uu
+    out["explicit_v"] = vv
+    out["explicit_dt"] = np.array(dt)
+    out["explicit_steps"] = np.array(n_steps)
+    out["m_lumped"] = ml
+    np.savez_compressed(os.path.join(HERE, "contact.npz"), **out)
+
+
+if __name__ == "__main__":
+    import sys
+
+    which = sys.argv[1:] or ["basis", "elements", "global", "contact", "config1"]
+    for w in which:
+        t = time.perf_counter()
+        globals()["gen_" + w]()
+        print(w, f"{time.perf_counter() - t:.1f}s")

@@ -1,0 +1,214 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the reference's golden
+vectors and the CPU oracle.
+
+Bars (north_star): 1e-12 relative on element/global vectors, PCG iteration
+counts +-1, displacements within 1e-9 relative, bit-identical reruns.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import element_cases, global_cases, load_golden, max_rel_err, rel_err
+from oracle import basis as ob
+from oracle import fem as of
+from oracle import solve as osv
+from paper_2104_13466_b200 import (BoxMesh, ContactParams, ElementInversionError, GpuFemProblem,
+                                   GpuPenaltyContact, NeoHookean, PCGError, RigidObstacle, ScaledLoad,
+                                   SolverConfig, build_basis, explicit_run, gauss_rule, newmark_run,
+                                   pcg_gpu)
+from paper_2104_13466_b200.basis import BasisKind
+
+pytestmark = pytest.mark.gpu
+
+MAT = NeoHookean.from_engineering(1.0e7, 0.3, 1.0e3)
+OMAT = of.Material(1.0e7, 0.3, 1.0e3)
+TOL = 1e-12
+
+
+def gpu_problem(tag, P, m, div, L, dr=None, origin=(0.0, 0.0, 0.0)):
+    return GpuFemProblem(BoxMesh(div, L, origin), build_basis(P, BasisKind(tag)), MAT, gauss_rule(m), dr)
+
+
+@pytest.mark.parametrize("case", element_cases(), ids=lambda c: f"{c[1]}-P{c[2]}-m{c[3]}-{c[0]}")
+def test_element_vectors_vs_reference(case):
+    """Single-element meshes: f_int, K.p, M.p, diag(K + c_m M) vs the
+    reference's element_internal_force / element_tangent / element_mass."""
+    i, tag, P, m, h = case
+    g = load_golden("elements")
+    pb = gpu_problem(tag, P, m, (1, 1, 1), h)
+    loc = of.DofMap(of.Mesh((1, 1, 1), h), P).evdofs(0)  # local order -> free index
+    u, p, cm = g[f"c{i}_u"], g[f"c{i}_p"], float(g[f"c{i}_cm"])
+    assert max_rel_err(pb.internal_force(u)[loc], g[f"c{i}_fint"]) <= TOL
+    assert max_rel_err(pb.apply_tangent(u, p)[loc], g[f"c{i}_kp"]) <= TOL
+    assert max_rel_err(pb.mass_apply(p)[loc], g[f"c{i}_mp"]) <= TOL
+    assert max_rel_err(pb.tangent_diagonal(u, cm)[loc], g[f"c{i}_diag"]) <= TOL
+
+
+@pytest.mark.parametrize("case", global_cases(), ids=lambda c: f"{c[1]}-P{c[2]}")
+def test_global_vectors_and_pcg_vs_reference(case):
+    i, tag, P, m, div, L, dr = case
+    g = load_golden("global")
+    pb = gpu_problem(tag, P, m, div, L, dr)
+    assert pb.n_free == g[f"g{i}_u"].size
+    u, p, cm = g[f"g{i}_u"], g[f"g{i}_p"], float(g[f"g{i}_cm"])
+    assert max_rel_err(pb.internal_force(u), g[f"g{i}_fint"]) <= TOL
+    assert max_rel_err(pb.apply_tangent(u, p), g[f"g{i}_kp"]) <= TOL
+    assert max_rel_err(pb.apply_tangent(u, p, cm), g[f"g{i}_kp"] + cm * g[f"g{i}_mp"]) <= TOL
+    assert max_rel_err(pb.mass_apply(p), g[f"g{i}_mp"]) <= TOL
+    assert max_rel_err(pb.tangent_diagonal(u, cm), g[f"g{i}_diag"]) <= TOL
+    x, st = pcg_gpu(pb, u, g[f"g{i}_pcg_b"], c_m=cm, precond="diagonal", tol=1e-10, maxit=100000)
+    assert abs(st.iterations - int(g[f"g{i}_pcg_iters"])) <= 1
+    assert max_rel_err(x, g[f"g{i}_pcg_x"]) <= 1e-9
+
+
+def test_config1_newmark_vs_reference():
+    """BASELINE config 1 (4^3, P=4 SDME, (P+2)^3 Gauss, 10 Newmark steps,
+    Jacobi-PCG 1e-10): Newton counts equal, PCG iterations +-1, u within 1e-9."""
+    g = load_golden("config1")
+    pb = gpu_problem("SDME_M", 4, 6, (4, 4, 4), (1.0, 1.0, 1.0), [("xmin", (0, 1, 2))])
+    base = pb.traction_vector("xmax", [0.0, 0.0, 1.0e5])
+    assert max_rel_err(base, g["load"]) <= TOL
+    load = ScaledLoad(base, lambda t: min(t / 1e-3, 1.0))
+    cfg = SolverConfig(precond="diagonal", tol=1e-10, maxit=200000, condense=False)
+    traj = newmark_run(pb, load, 1e-4, 10, newton_tol=1e-8, cfg=cfg)
+    assert traj.newton_iters == [int(v) for v in g["newton_iters"]]
+    ref_its = [int(r[2]) for r in g["pcg_rows"] if r[0] >= 0]
+    its = [r["iterations"] for r in traj.stats.rows if r["step"] >= 0]
+    assert len(its) == len(ref_its)
+    assert max(abs(a - b) for a, b in zip(its, ref_its)) <= 1
+    assert max_rel_err(traj.state.u, g["u"]) <= 1e-9
+    assert max_rel_err(traj.state.v, g["v"]) <= 1e-8
+
+
+def test_contact_force_vs_reference():
+    g = load_golden("contact")
+    pb = gpu_problem("SDME_M", 3, 4, (3, 2, 2), (0.3, 0.2, 0.2))
+    c = GpuPenaltyContact(pb, RigidObstacle([-1e-3, 0, 0], [1, 0, 0]), ContactParams(1e10), "xmin")
+    fc = c.evaluate_forces(g["u"])
+    assert fc.stiffness is None
+    assert max_rel_err(fc.force, g["force"]) <= TOL
+    assert max_rel_err(fc.gaps, g["gaps"]) <= TOL
+    assert fc.active.any()
+
+
+def test_explicit_lumped_contact_vs_reference_pieces():
+    """D6 loop: lumped mass + penalty contact, 40 steps, vs the loop built
+    from the reference's own internal_force / evaluate_forces / mass."""
+    g = load_golden("contact")
+    pb = gpu_problem("SDME_M", 3, 4, (3, 2, 2), (0.3, 0.2, 0.2))
+    c = GpuPenaltyContact(pb, RigidObstacle([-2e-5, 0, 0], [1, 0, 0]), ContactParams(1e10), "xmin")
+    traj = explicit_run(pb, None, float(g["explicit_dt"]), int(g["explicit_steps"]), v0=g["v0"],
+                        contact=c, record_every=1)
+    assert max(h[1] for h in traj.contact_history) > 0.0  # contact engaged
+    assert max_rel_err(traj.state.u, g["explicit_u"]) <= 1e-10
+    assert max_rel_err(traj.state.v, g["explicit_v"]) <= 1e-9
+
+
+def test_reruns_are_bit_identical():
+    pb = gpu_problem("SDME_M", 4, 5, (6, 5, 4), (1.0, 1.0, 1.0), [("xmin", (0, 1, 2))])
+    rng = np.random.default_rng(0)
+    u = 1e-4 * rng.uniform(-1, 1, pb.n_free)
+    p = rng.standard_normal(pb.n_free)
+    a = pb.apply_tangent(u, p, 3e4)
+    b = pb.apply_tangent(u, p, 3e4)
+    assert np.array_equal(a.view(np.int64), b.view(np.int64))
+    f1 = pb.internal_force(u)
+    f2 = pb.internal_force(u)
+    assert np.array_equal(f1.view(np.int64), f2.view(np.int64))
+    x1, s1 = pcg_gpu(pb, u, f1, c_m=3e4, tol=1e-10)
+    x2, s2 = pcg_gpu(pb, u, f1, c_m=3e4, tol=1e-10)
+    assert s1.iterations == s2.iterations and np.array_equal(x1.view(np.int64), x2.view(np.int64))
+
+
+@pytest.mark.parametrize("tag,P,m", [("SDME_M", 4, 5), ("LagrangeGLL", 3, 4), ("ModalJacobi", 2, 4),
+                                     ("SDME_H", 6, 7), ("SDME_K", 8, 9)])
+def test_multi_element_vs_oracle_h64(tag, P, m):
+    """h = 1/64 (config 2/3 element size) on a small mesh with Dirichlet:
+    GPU vs the dense oracle restatement, f_int / K.p / diag."""
+    div = (3, 2, 2) if P <= 4 else (2, 2, 1)
+    h = 1.0 / 64
+    L = tuple(d * h for d in div)
+    dr = [("xmin", (0, 1, 2))]
+    pb = gpu_problem(tag, P, m, div, L, dr)
+    opb = of.Problem(of.Mesh(div, L), ob.Basis(tag, P), OMAT, m, dr)
+    rng = np.random.default_rng(11)
+    u = 1e-3 * h * rng.uniform(-1, 1, pb.n_free)
+    p = rng.standard_normal(pb.n_free)
+    assert max_rel_err(pb.internal_force(u), opb.internal_force(u)) <= TOL
+    assert max_rel_err(pb.apply_tangent(u, p), opb.apply_tangent(u, p)) <= TOL
+    assert max_rel_err(pb.tangent_diagonal(u, 4e8), opb.assemble(u, 1.0, 4e8).diagonal()) <= TOL
+
+
+def test_inversion_error_reports_first_element_and_point():
+    """ElementInversionError carries the smallest element id and its first
+    offending point in reference order (femcore.py:93-94)."""
+    tag, P, m = "ModalJacobi", 2, 3
+    div = (3, 2, 2)
+    pb = gpu_problem(tag, P, m, div, (1.0, 1.0, 1.0))
+    opb = of.Problem(of.Mesh(div, (1.0, 1.0, 1.0)), ob.Basis(tag, P), OMAT, m)
+    u = np.zeros(pb.n_free)
+    # large interior (bubble) coefficients on elements 7 and 4: only they invert
+    for e, amp in ((7, -30.0), (4, -25.0)):
+        d = opb.dmap.evdofs(e).reshape(-1, 3)
+        interior = np.all(opb.dmap.index_map >= 2, axis=1)
+        u[d[interior, 0]] = amp
+    with pytest.raises(of.InversionError) as ref:
+        opb.internal_force(u)
+    with pytest.raises(ElementInversionError) as err:
+        pb.internal_force(u)
+    assert (err.value.elem_id, err.value.qp) == (ref.value.elem_id, ref.value.qp) == (4, ref.value.qp)
+
+
+def test_pcg_error_contract():
+    pb = gpu_problem("SDME_M", 2, 3, (2, 2, 2), (1.0, 1.0, 1.0), [("xmin", (0, 1, 2))])
+    rng = np.random.default_rng(1)
+    b = rng.standard_normal(pb.n_free)
+    with pytest.raises(ValueError):
+        pcg_gpu(pb, np.zeros(pb.n_free), b, tol=1.5)
+    x, st = pcg_gpu(pb, np.zeros(pb.n_free), np.zeros(pb.n_free))
+    assert st.iterations == 0 and not x.any()
+    with pytest.raises(PCGError) as e:
+        pcg_gpu(pb, np.zeros(pb.n_free), b, tol=1e-14, maxit=3)
+    assert e.value.stats.iterations == 3 and not e.value.stats.converged
+    # indefinite: negative mass coefficient dominates
+    with pytest.raises((PCGError, ValueError)):
+        pcg_gpu(pb, np.zeros(pb.n_free), b, c_m=-1e12, precond="none")
+
+
+def test_config2_properties_full_size():
+    """Config 2 (64^3, P=4, ~51M DOFs) size-independent properties: symmetry
+    q.Kp = p.Kq, linearity, FD consistency of K against f_int, determinism."""
+    pb = GpuFemProblem(BoxMesh((64, 64, 64), (1.0, 1.0, 1.0)), build_basis(4, BasisKind("SDME_M")), MAT,
+                       reference_order=False)
+    from bench import config2_fields
+
+    u_lat, p_lat = config2_fields(pb, seed_u=0, seed_p=1)
+    u = pb.vector().set_lattice(u_lat)
+    p = pb.vector().set_lattice(p_lat)
+    q = pb.vector().set_lattice(np.random.default_rng(5).standard_normal(pb.n_lattice))
+    kp, kq, t1, t2 = (pb.vector() for _ in range(4))
+    pb.apply_(u, p, kp)
+    pb.apply_(u, q, kq)
+    s1, s2 = q.dot(kp), p.dot(kq)
+    assert abs(s1 - s2) <= 1e-10 * max(abs(s1), abs(s2))
+    # linearity
+    t1.assign(2.5, p)
+    pb.apply_(u, t1, t2)
+    t2.assign(1.0, t2, -2.5, kp)
+    assert t2.norm() <= 1e-13 * kp.norm()
+    # FD: (f(u + e p) - f(u - e p)) / 2e ~ K p
+    eps = 1e-9
+    t1.assign(1.0, u, eps, p)
+    pb.fint_(t1, t2)
+    t1.assign(1.0, u, -eps, p)
+    fm = pb.vector()
+    pb.fint_(t1, fm)
+    t2.assign(1.0 / (2 * eps), t2, -1.0 / (2 * eps), fm)
+    t2.assign(1.0, t2, -1.0, kp)
+    assert t2.norm() <= 1e-5 * kp.norm()
+    # determinism
+    pb.apply_(u, p, t1)
+    t1.assign(1.0, t1, -1.0, kp)
+    assert t1.norm() == 0.0
