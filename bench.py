@@ -70,34 +70,54 @@ def measured_peaks():
     return out
 
 
-def config2_fields(pb, seed_u=0, seed_p=1):
-    """Lattice-order inputs of config 2/3: smooth part on vertex
-    modes (all lattice nodes for the nodal basis), uniform noise of amplitude
-    1e-3 h on every coefficient, p ~ N(0, 1)."""
+def _hat_lines(pb):
+    """Per axis, (lattice line coefficients of sin(2 pi x), cos(2 pi x)).
+
+    Nodal basis: the values at the GLL lattice nodes.  Modal / SDME bases:
+    the coefficients of the piecewise-linear interpolant through the vertex
+    values, expressed in the basis: a vertex ramp psi_v = sum_t (T^-1)[v, t]
+    phi_t, so an element with end values (cL, cR) has coefficient
+    cL T^-1[0, t] + cR T^-1[1, t] on function t.  (Vertex-only coefficients
+    would NOT be smooth for SDME, whose vertex functions carry bubbles.)
+    """
     from paper_2104_13466_b200.basis import gll_rule
 
     mesh, Pp = pb.mesh, pb.P
-    h = min(mesh.h)
-    shape = pb.lattice_shape
-    nodal = pb.basis.kind.is_nodal
-    if nodal:
+    out = []
+    if pb.basis.kind.is_nodal:
         nodes = gll_rule(Pp + 1).points
         xi = np.concatenate(([nodes[0]], [nodes[-1]], nodes[1:-1]))
-        xs = mesh.lattice_coords(Pp, xi)
-    else:
-        xs = mesh.lattice_coords(Pp)
-    sx = np.sin(2 * np.pi * xs[0])
-    cx = np.cos(2 * np.pi * xs[0])
-    sy, cy = np.sin(2 * np.pi * xs[1]), np.cos(2 * np.pi * xs[1])
-    sz, cz = np.sin(2 * np.pi * xs[2]), np.cos(2 * np.pi * xs[2])
-    # sin(a+b+c) by separable products (no 3D temporaries beyond the output)
+        for xs in mesh.lattice_coords(Pp, xi):
+            out.append((np.sin(2 * np.pi * xs), np.cos(2 * np.pi * xs)))
+        return out
+    tinv = np.linalg.inv(pb.basis.transform)
+    func_of = [0] + list(range(2, Pp + 1)) + [1]  # lattice offset l -> function t
+    for ax in range(3):
+        ne = mesh.divisions[ax]
+        xv = mesh.origin[ax] + mesh.h[ax] * np.arange(ne + 1)
+        H = np.zeros((Pp * ne + 1, ne + 1))
+        for e in range(ne):
+            for l in range(Pp + 1):
+                t = func_of[l]
+                H[Pp * e + l, e] = tinv[0, t]
+                H[Pp * e + l, e + 1] = tinv[1, t]
+        out.append((H @ np.sin(2 * np.pi * xv), H @ np.cos(2 * np.pi * xv)))
+    return out
+
+
+def config2_fields(pb, seed_u=0, seed_p=1):
+    """Lattice-order inputs of config 2/3: smooth part
+    0.02 sin(2 pi (x+y+z)) (nodal interpolant, or the exact-in-basis
+    piecewise-trilinear interpolant for modal/SDME), uniform noise of
+    amplitude 1e-3 h on every coefficient (seed 0), p ~ N(0, 1) (seed 1)."""
+    mesh = pb.mesh
+    h = min(mesh.h)
+    shape = pb.lattice_shape
+    (sx, cx), (sy, cy), (sz, cz) = _hat_lines(pb)
+    # sin(a+b+c) as 4 separable terms (the interpolant is linear, so it commutes)
     smooth = (np.einsum("z,y,x->zyx", cz, cy, sx) + np.einsum("z,y,x->zyx", cz, sy, cx)
               + np.einsum("z,y,x->zyx", sz, cy, cx) - np.einsum("z,y,x->zyx", sz, sy, sx))
     smooth *= 0.02
-    if not nodal:
-        vert = [np.arange(n) % Pp == 0 for n in (shape[3], shape[2], shape[1])]
-        mask = np.einsum("z,y,x->zyx", vert[2], vert[1], vert[0])
-        smooth *= mask
     rng = np.random.default_rng(seed_u)
     u = 1e-3 * h * rng.uniform(-1.0, 1.0, size=shape)
     u += smooth[None]
