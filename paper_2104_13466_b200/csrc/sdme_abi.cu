@@ -13,6 +13,7 @@
 #include "sdme.h"
 #include "contact_kernels.cuh"
 #include "element_kernels.cuh"
+#include "element_v2.cuh"
 #include "vector_kernels.cuh"
 
 using namespace sdme;
@@ -129,12 +130,45 @@ void launch_mode(sdme_ctx* c, const Tab<N, M>& tb, OpArgs a) {
 }
 
 template <int N, int M>
+struct ConfV2 {
+  static constexpr int bytes = V2<N, M, 1>::PER * 8;
+  static constexpr int WPE = bytes <= 40960 ? 1 : (bytes <= 65536 ? 4 : 8);
+  static constexpr int EPB = WPE == 1 ? 2 : 1;
+  static constexpr int smem = bytes * EPB;
+};
+
+template <int N, int M, int MODE, bool VAL>
+void launch_v2(sdme_ctx* c, const Tab<N, M>& tb, OpArgs a) {
+  using CF = ConfV2<N, M>;
+  auto kern = element_v2<N, M, CF::WPE, CF::EPB, MODE, VAL>;
+  static int blocks_per_sm = -1;
+  if (blocks_per_sm < 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, CF::EPB * CF::WPE * 32, CF::smem);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    blocks_per_sm = std::max(1, nb) * sms;
+  }
+  for (int col = 0; col < 8; ++col) {
+    const long long cnt = colour_count(c->geo, col);
+    if (cnt == 0) continue;
+    a.colour = col;
+    const long long need = (cnt + CF::EPB - 1) / CF::EPB;
+    const unsigned grid = (unsigned)std::min<long long>(need, blocks_per_sm);
+    kern<<<grid, CF::EPB * CF::WPE * 32, CF::smem, c->st>>>(tb, c->geo, a);
+    ++c->launches;
+  }
+}
+
+template <int N, int M>
 void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, double* y, double ck, double cm) {
   const Tab<N, M> tb = make_tab<N, M>(c);
   OpArgs a{u, p, y, ck, cm, 0, c->d_flag};
-  if (mode == MODE_FINT) launch_mode<N, M, MODE_FINT>(c, tb, a);
-  else if (mode == MODE_APPLY) launch_mode<N, M, MODE_APPLY>(c, tb, a);
-  else launch_mode<N, M, MODE_MASS>(c, tb, a);
+  if (mode == MODE_FINT) launch_v2<N, M, MODE_FINT, false>(c, tb, a);
+  else if (mode == MODE_APPLY && cm != 0.0) launch_v2<N, M, MODE_APPLY, true>(c, tb, a);
+  else if (mode == MODE_APPLY) launch_v2<N, M, MODE_APPLY, false>(c, tb, a);
+  else launch_v2<N, M, MODE_MASS, true>(c, tb, a);
 }
 
 template <int N, int M>
