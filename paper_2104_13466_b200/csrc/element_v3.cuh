@@ -1,0 +1,468 @@
+// Element kernels v3 (hot path): f_int, (c_k K + c_m M) p, c_m M p.
+//
+// Schedule: a group of WPE warps owns one element (named-barrier / __syncwarp
+// sync, no block-wide barriers), persistent over the elements of one colour
+// pass; all three components go through each contraction stage together;
+// grad u at the thread's own points stays in registers between the u and p
+// forward passes (two shared buffers per element); results leave with
+// fire-and-forget RED.ADD -- within a colour pass every lattice point gets at
+// most one contribution and passes are ordered launches, so sums are
+// bit-reproducible.  Changes over the v2 schedule, from its ncu profile
+// (profiles/ncu_apply_r01_v2.txt):
+//  1. constitutive point work in the F^{-T} form (fewer FP64 instructions):
+//       K = F^{-T} = cof(F)/det F,  lnJ = ln det F,
+//       P  = mu F + (lam lnJ - mu) K                       (f_int, = F S)
+//       dP = mu Hp + lam (K:Hp) K + (mu - lam lnJ) K Hp^T K  (= Hp S + F dS)
+//     identical to material.py:65-105 / femcore.py:99-146 in exact arithmetic;
+//  2. the 1D weights, det J and dxi/dX are folded into per-axis tables, so
+//     points carry raw physical gradients and fluxes (no scaling multiplies);
+//  3. padded shared strides and per-stage lane orders chosen with
+//     tools/bank_model.py to remove most shared-memory bank conflicts.
+// Next element's input rows are prefetched into L2 while the current one runs.
+#pragma once
+#include "element_kernels.cuh"
+
+namespace sdme {
+
+template <int N, int M>
+struct Tab3 {
+  double B[M][N];              // forward values
+  double Dx[M][N], Dy[M][N], Dz[M][N];    // forward physical derivatives (D * 2/h)
+  double bBx[M][N], bDx[M][N];  // backward x: B w, D w 2/hx
+  double bBy[M][N], bDy[M][N];  // backward y
+  double bBz[M][N], bDz[M][N];  // backward z (also carries det J)
+};
+
+// shared layout parameters (tools/bank_model.py search)
+template <int N, int M> struct Lay { static constexpr int xo = 0, yo = 0, sx = N * M, sy = M * M, sq = M * M * M; };
+#define SDME_LAY(NN, MM, XO, YO, SX, SY, SQ) \
+  template <> struct Lay<NN, MM> { static constexpr int xo = XO, yo = YO, sx = SX, sy = SY, sq = SQ; };
+// xo: 0 nat, 1 j-first ; yo: 0 nat, 1 ck-first, 2 k-first
+SDME_LAY(2, 2, 0, 0, 5, 6, 20)
+SDME_LAY(2, 3, 0, 0, 6, 9, 41)
+SDME_LAY(3, 3, 0, 0, 9, 13, 41)
+SDME_LAY(3, 4, 0, 1, 25, 19, 64)
+SDME_LAY(4, 4, 0, 0, 19, 20, 64)
+SDME_LAY(4, 5, 0, 1, 20, 27, 137)
+SDME_LAY(5, 5, 0, 1, 25, 39, 137)
+SDME_LAY(5, 6, 1, 0, 35, 42, 228)
+SDME_LAY(6, 6, 1, 0, 43, 42, 228)
+SDME_LAY(6, 7, 1, 0, 55, 55, 353)
+SDME_LAY(7, 7, 1, 0, 59, 55, 353)
+SDME_LAY(7, 8, 1, 2, 71, 71, 512)
+SDME_LAY(8, 8, 1, 0, 67, 68, 512)
+SDME_LAY(8, 9, 1, 0, 73, 89, 737)
+SDME_LAY(9, 9, 1, 0, 89, 89, 737)
+SDME_LAY(9, 10, 0, 2, 105, 105, 1012)
+#undef SDME_LAY
+
+template <int N, int M, int WPE>
+struct V3 {
+  using Ly = Lay<N, M>;
+  static constexpr int Q = M * M * M;
+  static constexpr int XS = 3 * N * Ly::sx;      // one X-layout array ([comp][k] rows of sx)
+  static constexpr int XO = 2 * XS;
+  static constexpr int YS = N * Ly::sy;          // one (comp, s) slab of the Y layout
+  static constexpr int YO = 9 * YS;
+  static constexpr int GO = 12 * Ly::sq;         // point slots [d][comp] of sq
+  static constexpr int SA = XO > GO ? XO : GO;
+  static constexpr int SB = YO;
+  static constexpr int PER = SA + SB;
+  static constexpr int T = 32 * WPE;
+  static constexpr int QPT = (Q + T - 1) / T;
+  // X layout: [s][comp][k] rows of stride sx, row = j*M + a
+  __device__ static int xi(int s, int ck, int j, int a) { return s * XS + ck * Ly::sx + j * M + a; }
+  // Y layout: [comp][s][k] rows of stride sy, row = b*M + a
+  __device__ static int yi(int comp, int s, int k, int ba) { return (comp * 3 + s) * YS + k * Ly::sy + ba; }
+  // point slots: [d][comp][q], d = 3 is the value slot
+  __device__ static int qi(int d, int comp, int q) { return (d * 3 + comp) * Ly::sq + q; }
+  // item decoding
+  __device__ static void item_x(int w, int& ck, int& j) {
+    if (Ly::xo == 0) { ck = w / N; j = w % N; }
+    else { j = w / (3 * N); ck = w % (3 * N); }
+  }
+  __device__ static void item_y(int w, int& ck, int& a) {
+    if (Ly::yo == 0) { ck = w / M; a = w % M; }
+    else if (Ly::yo == 1) { a = w / (3 * N); ck = w % (3 * N); }
+    else { const int c = w / (N * M), r = w % (N * M); a = r / N; ck = c * N + r % N; }
+  }
+};
+
+template <int WPE>
+__device__ __forceinline__ void group_sync(int gid) {
+  if (WPE == 1) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(gid + 1), "r"(WPE * 32) : "memory");
+  }
+}
+
+__device__ __forceinline__ void red_add(double* p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+template <int N, int M, int WPE>
+__device__ __forceinline__ void v3_prefetch(const Geo& g, const double* __restrict__ src, int X0, int Y0, int Z0,
+                                            int t) {
+  using C = V3<N, M, WPE>;
+  for (int w = t; w < 3 * N * N; w += C::T) {
+    const int comp = w / (N * N), kj = w % (N * N);
+    const double* row = src + comp * g.Ns + ((long long)(Z0 + kj / N) * g.Ly + (Y0 + kj % N)) * g.Lx + X0;
+    prefetch_l2(row);
+    prefetch_l2(row + N - 1);
+  }
+}
+
+template <int N, int M, int WPE, bool GRAD, bool VAL>
+__device__ __forceinline__ void v3_forward(const Tab3<N, M>& tb, const Geo& g, const double* __restrict__ src,
+                                           int X0, int Y0, int Z0, double* A, double* B, int t, int gid) {
+  using C = V3<N, M, WPE>;
+  constexpr int NX = 3 * N * N;
+#pragma unroll
+  for (int r = 0; r < (NX + C::T - 1) / C::T; ++r) {
+    const int w = t + r * C::T;
+    if (w < NX) {
+      int ck, j;
+      C::item_x(w, ck, j);
+      const int comp = ck / N, k = ck % N;
+      const double* row = src + comp * g.Ns + ((long long)(Z0 + k) * g.Ly + (Y0 + j)) * g.Lx + X0;
+      double v[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) v[i] = __ldg(row + i);
+#pragma unroll
+      for (int a = 0; a < M; ++a) {
+        double b0 = 0.0, b1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          b0 = fma(tb.B[a][i], v[i], b0);
+          if (GRAD) b1 = fma(tb.Dx[a][i], v[i], b1);
+        }
+        A[C::xi(0, ck, j, a)] = b0;
+        if (GRAD) A[C::xi(1, ck, j, a)] = b1;
+      }
+    }
+  }
+  group_sync<WPE>(gid);
+  constexpr int NY = 3 * N * M;
+#pragma unroll
+  for (int r = 0; r < (NY + C::T - 1) / C::T; ++r) {
+    const int w = t + r * C::T;
+    if (w < NY) {
+      int ck, a;
+      C::item_y(w, ck, a);
+      double x0[N], x1[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        x0[j] = A[C::xi(0, ck, j, a)];
+        if (GRAD) x1[j] = A[C::xi(1, ck, j, a)];
+      }
+      const int comp = ck / N, k = ck % N;
+#pragma unroll
+      for (int b = 0; b < M; ++b) {
+        double bb = 0.0, db = 0.0, bd = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          bb = fma(tb.B[b][j], x0[j], bb);
+          if (GRAD) {
+            db = fma(tb.Dy[b][j], x0[j], db);
+            bd = fma(tb.B[b][j], x1[j], bd);
+          }
+        }
+        B[C::yi(comp, 0, k, b * M + a)] = bb;  // B_y B_x
+        if (GRAD) {
+          B[C::yi(comp, 1, k, b * M + a)] = db;  // D_y B_x
+          B[C::yi(comp, 2, k, b * M + a)] = bd;  // B_y D_x
+        }
+      }
+    }
+  }
+  group_sync<WPE>(gid);
+  constexpr int NZ = 3 * M * M;
+#pragma unroll
+  for (int r = 0; r < (NZ + C::T - 1) / C::T; ++r) {
+    const int w = t + r * C::T;
+    if (w < NZ) {
+      const int comp = w / (M * M), ba = w % (M * M);
+      double y0[N], y1[N], y2[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        y0[k] = B[C::yi(comp, 0, k, ba)];
+        if (GRAD) {
+          y1[k] = B[C::yi(comp, 1, k, ba)];
+          y2[k] = B[C::yi(comp, 2, k, ba)];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        double gx = 0.0, gy = 0.0, gz = 0.0, vv = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          if (GRAD) {
+            gx = fma(tb.B[c][k], y2[k], gx);
+            gy = fma(tb.B[c][k], y1[k], gy);
+            gz = fma(tb.Dz[c][k], y0[k], gz);
+          }
+          if (VAL) vv = fma(tb.B[c][k], y0[k], vv);
+        }
+        const int q = c * M * M + ba;
+        if (GRAD) {
+          A[C::qi(0, comp, q)] = gx;
+          A[C::qi(1, comp, q)] = gy;
+          A[C::qi(2, comp, q)] = gz;
+        }
+        if (VAL) A[C::qi(3, comp, q)] = vv;
+      }
+    }
+  }
+  group_sync<WPE>(gid);
+}
+
+template <int N, int M, int WPE, bool GRAD, bool VAL>
+__device__ __forceinline__ void v3_backward(const Tab3<N, M>& tb, const Geo& g, double* __restrict__ dst,
+                                            int X0, int Y0, int Z0, double* A, double* B, int t, int gid) {
+  using C = V3<N, M, WPE>;
+  constexpr int NZ = 3 * M * M;
+#pragma unroll
+  for (int r = 0; r < (NZ + C::T - 1) / C::T; ++r) {
+    const int w = t + r * C::T;
+    if (w < NZ) {
+      const int comp = w / (M * M), ba = w % (M * M);
+      double qx[M], qy[M], qz[M], qv[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        const int q = c * M * M + ba;
+        if (GRAD) {
+          qx[c] = A[C::qi(0, comp, q)];
+          qy[c] = A[C::qi(1, comp, q)];
+          qz[c] = A[C::qi(2, comp, q)];
+        }
+        if (VAL) qv[c] = A[C::qi(3, comp, q)];
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double hx = 0.0, hy = 0.0, hz = 0.0;
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          if (GRAD) {
+            hx = fma(tb.bBz[c][k], qx[c], hx);
+            hy = fma(tb.bBz[c][k], qy[c], hy);
+            hz = fma(tb.bDz[c][k], qz[c], hz);
+          }
+          if (VAL) hz = fma(tb.bBz[c][k], qv[c], hz);
+        }
+        if (GRAD) {
+          B[C::yi(comp, 0, k, ba)] = hx;
+          B[C::yi(comp, 1, k, ba)] = hy;
+        }
+        B[C::yi(comp, 2, k, ba)] = hz;
+      }
+    }
+  }
+  group_sync<WPE>(gid);
+  constexpr int NY = 3 * N * M;
+#pragma unroll
+  for (int r = 0; r < (NY + C::T - 1) / C::T; ++r) {
+    const int w = t + r * C::T;
+    if (w < NY) {
+      int ck, a;
+      C::item_y(w, ck, a);
+      const int comp = ck / N, k = ck % N;
+      double hx[M], hy[M], hz[M];
+#pragma unroll
+      for (int b = 0; b < M; ++b) {
+        if (GRAD) {
+          hx[b] = B[C::yi(comp, 0, k, b * M + a)];
+          hy[b] = B[C::yi(comp, 1, k, b * M + a)];
+        }
+        hz[b] = B[C::yi(comp, 2, k, b * M + a)];
+      }
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double jx = 0.0, jyz = 0.0;
+#pragma unroll
+        for (int b = 0; b < M; ++b) {
+          if (GRAD) {
+            jx = fma(tb.bBy[b][j], hx[b], jx);
+            jyz = fma(tb.bDy[b][j], hy[b], jyz);
+          }
+          jyz = fma(tb.bBy[b][j], hz[b], jyz);
+        }
+        if (GRAD) A[C::xi(0, ck, j, a)] = jx;
+        A[C::xi(1, ck, j, a)] = jyz;
+      }
+    }
+  }
+  group_sync<WPE>(gid);
+  constexpr int NX = 3 * N * N;
+#pragma unroll
+  for (int r = 0; r < (NX + C::T - 1) / C::T; ++r) {
+    const int w = t + r * C::T;
+    if (w < NX) {
+      int ck, j;
+      C::item_x(w, ck, j);
+      const int comp = ck / N, k = ck % N;
+      double jx[M], jyz[M];
+#pragma unroll
+      for (int a = 0; a < M; ++a) {
+        if (GRAD) jx[a] = A[C::xi(0, ck, j, a)];
+        jyz[a] = A[C::xi(1, ck, j, a)];
+      }
+      const int Z = Z0 + k, Y = Y0 + j;
+      double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Lx + X0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < M; ++a) {
+          if (GRAD) acc = fma(tb.bDx[a][i], jx[a], acc);
+          acc = fma(tb.bBx[a][i], jyz[a], acc);
+        }
+        if (!constrained(g, comp, X0 + i, Y, Z)) red_add(row + i, acc);
+      }
+    }
+  }
+  group_sync<WPE>(gid);
+}
+
+// K = F^{-T}, det F, ln det F from H = grad u
+struct QpK {
+  double F[3][3];
+  double K[3][3];
+  double det, lnJ;
+};
+
+__device__ __forceinline__ void qp_k(const double (&H)[9], QpK& s) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) s.F[i][j] = H[i * 3 + j] + (i == j ? 1.0 : 0.0);
+  const double(&F)[3][3] = s.F;
+  const double c00 = F[1][1] * F[2][2] - F[1][2] * F[2][1];
+  const double c01 = F[1][2] * F[2][0] - F[1][0] * F[2][2];
+  const double c02 = F[1][0] * F[2][1] - F[1][1] * F[2][0];
+  const double c10 = F[0][2] * F[2][1] - F[0][1] * F[2][2];
+  const double c11 = F[0][0] * F[2][2] - F[0][2] * F[2][0];
+  const double c12 = F[0][1] * F[2][0] - F[0][0] * F[2][1];
+  const double c20 = F[0][1] * F[1][2] - F[0][2] * F[1][1];
+  const double c21 = F[0][2] * F[1][0] - F[0][0] * F[1][2];
+  const double c22 = F[0][0] * F[1][1] - F[0][1] * F[1][0];
+  s.det = F[0][0] * c00 + F[0][1] * c01 + F[0][2] * c02;
+  const double inv = 1.0 / s.det;
+  s.K[0][0] = c00 * inv; s.K[0][1] = c01 * inv; s.K[0][2] = c02 * inv;
+  s.K[1][0] = c10 * inv; s.K[1][1] = c11 * inv; s.K[1][2] = c12 * inv;
+  s.K[2][0] = c20 * inv; s.K[2][1] = c21 * inv; s.K[2][2] = c22 * inv;
+  s.lnJ = log(s.det);
+}
+
+template <int N, int M, int WPE, int EPB, int MODE, bool VAL>
+__global__ void __launch_bounds__(EPB * WPE * 32) element_v3(const __grid_constant__ Tab3<N, M> tb,
+                                                               const __grid_constant__ Geo g, OpArgs args) {
+  using C = V3<N, M, WPE>;
+  extern __shared__ double smem[];
+  const int gid = threadIdx.x / C::T;
+  const int t = threadIdx.x % C::T;
+  double* A = smem + gid * C::PER;
+  double* Bf = A + C::SA;
+  const long long cnt = colour_count(g, args.colour);
+  constexpr bool GRADP = (MODE == MODE_APPLY);
+  const long long stride = (long long)gridDim.x * EPB;
+  // dP constants with c_k folded in
+  const double mu_k = args.c_k * g.mu, lam_k = args.c_k * g.lam;
+  const double cmr = args.c_m * g.rho;
+  for (long long idx = (long long)blockIdx.x * EPB + gid; idx < cnt; idx += stride) {
+    int ei, ej, ek;
+    colour_element(g, args.colour, idx, ei, ej, ek);
+    const int X0 = (N - 1) * ei, Y0 = (N - 1) * ej, Z0 = (N - 1) * ek;
+    if (idx + stride < cnt) {  // warm L2 with the next element's rows
+      int ni, nj, nk;
+      colour_element(g, args.colour, idx + stride, ni, nj, nk);
+      if (MODE != MODE_MASS) v3_prefetch<N, M, WPE>(g, args.u, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk, t);
+      if (MODE != MODE_FINT) v3_prefetch<N, M, WPE>(g, args.p, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk, t);
+    }
+    double Hu[C::QPT][9];
+    if (MODE != MODE_MASS) {
+      v3_forward<N, M, WPE, true, false>(tb, g, args.u, X0, Y0, Z0, A, Bf, t, gid);
+#pragma unroll
+      for (int r = 0; r < C::QPT; ++r) {
+        const int q = t + r * C::T;
+        if (q < C::Q) {
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) Hu[r][i * 3 + d] = A[C::qi(d, i, q)];
+        }
+      }
+      group_sync<WPE>(gid);
+    }
+    if (MODE != MODE_FINT)
+      v3_forward<N, M, WPE, GRADP, VAL>(tb, g, args.p, X0, Y0, Z0, A, Bf, t, gid);
+#pragma unroll
+    for (int r = 0; r < C::QPT; ++r) {
+      const int q = t + r * C::T;
+      if (q >= C::Q) continue;
+      if (MODE == MODE_MASS) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) A[C::qi(3, i, q)] *= cmr;
+        continue;
+      }
+      QpK s;
+      qp_k(Hu[r], s);
+      if (!(s.det > 0.0)) {
+        const int a = q % M, b = (q / M) % M, c = q / (M * M);
+        const long long e = ((long long)ek * g.ny + ej) * g.nx + ei;
+        atomicMin(args.inv_flag, (unsigned long long)e * C::Q + (unsigned long long)((a * M + b) * M + c));
+      }
+      if (MODE == MODE_FINT) {
+        const double cK = g.lam * s.lnJ - g.mu;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) A[C::qi(d, i, q)] = fma(g.mu, s.F[i][d], cK * s.K[i][d]);
+      } else {
+        double Hp[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) Hp[i][d] = A[C::qi(d, i, q)];
+        double tr = 0.0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) tr = fma(s.K[i][d], Hp[i][d], tr);
+        // M1 = K Hp^T
+        double M1[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            M1[i][j] = fma(s.K[i][0], Hp[j][0], fma(s.K[i][1], Hp[j][1], s.K[i][2] * Hp[j][2]));
+        const double cc = mu_k - lam_k * s.lnJ;
+        const double lt = lam_k * tr;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            const double m2 = fma(M1[i][0], s.K[0][d], fma(M1[i][1], s.K[1][d], M1[i][2] * s.K[2][d]));
+            A[C::qi(d, i, q)] = fma(cc, m2, fma(lt, s.K[i][d], mu_k * Hp[i][d]));
+          }
+        if (VAL) {
+#pragma unroll
+          for (int i = 0; i < 3; ++i) A[C::qi(3, i, q)] *= cmr;
+        }
+      }
+    }
+    group_sync<WPE>(gid);
+    if (MODE == MODE_MASS)
+      v3_backward<N, M, WPE, false, true>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid);
+    else if (MODE == MODE_FINT)
+      v3_backward<N, M, WPE, true, false>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid);
+    else
+      v3_backward<N, M, WPE, true, VAL>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid);
+  }
+}
+
+}  // namespace sdme

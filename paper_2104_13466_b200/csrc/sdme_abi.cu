@@ -13,7 +13,7 @@
 #include "sdme.h"
 #include "contact_kernels.cuh"
 #include "element_kernels.cuh"
-#include "element_v2.cuh"
+#include "element_v3.cuh"
 #include "vector_kernels.cuh"
 
 using namespace sdme;
@@ -110,52 +110,57 @@ Tab<N, M> make_tab(const sdme_ctx* c) {
   return t;
 }
 
-template <int N, int M, int MODE>
-void launch_mode(sdme_ctx* c, const Tab<N, M>& tb, OpArgs a) {
-  constexpr int EB = Conf<N, M>::EB;
-  constexpr int smem = Conf<N, M>::bytes * EB;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(element_op<N, M, EB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_done = true;
+// v3 tables: weights, det J and dxi/dX folded per axis (element_v3.cuh)
+template <int N, int M>
+Tab3<N, M> make_tab3(const sdme_ctx* c) {
+  Tab3<N, M> t;
+  const Geo& g = c->geo;
+  for (int a = 0; a < M; ++a) {
+    const double w = c->w[a];
+    for (int l = 0; l < N; ++l) {
+      const double b = c->Bl[a * N + l], d = c->Dl[a * N + l];
+      t.B[a][l] = b;
+      t.Dx[a][l] = d * g.s[0];
+      t.Dy[a][l] = d * g.s[1];
+      t.Dz[a][l] = d * g.s[2];
+      t.bBx[a][l] = b * w;
+      t.bDx[a][l] = d * w * g.s[0];
+      t.bBy[a][l] = b * w;
+      t.bDy[a][l] = d * w * g.s[1];
+      t.bBz[a][l] = b * w * g.detJ;
+      t.bDz[a][l] = d * w * g.s[2] * g.detJ;
+    }
   }
-  for (int col = 0; col < 8; ++col) {
-    const long long cnt = colour_count(c->geo, col);
-    if (cnt == 0) continue;
-    a.colour = col;
-    const long long grid = (cnt + EB - 1) / EB;
-    element_op<N, M, EB, MODE><<<(unsigned)grid, 128, smem, c->st>>>(tb, c->geo, a);
-    ++c->launches;
-  }
+  return t;
 }
 
 template <int N, int M>
-struct ConfV2 {
-  static constexpr int bytes = V2<N, M, 1>::PER * 8;
+struct ConfV3 {
+  static constexpr int bytes = V3<N, M, 1>::PER * 8;
   static constexpr int WPE = bytes <= 40960 ? 1 : (bytes <= 65536 ? 4 : 8);
   static constexpr int EPB = WPE == 1 ? 2 : 1;
-  static constexpr int smem = bytes * EPB;
+  static constexpr int smem = V3<N, M, WPE>::PER * 8 * EPB;
 };
 
 template <int N, int M, int MODE, bool VAL>
-void launch_v2(sdme_ctx* c, const Tab<N, M>& tb, OpArgs a) {
-  using CF = ConfV2<N, M>;
-  auto kern = element_v2<N, M, CF::WPE, CF::EPB, MODE, VAL>;
-  static int blocks_per_sm = -1;
-  if (blocks_per_sm < 0) {
+void launch_v3(sdme_ctx* c, const Tab3<N, M>& tb, OpArgs a) {
+  using CF = ConfV3<N, M>;
+  auto kern = element_v3<N, M, CF::WPE, CF::EPB, MODE, VAL>;
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::smem);
     int nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, CF::EPB * CF::WPE * 32, CF::smem);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    blocks_per_sm = std::max(1, nb) * sms;
+    max_blocks = std::max(1, nb) * sms;
   }
   for (int col = 0; col < 8; ++col) {
     const long long cnt = colour_count(c->geo, col);
     if (cnt == 0) continue;
     a.colour = col;
     const long long need = (cnt + CF::EPB - 1) / CF::EPB;
-    const unsigned grid = (unsigned)std::min<long long>(need, blocks_per_sm);
+    const unsigned grid = (unsigned)std::min<long long>(need, max_blocks);
     kern<<<grid, CF::EPB * CF::WPE * 32, CF::smem, c->st>>>(tb, c->geo, a);
     ++c->launches;
   }
@@ -163,12 +168,12 @@ void launch_v2(sdme_ctx* c, const Tab<N, M>& tb, OpArgs a) {
 
 template <int N, int M>
 void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, double* y, double ck, double cm) {
-  const Tab<N, M> tb = make_tab<N, M>(c);
+  const Tab3<N, M> tb = make_tab3<N, M>(c);
   OpArgs a{u, p, y, ck, cm, 0, c->d_flag};
-  if (mode == MODE_FINT) launch_v2<N, M, MODE_FINT, false>(c, tb, a);
-  else if (mode == MODE_APPLY && cm != 0.0) launch_v2<N, M, MODE_APPLY, true>(c, tb, a);
-  else if (mode == MODE_APPLY) launch_v2<N, M, MODE_APPLY, false>(c, tb, a);
-  else launch_v2<N, M, MODE_MASS, true>(c, tb, a);
+  if (mode == MODE_FINT) launch_v3<N, M, MODE_FINT, false>(c, tb, a);
+  else if (mode == MODE_APPLY && cm != 0.0) launch_v3<N, M, MODE_APPLY, true>(c, tb, a);
+  else if (mode == MODE_APPLY) launch_v3<N, M, MODE_APPLY, false>(c, tb, a);
+  else launch_v3<N, M, MODE_MASS, true>(c, tb, a);
 }
 
 template <int N, int M>
