@@ -2,13 +2,15 @@
 //
 // Schedule: a group of WPE warps owns one element (named-barrier / __syncwarp
 // sync, no block-wide barriers), persistent over the elements of one colour
-// pass; all three components go through each contraction stage together;
-// grad u at the thread's own points stays in registers between the u and p
-// forward passes (two shared buffers per element); results leave with
-// fire-and-forget RED.ADD -- within a colour pass every lattice point gets at
-// most one contribution and passes are ordered launches, so sums are
-// bit-reproducible.  Changes over the v2 schedule, from its ncu profile
-// (profiles/ncu_apply_r01_v2.txt):
+// pass; grad u at the thread's own points stays in registers between the u and
+// p forward passes; results leave with fire-and-forget RED.ADD -- within a
+// colour pass every lattice point gets at most one contribution and passes
+// are ordered launches, so sums are bit-reproducible.  The contraction stages
+// run NC displacement components at a time (NC = 3: more pencils per stage;
+// NC = 1: 3x smaller stage buffers, so more elements fit per SM).
+//
+// Changes over the first (v1/v2) schedules, from their ncu profiles
+// (profiles/ncu_apply_r01_v*.txt):
 //  1. constitutive point work in the F^{-T} form (fewer FP64 instructions):
 //       K = F^{-T} = cof(F)/det F,  lnJ = ln det F,
 //       P  = mu F + (lam lnJ - mu) K                       (f_int, = F S)
@@ -17,7 +19,7 @@
 //  2. the 1D weights, det J and dxi/dX are folded into per-axis tables, so
 //     points carry raw physical gradients and fluxes (no scaling multiplies);
 //  3. padded shared strides and per-stage lane orders chosen with
-//     tools/bank_model.py to remove most shared-memory bank conflicts.
+//     tools/bank_model.py (half-warp 64-bit bank model, matches ncu counts).
 // Next element's input rows are prefetched into L2 while the current one runs.
 #pragma once
 #include "element_kernels.cuh"
@@ -26,64 +28,70 @@ namespace sdme {
 
 template <int N, int M>
 struct Tab3 {
-  double B[M][N];              // forward values
-  double Dx[M][N], Dy[M][N], Dz[M][N];    // forward physical derivatives (D * 2/h)
-  double bBx[M][N], bDx[M][N];  // backward x: B w, D w 2/hx
-  double bBy[M][N], bDy[M][N];  // backward y
-  double bBz[M][N], bDz[M][N];  // backward z (also carries det J)
+  double B[M][N];                          // forward values
+  double Dx[M][N], Dy[M][N], Dz[M][N];     // forward physical derivatives (D * 2/h)
+  double bBx[M][N], bDx[M][N];             // backward x: B w, D w 2/hx
+  double bBy[M][N], bDy[M][N];             // backward y
+  double bBz[M][N], bDz[M][N];             // backward z (also carries det J)
 };
 
-// shared layout parameters (tools/bank_model.py search)
-template <int N, int M> struct Lay { static constexpr int xo = 0, yo = 0, sx = N * M, sy = M * M, sq = M * M * M; };
-#define SDME_LAY(NN, MM, XO, YO, SX, SY, SQ) \
-  template <> struct Lay<NN, MM> { static constexpr int xo = XO, yo = YO, sx = SX, sy = SY, sq = SQ; };
-// xo: 0 nat, 1 j-first ; yo: 0 nat, 1 ck-first, 2 k-first
-SDME_LAY(2, 2, 0, 0, 5, 6, 20)
-SDME_LAY(2, 3, 0, 0, 6, 9, 41)
-SDME_LAY(3, 3, 0, 0, 9, 13, 41)
-SDME_LAY(3, 4, 0, 1, 25, 19, 64)
-SDME_LAY(4, 4, 0, 0, 19, 20, 64)
-SDME_LAY(4, 5, 0, 1, 20, 27, 137)
-SDME_LAY(5, 5, 0, 1, 25, 39, 137)
-SDME_LAY(5, 6, 1, 0, 35, 42, 228)
-SDME_LAY(6, 6, 1, 0, 43, 42, 228)
-SDME_LAY(6, 7, 1, 0, 55, 55, 353)
-SDME_LAY(7, 7, 1, 0, 59, 55, 353)
-SDME_LAY(7, 8, 1, 2, 71, 71, 512)
-SDME_LAY(8, 8, 1, 0, 67, 68, 512)
-SDME_LAY(8, 9, 1, 0, 73, 89, 737)
-SDME_LAY(9, 9, 1, 0, 89, 89, 737)
-SDME_LAY(9, 10, 0, 2, 105, 105, 1012)
+// shared layout parameters (tools/bank_model.py search); xo: 0 natural,
+// 1 j-first; yo: 0 natural, 1 ck-first, 2 k-first
+template <int N, int M, int NC>
+struct Lay {
+  static constexpr int xo = 0, yo = 0, sx = N * M, sy = M * M;
+  static constexpr int sq = M * M * M + (((M * M - M * M * M) % 16) + 16) % 16;
+};
+#define SDME_LAY(NN, MM, NCC, XO, YO, SX, SY, SQ) \
+  template <> struct Lay<NN, MM, NCC> { static constexpr int xo = XO, yo = YO, sx = SX, sy = SY, sq = SQ; };
+SDME_LAY(2, 2, 3, 0, 0, 5, 6, 20)
+SDME_LAY(2, 3, 3, 0, 0, 6, 9, 41)
+SDME_LAY(3, 3, 3, 0, 0, 9, 13, 41)
+SDME_LAY(3, 4, 3, 0, 1, 25, 19, 64)
+SDME_LAY(4, 4, 3, 0, 0, 19, 20, 64)
+SDME_LAY(4, 5, 3, 0, 2, 20, 28, 137)
+SDME_LAY(5, 5, 3, 1, 0, 27, 37, 137)
+SDME_LAY(5, 6, 3, 0, 2, 45, 45, 228)
+SDME_LAY(6, 6, 3, 1, 0, 43, 42, 228)
+SDME_LAY(6, 7, 3, 1, 0, 55, 55, 353)
+SDME_LAY(7, 7, 3, 1, 0, 59, 55, 353)
+SDME_LAY(7, 8, 3, 1, 2, 71, 71, 512)
+SDME_LAY(8, 8, 3, 1, 0, 67, 68, 512)
+SDME_LAY(8, 9, 3, 1, 0, 73, 89, 737)
+SDME_LAY(9, 9, 3, 1, 0, 89, 89, 737)
+SDME_LAY(9, 10, 3, 0, 2, 105, 105, 1012)
+SDME_LAY(5, 5, 1, 0, 0, 25, 37, 137)
 #undef SDME_LAY
 
-template <int N, int M, int WPE>
+template <int N, int M, int WPE, int NC, bool VALS = true>
 struct V3 {
-  using Ly = Lay<N, M>;
+  using Ly = Lay<N, M, NC>;
   static constexpr int Q = M * M * M;
-  static constexpr int XS = 3 * N * Ly::sx;      // one X-layout array ([comp][k] rows of sx)
+  static constexpr int XS = NC * N * Ly::sx;     // one X-layout array ([comp][k] rows of sx)
   static constexpr int XO = 2 * XS;
   static constexpr int YS = N * Ly::sy;          // one (comp, s) slab of the Y layout
-  static constexpr int YO = 9 * YS;
-  static constexpr int GO = 12 * Ly::sq;         // point slots [d][comp] of sq
-  static constexpr int SA = XO > GO ? XO : GO;
-  static constexpr int SB = YO;
+  static constexpr int YO = 3 * NC * YS;
+  static constexpr int GO = (VALS ? 12 : 9) * Ly::sq;  // point slots [d][comp] of sq
+  // NC = 3: the x-stage scratch reuses A (free before the points are written);
+  // NC < 3: A keeps earlier groups' points, so the x scratch sits after YO in B.
+  static constexpr int SA = (NC == 3 && XO > GO) ? XO : GO;
+  static constexpr int SB = YO + (NC == 3 ? 0 : XO);
   static constexpr int PER = SA + SB;
   static constexpr int T = 32 * WPE;
   static constexpr int QPT = (Q + T - 1) / T;
-  // X layout: [s][comp][k] rows of stride sx, row = j*M + a
+  // X layout: [s][comp][k] rows of stride sx, row = j*M + a   (comp local to the group)
   __device__ static int xi(int s, int ck, int j, int a) { return s * XS + ck * Ly::sx + j * M + a; }
   // Y layout: [comp][s][k] rows of stride sy, row = b*M + a
   __device__ static int yi(int comp, int s, int k, int ba) { return (comp * 3 + s) * YS + k * Ly::sy + ba; }
-  // point slots: [d][comp][q], d = 3 is the value slot
+  // point slots: [d][comp][q], d = 3 is the value slot (comp global)
   __device__ static int qi(int d, int comp, int q) { return (d * 3 + comp) * Ly::sq + q; }
-  // item decoding
   __device__ static void item_x(int w, int& ck, int& j) {
     if (Ly::xo == 0) { ck = w / N; j = w % N; }
-    else { j = w / (3 * N); ck = w % (3 * N); }
+    else { j = w / (NC * N); ck = w % (NC * N); }
   }
   __device__ static void item_y(int w, int& ck, int& a) {
     if (Ly::yo == 0) { ck = w / M; a = w % M; }
-    else if (Ly::yo == 1) { a = w / (3 * N); ck = w % (3 * N); }
+    else if (Ly::yo == 1) { a = w / (NC * N); ck = w % (NC * N); }
     else { const int c = w / (N * M), r = w % (N * M); a = r / N; ck = c * N + r % N; }
   }
 };
@@ -105,11 +113,10 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-template <int N, int M, int WPE>
+template <int N, int T>
 __device__ __forceinline__ void v3_prefetch(const Geo& g, const double* __restrict__ src, int X0, int Y0, int Z0,
                                             int t) {
-  using C = V3<N, M, WPE>;
-  for (int w = t; w < 3 * N * N; w += C::T) {
+  for (int w = t; w < 3 * N * N; w += T) {
     const int comp = w / (N * N), kj = w % (N * N);
     const double* row = src + comp * g.Ns + ((long long)(Z0 + kj / N) * g.Ly + (Y0 + kj % N)) * g.Lx + X0;
     prefetch_l2(row);
@@ -117,215 +124,222 @@ __device__ __forceinline__ void v3_prefetch(const Geo& g, const double* __restri
   }
 }
 
-template <int N, int M, int WPE, bool GRAD, bool VAL>
+template <int N, int M, int WPE, int NC, bool GRAD, bool VAL>
 __device__ __forceinline__ void v3_forward(const Tab3<N, M>& tb, const Geo& g, const double* __restrict__ src,
                                            int X0, int Y0, int Z0, double* A, double* B, int t, int gid) {
-  using C = V3<N, M, WPE>;
-  constexpr int NX = 3 * N * N;
+  using C = V3<N, M, WPE, NC>;
+  constexpr int NX = NC * N * N, NY = NC * N * M, NZ = NC * M * M;
+  double* const P = A;  // points buffer (all components)
+#pragma unroll 1
+  for (int c0 = 0; c0 < 3; c0 += NC) {
+    double* const X = (NC == 3) ? A : B + C::YO;  // x-stage scratch (see V3::SB)
 #pragma unroll
-  for (int r = 0; r < (NX + C::T - 1) / C::T; ++r) {
-    const int w = t + r * C::T;
-    if (w < NX) {
-      int ck, j;
-      C::item_x(w, ck, j);
-      const int comp = ck / N, k = ck % N;
-      const double* row = src + comp * g.Ns + ((long long)(Z0 + k) * g.Ly + (Y0 + j)) * g.Lx + X0;
-      double v[N];
+    for (int r = 0; r < (NX + C::T - 1) / C::T; ++r) {
+      const int w = t + r * C::T;
+      if (w < NX) {
+        int ck, j;
+        C::item_x(w, ck, j);
+        const int comp = c0 + ck / N, k = ck % N;
+        const double* row = src + comp * g.Ns + ((long long)(Z0 + k) * g.Ly + (Y0 + j)) * g.Lx + X0;
+        double v[N];
 #pragma unroll
-      for (int i = 0; i < N; ++i) v[i] = __ldg(row + i);
+        for (int i = 0; i < N; ++i) v[i] = __ldg(row + i);
 #pragma unroll
-      for (int a = 0; a < M; ++a) {
-        double b0 = 0.0, b1 = 0.0;
+        for (int a = 0; a < M; ++a) {
+          double b0 = 0.0, b1 = 0.0;
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-          b0 = fma(tb.B[a][i], v[i], b0);
-          if (GRAD) b1 = fma(tb.Dx[a][i], v[i], b1);
+          for (int i = 0; i < N; ++i) {
+            b0 = fma(tb.B[a][i], v[i], b0);
+            if (GRAD) b1 = fma(tb.Dx[a][i], v[i], b1);
+          }
+          X[C::xi(0, ck, j, a)] = b0;
+          if (GRAD) X[C::xi(1, ck, j, a)] = b1;
         }
-        A[C::xi(0, ck, j, a)] = b0;
-        if (GRAD) A[C::xi(1, ck, j, a)] = b1;
       }
     }
-  }
-  group_sync<WPE>(gid);
-  constexpr int NY = 3 * N * M;
+    group_sync<WPE>(gid);
 #pragma unroll
-  for (int r = 0; r < (NY + C::T - 1) / C::T; ++r) {
-    const int w = t + r * C::T;
-    if (w < NY) {
-      int ck, a;
-      C::item_y(w, ck, a);
-      double x0[N], x1[N];
-#pragma unroll
-      for (int j = 0; j < N; ++j) {
-        x0[j] = A[C::xi(0, ck, j, a)];
-        if (GRAD) x1[j] = A[C::xi(1, ck, j, a)];
-      }
-      const int comp = ck / N, k = ck % N;
-#pragma unroll
-      for (int b = 0; b < M; ++b) {
-        double bb = 0.0, db = 0.0, bd = 0.0;
+    for (int r = 0; r < (NY + C::T - 1) / C::T; ++r) {
+      const int w = t + r * C::T;
+      if (w < NY) {
+        int ck, a;
+        C::item_y(w, ck, a);
+        double x0[N], x1[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) {
-          bb = fma(tb.B[b][j], x0[j], bb);
-          if (GRAD) {
-            db = fma(tb.Dy[b][j], x0[j], db);
-            bd = fma(tb.B[b][j], x1[j], bd);
-          }
+          x0[j] = X[C::xi(0, ck, j, a)];
+          if (GRAD) x1[j] = X[C::xi(1, ck, j, a)];
         }
-        B[C::yi(comp, 0, k, b * M + a)] = bb;  // B_y B_x
-        if (GRAD) {
-          B[C::yi(comp, 1, k, b * M + a)] = db;  // D_y B_x
-          B[C::yi(comp, 2, k, b * M + a)] = bd;  // B_y D_x
+        const int cl = ck / N, k = ck % N;
+#pragma unroll
+        for (int b = 0; b < M; ++b) {
+          double bb = 0.0, db = 0.0, bd = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) {
+            bb = fma(tb.B[b][j], x0[j], bb);
+            if (GRAD) {
+              db = fma(tb.Dy[b][j], x0[j], db);
+              bd = fma(tb.B[b][j], x1[j], bd);
+            }
+          }
+          B[C::yi(cl, 0, k, b * M + a)] = bb;  // B_y B_x
+          if (GRAD) {
+            B[C::yi(cl, 1, k, b * M + a)] = db;  // D_y B_x
+            B[C::yi(cl, 2, k, b * M + a)] = bd;  // B_y D_x
+          }
         }
       }
     }
-  }
-  group_sync<WPE>(gid);
-  constexpr int NZ = 3 * M * M;
+    group_sync<WPE>(gid);
 #pragma unroll
-  for (int r = 0; r < (NZ + C::T - 1) / C::T; ++r) {
-    const int w = t + r * C::T;
-    if (w < NZ) {
-      const int comp = w / (M * M), ba = w % (M * M);
-      double y0[N], y1[N], y2[N];
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        y0[k] = B[C::yi(comp, 0, k, ba)];
-        if (GRAD) {
-          y1[k] = B[C::yi(comp, 1, k, ba)];
-          y2[k] = B[C::yi(comp, 2, k, ba)];
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < M; ++c) {
-        double gx = 0.0, gy = 0.0, gz = 0.0, vv = 0.0;
+    for (int r = 0; r < (NZ + C::T - 1) / C::T; ++r) {
+      const int w = t + r * C::T;
+      if (w < NZ) {
+        const int cl = w / (M * M), ba = w % (M * M);
+        const int comp = c0 + cl;
+        double y0[N], y1[N], y2[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) {
+          y0[k] = B[C::yi(cl, 0, k, ba)];
           if (GRAD) {
-            gx = fma(tb.B[c][k], y2[k], gx);
-            gy = fma(tb.B[c][k], y1[k], gy);
-            gz = fma(tb.Dz[c][k], y0[k], gz);
+            y1[k] = B[C::yi(cl, 1, k, ba)];
+            y2[k] = B[C::yi(cl, 2, k, ba)];
           }
-          if (VAL) vv = fma(tb.B[c][k], y0[k], vv);
         }
-        const int q = c * M * M + ba;
-        if (GRAD) {
-          A[C::qi(0, comp, q)] = gx;
-          A[C::qi(1, comp, q)] = gy;
-          A[C::qi(2, comp, q)] = gz;
-        }
-        if (VAL) A[C::qi(3, comp, q)] = vv;
-      }
-    }
-  }
-  group_sync<WPE>(gid);
-}
-
-template <int N, int M, int WPE, bool GRAD, bool VAL>
-__device__ __forceinline__ void v3_backward(const Tab3<N, M>& tb, const Geo& g, double* __restrict__ dst,
-                                            int X0, int Y0, int Z0, double* A, double* B, int t, int gid) {
-  using C = V3<N, M, WPE>;
-  constexpr int NZ = 3 * M * M;
-#pragma unroll
-  for (int r = 0; r < (NZ + C::T - 1) / C::T; ++r) {
-    const int w = t + r * C::T;
-    if (w < NZ) {
-      const int comp = w / (M * M), ba = w % (M * M);
-      double qx[M], qy[M], qz[M], qv[M];
-#pragma unroll
-      for (int c = 0; c < M; ++c) {
-        const int q = c * M * M + ba;
-        if (GRAD) {
-          qx[c] = A[C::qi(0, comp, q)];
-          qy[c] = A[C::qi(1, comp, q)];
-          qz[c] = A[C::qi(2, comp, q)];
-        }
-        if (VAL) qv[c] = A[C::qi(3, comp, q)];
-      }
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        double hx = 0.0, hy = 0.0, hz = 0.0;
 #pragma unroll
         for (int c = 0; c < M; ++c) {
-          if (GRAD) {
-            hx = fma(tb.bBz[c][k], qx[c], hx);
-            hy = fma(tb.bBz[c][k], qy[c], hy);
-            hz = fma(tb.bDz[c][k], qz[c], hz);
+          double gx = 0.0, gy = 0.0, gz = 0.0, vv = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            if (GRAD) {
+              gx = fma(tb.B[c][k], y2[k], gx);
+              gy = fma(tb.B[c][k], y1[k], gy);
+              gz = fma(tb.Dz[c][k], y0[k], gz);
+            }
+            if (VAL) vv = fma(tb.B[c][k], y0[k], vv);
           }
-          if (VAL) hz = fma(tb.bBz[c][k], qv[c], hz);
+          const int q = c * M * M + ba;
+          if (GRAD) {
+            P[C::qi(0, comp, q)] = gx;
+            P[C::qi(1, comp, q)] = gy;
+            P[C::qi(2, comp, q)] = gz;
+          }
+          if (VAL) P[C::qi(3, comp, q)] = vv;
         }
-        if (GRAD) {
-          B[C::yi(comp, 0, k, ba)] = hx;
-          B[C::yi(comp, 1, k, ba)] = hy;
-        }
-        B[C::yi(comp, 2, k, ba)] = hz;
       }
     }
+    group_sync<WPE>(gid);
   }
-  group_sync<WPE>(gid);
-  constexpr int NY = 3 * N * M;
+}
+
+template <int N, int M, int WPE, int NC, bool GRAD, bool VAL>
+__device__ __forceinline__ void v3_backward(const Tab3<N, M>& tb, const Geo& g, double* __restrict__ dst,
+                                            int X0, int Y0, int Z0, double* A, double* B, int t, int gid) {
+  using C = V3<N, M, WPE, NC>;
+  constexpr int NX = NC * N * N, NY = NC * N * M, NZ = NC * M * M;
+#pragma unroll 1
+  for (int c0 = 0; c0 < 3; c0 += NC) {
+    double* const X = (NC == 3) ? A : B + C::YO;
 #pragma unroll
-  for (int r = 0; r < (NY + C::T - 1) / C::T; ++r) {
-    const int w = t + r * C::T;
-    if (w < NY) {
-      int ck, a;
-      C::item_y(w, ck, a);
-      const int comp = ck / N, k = ck % N;
-      double hx[M], hy[M], hz[M];
+    for (int r = 0; r < (NZ + C::T - 1) / C::T; ++r) {
+      const int w = t + r * C::T;
+      if (w < NZ) {
+        const int cl = w / (M * M), ba = w % (M * M);
+        const int comp = c0 + cl;
+        double qx[M], qy[M], qz[M], qv[M];
 #pragma unroll
-      for (int b = 0; b < M; ++b) {
-        if (GRAD) {
-          hx[b] = B[C::yi(comp, 0, k, b * M + a)];
-          hy[b] = B[C::yi(comp, 1, k, b * M + a)];
+        for (int c = 0; c < M; ++c) {
+          const int q = c * M * M + ba;
+          if (GRAD) {
+            qx[c] = A[C::qi(0, comp, q)];
+            qy[c] = A[C::qi(1, comp, q)];
+            qz[c] = A[C::qi(2, comp, q)];
+          }
+          if (VAL) qv[c] = A[C::qi(3, comp, q)];
         }
-        hz[b] = B[C::yi(comp, 2, k, b * M + a)];
-      }
 #pragma unroll
-      for (int j = 0; j < N; ++j) {
-        double jx = 0.0, jyz = 0.0;
+        for (int k = 0; k < N; ++k) {
+          double hx = 0.0, hy = 0.0, hz = 0.0;
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            if (GRAD) {
+              hx = fma(tb.bBz[c][k], qx[c], hx);
+              hy = fma(tb.bBz[c][k], qy[c], hy);
+              hz = fma(tb.bDz[c][k], qz[c], hz);
+            }
+            if (VAL) hz = fma(tb.bBz[c][k], qv[c], hz);
+          }
+          if (GRAD) {
+            B[C::yi(cl, 0, k, ba)] = hx;
+            B[C::yi(cl, 1, k, ba)] = hy;
+          }
+          B[C::yi(cl, 2, k, ba)] = hz;
+        }
+      }
+    }
+    group_sync<WPE>(gid);
+#pragma unroll
+    for (int r = 0; r < (NY + C::T - 1) / C::T; ++r) {
+      const int w = t + r * C::T;
+      if (w < NY) {
+        int ck, a;
+        C::item_y(w, ck, a);
+        const int cl = ck / N, k = ck % N;
+        double hx[M], hy[M], hz[M];
 #pragma unroll
         for (int b = 0; b < M; ++b) {
           if (GRAD) {
-            jx = fma(tb.bBy[b][j], hx[b], jx);
-            jyz = fma(tb.bDy[b][j], hy[b], jyz);
+            hx[b] = B[C::yi(cl, 0, k, b * M + a)];
+            hy[b] = B[C::yi(cl, 1, k, b * M + a)];
           }
-          jyz = fma(tb.bBy[b][j], hz[b], jyz);
+          hz[b] = B[C::yi(cl, 2, k, b * M + a)];
         }
-        if (GRAD) A[C::xi(0, ck, j, a)] = jx;
-        A[C::xi(1, ck, j, a)] = jyz;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          double jx = 0.0, jyz = 0.0;
+#pragma unroll
+          for (int b = 0; b < M; ++b) {
+            if (GRAD) {
+              jx = fma(tb.bBy[b][j], hx[b], jx);
+              jyz = fma(tb.bDy[b][j], hy[b], jyz);
+            }
+            jyz = fma(tb.bBy[b][j], hz[b], jyz);
+          }
+          if (GRAD) X[C::xi(0, ck, j, a)] = jx;
+          X[C::xi(1, ck, j, a)] = jyz;
+        }
       }
     }
-  }
-  group_sync<WPE>(gid);
-  constexpr int NX = 3 * N * N;
+    group_sync<WPE>(gid);
 #pragma unroll
-  for (int r = 0; r < (NX + C::T - 1) / C::T; ++r) {
-    const int w = t + r * C::T;
-    if (w < NX) {
-      int ck, j;
-      C::item_x(w, ck, j);
-      const int comp = ck / N, k = ck % N;
-      double jx[M], jyz[M];
-#pragma unroll
-      for (int a = 0; a < M; ++a) {
-        if (GRAD) jx[a] = A[C::xi(0, ck, j, a)];
-        jyz[a] = A[C::xi(1, ck, j, a)];
-      }
-      const int Z = Z0 + k, Y = Y0 + j;
-      double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Lx + X0;
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        double acc = 0.0;
+    for (int r = 0; r < (NX + C::T - 1) / C::T; ++r) {
+      const int w = t + r * C::T;
+      if (w < NX) {
+        int ck, j;
+        C::item_x(w, ck, j);
+        const int comp = c0 + ck / N, k = ck % N;
+        double jx[M], jyz[M];
 #pragma unroll
         for (int a = 0; a < M; ++a) {
-          if (GRAD) acc = fma(tb.bDx[a][i], jx[a], acc);
-          acc = fma(tb.bBx[a][i], jyz[a], acc);
+          if (GRAD) jx[a] = X[C::xi(0, ck, j, a)];
+          jyz[a] = X[C::xi(1, ck, j, a)];
         }
-        if (!constrained(g, comp, X0 + i, Y, Z)) red_add(row + i, acc);
+        const int Z = Z0 + k, Y = Y0 + j;
+        double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Lx + X0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double acc = 0.0;
+#pragma unroll
+          for (int a = 0; a < M; ++a) {
+            if (GRAD) acc = fma(tb.bDx[a][i], jx[a], acc);
+            acc = fma(tb.bBx[a][i], jyz[a], acc);
+          }
+          if (!constrained(g, comp, X0 + i, Y, Z)) red_add(row + i, acc);
+        }
       }
     }
+    group_sync<WPE>(gid);
   }
-  group_sync<WPE>(gid);
 }
 
 // K = F^{-T}, det F, ln det F from H = grad u
@@ -358,10 +372,10 @@ __device__ __forceinline__ void qp_k(const double (&H)[9], QpK& s) {
   s.lnJ = log(s.det);
 }
 
-template <int N, int M, int WPE, int EPB, int MODE, bool VAL>
-__global__ void __launch_bounds__(EPB * WPE * 32) element_v3(const __grid_constant__ Tab3<N, M> tb,
-                                                               const __grid_constant__ Geo g, OpArgs args) {
-  using C = V3<N, M, WPE>;
+template <int N, int M, int WPE, int NC, int EPB, int MINB, int MODE, bool VAL>
+__global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_constant__ Tab3<N, M> tb,
+                                                                     const __grid_constant__ Geo g, OpArgs args) {
+  using C = V3<N, M, WPE, NC, VAL || MODE == MODE_MASS>;
   extern __shared__ double smem[];
   const int gid = threadIdx.x / C::T;
   const int t = threadIdx.x % C::T;
@@ -380,12 +394,12 @@ __global__ void __launch_bounds__(EPB * WPE * 32) element_v3(const __grid_consta
     if (idx + stride < cnt) {  // warm L2 with the next element's rows
       int ni, nj, nk;
       colour_element(g, args.colour, idx + stride, ni, nj, nk);
-      if (MODE != MODE_MASS) v3_prefetch<N, M, WPE>(g, args.u, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk, t);
-      if (MODE != MODE_FINT) v3_prefetch<N, M, WPE>(g, args.p, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk, t);
+      if (MODE != MODE_MASS) v3_prefetch<N, C::T>(g, args.u, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk, t);
+      if (MODE != MODE_FINT) v3_prefetch<N, C::T>(g, args.p, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk, t);
     }
     double Hu[C::QPT][9];
     if (MODE != MODE_MASS) {
-      v3_forward<N, M, WPE, true, false>(tb, g, args.u, X0, Y0, Z0, A, Bf, t, gid);
+      v3_forward<N, M, WPE, NC, true, false>(tb, g, args.u, X0, Y0, Z0, A, Bf, t, gid);
 #pragma unroll
       for (int r = 0; r < C::QPT; ++r) {
         const int q = t + r * C::T;
@@ -399,7 +413,7 @@ __global__ void __launch_bounds__(EPB * WPE * 32) element_v3(const __grid_consta
       group_sync<WPE>(gid);
     }
     if (MODE != MODE_FINT)
-      v3_forward<N, M, WPE, GRADP, VAL>(tb, g, args.p, X0, Y0, Z0, A, Bf, t, gid);
+      v3_forward<N, M, WPE, NC, GRADP, VAL>(tb, g, args.p, X0, Y0, Z0, A, Bf, t, gid);
 #pragma unroll
     for (int r = 0; r < C::QPT; ++r) {
       const int q = t + r * C::T;
@@ -457,11 +471,11 @@ __global__ void __launch_bounds__(EPB * WPE * 32) element_v3(const __grid_consta
     }
     group_sync<WPE>(gid);
     if (MODE == MODE_MASS)
-      v3_backward<N, M, WPE, false, true>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid);
+      v3_backward<N, M, WPE, NC, false, true>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid);
     else if (MODE == MODE_FINT)
-      v3_backward<N, M, WPE, true, false>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid);
+      v3_backward<N, M, WPE, NC, true, false>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid);
     else
-      v3_backward<N, M, WPE, true, VAL>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid);
+      v3_backward<N, M, WPE, NC, true, VAL>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid);
   }
 }
 

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -54,6 +55,7 @@ struct sdme_ctx {
   int err_qp = -1;
   std::string err_msg;
   int64_t launches = 0;
+  int variant = 0;  // schedule variant (SDME_VARIANT env), tuning only
 };
 
 namespace {
@@ -134,23 +136,31 @@ Tab3<N, M> make_tab3(const sdme_ctx* c) {
   return t;
 }
 
-template <int N, int M>
-struct ConfV3 {
-  static constexpr int bytes = V3<N, M, 1>::PER * 8;
-  static constexpr int WPE = bytes <= 40960 ? 1 : (bytes <= 65536 ? 4 : 8);
-  static constexpr int EPB = WPE == 1 ? 2 : 1;
-  static constexpr int smem = V3<N, M, WPE>::PER * 8 * EPB;
+// Launch shape of the v3 element kernels.  WPE warps per element, EPB
+// elements per block, NC components per contraction stage, MINB minimum
+// resident blocks per SM (register cap for __launch_bounds__).
+template <int N, int M, int WPE_, int NC_, int EPB_, int MINB_>
+struct Shape {
+  static constexpr int WPE = WPE_, NC = NC_, EPB = EPB_, MINB = MINB_;
 };
 
-template <int N, int M, int MODE, bool VAL>
+template <int N, int M>
+struct DefaultShape {
+  static constexpr int bytes = V3<N, M, 1, 3>::PER * 8;
+  static constexpr int WPE = bytes <= 40960 ? 1 : (bytes <= 65536 ? 4 : 8);
+  using type = Shape<N, M, WPE, 3, (WPE == 1 ? 2 : 1), 1>;
+};
+
+template <int N, int M, class S, int MODE, bool VAL>
 void launch_v3(sdme_ctx* c, const Tab3<N, M>& tb, OpArgs a) {
-  using CF = ConfV3<N, M>;
-  auto kern = element_v3<N, M, CF::WPE, CF::EPB, MODE, VAL>;
+  constexpr bool VALS = VAL || MODE == MODE_MASS;
+  constexpr int smem = V3<N, M, S::WPE, S::NC, VALS>::PER * 8 * S::EPB;
+  auto kern = element_v3<N, M, S::WPE, S::NC, S::EPB, S::MINB, MODE, VAL>;
   static int max_blocks = -1;
   if (max_blocks < 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, CF::EPB * CF::WPE * 32, CF::smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, S::EPB * S::WPE * 32, smem);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     max_blocks = std::max(1, nb) * sms;
@@ -159,21 +169,38 @@ void launch_v3(sdme_ctx* c, const Tab3<N, M>& tb, OpArgs a) {
     const long long cnt = colour_count(c->geo, col);
     if (cnt == 0) continue;
     a.colour = col;
-    const long long need = (cnt + CF::EPB - 1) / CF::EPB;
+    const long long need = (cnt + S::EPB - 1) / S::EPB;
     const unsigned grid = (unsigned)std::min<long long>(need, max_blocks);
-    kern<<<grid, CF::EPB * CF::WPE * 32, CF::smem, c->st>>>(tb, c->geo, a);
+    kern<<<grid, S::EPB * S::WPE * 32, smem, c->st>>>(tb, c->geo, a);
     ++c->launches;
   }
+}
+
+template <int N, int M, class S>
+void element_shape(sdme_ctx* c, int mode, const Tab3<N, M>& tb, OpArgs a) {
+  if (mode == MODE_FINT) launch_v3<N, M, S, MODE_FINT, false>(c, tb, a);
+  else if (mode == MODE_APPLY && a.c_m != 0.0) launch_v3<N, M, S, MODE_APPLY, true>(c, tb, a);
+  else if (mode == MODE_APPLY) launch_v3<N, M, S, MODE_APPLY, false>(c, tb, a);
+  else launch_v3<N, M, S, MODE_MASS, true>(c, tb, a);
 }
 
 template <int N, int M>
 void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, double* y, double ck, double cm) {
   const Tab3<N, M> tb = make_tab3<N, M>(c);
   OpArgs a{u, p, y, ck, cm, 0, c->d_flag};
-  if (mode == MODE_FINT) launch_v3<N, M, MODE_FINT, false>(c, tb, a);
-  else if (mode == MODE_APPLY && cm != 0.0) launch_v3<N, M, MODE_APPLY, true>(c, tb, a);
-  else if (mode == MODE_APPLY) launch_v3<N, M, MODE_APPLY, false>(c, tb, a);
-  else launch_v3<N, M, MODE_MASS, true>(c, tb, a);
+  if constexpr (N == 5 && M == 5) {
+    // P = 4, m = 5 (BASELINE config 2).  Measured (profiles/variants_r01.txt):
+    // component-serial stages, one element per 32-thread block, 12 blocks/SM
+    // (168-register cap) beats the 3-component, 8-warp shape by 11%.
+    // SDME_VARIANT=3 keeps the 3-component shape for comparison.
+    if (c->variant == 3) {
+      element_shape<N, M, Shape<N, M, 1, 3, 2, 4>>(c, mode, tb, a);
+      return;
+    }
+    element_shape<N, M, Shape<N, M, 1, 1, 1, 12>>(c, mode, tb, a);
+    return;
+  }
+  element_shape<N, M, typename DefaultShape<N, M>::type>(c, mode, tb, a);
 }
 
 template <int N, int M>
@@ -296,6 +323,7 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
     return SDME_BAD_ARGUMENT;
   sdme_ctx* ctx = new sdme_ctx();
   ctx->ops = ops;
+  if (const char* v = getenv("SDME_VARIANT")) ctx->variant = atoi(v);
   ctx->P = d->P;
   ctx->m = d->m;
   ctx->n = d->P + 1;
