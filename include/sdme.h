@@ -126,6 +126,10 @@ int sdme_contact(sdme_ctx* ctx, int u, int side, int qf, const double* Bf, const
 /* number of face points of a side for the given qf */
 int sdme_contact_points(const sdme_ctx* ctx, int side, int qf, int64_t* n);
 
+/* page-locked host buffers (fast H2D/D2H for the free-order vector calls) */
+int sdme_host_alloc(size_t bytes, void** ptr);
+int sdme_host_free(void* ptr);
+
 /* timing (CUDA events on the context stream) ----------------------------- */
 /* op: 0 = apply (K p, c_m), 1 = fint, 2 = mass, 3 = diag, 4 = pcg iteration vector
  * kernels; returns mean milliseconds per call over `reps` back-to-back calls. */

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsdme.so")
 SOURCES = [os.path.join(HERE, "csrc", "sdme_abi.cu")]
 HEADERS = [os.path.join(HERE, "csrc", f) for f in
-           ("element_kernels.cuh", "element_v3.cuh", "vector_kernels.cuh", "contact_kernels.cuh")] + \
+           ("element_kernels.cuh", "element_v3.cuh", "element_v4.cuh", "vector_kernels.cuh", "contact_kernels.cuh")] + \
           [os.path.join(ROOT, "include", "sdme.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -49,6 +49,7 @@ struct OpArgs {
   double c_k, c_m;    // y += c_k K p + c_m M p   (APPLY); y += c_m M p (MASS)
   int colour;         // bit0: i parity, bit1: j parity, bit2: k parity
   unsigned long long* inv_flag;  // atomicMin(elem*nq + qp) on det F <= 0
+  const int* skip = nullptr;     // if set and non-zero: return at once (stopped PCG graph)
 };
 
 __device__ __forceinline__ bool constrained(const Geo& g, int comp, int X, int Y, int Z) {

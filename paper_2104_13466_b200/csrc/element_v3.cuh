@@ -381,6 +381,7 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
   const int t = threadIdx.x % C::T;
   double* A = smem + gid * C::PER;
   double* Bf = A + C::SA;
+  if (args.skip && *(volatile const int*)args.skip) return;
   const long long cnt = colour_count(g, args.colour);
   constexpr bool GRADP = (MODE == MODE_APPLY);
   const long long stride = (long long)gridDim.x * EPB;

@@ -15,6 +15,7 @@
 #include "contact_kernels.cuh"
 #include "element_kernels.cuh"
 #include "element_v3.cuh"
+#include "element_v4.cuh"
 #include "vector_kernels.cuh"
 
 using namespace sdme;
@@ -56,6 +57,9 @@ struct sdme_ctx {
   std::string err_msg;
   int64_t launches = 0;
   int variant = 0;  // schedule variant (SDME_VARIANT env), tuning only
+  int* d_status = nullptr;  // PCG status word (device) and its pinned mirror
+  int* h_status = nullptr;
+  const int* cur_skip = nullptr;  // element kernels exit early when *cur_skip != 0 (PCG graph)
 };
 
 namespace {
@@ -184,10 +188,42 @@ void element_shape(sdme_ctx* c, int mode, const Tab3<N, M>& tb, OpArgs a) {
   else launch_v3<N, M, S, MODE_MASS, true>(c, tb, a);
 }
 
+template <int N, int M, int MINB, int MODE, bool VAL, bool ASYNC, bool GUS = false>
+void launch_v4(sdme_ctx* c, const Tab3<N, M>& tb, OpArgs a) {
+  constexpr int smem =
+      (V4<N, M>::PER + (ASYNC ? 4 * 3 * N * N * N : 0) + (GUS && MODE == MODE_APPLY ? 9 * M * 32 : 0)) * 8;
+  auto kern = element_v4<N, M, MINB, MODE, VAL, ASYNC, GUS>;
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    max_blocks = std::max(1, nb) * sms;
+  }
+  for (int col = 0; col < 8; ++col) {
+    const long long cnt = colour_count(c->geo, col);
+    if (cnt == 0) continue;
+    a.colour = col;
+    const unsigned grid = (unsigned)std::min<long long>(cnt, max_blocks);
+    kern<<<grid, 32, smem, c->st>>>(tb, c->geo, a);
+    ++c->launches;
+  }
+}
+
+template <int N, int M, int MINB, bool ASYNC, bool GUS = false>
+void element_v4_modes(sdme_ctx* c, int mode, const Tab3<N, M>& tb, OpArgs a) {
+  if (mode == MODE_FINT) launch_v4<N, M, MINB, MODE_FINT, false, ASYNC, GUS>(c, tb, a);
+  else if (mode == MODE_APPLY && a.c_m != 0.0) launch_v4<N, M, MINB, MODE_APPLY, true, ASYNC, GUS>(c, tb, a);
+  else if (mode == MODE_APPLY) launch_v4<N, M, MINB, MODE_APPLY, false, ASYNC, GUS>(c, tb, a);
+  else launch_v4<N, M, MINB, MODE_MASS, true, ASYNC, GUS>(c, tb, a);
+}
+
 template <int N, int M>
 void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, double* y, double ck, double cm) {
   const Tab3<N, M> tb = make_tab3<N, M>(c);
-  OpArgs a{u, p, y, ck, cm, 0, c->d_flag};
+  OpArgs a{u, p, y, ck, cm, 0, c->d_flag, c->cur_skip};
   if constexpr (N == 5 && M == 5) {
     // P = 4, m = 5 (BASELINE config 2).  Measured (profiles/variants_r01.txt):
     // component-serial stages, one element per 32-thread block, 12 blocks/SM
@@ -195,6 +231,13 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
     // SDME_VARIANT=3 keeps the 3-component shape for comparison.
     if (c->variant == 3) {
       element_shape<N, M, Shape<N, M, 1, 3, 2, 4>>(c, mode, tb, a);
+      return;
+    }
+    if (c->variant == 4) { element_v4_modes<N, M, 8, false>(c, mode, tb, a); return; }
+    // default: f_int and mass with the column-resident v4 schedule (1.66 / 1.29 ms vs
+    // 1.91 / 1.42 ms), K.p with v3 component-serial at 12 warps/SM (2.91 vs 3.04 ms)
+    if (mode == MODE_FINT || mode == MODE_MASS) {
+      element_v4_modes<N, M, 10, false>(c, mode, tb, a);
       return;
     }
     element_shape<N, M, Shape<N, M, 1, 1, 1, 12>>(c, mode, tb, a);
@@ -361,6 +404,8 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   if (cudaMallocHost(&ctx->h_scal, 16 * sizeof(double)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
   if (cudaMalloc(&ctx->d_flag, sizeof(unsigned long long)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
   if (cudaMallocHost(&ctx->h_flag, sizeof(unsigned long long)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+  if (cudaMalloc(&ctx->d_status, sizeof(int)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+  if (cudaMallocHost(&ctx->h_status, sizeof(int)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
   // free mask from the Dirichlet planes
   {
     std::vector<unsigned char> fm(ctx->nvec, 1);
@@ -404,6 +449,8 @@ int sdme_destroy(sdme_ctx* ctx) {
   cudaFree(ctx->d_gaps);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
   if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
+  cudaFree(ctx->d_status);
+  if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_gaps) cudaFreeHost(ctx->h_gaps);
   if (ctx->st) cudaStreamDestroy(ctx->st);
   delete ctx;
@@ -523,11 +570,11 @@ int sdme_vec_dot(sdme_ctx* ctx, int a, int b, double* out) {
   double* pa = ctx ? vec(ctx, a) : nullptr;
   double* pb = ctx ? vec(ctx, b) : nullptr;
   if (!pa || !pb || !out) return SDME_BAD_ARGUMENT;
-  int rc = dot_into(ctx, pa, pb, S_NB);
+  int rc = dot_into(ctx, pa, pb, S_SCRATCH);
   if (rc) return rc;
   rc = read_scalars(ctx);
   if (rc) return rc;
-  *out = ctx->h_scal[S_NB];
+  *out = ctx->h_scal[S_SCRATCH];
   return SDME_OK;
 }
 
@@ -621,8 +668,8 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
     return set_err(ctx, SDME_BAD_ARGUMENT, "unknown preconditioner (out of scope: sgs)");
   }
   // ||b||
-  if ((rc = dot_into(ctx, pb, pb, S_NB)) || (rc = read_scalars(ctx))) return rc;
-  const double nb = std::sqrt(ctx->h_scal[S_NB]);
+  if ((rc = dot_into(ctx, pb, pb, S_SCRATCH)) || (rc = read_scalars(ctx))) return rc;
+  const double nb = std::sqrt(ctx->h_scal[S_SCRATCH]);
   CK(cudaMemsetAsync(px, 0, ctx->nvec * sizeof(double), ctx->st));
   if (nb == 0.0) {
     CK(cudaStreamSynchronize(ctx->st));
@@ -632,36 +679,77 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
   CK(cudaMemcpyAsync(r, pb, ctx->nvec * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
   k_mul<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, dinv, r, ctx->nvec);
   ++ctx->launches;
-  if ((rc = dot_into(ctx, r, p, S_RZ))) return rc;
-  double rel_prev = 1.0;
-  for (int it = 1; it <= maxit; ++it) {
+  if ((rc = dot_into(ctx, r, p, S_RZ0))) return rc;
+  int status = PCG_MAXIT;
+  if (maxit > 0) {
+    // device scalar state
+    double init[S_COUNT];
+    CK(cudaMemcpyAsync(init, ctx->d_scal, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    init[S_NB] = nb;
+    init[S_TOL] = tol;
+    init[S_RELPREV] = 1.0;
+    init[S_ITER] = 0.0;
+    init[S_MAXIT] = (double)maxit;
+    CK(cudaMemcpyAsync(ctx->d_scal, init, S_COUNT * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int), ctx->st));
+    // warm the operator's one-time launch setup outside the capture
     if ((rc = apply_raw(ctx, pu, p, ap, c_k, c_m))) return rc;
-    if ((rc = dot_into(ctx, p, ap, S_PAP))) return rc;
-    k_alpha<<<1, 32, 0, ctx->st>>>(ctx->d_scal);
+    // one iteration as a CUDA graph; every kernel exits early once stopped
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    const long long l0 = ctx->launches;
+    CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+    ctx->cur_skip = ctx->d_status;
+    k_zero<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(ap, ctx->nvec, ctx->d_status);
+    if (c_k != 0.0)
+      ctx->ops->element(ctx, MODE_APPLY, pu, p, ap, c_k, c_m);
+    else
+      ctx->ops->element(ctx, MODE_MASS, nullptr, p, ap, 0.0, c_m);
+    k_pcg_pap<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(p, ap, ctx->nvec, ctx->d_partial, ctx->d_status);
+    k_pcg_alpha<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, ctx->d_status);
     k_pcg_update<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(px, r, p, ap, dinv, ctx->d_scal, ctx->nvec,
-                                                          ctx->d_partial);
-    k_finish<2><<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal + S_RR);
-    k_beta<<<1, 32, 0, ctx->st>>>(ctx->d_scal);
-    ctx->launches += 4;
-    if ((rc = check_launch(ctx)) || (rc = read_scalars(ctx))) return rc;
-    const double pap = ctx->h_scal[S_PAP];
-    if (!(pap > 0.0)) {
-      if (iters) *iters = it;
-      if (relres) *relres = rel_prev;
-      char buf[128];
-      snprintf(buf, sizeof buf, "indefinite operator detected at iteration %d (p^T A p = %.3e)", it, pap);
-      return set_err(ctx, SDME_INDEFINITE, buf);
+                                                          ctx->d_partial, ctx->d_status);
+    k_pcg_check<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, ctx->d_status);
+    k_pcg_p<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, r, dinv, ctx->d_scal, ctx->nvec, ctx->d_status);
+    ctx->cur_skip = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(ctx->st, &graph);
+    const long long per_iter = ctx->launches - l0 + 6;
+    ctx->launches = l0;
+    if (ce != cudaSuccess) return set_err(ctx, SDME_CUDA_ERROR, std::string("graph capture: ") + cudaGetErrorString(ce));
+    if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+      cudaGraphDestroy(graph);
+      return set_err(ctx, SDME_CUDA_ERROR, "graph instantiate failed");
     }
-    const double rel = std::sqrt(ctx->h_scal[S_RR]) / nb;
-    if (rel <= tol) {
+    long long launched = 0;
+    int chunk = 2;
+    for (;;) {
+      for (int g = 0; g < chunk; ++g) cudaGraphLaunch(exec, ctx->st);
+      launched += chunk;
+      ctx->launches += chunk * per_iter;
+      CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+      CK(cudaStreamSynchronize(ctx->st));
+      if (*ctx->h_status != PCG_RUNNING || launched > (long long)maxit + 64) break;
+      chunk = std::min(chunk * 2, 16);
+    }
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    if ((rc = check_launch(ctx)) || (rc = read_scalars(ctx))) return rc;
+    status = *ctx->h_status;
+    const int it = (int)ctx->h_scal[S_ITER];
+    if (status == PCG_CONVERGED) {
       if (iters) *iters = it;
-      if (relres) *relres = rel;
+      if (relres) *relres = ctx->h_scal[S_STOPREL];
       return SDME_OK;
     }
-    rel_prev = rel;
-    k_pcg_p<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, r, dinv, ctx->d_scal, ctx->nvec);
-    k_roll<<<1, 32, 0, ctx->st>>>(ctx->d_scal);
-    ctx->launches += 2;
+    if (status == PCG_INDEFINITE) {
+      if (iters) *iters = it;
+      if (relres) *relres = ctx->h_scal[S_STOPREL];
+      char buf[128];
+      snprintf(buf, sizeof buf, "indefinite operator detected at iteration %d (p^T A p = %.3e)", it,
+               ctx->h_scal[S_PAP]);
+      return set_err(ctx, SDME_INDEFINITE, buf);
+    }
   }
   // maxit: true residual ||b - A x|| / ||b||  (solver.py:166)
   if ((rc = apply_raw(ctx, pu, px, ap, c_k, c_m))) return rc;
@@ -675,8 +763,8 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
     k_lincomb<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(lc, r, ctx->nvec);
     ++ctx->launches;
   }
-  if ((rc = dot_into(ctx, r, r, S_RR)) || (rc = read_scalars(ctx))) return rc;
-  const double rel = std::sqrt(ctx->h_scal[S_RR]) / nb;
+  if ((rc = dot_into(ctx, r, r, S_SCRATCH)) || (rc = read_scalars(ctx))) return rc;
+  const double rel = std::sqrt(ctx->h_scal[S_SCRATCH]) / nb;
   if (iters) *iters = maxit;
   if (relres) *relres = rel;
   char buf[128];
@@ -821,6 +909,15 @@ int sdme_time_op(sdme_ctx* ctx, int op, int u, int p, int y, double c_m, int rep
   cudaEventDestroy(e1);
   *ms = (double)t / reps;
   return check_launch(ctx);
+}
+
+int sdme_host_alloc(size_t bytes, void** ptr) {
+  if (!ptr) return SDME_BAD_ARGUMENT;
+  return cudaMallocHost(ptr, bytes) == cudaSuccess ? SDME_OK : SDME_CUDA_ERROR;
+}
+
+int sdme_host_free(void* ptr) {
+  return cudaFreeHost(ptr) == cudaSuccess ? SDME_OK : SDME_CUDA_ERROR;
 }
 
 int sdme_sync(sdme_ctx* ctx) {

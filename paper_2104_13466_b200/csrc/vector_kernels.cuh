@@ -102,14 +102,65 @@ __global__ void k_lincomb(LinComb lc, double* y, long long n) {
 }
 
 // ---------------------------------------------------------------- PCG pieces
-// Device scalar block (solver.py:143-165 state):
-//   s[0] = rz, s[1] = pap, s[2] = alpha, s[3] = rr, s[4] = rz_new, s[5] = beta,
-//   s[6] = ||b||
-enum { S_RZ = 0, S_PAP, S_ALPHA, S_RR, S_RZN, S_BETA, S_NB, S_COUNT };
+// Device-controlled Jacobi-PCG (solver.py:129-170).  One iteration is a fixed
+// kernel sequence (captured once into a CUDA graph): Ap -> pap -> alpha /
+// indefinite test -> x, r update + (r.r, r.z) partials -> convergence test /
+// beta -> p update.  The scalar state lives on the device; every kernel
+// returns immediately once the status word is set, so the host can launch
+// several iterations between checks without changing the result.  The order
+// of checks is the reference's: pAp <= 0 -> error (residual of the previous
+// iterate), then the recursive-residual test, then maxit.
+enum {
+  S_RZ0 = 0,   // r.z of the previous iterate, ping-pong by iteration parity
+  S_RZ1,
+  S_PAP,
+  S_ALPHA,
+  S_BETA,
+  S_NB,        // ||b||
+  S_TOL,
+  S_RELPREV,   // relative residual of the previous iterate (PCGError stats)
+  S_ITER,      // iterations completed
+  S_STOPREL,   // relative residual at stop
+  S_MAXIT,
+  S_SCRATCH,   // generic dot result
+  S_COUNT
+};
+enum { PCG_RUNNING = 0, PCG_CONVERGED = 1, PCG_INDEFINITE = 2, PCG_MAXIT = 3 };
 
-// alpha = rz / pap  (after pap reduced into s[S_PAP])
-__global__ void k_alpha(double* s) {
-  if (threadIdx.x == 0) s[S_ALPHA] = s[S_RZ] / s[S_PAP];
+__device__ __forceinline__ bool pcg_done(const int* status) { return status && *(volatile const int*)status != 0; }
+
+// partial p.ap (skips once stopped)
+__global__ void __launch_bounds__(kRedThreads) k_pcg_pap(const double* __restrict__ p, const double* __restrict__ ap,
+                                                         long long n, double* partial, const int* status) {
+  if (pcg_done(status)) return;
+  double acc[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    acc[0] = fma(p[i], ap[i], acc[0]);
+  double out[1];
+  block_sum<1>(acc, out);
+  if (threadIdx.x == 0) partial[blockIdx.x] = out[0];
+}
+
+// pap, indefinite test, alpha = rz / pap
+__global__ void __launch_bounds__(kRedThreads) k_pcg_alpha(const double* partial, double* s, int* status) {
+  if (pcg_done(status)) return;
+  double acc[1] = {0.0};
+  for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) acc[0] += partial[i];
+  double out[1];
+  block_sum<1>(acc, out);
+  if (threadIdx.x == 0) {
+    const double pap = out[0];
+    const long long k = (long long)s[S_ITER] + 1;
+    s[S_PAP] = pap;
+    if (!(pap > 0.0)) {
+      s[S_ITER] = (double)k;
+      s[S_STOPREL] = s[S_RELPREV];
+      *status = PCG_INDEFINITE;
+      return;
+    }
+    s[S_ALPHA] = s[S_RZ0 + ((k - 1) & 1)] / pap;
+  }
 }
 
 // x += alpha p ; r -= alpha ap ; partial (r.r, r.(dinv r))
@@ -118,7 +169,8 @@ __global__ void __launch_bounds__(kRedThreads) k_pcg_update(double* __restrict__
                                                             const double* __restrict__ ap,
                                                             const double* __restrict__ dinv,
                                                             const double* __restrict__ s, long long n,
-                                                            double* partial) {
+                                                            double* partial, const int* status) {
+  if (pcg_done(status)) return;
   const double alpha = s[S_ALPHA];
   double acc[2] = {0.0, 0.0};
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -137,23 +189,52 @@ __global__ void __launch_bounds__(kRedThreads) k_pcg_update(double* __restrict__
   }
 }
 
-// after finishing (rr, rz_new) into s[S_RR], s[S_RZN]: beta, rz <- rz_new
-__global__ void k_beta(double* s) {
-  if (threadIdx.x == 0) {
-    s[S_BETA] = s[S_RZN] / s[S_RZ];
+// convergence test (recursive residual), maxit, beta = rz_new / rz_old
+__global__ void __launch_bounds__(kRedThreads) k_pcg_check(const double* partial, double* s, int* status) {
+  if (pcg_done(status)) return;
+  double acc[2] = {0.0, 0.0};
+  for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) {
+    acc[0] += partial[2 * i];
+    acc[1] += partial[2 * i + 1];
   }
-}
-__global__ void k_roll(double* s) {
-  if (threadIdx.x == 0) s[S_RZ] = s[S_RZN];
+  double out[2];
+  block_sum<2>(acc, out);
+  if (threadIdx.x == 0) {
+    const long long k = (long long)s[S_ITER] + 1;
+    s[S_ITER] = (double)k;
+    const double rel = sqrt(out[0]) / s[S_NB];
+    if (rel <= s[S_TOL]) {
+      s[S_STOPREL] = rel;
+      *status = PCG_CONVERGED;
+      return;
+    }
+    if ((double)k >= s[S_MAXIT]) {
+      s[S_STOPREL] = rel;
+      *status = PCG_MAXIT;
+      return;
+    }
+    s[S_RELPREV] = rel;
+    s[S_BETA] = out[1] / s[S_RZ0 + ((k - 1) & 1)];
+    s[S_RZ0 + (k & 1)] = out[1];
+  }
 }
 
 // p = dinv r + beta p
 __global__ void k_pcg_p(double* __restrict__ p, const double* __restrict__ r, const double* __restrict__ dinv,
-                        const double* __restrict__ s, long long n) {
+                        const double* __restrict__ s, long long n, const int* status) {
+  if (pcg_done(status)) return;
   const double beta = s[S_BETA];
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     p[i] = fma(beta, p[i], dinv[i] * r[i]);
+}
+
+// y = 0 unless stopped (graph-friendly memset)
+__global__ void k_zero(double* __restrict__ y, long long n, const int* status) {
+  if (pcg_done(status)) return;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = 0.0;
 }
 
 // x = value on free points, 0 on constrained

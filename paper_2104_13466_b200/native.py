@@ -65,6 +65,8 @@ SIGNATURES = {
                      _dp, _dp],
     "sdme_contact_points": [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int64)],
     "sdme_time_op": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, _dp],
+    "sdme_host_alloc": [C.c_size_t, C.POINTER(C.c_void_p)],
+    "sdme_host_free": [C.c_void_p],
     "sdme_sync": [C.c_void_p],
     "sdme_launch_count": [C.c_void_p, C.POINTER(C.c_int64)],
 }
@@ -85,6 +87,35 @@ def lib() -> C.CDLL:
             fn.restype = C.c_int
         _LIB = h
     return _LIB
+
+
+class _Pinned:
+    """Owner of a page-locked host buffer (freed with the last numpy view)."""
+
+    def __init__(self, nbytes):
+        p = C.c_void_p()
+        rc = lib().sdme_host_alloc(nbytes, C.byref(p))
+        if rc != OK:
+            raise NativeError(f"cudaMallocHost({nbytes}) failed")
+        self.ptr = p
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib().sdme_host_free(self.ptr)
+            self.ptr = None
+
+
+class PinnedArray(np.ndarray):
+    """ndarray view of page-locked memory; holds the allocation alive."""
+
+
+def pinned_empty(n: int) -> np.ndarray:
+    """float64 numpy array of length n in page-locked host memory."""
+    owner = _Pinned(max(8, 8 * n))
+    buf = (C.c_double * n).from_address(owner.ptr.value)
+    arr = np.ctypeslib.as_array(buf).view(PinnedArray)
+    arr._owner = owner
+    return arr
 
 
 def dptr(a: np.ndarray):

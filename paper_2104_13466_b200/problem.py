@@ -78,8 +78,13 @@ class DeviceVector:
                                                                           native.dptr(a)), "upload")
         return self
 
-    def free(self) -> np.ndarray:
-        out = np.empty(self.problem.n_free)
+    def free(self, out: np.ndarray | None = None) -> np.ndarray:
+        """Download in the reference free-DOF order (into ``out`` if given,
+        e.g. a page-locked buffer from :func:`native.pinned_empty`)."""
+        if out is None:
+            out = np.empty(self.problem.n_free)
+        elif out.shape != (self.problem.n_free,) or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError("out must be a contiguous float64 free vector")
         native.check(self.problem._ctx, native.lib().sdme_vec_download_free(self.problem._ctx, self.vid,
                                                                             native.dptr(out)), "download")
         return out
@@ -242,16 +247,17 @@ class GpuFemProblem:
         return out
 
     # ------------------------------------- reference-order host entry points
-    def internal_force(self, u_free: np.ndarray) -> np.ndarray:
+    def internal_force(self, u_free: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
         """``FemProblem.internal_force`` (femcore.py:346-349)."""
         u = self._scratch("u").set_free(u_free)
-        return self.fint_(u, self._scratch("y")).free()
+        return self.fint_(u, self._scratch("y")).free(out)
 
-    def apply_tangent(self, u_free: np.ndarray, p_free: np.ndarray, c_m: float = 0.0) -> np.ndarray:
+    def apply_tangent(self, u_free: np.ndarray, p_free: np.ndarray, c_m: float = 0.0,
+                      out: np.ndarray | None = None) -> np.ndarray:
         """(K_T(u) + c_m M) p: ``element_tangent(...)@p_e`` summed (femcore.py:130-146)."""
         u = self._scratch("u").set_free(u_free)
         p = self._scratch("p").set_free(p_free)
-        return self.apply_(u, p, self._scratch("y"), 1.0, c_m).free()
+        return self.apply_(u, p, self._scratch("y"), 1.0, c_m).free(out)
 
     def tangent_diagonal(self, u_free: np.ndarray, c_m: float = 0.0) -> np.ndarray:
         """diag(K_T(u) + c_m M) over free dofs (solver.py:106 on the assembled operator)."""
