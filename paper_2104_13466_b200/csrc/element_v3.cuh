@@ -113,6 +113,33 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory"); }
+
+// Asynchronous staging of one component's (P+1)^2 rows of an element box into
+// shared memory, rows [k][j] of N doubles (cp.async, no registers held).
+template <int N, int T>
+__device__ __forceinline__ void v3_stage_rows(const Geo& g, const double* __restrict__ field, int comp, int X0,
+                                              int Y0, int Z0, double* rows, int t) {
+  for (int w = t; w < N * N * N; w += T) {
+    const int kj = w / N, i = w % N;
+    const int k = kj / N, j = kj % N;
+    cp_async8(rows + w, field + comp * g.Ns + ((long long)(Z0 + k) * g.Ly + (Y0 + j)) * g.Lx + X0 + i);
+  }
+  cp_async_commit();
+}
+
+// What to stage after the last component of a forward pass.
+struct NextRows {
+  const double* field;  // nullptr: nothing to stage
+  int X0, Y0, Z0;
+};
+
 template <int N, int T>
 __device__ __forceinline__ void v3_prefetch(const Geo& g, const double* __restrict__ src, int X0, int Y0, int Z0,
                                             int t) {
@@ -124,15 +151,35 @@ __device__ __forceinline__ void v3_prefetch(const Geo& g, const double* __restri
   }
 }
 
-template <int N, int M, int WPE, int NC, bool GRAD, bool VAL>
+// Forward pass of the three components of one field.  STAGED (NC == 1): the
+// element rows come from the cp.async double buffer R (component c0 already
+// staged into R + buf*N^3 by the caller / previous pass); the next
+// component's rows -- or `next` after the last one -- are staged while this
+// component computes, so global latency is off the critical path.
+template <int N, int M, int WPE, int NC, bool GRAD, bool VAL, bool STAGED = false>
 __device__ __forceinline__ void v3_forward(const Tab3<N, M>& tb, const Geo& g, const double* __restrict__ src,
-                                           int X0, int Y0, int Z0, double* A, double* B, int t, int gid) {
+                                           int X0, int Y0, int Z0, double* A, double* B, int t, int gid,
+                                           double* R = nullptr, int* buf = nullptr, NextRows next = {}) {
   using C = V3<N, M, WPE, NC>;
+  static_assert(!STAGED || NC == 1, "row staging is per component");
   constexpr int NX = NC * N * N, NY = NC * N * M, NZ = NC * M * M;
   double* const P = A;  // points buffer (all components)
 #pragma unroll 1
   for (int c0 = 0; c0 < 3; c0 += NC) {
     double* const X = (NC == 3) ? A : B + C::YO;  // x-stage scratch (see V3::SB)
+    if (STAGED) {
+      double* nb = R + (*buf ^ 1) * N * N * N;
+      if (c0 + 1 < 3) {
+        v3_stage_rows<N, C::T>(g, src, c0 + 1, X0, Y0, Z0, nb, t);
+        cp_async_wait<1>();
+      } else if (next.field) {
+        v3_stage_rows<N, C::T>(g, next.field, 0, next.X0, next.Y0, next.Z0, nb, t);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      group_sync<WPE>(gid);
+    }
 #pragma unroll
     for (int r = 0; r < (NX + C::T - 1) / C::T; ++r) {
       const int w = t + r * C::T;
@@ -140,10 +187,16 @@ __device__ __forceinline__ void v3_forward(const Tab3<N, M>& tb, const Geo& g, c
         int ck, j;
         C::item_x(w, ck, j);
         const int comp = c0 + ck / N, k = ck % N;
-        const double* row = src + comp * g.Ns + ((long long)(Z0 + k) * g.Ly + (Y0 + j)) * g.Lx + X0;
         double v[N];
+        if (STAGED) {
+          const double* row = R + *buf * N * N * N + (k * N + j) * N;
 #pragma unroll
-        for (int i = 0; i < N; ++i) v[i] = __ldg(row + i);
+          for (int i = 0; i < N; ++i) v[i] = row[i];
+        } else {
+          const double* row = src + comp * g.Ns + ((long long)(Z0 + k) * g.Ly + (Y0 + j)) * g.Lx + X0;
+#pragma unroll
+          for (int i = 0; i < N; ++i) v[i] = __ldg(row + i);
+        }
 #pragma unroll
         for (int a = 0; a < M; ++a) {
           double b0 = 0.0, b1 = 0.0;
@@ -228,6 +281,7 @@ __device__ __forceinline__ void v3_forward(const Tab3<N, M>& tb, const Geo& g, c
         }
       }
     }
+    if (STAGED) *buf ^= 1;
     group_sync<WPE>(gid);
   }
 }
@@ -372,15 +426,20 @@ __device__ __forceinline__ void qp_k(const double (&H)[9], QpK& s) {
   s.lnJ = log(s.det);
 }
 
-template <int N, int M, int WPE, int NC, int EPB, int MINB, int MODE, bool VAL>
+// STG: cp.async double-buffered row staging (NC == 1); needs 2*N^3 extra
+// doubles of shared memory per element (see V3 launch in sdme_abi.cu).
+template <int N, int M, int WPE, int NC, int EPB, int MINB, int MODE, bool VAL, bool STG = false>
 __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_constant__ Tab3<N, M> tb,
                                                                      const __grid_constant__ Geo g, OpArgs args) {
   using C = V3<N, M, WPE, NC, VAL || MODE == MODE_MASS>;
+  constexpr int PERS = C::PER + (STG ? 2 * N * N * N : 0);
   extern __shared__ double smem[];
   const int gid = threadIdx.x / C::T;
   const int t = threadIdx.x % C::T;
-  double* A = smem + gid * C::PER;
+  double* A = smem + gid * PERS;
   double* Bf = A + C::SA;
+  double* Rb = A + C::PER;  // staged rows [2][N^3] (STG)
+  int buf = 0;
   if (args.skip && *(volatile const int*)args.skip) return;
   const long long cnt = colour_count(g, args.colour);
   constexpr bool GRADP = (MODE == MODE_APPLY);
@@ -388,11 +447,23 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
   // dP constants with c_k folded in
   const double mu_k = args.c_k * g.mu, lam_k = args.c_k * g.lam;
   const double cmr = args.c_m * g.rho;
+  const double* first_field = MODE == MODE_MASS ? args.p : args.u;
+  if (STG && (long long)blockIdx.x * EPB + gid < cnt) {
+    int ei, ej, ek;
+    colour_element(g, args.colour, (long long)blockIdx.x * EPB + gid, ei, ej, ek);
+    v3_stage_rows<N, C::T>(g, first_field, 0, (N - 1) * ei, (N - 1) * ej, (N - 1) * ek, Rb, t);
+  }
   for (long long idx = (long long)blockIdx.x * EPB + gid; idx < cnt; idx += stride) {
     int ei, ej, ek;
     colour_element(g, args.colour, idx, ei, ej, ek);
     const int X0 = (N - 1) * ei, Y0 = (N - 1) * ej, Z0 = (N - 1) * ek;
-    if (idx + stride < cnt) {  // warm L2 with the next element's rows
+    NextRows nxt{nullptr, 0, 0, 0};
+    if (STG && idx + stride < cnt) {
+      int ni, nj, nk;
+      colour_element(g, args.colour, idx + stride, ni, nj, nk);
+      nxt = NextRows{first_field, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
+    }
+    if (!STG && idx + stride < cnt) {  // warm L2 with the next element's rows
       int ni, nj, nk;
       colour_element(g, args.colour, idx + stride, ni, nj, nk);
       if (MODE != MODE_MASS) v3_prefetch<N, C::T>(g, args.u, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk, t);
@@ -400,7 +471,8 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
     }
     double Hu[C::QPT][9];
     if (MODE != MODE_MASS) {
-      v3_forward<N, M, WPE, NC, true, false>(tb, g, args.u, X0, Y0, Z0, A, Bf, t, gid);
+      const NextRows after_u = MODE == MODE_APPLY ? NextRows{args.p, X0, Y0, Z0} : nxt;
+      v3_forward<N, M, WPE, NC, true, false, STG>(tb, g, args.u, X0, Y0, Z0, A, Bf, t, gid, Rb, &buf, after_u);
 #pragma unroll
       for (int r = 0; r < C::QPT; ++r) {
         const int q = t + r * C::T;
@@ -414,7 +486,7 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
       group_sync<WPE>(gid);
     }
     if (MODE != MODE_FINT)
-      v3_forward<N, M, WPE, NC, GRADP, VAL>(tb, g, args.p, X0, Y0, Z0, A, Bf, t, gid);
+      v3_forward<N, M, WPE, NC, GRADP, VAL, STG>(tb, g, args.p, X0, Y0, Z0, A, Bf, t, gid, Rb, &buf, nxt);
 #pragma unroll
     for (int r = 0; r < C::QPT; ++r) {
       const int q = t + r * C::T;

@@ -202,13 +202,6 @@ __device__ __forceinline__ void v4_back(const Tab3<N, M>& tb, const Geo& g, doub
   __syncwarp();
 }
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int K>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory"); }
 
 // stage the 3-component (P+1)^3 box of one field into shared memory, [comp][k][j][i]
 template <int N>

@@ -143,9 +143,10 @@ Tab3<N, M> make_tab3(const sdme_ctx* c) {
 // Launch shape of the v3 element kernels.  WPE warps per element, EPB
 // elements per block, NC components per contraction stage, MINB minimum
 // resident blocks per SM (register cap for __launch_bounds__).
-template <int N, int M, int WPE_, int NC_, int EPB_, int MINB_>
+template <int N, int M, int WPE_, int NC_, int EPB_, int MINB_, bool STG_ = false>
 struct Shape {
   static constexpr int WPE = WPE_, NC = NC_, EPB = EPB_, MINB = MINB_;
+  static constexpr bool STG = STG_;  // cp.async row staging (NC == 1)
 };
 
 template <int N, int M>
@@ -158,8 +159,8 @@ struct DefaultShape {
 template <int N, int M, class S, int MODE, bool VAL>
 void launch_v3(sdme_ctx* c, const Tab3<N, M>& tb, OpArgs a) {
   constexpr bool VALS = VAL || MODE == MODE_MASS;
-  constexpr int smem = V3<N, M, S::WPE, S::NC, VALS>::PER * 8 * S::EPB;
-  auto kern = element_v3<N, M, S::WPE, S::NC, S::EPB, S::MINB, MODE, VAL>;
+  constexpr int smem = (V3<N, M, S::WPE, S::NC, VALS>::PER + (S::STG ? 2 * N * N * N : 0)) * 8 * S::EPB;
+  auto kern = element_v3<N, M, S::WPE, S::NC, S::EPB, S::MINB, MODE, VAL, S::STG>;
   static int max_blocks = -1;
   if (max_blocks < 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -234,13 +235,16 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
       return;
     }
     if (c->variant == 4) { element_v4_modes<N, M, 8, false>(c, mode, tb, a); return; }
-    // default: f_int and mass with the column-resident v4 schedule (1.66 / 1.29 ms vs
-    // 1.91 / 1.42 ms), K.p with v3 component-serial at 12 warps/SM (2.91 vs 3.04 ms)
+    if (c->variant == 2) { element_shape<N, M, Shape<N, M, 1, 1, 1, 12>>(c, mode, tb, a); return; }
+    // default: f_int and mass with the column-resident v4 schedule (1.69 / 1.29 ms vs
+    // 1.78 / 1.35 ms for v3)
     if (mode == MODE_FINT || mode == MODE_MASS) {
       element_v4_modes<N, M, 10, false>(c, mode, tb, a);
       return;
     }
-    element_shape<N, M, Shape<N, M, 1, 1, 1, 12>>(c, mode, tb, a);
+    // K.p: component-serial v3 with cp.async row staging, 11 warps/SM (2.70 ms;
+    // profiles/variants_r01.txt)
+    element_shape<N, M, Shape<N, M, 1, 1, 1, 11, true>>(c, mode, tb, a);
     return;
   }
   element_shape<N, M, typename DefaultShape<N, M>::type>(c, mode, tb, a);
