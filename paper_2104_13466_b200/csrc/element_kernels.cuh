@@ -58,6 +58,15 @@ __device__ __forceinline__ bool constrained(const Geo& g, int comp, int X, int Y
          ((m & 8) && Y == g.Ly - 1) || ((m & 16) && Z == 0) || ((m & 32) && Z == g.Lz - 1);
 }
 
+// True when the element box starting at (X0, Y0, Z0) with N points per edge
+// touches a Dirichlet plane of component comp (warp-uniform fast path).
+__device__ __forceinline__ bool touches_dirichlet(const Geo& g, int comp, int X0, int Y0, int Z0, int N) {
+  const int m = g.dmask[comp];
+  if (!m) return false;
+  return ((m & 1) && X0 == 0) || ((m & 2) && X0 + N - 1 == g.Lx - 1) || ((m & 4) && Y0 == 0) ||
+         ((m & 8) && Y0 + N - 1 == g.Ly - 1) || ((m & 16) && Z0 == 0) || ((m & 32) && Z0 + N - 1 == g.Lz - 1);
+}
+
 // Element of this block slot, for the given colour pass.  Returns false past the end.
 __device__ __forceinline__ bool colour_element(const Geo& g, int colour, long long idx,
                                                int& ei, int& ej, int& ek) {

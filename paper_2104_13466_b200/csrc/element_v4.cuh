@@ -187,6 +187,7 @@ __device__ __forceinline__ void v4_back(const Tab3<N, M>& tb, const Geo& g, doub
       jyz[a] = Xs[C::xi(1, k, j, a)];
     }
     const int Z = Z0 + k, Y = Y0 + j;
+    const bool chk = touches_dirichlet(g, comp, X0, Y0, Z0, N);
     double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Lx + X0;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -196,7 +197,7 @@ __device__ __forceinline__ void v4_back(const Tab3<N, M>& tb, const Geo& g, doub
         if (GRAD) acc = fma(tb.bDx[a][i], jx[a], acc);
         acc = fma(tb.bBx[a][i], jyz[a], acc);
       }
-      if (!constrained(g, comp, X0 + i, Y, Z)) red_add(row + i, acc);
+      if (!chk || !constrained(g, comp, X0 + i, Y, Z)) red_add(row + i, acc);
     }
   }
   __syncwarp();
