@@ -307,8 +307,16 @@ def run_ours(args):
     peaks = measured_peaks()
     fp64_peak = peaks.get("fp64_tflops")
     achieved = flops / t_step / 1e12
+    traffic = None
+    try:  # DRAM bytes of one K.p (8 colour launches) from the committed ncu capture
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")))
+        traffic = tr["kp"]["traffic_bytes"]
+    except Exception:
+        pass
     roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-            "frac": achieved / fp64_peak if fp64_peak else None, "traffic": None,
+            "frac": achieved / fp64_peak if fp64_peak else None, "traffic": traffic,
+            "traffic_note": "dram read+write bytes per K.p (8 launches), profiles/ncu_traffic_r01.json; "
+                            "algorithmic bytes = algorithmic_bytes_per_step",
             "peak_source": "profiles/fp64_peak.json (measured DFMA chain on this pool's B200)",
             "hbm": {"achieved_gbs": bytes_alg / t_step / 1e9, "peak_gbs": peaks.get("hbm_gbs"),
                     "frac": bytes_alg / t_step / 1e9 / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None},
