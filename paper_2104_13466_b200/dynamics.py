@@ -247,13 +247,23 @@ def _mul(pb, out, a, b):
 
 def explicit_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int, u0=None, v0=None,
                  cfg: SolverConfig | None = None, snapshot_stride: int = 0, contact=None,
-                 record_every: int = 0) -> Trajectory:
-    """Central difference with lumped mass (+ penalty contact) on the GPU.
+                 record_every: int = 0, mass: str = "lumped") -> Trajectory:
+    """Central difference on the GPU.
 
+    ``mass="lumped"`` (default): row-sum lumped mass with optional
+    penalty contact.  ``mass="consistent"``: the reference's own
+    scheme (``dynamics.py:130-170``) -- each step solves (M/dt^2) w = psi with
+    matrix-free Jacobi-PCG (``cfg``, full system) and records SolveStats.
     ``external_load`` may be None (no load), a :class:`ScaledLoad`, or any
-    callable of t returning a free vector.  Startup a0 = M_L^-1 psi0,
+    callable of t returning a free vector.  Startup a0 = M^-1 psi0,
     u_-1 = u0 - dt v0 + dt^2/2 a0 (``dynamics.py:152-155``).
     """
+    if mass == "consistent":
+        if contact is not None:
+            raise NotImplementedError("contact with the consistent-mass explicit scheme")
+        return _explicit_consistent(problem, external_load, dt, n_steps, u0, v0, cfg, snapshot_stride)
+    if mass != "lumped":
+        raise ValueError(f"unknown mass treatment {mass!r}")
     pb = problem
     u = _dev(pb, u0)
     v = _dev(pb, v0)
@@ -297,4 +307,46 @@ def explicit_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
     traj.state = TimeState(t, u.free(), v.free(), a0.free(), u_prev.free())
     if contact is not None:
         traj.contact_history = list(contact.history)
+    return traj
+
+
+def _explicit_consistent(pb: GpuFemProblem, external_load, dt, n_steps, u0, v0, cfg, snapshot_stride):
+    """``explicit_run`` of the reference with a full (uncondensed) Jacobi-PCG
+    mass solve per step (``dynamics.py:147-170``)."""
+    cfg = cfg or SolverConfig(precond="diagonal", tol=1e-12, condense=False)
+    cfg.validate()
+    u = _dev(pb, u0)
+    v = _dev(pb, v0)
+    traj = Trajectory()
+    load = _Load(pb, external_load) if external_load is not None else None
+    fint, psi, a, w, un, up = (DeviceVector(pb) for _ in range(6))
+
+    def residual(t):
+        pb.fint_(u, fint)
+        if load is not None:
+            psi.assign(1.0, load.at(t), -1.0, fint)
+        else:
+            psi.assign(-1.0, fint)
+        return psi
+
+    _, st = pcg_gpu(pb, None, residual(0.0), c_m=1.0, precond=cfg.precond, tol=cfg.tol, maxit=cfg.maxit,
+                    c_k=0.0, x=a)
+    traj.stats.add(-1, 0, "explicit-init", st)
+    up.assign(1.0, u, -dt, v, 0.5 * dt * dt, a)
+    t = 0.0
+    inv_dt2 = 1.0 / dt ** 2
+    for step in range(n_steps):
+        _, st = pcg_gpu(pb, None, residual(t), c_m=inv_dt2, precond=cfg.precond, tol=cfg.tol,
+                        maxit=cfg.maxit, c_k=0.0, x=w)
+        traj.stats.add(step, 0, "explicit", st)
+        un.assign(2.0, u, -1.0, up, 1.0, w)        # (2u - u_prev) + w
+        v.assign(1.0, un, -1.0, up)                # (u_next - u_prev) ...
+        v.assign(1.0 / (2.0 * dt), v)              # ... / (2 dt)
+        up.copy_from(u)
+        u.copy_from(un)
+        t += dt
+        if snapshot_stride and (step + 1) % snapshot_stride == 0:
+            traj.times.append(t)
+            traj.snapshots.append(u.free())
+    traj.state = TimeState(t, u.free(), v.free(), a.free(), up.free())
     return traj

@@ -202,10 +202,30 @@ def gen_contact():
     np.savez_compressed(os.path.join(HERE, "contact.npz"), **out)
 
 
+def gen_explicit():
+    """Reference explicit_run (consistent mass, Jacobi-PCG, condense=False):
+    the SURVEY F2 row, pinned against the reference's own explicit path."""
+    from sdmefem.dynamics import explicit_run
+
+    P = 3
+    prob = problem("SDME_M", P, (3, 2, 2), (1.0, 0.5, 0.5), P + 1, [("xmin", (0, 1, 2))])
+    faces = build_face_tables(prob.mesh, prob.element, "xmax", prob.rule)
+    base = prob.traction_vector(faces, lambda f: np.tile([0.0, 0.0, 2.0e4], (len(f.pts), 1)))
+    load = lambda t: base * min(t / 5e-5, 1.0)
+    cfg = SolverConfig(precond="diagonal", tol=1e-12, maxit=100000, condense=False)
+    dt, n_steps = 1e-5, 20
+    traj = explicit_run(prob, load, dt, n_steps, cfg=cfg)
+    rows = [(r["step"], r["iterations"]) for r in traj.stats.rows]
+    np.savez_compressed(os.path.join(HERE, "explicit.npz"), u=traj.state.u, v=traj.state.v,
+                        u_prev=traj.state.u_prev, load=base, dt=np.array(dt), steps=np.array(n_steps),
+                        pcg_rows=np.array(rows))
+    print("explicit", [r[1] for r in rows][:6])
+
+
 if __name__ == "__main__":
     import sys
 
-    which = sys.argv[1:] or ["basis", "elements", "global", "contact", "config1"]
+    which = sys.argv[1:] or ["basis", "elements", "global", "contact", "explicit", "config1"]
     for w in which:
         t = time.perf_counter()
         globals()["gen_" + w]()

@@ -212,3 +212,20 @@ def test_config2_properties_full_size():
     pb.apply_(u, p, t1)
     t1.assign(1.0, t1, -1.0, kp)
     assert t1.norm() == 0.0
+
+
+def test_explicit_consistent_mass_vs_reference():
+    """the reference's own explicit_run (consistent mass, full
+    Jacobi-PCG) -- per-step PCG counts +-1, final u, v within 1e-9."""
+    g = load_golden("explicit")
+    pb = gpu_problem("SDME_M", 3, 4, (3, 2, 2), (1.0, 0.5, 0.5), [("xmin", (0, 1, 2))])
+    base = pb.traction_vector("xmax", [0.0, 0.0, 2.0e4])
+    assert max_rel_err(base, g["load"]) <= TOL
+    cfg = SolverConfig(precond="diagonal", tol=1e-12, maxit=100000, condense=False)
+    traj = explicit_run(pb, ScaledLoad(base, lambda t: min(t / 5e-5, 1.0)), float(g["dt"]), int(g["steps"]),
+                        cfg=cfg, mass="consistent")
+    ref = [int(r[1]) for r in g["pcg_rows"]]
+    got = [r["iterations"] for r in traj.stats.rows]
+    assert len(ref) == len(got) and max(abs(a - b) for a, b in zip(ref, got)) <= 1
+    assert max_rel_err(traj.state.u, g["u"]) <= 1e-9
+    assert max_rel_err(traj.state.v, g["v"]) <= 1e-9
