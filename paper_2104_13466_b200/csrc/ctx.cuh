@@ -1,0 +1,63 @@
+// Internal: the context object shared by the C-ABI translation unit and the
+// per-order operator translation units (ops.cu, compiled once per P).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "element_kernels.cuh"
+
+struct sdme_ctx;
+
+// Operator entry points of one (P, m) instantiation.
+struct SdmeOps {
+  void (*element)(sdme_ctx*, int mode, const double* u, const double* p, double* y, double ck, double cm);
+  void (*diag)(sdme_ctx*, const double* u, double* d, double ck, double cm);
+};
+
+struct sdme_ctx {
+  int P = 0, m = 0, n = 0;
+  sdme::Geo geo{};
+  double h[3]{}, origin[3]{};
+  std::vector<double> Bl, Dl, w;  // lattice-local order, m x n
+  cudaStream_t st = nullptr;
+  long long nvec = 0;             // 3 * Ns
+  std::vector<double*> vecs;
+  int* d_perm = nullptr;
+  int64_t n_free = 0;
+  unsigned char* d_free = nullptr;  // 1 on free lattice dofs
+  double* d_fbuf = nullptr;         // staging for free-order vectors
+  double* d_partial = nullptr;
+  double* d_scal = nullptr;
+  double* h_scal = nullptr;         // pinned
+  unsigned long long* d_flag = nullptr;
+  unsigned long long* h_flag = nullptr;
+  double* d_gaps = nullptr;
+  long long gaps_cap = 0;
+  double* h_gaps = nullptr;
+  // PCG scratch vectors (lazily allocated ids)
+  int v_r = -1, v_p = -1, v_ap = -1, v_dinv = -1, v_tmp = -1;
+  const SdmeOps* ops = nullptr;
+  int err_code = 0;
+  int64_t err_elem = -1;
+  int err_qp = -1;
+  std::string err_msg;
+  int64_t launches = 0;
+  int variant = 0;  // schedule variant (SDME_VARIANT env), tuning only
+  int mir = -1;     // mirror structure of the 1D tables: 0 nodal, 1 modal/SDME, -1 none (no even-odd)
+  int* d_status = nullptr;  // PCG status word (device) and its pinned mirror
+  int* h_status = nullptr;
+  const int* cur_skip = nullptr;  // element kernels exit early when *cur_skip != 0 (PCG graph)
+};
+
+// per-order operator tables (ops.cu, one object file per P)
+const SdmeOps* sdme_ops_p1(int m);
+const SdmeOps* sdme_ops_p2(int m);
+const SdmeOps* sdme_ops_p3(int m);
+const SdmeOps* sdme_ops_p4(int m);
+const SdmeOps* sdme_ops_p5(int m);
+const SdmeOps* sdme_ops_p6(int m);
+const SdmeOps* sdme_ops_p7(int m);
+const SdmeOps* sdme_ops_p8(int m);

@@ -1,0 +1,242 @@
+// Even-odd (eo.cuh) overloads of the v3 contraction stages, component-serial
+// (NC = 1).  Selected by passing a TabEO table to element_v3; the schedule,
+// shared layouts, staging and point work are the v3 ones -- only the 1D
+// contractions change (about half the multiply-adds).
+#pragma once
+#include "element_v3.cuh"
+#include "eo.cuh"
+
+namespace sdme {
+
+template <int N, int M, int WPE, int NC, bool GRAD, bool VAL, bool STAGED = false, int MIR>
+__device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo& g, const double* __restrict__ src,
+                                           int X0, int Y0, int Z0, double* A, double* B, int t, int gid,
+                                           double* R = nullptr, int* buf = nullptr, NextRows next = {}) {
+  static_assert(NC == 1, "even-odd stages are component-serial");
+  using C = V3<N, M, WPE, 1>;
+  using Mr = Mir<N, MIR>;
+  constexpr int NE = Mr::NE > 0 ? Mr::NE : 1, NO = Mr::NO > 0 ? Mr::NO : 1;
+  double* const P = A;
+#pragma unroll 1
+  for (int comp = 0; comp < 3; ++comp) {
+    double* const X = B + C::YO;
+    if (STAGED) {
+      double* nb = R + (*buf ^ 1) * N * N * N;
+      if (comp + 1 < 3) {
+        v3_stage_rows<N, C::T>(g, src, comp + 1, X0, Y0, Z0, nb, t);
+        cp_async_wait<1>();
+      } else if (next.field) {
+        v3_stage_rows<N, C::T>(g, next.field, 0, next.X0, next.Y0, next.Z0, nb, t);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      group_sync<WPE>(gid);
+    }
+    // x stage: item (k, j)
+    for (int w = t; w < N * N; w += C::T) {
+      int ck, j;
+      C::item_x(w, ck, j);
+      const int k = ck;
+      double v[N];
+      if (STAGED) {
+        const double* row = R + *buf * N * N * N + (k * N + j) * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] = row[i];
+      } else {
+        const double* row = src + comp * g.Ns + ((long long)(Z0 + k) * g.Ly + (Y0 + j)) * g.Lx + X0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] = __ldg(row + i);
+      }
+      double E[NE], O[NO], o0[M], o1[M];
+      eo_split<N, MIR>(v, E, O);
+      eo_fwd<M, Mr::NE, Mr::NO>(tb.B, E, O, o0);
+      if (GRAD) eo_fwd<M, Mr::NO, Mr::NE>(tb.Dx, O, E, o1);
+#pragma unroll
+      for (int a = 0; a < M; ++a) {
+        X[C::xi(0, ck, j, a)] = o0[a];
+        if (GRAD) X[C::xi(1, ck, j, a)] = o1[a];
+      }
+    }
+    group_sync<WPE>(gid);
+    // y stage: item (k, a)
+    for (int w = t; w < N * M; w += C::T) {
+      int ck, a;
+      C::item_y(w, ck, a);
+      const int k = ck;
+      double x0[N], x1[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        x0[j] = X[C::xi(0, ck, j, a)];
+        if (GRAD) x1[j] = X[C::xi(1, ck, j, a)];
+      }
+      double E0[NE], O0[NO], bb[M], db[M], bd[M];
+      eo_split<N, MIR>(x0, E0, O0);
+      eo_fwd<M, Mr::NE, Mr::NO>(tb.B, E0, O0, bb);
+      if (GRAD) {
+        double E1[NE], O1[NO];
+        eo_split<N, MIR>(x1, E1, O1);
+        eo_fwd<M, Mr::NO, Mr::NE>(tb.Dy, O0, E0, db);
+        eo_fwd<M, Mr::NE, Mr::NO>(tb.B, E1, O1, bd);
+      }
+#pragma unroll
+      for (int b = 0; b < M; ++b) {
+        B[C::yi(0, 0, k, b * M + a)] = bb[b];
+        if (GRAD) {
+          B[C::yi(0, 1, k, b * M + a)] = db[b];
+          B[C::yi(0, 2, k, b * M + a)] = bd[b];
+        }
+      }
+    }
+    group_sync<WPE>(gid);
+    // z stage: item (b, a) -> points
+    for (int ba = t; ba < M * M; ba += C::T) {
+      double y0[N], y1[N], y2[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        y0[k] = B[C::yi(0, 0, k, ba)];
+        if (GRAD) {
+          y1[k] = B[C::yi(0, 1, k, ba)];
+          y2[k] = B[C::yi(0, 2, k, ba)];
+        }
+      }
+      double E0[NE], O0[NO];
+      eo_split<N, MIR>(y0, E0, O0);
+      if (GRAD) {
+        double E1[NE], O1[NO], E2[NE], O2[NO], gx[M], gy[M], gz[M];
+        eo_split<N, MIR>(y1, E1, O1);
+        eo_split<N, MIR>(y2, E2, O2);
+        eo_fwd<M, Mr::NE, Mr::NO>(tb.B, E2, O2, gx);
+        eo_fwd<M, Mr::NE, Mr::NO>(tb.B, E1, O1, gy);
+        eo_fwd<M, Mr::NO, Mr::NE>(tb.Dz, O0, E0, gz);
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          const int q = c * M * M + ba;
+          P[C::qi(0, comp, q)] = gx[c];
+          P[C::qi(1, comp, q)] = gy[c];
+          P[C::qi(2, comp, q)] = gz[c];
+        }
+      }
+      if (VAL) {
+        double vv[M];
+        eo_fwd<M, Mr::NE, Mr::NO>(tb.B, E0, O0, vv);
+#pragma unroll
+        for (int c = 0; c < M; ++c) P[C::qi(3, comp, c * M * M + ba)] = vv[c];
+      }
+    }
+    if (STAGED) *buf ^= 1;
+    group_sync<WPE>(gid);
+  }
+}
+
+template <int N, int M, int WPE, int NC, bool GRAD, bool VAL, int MIR>
+__device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Geo& g, double* __restrict__ dst,
+                                            int X0, int Y0, int Z0, double* A, double* B, int t, int gid) {
+  static_assert(NC == 1, "even-odd stages are component-serial");
+  using C = V3<N, M, WPE, 1>;
+  using Mr = Mir<N, MIR>;
+  constexpr int HP = Half<M>::HP, H = Half<M>::H > 0 ? Half<M>::H : 1;
+#pragma unroll 1
+  for (int comp = 0; comp < 3; ++comp) {
+    double* const X = B + C::YO;
+    // z' stage: item (b, a), contract over c
+    for (int ba = t; ba < M * M; ba += C::T) {
+      double hx[N], hy[N], hz[N];
+      if (GRAD) {
+        double q[M], qe[HP], qo[H];
+#pragma unroll
+        for (int c = 0; c < M; ++c) q[c] = A[C::qi(0, comp, c * M * M + ba)];
+        eo_qsplit<M>(q, qe, qo);
+        eo_bwd<N, M, MIR, 1, Mr::NE, Mr::NO, false>(tb.bBz, qe, qo, hx);
+#pragma unroll
+        for (int c = 0; c < M; ++c) q[c] = A[C::qi(1, comp, c * M * M + ba)];
+        eo_qsplit<M>(q, qe, qo);
+        eo_bwd<N, M, MIR, 1, Mr::NE, Mr::NO, false>(tb.bBz, qe, qo, hy);
+#pragma unroll
+        for (int c = 0; c < M; ++c) q[c] = A[C::qi(2, comp, c * M * M + ba)];
+        eo_qsplit<M>(q, qe, qo);
+        eo_bwd<N, M, MIR, -1, Mr::NO, Mr::NE, false>(tb.bDz, qe, qo, hz);
+      }
+      if (VAL) {
+        double q[M], qe[HP], qo[H];
+#pragma unroll
+        for (int c = 0; c < M; ++c) q[c] = A[C::qi(3, comp, c * M * M + ba)];
+        eo_qsplit<M>(q, qe, qo);
+        if (GRAD)
+          eo_bwd<N, M, MIR, 1, Mr::NE, Mr::NO, true>(tb.bBz, qe, qo, hz);
+        else
+          eo_bwd<N, M, MIR, 1, Mr::NE, Mr::NO, false>(tb.bBz, qe, qo, hz);
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        if (GRAD) {
+          B[C::yi(0, 0, k, ba)] = hx[k];
+          B[C::yi(0, 1, k, ba)] = hy[k];
+        }
+        B[C::yi(0, 2, k, ba)] = hz[k];
+      }
+    }
+    group_sync<WPE>(gid);
+    // y' stage: item (k, a), contract over b
+    for (int w = t; w < N * M; w += C::T) {
+      int ck, a;
+      C::item_y(w, ck, a);
+      const int k = ck;
+      double jx[N], jyz[N];
+      double q[M], qe[HP], qo[H];
+      if (GRAD) {
+#pragma unroll
+        for (int b = 0; b < M; ++b) q[b] = B[C::yi(0, 0, k, b * M + a)];
+        eo_qsplit<M>(q, qe, qo);
+        eo_bwd<N, M, MIR, 1, Mr::NE, Mr::NO, false>(tb.bBy, qe, qo, jx);
+#pragma unroll
+        for (int b = 0; b < M; ++b) q[b] = B[C::yi(0, 1, k, b * M + a)];
+        eo_qsplit<M>(q, qe, qo);
+        eo_bwd<N, M, MIR, -1, Mr::NO, Mr::NE, false>(tb.bDy, qe, qo, jyz);
+      }
+#pragma unroll
+      for (int b = 0; b < M; ++b) q[b] = B[C::yi(0, 2, k, b * M + a)];
+      eo_qsplit<M>(q, qe, qo);
+      if (GRAD)
+        eo_bwd<N, M, MIR, 1, Mr::NE, Mr::NO, true>(tb.bBy, qe, qo, jyz);
+      else
+        eo_bwd<N, M, MIR, 1, Mr::NE, Mr::NO, false>(tb.bBy, qe, qo, jyz);
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        if (GRAD) X[C::xi(0, ck, j, a)] = jx[j];
+        X[C::xi(1, ck, j, a)] = jyz[j];
+      }
+    }
+    group_sync<WPE>(gid);
+    // x' stage: item (k, j), contract over a, RED into the lattice
+    for (int w = t; w < N * N; w += C::T) {
+      int ck, j;
+      C::item_x(w, ck, j);
+      const int k = ck;
+      double acc[N];
+      double q[M], qe[HP], qo[H];
+      if (GRAD) {
+#pragma unroll
+        for (int a = 0; a < M; ++a) q[a] = X[C::xi(0, ck, j, a)];
+        eo_qsplit<M>(q, qe, qo);
+        eo_bwd<N, M, MIR, -1, Mr::NO, Mr::NE, false>(tb.bDx, qe, qo, acc);
+      }
+#pragma unroll
+      for (int a = 0; a < M; ++a) q[a] = X[C::xi(1, ck, j, a)];
+      eo_qsplit<M>(q, qe, qo);
+      if (GRAD)
+        eo_bwd<N, M, MIR, 1, Mr::NE, Mr::NO, true>(tb.bBx, qe, qo, acc);
+      else
+        eo_bwd<N, M, MIR, 1, Mr::NE, Mr::NO, false>(tb.bBx, qe, qo, acc);
+      const int Z = Z0 + k, Y = Y0 + j;
+      const bool chk = touches_dirichlet(g, comp, X0, Y0, Z0, N);
+      double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Lx + X0;
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+        if (!chk || !constrained(g, comp, X0 + i, Y, Z)) red_add(row + i, acc[i]);
+    }
+    group_sync<WPE>(gid);
+  }
+}
+
+}  // namespace sdme

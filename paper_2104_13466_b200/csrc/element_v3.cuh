@@ -429,8 +429,10 @@ __device__ __forceinline__ void qp_k(const double (&H)[9], QpK& s) {
 
 // STG: cp.async double-buffered row staging (NC == 1); needs 2*N^3 extra
 // doubles of shared memory per element (see V3 launch in sdme_abi.cu).
-template <int N, int M, int WPE, int NC, int EPB, int MINB, int MODE, bool VAL, bool STG = false>
-__global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_constant__ Tab3<N, M> tb,
+// TB: Tab3 (plain contractions) or TabEO (even-odd, element_eo.cuh).
+template <int N, int M, int WPE, int NC, int EPB, int MINB, int MODE, bool VAL, bool STG = false,
+          class TB = Tab3<N, M>>
+__global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_constant__ TB tb,
                                                                      const __grid_constant__ Geo g, OpArgs args) {
   using C = V3<N, M, WPE, NC, VAL || MODE == MODE_MASS>;
   constexpr int PERS = C::PER + (STG ? 2 * N * N * N : 0);

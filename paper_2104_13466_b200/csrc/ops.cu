@@ -1,0 +1,317 @@
+// Operator dispatch and launch shapes for one polynomial order P (compiled
+// once per P with -DSDME_ORDER=P by build.py, in parallel): element kernels
+// (f_int, K.p, mass) and the Jacobi diagonal for m in {P+1, P+2}.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "ctx.cuh"
+#include "element_eo.cuh"
+#include "element_kernels.cuh"
+#include "element_v3.cuh"
+#include "element_v4.cuh"
+
+#ifndef SDME_ORDER
+#error "compile with -DSDME_ORDER=P"
+#endif
+
+using namespace sdme;
+using Ops = SdmeOps;
+
+namespace {
+
+template <int N, int M>
+struct Conf {
+  static constexpr int bytes = Smem<N, M>::per_elem * 8;
+  static constexpr int EB = bytes > 100000 ? 1 : (100000 / bytes > 8 ? 8 : 100000 / bytes);
+};
+
+template <int N, int M>
+Tab<N, M> make_tab(const sdme_ctx* c) {
+  Tab<N, M> t;
+  for (int a = 0; a < M; ++a) {
+    for (int l = 0; l < N; ++l) {
+      t.B[a][l] = c->Bl[a * N + l];
+      t.D[a][l] = c->Dl[a * N + l];
+    }
+    t.W[a] = c->w[a];
+  }
+  return t;
+}
+
+// v3 tables: weights, det J and dxi/dX folded per axis (element_v3.cuh)
+template <int N, int M>
+Tab3<N, M> make_tab3(const sdme_ctx* c) {
+  Tab3<N, M> t;
+  const Geo& g = c->geo;
+  for (int a = 0; a < M; ++a) {
+    const double w = c->w[a];
+    for (int l = 0; l < N; ++l) {
+      const double b = c->Bl[a * N + l], d = c->Dl[a * N + l];
+      t.B[a][l] = b;
+      t.Dx[a][l] = d * g.s[0];
+      t.Dy[a][l] = d * g.s[1];
+      t.Dz[a][l] = d * g.s[2];
+      t.bBx[a][l] = b * w;
+      t.bDx[a][l] = d * w * g.s[0];
+      t.bBy[a][l] = b * w;
+      t.bDy[a][l] = d * w * g.s[1];
+      t.bBz[a][l] = b * w * g.detJ;
+      t.bDz[a][l] = d * w * g.s[2] * g.detJ;
+    }
+  }
+  return t;
+}
+
+// Launch shape of the v3 element kernels.  WPE warps per element, EPB
+// elements per block, NC components per contraction stage, MINB minimum
+// resident blocks per SM (register cap for __launch_bounds__).
+template <int N, int M, int WPE_, int NC_, int EPB_, int MINB_, bool STG_ = false>
+struct Shape {
+  static constexpr int WPE = WPE_, NC = NC_, EPB = EPB_, MINB = MINB_;
+  static constexpr bool STG = STG_;  // cp.async row staging (NC == 1)
+};
+
+template <int N, int M>
+struct DefaultShape {
+  static constexpr int bytes = V3<N, M, 1, 3>::PER * 8;
+  static constexpr int WPE = bytes <= 40960 ? 1 : (bytes <= 65536 ? 4 : 8);
+  using type = Shape<N, M, WPE, 3, (WPE == 1 ? 2 : 1), 1>;
+};
+
+template <int N, int M, class S, int MODE, bool VAL, class TB = Tab3<N, M>>
+void launch_v3(sdme_ctx* c, const TB& tb, OpArgs a) {
+  constexpr bool VALS = VAL || MODE == MODE_MASS;
+  constexpr int smem = (V3<N, M, S::WPE, S::NC, VALS>::PER + (S::STG ? 2 * N * N * N : 0)) * 8 * S::EPB;
+  auto kern = element_v3<N, M, S::WPE, S::NC, S::EPB, S::MINB, MODE, VAL, S::STG, TB>;
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, S::EPB * S::WPE * 32, smem);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    max_blocks = std::max(1, nb) * sms;
+  }
+  for (int col = 0; col < 8; ++col) {
+    const long long cnt = colour_count(c->geo, col);
+    if (cnt == 0) continue;
+    a.colour = col;
+    const long long need = (cnt + S::EPB - 1) / S::EPB;
+    const unsigned grid = (unsigned)std::min<long long>(need, max_blocks);
+    kern<<<grid, S::EPB * S::WPE * 32, smem, c->st>>>(tb, c->geo, a);
+    ++c->launches;
+  }
+}
+
+template <int N, int M, class S, class TB = Tab3<N, M>>
+void element_shape(sdme_ctx* c, int mode, const TB& tb, OpArgs a) {
+  if (mode == MODE_FINT) launch_v3<N, M, S, MODE_FINT, false, TB>(c, tb, a);
+  else if (mode == MODE_APPLY && a.c_m != 0.0) launch_v3<N, M, S, MODE_APPLY, true, TB>(c, tb, a);
+  else if (mode == MODE_APPLY) launch_v3<N, M, S, MODE_APPLY, false, TB>(c, tb, a);
+  else launch_v3<N, M, S, MODE_MASS, true, TB>(c, tb, a);
+}
+
+// Even-odd tables (eo.cuh) from the lattice-order 1D tables, with the same
+// folding of weights, det J and 2/h as make_tab3.
+template <int N, int M, int MIR>
+TabEO<N, M, MIR> make_tabeo(const sdme_ctx* c) {
+  using Mr = Mir<N, MIR>;
+  constexpr int H = M / 2, HP = (M + 1) / 2;
+  const Geo& g = c->geo;
+  double Bv[M][N], Dv[3][M][N], bB[3][M][N], bD[3][M][N];
+  for (int a = 0; a < M; ++a)
+    for (int l = 0; l < N; ++l) {
+      const double b = c->Bl[a * N + l], d = c->Dl[a * N + l], w = c->w[a];
+      Bv[a][l] = b;
+      for (int ax = 0; ax < 3; ++ax) {
+        const double jz = ax == 2 ? g.detJ : 1.0;
+        Dv[ax][a][l] = d * g.s[ax];
+        bB[ax][a][l] = b * w * jz;
+        bD[ax][a][l] = d * w * g.s[ax] * jz;
+      }
+    }
+  // column / row sets of a type-F operator: pairs first, then the fixed points
+  // whose sign (F * s) is + (even set) or - (odd set)
+  auto set_of = [](int F, bool even, int idx) {
+    if (idx < Mr::NP) return Mr::nth(0, idx);
+    const int kind = (F > 0) == even ? 1 : 2;
+    return Mr::nth(kind, idx - Mr::NP);
+  };
+  auto fwd = [&](auto& dst, const double (&T)[M][N], int F) {
+    constexpr int WS = sizeof(dst.S[0]) / sizeof(double), WT = sizeof(dst.T[0]) / sizeof(double);
+    const int nS = F > 0 ? Mr::NE : Mr::NO, nT = F > 0 ? Mr::NO : Mr::NE;
+    for (int a = 0; a < HP; ++a)
+      for (int e = 0; e < WS; ++e) {
+        double v = 0.0;
+        if (e < nS) {
+          const int l = set_of(F, true, e), r = Mr::sig(l);
+          v = e < Mr::NP ? 0.5 * (T[a][l] + F * Mr::sg(l) * T[a][r]) : T[a][l];
+        }
+        dst.S[a][e] = v;
+      }
+    for (int a = 0; a < H; ++a)
+      for (int o = 0; o < WT; ++o) {
+        double v = 0.0;
+        if (o < nT) {
+          const int l = set_of(F, false, o), r = Mr::sig(l);
+          v = o < Mr::NP ? 0.5 * (T[a][l] - F * Mr::sg(l) * T[a][r]) : T[a][l];
+        }
+        dst.T[a][o] = v;
+      }
+  };
+  auto bwd = [&](auto& dst, const double (&T)[M][N], int F) {
+    constexpr int WE = sizeof(dst.E) / sizeof(dst.E[0]), WO = sizeof(dst.O) / sizeof(dst.O[0]);
+    const int nE = F > 0 ? Mr::NE : Mr::NO, nO = F > 0 ? Mr::NO : Mr::NE;
+    for (int e = 0; e < WE; ++e)
+      for (int a = 0; a < HP; ++a) {
+        double v = 0.0;
+        if (e < nE) {
+          const int l = set_of(F, true, e);
+          v = (a < H) ? 0.5 * (T[a][l] + T[M - 1 - a][l]) : T[a][l];
+        }
+        dst.E[e][a] = v;
+      }
+    for (int o = 0; o < WO; ++o)
+      for (int a = 0; a < (H > 0 ? H : 1); ++a) {
+        double v = 0.0;
+        if (o < nO && a < H) {
+          const int l = set_of(F, false, o);
+          v = 0.5 * (T[a][l] - T[M - 1 - a][l]);
+        }
+        dst.O[o][a] = v;
+      }
+  };
+  TabEO<N, M, MIR> t;
+  fwd(t.B, Bv, 1);
+  fwd(t.Dx, Dv[0], -1);
+  fwd(t.Dy, Dv[1], -1);
+  fwd(t.Dz, Dv[2], -1);
+  bwd(t.bBx, bB[0], 1);
+  bwd(t.bBy, bB[1], 1);
+  bwd(t.bBz, bB[2], 1);
+  bwd(t.bDx, bD[0], -1);
+  bwd(t.bDy, bD[1], -1);
+  bwd(t.bDz, bD[2], -1);
+  return t;
+}
+
+
+template <int N, int M, int MINB, int MODE, bool VAL, bool ASYNC, bool GUS = false>
+void launch_v4(sdme_ctx* c, const Tab3<N, M>& tb, OpArgs a) {
+  constexpr int smem =
+      (V4<N, M>::PER + (ASYNC ? 4 * 3 * N * N * N : 0) + (GUS && MODE == MODE_APPLY ? 9 * M * 32 : 0)) * 8;
+  auto kern = element_v4<N, M, MINB, MODE, VAL, ASYNC, GUS>;
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    max_blocks = std::max(1, nb) * sms;
+  }
+  for (int col = 0; col < 8; ++col) {
+    const long long cnt = colour_count(c->geo, col);
+    if (cnt == 0) continue;
+    a.colour = col;
+    const unsigned grid = (unsigned)std::min<long long>(cnt, max_blocks);
+    kern<<<grid, 32, smem, c->st>>>(tb, c->geo, a);
+    ++c->launches;
+  }
+}
+
+template <int N, int M, int MINB, bool ASYNC, bool GUS = false>
+void element_v4_modes(sdme_ctx* c, int mode, const Tab3<N, M>& tb, OpArgs a) {
+  if (mode == MODE_FINT) launch_v4<N, M, MINB, MODE_FINT, false, ASYNC, GUS>(c, tb, a);
+  else if (mode == MODE_APPLY && a.c_m != 0.0) launch_v4<N, M, MINB, MODE_APPLY, true, ASYNC, GUS>(c, tb, a);
+  else if (mode == MODE_APPLY) launch_v4<N, M, MINB, MODE_APPLY, false, ASYNC, GUS>(c, tb, a);
+  else launch_v4<N, M, MINB, MODE_MASS, true, ASYNC, GUS>(c, tb, a);
+}
+
+// Component-serial staged shape for P >= 5: enough warps per element that the
+// element's shared memory (points, stage scratch, staged rows) is shared by
+// 4 or 8 warps.
+template <int N, int M>
+struct LargeShape {
+  static constexpr int bytes = (V3<N, M, 1, 1>::PER + 2 * N * N * N) * 8;
+  static constexpr int WPE = bytes <= 40960 ? 1 : (bytes <= 65536 ? 4 : 8);
+  using type = Shape<N, M, WPE, 1, 1, 1, true>;
+};
+
+// even-odd tables when the 1D tables mirror (ctx->mir), else the plain ones
+template <int N, int M, class S>
+void element_eo_or_plain(sdme_ctx* c, int mode, const Tab3<N, M>& tb, OpArgs a) {
+  if (c->mir == 0)
+    element_shape<N, M, S>(c, mode, make_tabeo<N, M, 0>(c), a);
+  else if (c->mir == 1)
+    element_shape<N, M, S>(c, mode, make_tabeo<N, M, 1>(c), a);
+  else
+    element_shape<N, M, S>(c, mode, tb, a);
+}
+
+template <int N, int M>
+void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, double* y, double ck, double cm) {
+  const Tab3<N, M> tb = make_tab3<N, M>(c);
+  OpArgs a{u, p, y, ck, cm, 0, c->d_flag, c->cur_skip};
+  if constexpr (N == 5 && M == 5) {
+    // P = 4, m = 5 (BASELINE config 2); schedule history in profiles/variants_r01.txt.
+    // SDME_VARIANT: 3 = 3-component shape (8 warps/SM), 2 = component-serial,
+    // 12 warps/SM, 4 = column-resident v4, 5 = staged without even-odd.
+    if (c->variant == 3) {
+      element_shape<N, M, Shape<N, M, 1, 3, 2, 4>>(c, mode, tb, a);
+      return;
+    }
+    if (c->variant == 4) { element_v4_modes<N, M, 8, false>(c, mode, tb, a); return; }
+    if (c->variant == 2) { element_shape<N, M, Shape<N, M, 1, 1, 1, 12>>(c, mode, tb, a); return; }
+    using SK = Shape<N, M, 1, 1, 1, 11, true>;
+    if (c->variant == 5) { element_shape<N, M, SK>(c, mode, tb, a); return; }
+    // default for every mode: component-serial, cp.async-staged rows,
+    // even-odd contractions, 11 warps/SM (K.p 2.47 ms, f_int 1.60 ms, mass 1.27 ms)
+    element_eo_or_plain<N, M, SK>(c, mode, tb, a);
+    return;
+  } else if constexpr (N >= 6) {
+    element_eo_or_plain<N, M, typename LargeShape<N, M>::type>(c, mode, tb, a);
+    return;
+  } else {
+    element_shape<N, M, typename DefaultShape<N, M>::type>(c, mode, tb, a);
+  }
+}
+
+template <int N, int M>
+void diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm) {
+  constexpr int EB = Conf<N, M>::EB;
+  constexpr int smem = Conf<N, M>::bytes * EB;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(element_diag<N, M, EB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_done = true;
+  }
+  const Tab<N, M> tb = make_tab<N, M>(c);
+  OpArgs a{u, nullptr, d, ck, cm, 0, c->d_flag};
+  for (int col = 0; col < 8; ++col) {
+    const long long cnt = colour_count(c->geo, col);
+    if (cnt == 0) continue;
+    a.colour = col;
+    element_diag<N, M, EB><<<(unsigned)((cnt + EB - 1) / EB), 128, smem, c->st>>>(tb, c->geo, a);
+    ++c->launches;
+  }
+}
+
+template <int N, int M>
+const Ops* ops_for() {
+  static const Ops o{&element_impl<N, M>, &diag_impl<N, M>};
+  return &o;
+}
+
+}  // namespace
+
+#define SDME_CAT2(a, b) a##b
+#define SDME_CAT(a, b) SDME_CAT2(a, b)
+const SdmeOps* SDME_CAT(sdme_ops_p, SDME_ORDER)(int m) {
+  if (m == SDME_ORDER + 1) return ops_for<SDME_ORDER + 1, SDME_ORDER + 1>();
+  if (m == SDME_ORDER + 2) return ops_for<SDME_ORDER + 1, SDME_ORDER + 2>();
+  return nullptr;
+}

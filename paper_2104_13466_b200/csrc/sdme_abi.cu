@@ -14,60 +14,16 @@
 #include "sdme.h"
 #include "contact_kernels.cuh"
 #include "element_kernels.cuh"
-#include "element_v3.cuh"
-#include "element_v4.cuh"
 #include "vector_kernels.cuh"
+
+#include "ctx.cuh"
 
 using namespace sdme;
 
 namespace {
 
 constexpr unsigned long long kNoFlag = ~0ull;
-
-struct Ops;
-
-}  // namespace
-
-struct sdme_ctx {
-  int P = 0, m = 0, n = 0;
-  Geo geo{};
-  double h[3]{}, origin[3]{};
-  std::vector<double> Bl, Dl, w;  // lattice-local order, m x n
-  cudaStream_t st = nullptr;
-  long long nvec = 0;             // 3 * Ns
-  std::vector<double*> vecs;
-  int* d_perm = nullptr;
-  int64_t n_free = 0;
-  unsigned char* d_free = nullptr;  // 1 on free lattice dofs
-  double* d_fbuf = nullptr;         // staging for free-order vectors
-  double* d_partial = nullptr;
-  double* d_scal = nullptr;
-  double* h_scal = nullptr;         // pinned
-  unsigned long long* d_flag = nullptr;
-  unsigned long long* h_flag = nullptr;
-  double* d_gaps = nullptr;
-  long long gaps_cap = 0;
-  double* h_gaps = nullptr;
-  // PCG scratch vectors (lazily allocated ids)
-  int v_r = -1, v_p = -1, v_ap = -1, v_dinv = -1, v_tmp = -1;
-  const Ops* ops = nullptr;
-  int err_code = 0;
-  int64_t err_elem = -1;
-  int err_qp = -1;
-  std::string err_msg;
-  int64_t launches = 0;
-  int variant = 0;  // schedule variant (SDME_VARIANT env), tuning only
-  int* d_status = nullptr;  // PCG status word (device) and its pinned mirror
-  int* h_status = nullptr;
-  const int* cur_skip = nullptr;  // element kernels exit early when *cur_skip != 0 (PCG graph)
-};
-
-namespace {
-
-struct Ops {
-  void (*element)(sdme_ctx*, int mode, const double* u, const double* p, double* y, double ck, double cm);
-  void (*diag)(sdme_ctx*, const double* u, double* d, double ck, double cm);
-};
+using Ops = SdmeOps;
 
 int set_err(sdme_ctx* c, int code, const std::string& msg, int64_t elem = -1, int qp = -1) {
   if (c) {
@@ -97,193 +53,42 @@ inline int grid_for(long long n, int threads = 256) {
   return (int)std::max<long long>(1, std::min<long long>(g, 148LL * 16));
 }
 
-template <int N, int M>
-struct Conf {
-  static constexpr int bytes = Smem<N, M>::per_elem * 8;
-  static constexpr int EB = bytes > 100000 ? 1 : (100000 / bytes > 8 ? 8 : 100000 / bytes);
-};
-
-template <int N, int M>
-Tab<N, M> make_tab(const sdme_ctx* c) {
-  Tab<N, M> t;
-  for (int a = 0; a < M; ++a) {
-    for (int l = 0; l < N; ++l) {
-      t.B[a][l] = c->Bl[a * N + l];
-      t.D[a][l] = c->Dl[a * N + l];
+// Mirror structure of the lattice-order tables (eo.cuh); -1 if none applies.
+int detect_mirror(const sdme_ctx* c) {
+  const int n = c->n, m = c->m, P = c->P;
+  for (int mir = 0; mir < 2; ++mir) {
+    auto sig = [&](int l) { return mir == 0 ? n - 1 - l : (l == 0 ? n - 1 : (l == n - 1 ? 0 : l)); };
+    auto sg = [&](int l) { return mir == 0 ? 1 : ((l == 0 || l == n - 1) ? 1 : ((l % 2) ? 1 : -1)); };
+    double scale = 0.0;
+    for (double v : c->Bl) scale = std::max(scale, std::fabs(v));
+    for (double v : c->Dl) scale = std::max(scale, std::fabs(v));
+    bool ok = true;
+    for (int a = 0; a < m && ok; ++a) {
+      if (std::fabs(c->w[a] - c->w[m - 1 - a]) > 1e-14 * std::fabs(c->w[a])) ok = false;
+      for (int l = 0; l < n && ok; ++l) {
+        const double b1 = c->Bl[(m - 1 - a) * n + l], b2 = sg(l) * c->Bl[a * n + sig(l)];
+        const double d1 = c->Dl[(m - 1 - a) * n + l], d2 = -sg(l) * c->Dl[a * n + sig(l)];
+        if (std::fabs(b1 - b2) > 1e-13 * scale || std::fabs(d1 - d2) > 1e-13 * scale) ok = false;
+      }
     }
-    t.W[a] = c->w[a];
+    (void)P;
+    if (ok) return mir;
   }
-  return t;
-}
-
-// v3 tables: weights, det J and dxi/dX folded per axis (element_v3.cuh)
-template <int N, int M>
-Tab3<N, M> make_tab3(const sdme_ctx* c) {
-  Tab3<N, M> t;
-  const Geo& g = c->geo;
-  for (int a = 0; a < M; ++a) {
-    const double w = c->w[a];
-    for (int l = 0; l < N; ++l) {
-      const double b = c->Bl[a * N + l], d = c->Dl[a * N + l];
-      t.B[a][l] = b;
-      t.Dx[a][l] = d * g.s[0];
-      t.Dy[a][l] = d * g.s[1];
-      t.Dz[a][l] = d * g.s[2];
-      t.bBx[a][l] = b * w;
-      t.bDx[a][l] = d * w * g.s[0];
-      t.bBy[a][l] = b * w;
-      t.bDy[a][l] = d * w * g.s[1];
-      t.bBz[a][l] = b * w * g.detJ;
-      t.bDz[a][l] = d * w * g.s[2] * g.detJ;
-    }
-  }
-  return t;
-}
-
-// Launch shape of the v3 element kernels.  WPE warps per element, EPB
-// elements per block, NC components per contraction stage, MINB minimum
-// resident blocks per SM (register cap for __launch_bounds__).
-template <int N, int M, int WPE_, int NC_, int EPB_, int MINB_, bool STG_ = false>
-struct Shape {
-  static constexpr int WPE = WPE_, NC = NC_, EPB = EPB_, MINB = MINB_;
-  static constexpr bool STG = STG_;  // cp.async row staging (NC == 1)
-};
-
-template <int N, int M>
-struct DefaultShape {
-  static constexpr int bytes = V3<N, M, 1, 3>::PER * 8;
-  static constexpr int WPE = bytes <= 40960 ? 1 : (bytes <= 65536 ? 4 : 8);
-  using type = Shape<N, M, WPE, 3, (WPE == 1 ? 2 : 1), 1>;
-};
-
-template <int N, int M, class S, int MODE, bool VAL>
-void launch_v3(sdme_ctx* c, const Tab3<N, M>& tb, OpArgs a) {
-  constexpr bool VALS = VAL || MODE == MODE_MASS;
-  constexpr int smem = (V3<N, M, S::WPE, S::NC, VALS>::PER + (S::STG ? 2 * N * N * N : 0)) * 8 * S::EPB;
-  auto kern = element_v3<N, M, S::WPE, S::NC, S::EPB, S::MINB, MODE, VAL, S::STG>;
-  static int max_blocks = -1;
-  if (max_blocks < 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, S::EPB * S::WPE * 32, smem);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    max_blocks = std::max(1, nb) * sms;
-  }
-  for (int col = 0; col < 8; ++col) {
-    const long long cnt = colour_count(c->geo, col);
-    if (cnt == 0) continue;
-    a.colour = col;
-    const long long need = (cnt + S::EPB - 1) / S::EPB;
-    const unsigned grid = (unsigned)std::min<long long>(need, max_blocks);
-    kern<<<grid, S::EPB * S::WPE * 32, smem, c->st>>>(tb, c->geo, a);
-    ++c->launches;
-  }
-}
-
-template <int N, int M, class S>
-void element_shape(sdme_ctx* c, int mode, const Tab3<N, M>& tb, OpArgs a) {
-  if (mode == MODE_FINT) launch_v3<N, M, S, MODE_FINT, false>(c, tb, a);
-  else if (mode == MODE_APPLY && a.c_m != 0.0) launch_v3<N, M, S, MODE_APPLY, true>(c, tb, a);
-  else if (mode == MODE_APPLY) launch_v3<N, M, S, MODE_APPLY, false>(c, tb, a);
-  else launch_v3<N, M, S, MODE_MASS, true>(c, tb, a);
-}
-
-template <int N, int M, int MINB, int MODE, bool VAL, bool ASYNC, bool GUS = false>
-void launch_v4(sdme_ctx* c, const Tab3<N, M>& tb, OpArgs a) {
-  constexpr int smem =
-      (V4<N, M>::PER + (ASYNC ? 4 * 3 * N * N * N : 0) + (GUS && MODE == MODE_APPLY ? 9 * M * 32 : 0)) * 8;
-  auto kern = element_v4<N, M, MINB, MODE, VAL, ASYNC, GUS>;
-  static int max_blocks = -1;
-  if (max_blocks < 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    max_blocks = std::max(1, nb) * sms;
-  }
-  for (int col = 0; col < 8; ++col) {
-    const long long cnt = colour_count(c->geo, col);
-    if (cnt == 0) continue;
-    a.colour = col;
-    const unsigned grid = (unsigned)std::min<long long>(cnt, max_blocks);
-    kern<<<grid, 32, smem, c->st>>>(tb, c->geo, a);
-    ++c->launches;
-  }
-}
-
-template <int N, int M, int MINB, bool ASYNC, bool GUS = false>
-void element_v4_modes(sdme_ctx* c, int mode, const Tab3<N, M>& tb, OpArgs a) {
-  if (mode == MODE_FINT) launch_v4<N, M, MINB, MODE_FINT, false, ASYNC, GUS>(c, tb, a);
-  else if (mode == MODE_APPLY && a.c_m != 0.0) launch_v4<N, M, MINB, MODE_APPLY, true, ASYNC, GUS>(c, tb, a);
-  else if (mode == MODE_APPLY) launch_v4<N, M, MINB, MODE_APPLY, false, ASYNC, GUS>(c, tb, a);
-  else launch_v4<N, M, MINB, MODE_MASS, true, ASYNC, GUS>(c, tb, a);
-}
-
-template <int N, int M>
-void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, double* y, double ck, double cm) {
-  const Tab3<N, M> tb = make_tab3<N, M>(c);
-  OpArgs a{u, p, y, ck, cm, 0, c->d_flag, c->cur_skip};
-  if constexpr (N == 5 && M == 5) {
-    // P = 4, m = 5 (BASELINE config 2).  Measured (profiles/variants_r01.txt):
-    // component-serial stages, one element per 32-thread block, 12 blocks/SM
-    // (168-register cap) beats the 3-component, 8-warp shape by 11%.
-    // SDME_VARIANT=3 keeps the 3-component shape for comparison.
-    if (c->variant == 3) {
-      element_shape<N, M, Shape<N, M, 1, 3, 2, 4>>(c, mode, tb, a);
-      return;
-    }
-    if (c->variant == 4) { element_v4_modes<N, M, 8, false>(c, mode, tb, a); return; }
-    if (c->variant == 2) { element_shape<N, M, Shape<N, M, 1, 1, 1, 12>>(c, mode, tb, a); return; }
-    // default: f_int and mass with the column-resident v4 schedule (1.69 / 1.29 ms vs
-    // 1.78 / 1.35 ms for v3)
-    if (mode == MODE_FINT || mode == MODE_MASS) {
-      element_v4_modes<N, M, 10, false>(c, mode, tb, a);
-      return;
-    }
-    // K.p: component-serial v3 with cp.async row staging, 11 warps/SM (2.70 ms;
-    // profiles/variants_r01.txt)
-    element_shape<N, M, Shape<N, M, 1, 1, 1, 11, true>>(c, mode, tb, a);
-    return;
-  }
-  element_shape<N, M, typename DefaultShape<N, M>::type>(c, mode, tb, a);
-}
-
-template <int N, int M>
-void diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm) {
-  constexpr int EB = Conf<N, M>::EB;
-  constexpr int smem = Conf<N, M>::bytes * EB;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(element_diag<N, M, EB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_done = true;
-  }
-  const Tab<N, M> tb = make_tab<N, M>(c);
-  OpArgs a{u, nullptr, d, ck, cm, 0, c->d_flag};
-  for (int col = 0; col < 8; ++col) {
-    const long long cnt = colour_count(c->geo, col);
-    if (cnt == 0) continue;
-    a.colour = col;
-    element_diag<N, M, EB><<<(unsigned)((cnt + EB - 1) / EB), 128, smem, c->st>>>(tb, c->geo, a);
-    ++c->launches;
-  }
-}
-
-template <int N, int M>
-const Ops* ops_for() {
-  static const Ops o{&element_impl<N, M>, &diag_impl<N, M>};
-  return &o;
+  return -1;
 }
 
 const Ops* select_ops(int P, int m) {
-#define SDME_CASE(PP, MM) \
-  if (P == PP && m == MM) return ops_for<PP + 1, MM>();
-#define SDME_P(PP) SDME_CASE(PP, PP + 1) SDME_CASE(PP, PP + 2)
-  SDME_P(1) SDME_P(2) SDME_P(3) SDME_P(4) SDME_P(5) SDME_P(6) SDME_P(7) SDME_P(8)
-#undef SDME_P
-#undef SDME_CASE
-  return nullptr;
+  switch (P) {
+    case 1: return sdme_ops_p1(m);
+    case 2: return sdme_ops_p2(m);
+    case 3: return sdme_ops_p3(m);
+    case 4: return sdme_ops_p4(m);
+    case 5: return sdme_ops_p5(m);
+    case 6: return sdme_ops_p6(m);
+    case 7: return sdme_ops_p7(m);
+    case 8: return sdme_ops_p8(m);
+    default: return nullptr;
+  }
 }
 
 double* vec(sdme_ctx* c, int id) {
@@ -385,6 +190,7 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
       ctx->Bl[a * n + l] = d->B[a * n + func_of(l)];
       ctx->Dl[a * n + l] = d->D[a * n + func_of(l)];
     }
+  ctx->mir = detect_mirror(ctx);
   Geo& g = ctx->geo;
   g.nx = d->nx; g.ny = d->ny; g.nz = d->nz;
   g.Lx = P * d->nx + 1; g.Ly = P * d->ny + 1; g.Lz = P * d->nz + 1;
