@@ -1,7 +1,8 @@
-// Even-odd (eo.cuh) overloads of the v3 contraction stages, component-serial
-// (NC = 1).  Selected by passing a TabEO table to element_v3; the schedule,
-// shared layouts, staging and point work are the v3 ones -- only the 1D
-// contractions change (about half the multiply-adds).
+// Even-odd (eo.cuh) overloads of the v3 contraction stages.  Selected by
+// passing a TabEO table to element_v3; the schedule, shared layouts, staging
+// and point work are the v3 ones -- only the 1D contractions change (about
+// half the multiply-adds).  NC = 1 (component-serial, optionally with staged
+// rows) or NC = 3 (all components per stage, small P).
 #pragma once
 #include "element_v3.cuh"
 #include "eo.cuh"
@@ -12,18 +13,18 @@ template <int N, int M, int WPE, int NC, bool GRAD, bool VAL, bool STAGED = fals
 __device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo& g, const double* __restrict__ src,
                                            int X0, int Y0, int Z0, double* A, double* B, int t, int gid,
                                            double* R = nullptr, int* buf = nullptr, NextRows next = {}) {
-  static_assert(NC == 1, "even-odd stages are component-serial");
-  using C = V3<N, M, WPE, 1>;
+  static_assert(!STAGED || NC == 1, "row staging is per component");
+  using C = V3<N, M, WPE, NC>;
   using Mr = Mir<N, MIR>;
   constexpr int NE = Mr::NE > 0 ? Mr::NE : 1, NO = Mr::NO > 0 ? Mr::NO : 1;
   double* const P = A;
 #pragma unroll 1
-  for (int comp = 0; comp < 3; ++comp) {
-    double* const X = B + C::YO;
+  for (int c0 = 0; c0 < 3; c0 += NC) {
+    double* const X = (NC == 3) ? A : B + C::YO;
     if (STAGED) {
       double* nb = R + (*buf ^ 1) * N * N * N;
-      if (comp + 1 < 3) {
-        v3_stage_rows<N, C::T>(g, src, comp + 1, X0, Y0, Z0, nb, t);
+      if (c0 + 1 < 3) {
+        v3_stage_rows<N, C::T>(g, src, c0 + 1, X0, Y0, Z0, nb, t);
         cp_async_wait<1>();
       } else if (next.field) {
         v3_stage_rows<N, C::T>(g, next.field, 0, next.X0, next.Y0, next.Z0, nb, t);
@@ -33,11 +34,11 @@ __device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo
       }
       group_sync<WPE>(gid);
     }
-    // x stage: item (k, j)
-    for (int w = t; w < N * N; w += C::T) {
+    // x stage: item (comp, k, j)
+    for (int w = t; w < NC * N * N; w += C::T) {
       int ck, j;
       C::item_x(w, ck, j);
-      const int k = ck;
+      const int comp = c0 + ck / N, k = ck % N;
       double v[N];
       if (STAGED) {
         const double* row = R + *buf * N * N * N + (k * N + j) * N;
@@ -59,11 +60,11 @@ __device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo
       }
     }
     group_sync<WPE>(gid);
-    // y stage: item (k, a)
-    for (int w = t; w < N * M; w += C::T) {
+    // y stage: item (comp, k, a)
+    for (int w = t; w < NC * N * M; w += C::T) {
       int ck, a;
       C::item_y(w, ck, a);
-      const int k = ck;
+      const int cl = ck / N, k = ck % N;
       double x0[N], x1[N];
 #pragma unroll
       for (int j = 0; j < N; ++j) {
@@ -81,23 +82,25 @@ __device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo
       }
 #pragma unroll
       for (int b = 0; b < M; ++b) {
-        B[C::yi(0, 0, k, b * M + a)] = bb[b];
+        B[C::yi(cl, 0, k, b * M + a)] = bb[b];
         if (GRAD) {
-          B[C::yi(0, 1, k, b * M + a)] = db[b];
-          B[C::yi(0, 2, k, b * M + a)] = bd[b];
+          B[C::yi(cl, 1, k, b * M + a)] = db[b];
+          B[C::yi(cl, 2, k, b * M + a)] = bd[b];
         }
       }
     }
     group_sync<WPE>(gid);
-    // z stage: item (b, a) -> points
-    for (int ba = t; ba < M * M; ba += C::T) {
+    // z stage: item (comp, b, a) -> points
+    for (int w = t; w < NC * M * M; w += C::T) {
+      const int cl = w / (M * M), ba = w % (M * M);
+      const int comp = c0 + cl;
       double y0[N], y1[N], y2[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        y0[k] = B[C::yi(0, 0, k, ba)];
+        y0[k] = B[C::yi(cl, 0, k, ba)];
         if (GRAD) {
-          y1[k] = B[C::yi(0, 1, k, ba)];
-          y2[k] = B[C::yi(0, 2, k, ba)];
+          y1[k] = B[C::yi(cl, 1, k, ba)];
+          y2[k] = B[C::yi(cl, 2, k, ba)];
         }
       }
       double E0[NE], O0[NO];
@@ -132,15 +135,16 @@ __device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo
 template <int N, int M, int WPE, int NC, bool GRAD, bool VAL, int MIR>
 __device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Geo& g, double* __restrict__ dst,
                                             int X0, int Y0, int Z0, double* A, double* B, int t, int gid) {
-  static_assert(NC == 1, "even-odd stages are component-serial");
-  using C = V3<N, M, WPE, 1>;
+  using C = V3<N, M, WPE, NC>;
   using Mr = Mir<N, MIR>;
   constexpr int HP = Half<M>::HP, H = Half<M>::H > 0 ? Half<M>::H : 1;
 #pragma unroll 1
-  for (int comp = 0; comp < 3; ++comp) {
-    double* const X = B + C::YO;
-    // z' stage: item (b, a), contract over c
-    for (int ba = t; ba < M * M; ba += C::T) {
+  for (int c0 = 0; c0 < 3; c0 += NC) {
+    double* const X = (NC == 3) ? A : B + C::YO;
+    // z' stage: item (comp, b, a), contract over c
+    for (int w = t; w < NC * M * M; w += C::T) {
+      const int cl = w / (M * M), ba = w % (M * M);
+      const int comp = c0 + cl;
       double hx[N], hy[N], hz[N];
       if (GRAD) {
         double q[M], qe[HP], qo[H];
@@ -170,32 +174,32 @@ __device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Ge
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         if (GRAD) {
-          B[C::yi(0, 0, k, ba)] = hx[k];
-          B[C::yi(0, 1, k, ba)] = hy[k];
+          B[C::yi(cl, 0, k, ba)] = hx[k];
+          B[C::yi(cl, 1, k, ba)] = hy[k];
         }
-        B[C::yi(0, 2, k, ba)] = hz[k];
+        B[C::yi(cl, 2, k, ba)] = hz[k];
       }
     }
     group_sync<WPE>(gid);
-    // y' stage: item (k, a), contract over b
-    for (int w = t; w < N * M; w += C::T) {
+    // y' stage: item (comp, k, a), contract over b
+    for (int w = t; w < NC * N * M; w += C::T) {
       int ck, a;
       C::item_y(w, ck, a);
-      const int k = ck;
+      const int cl = ck / N, k = ck % N;
       double jx[N], jyz[N];
       double q[M], qe[HP], qo[H];
       if (GRAD) {
 #pragma unroll
-        for (int b = 0; b < M; ++b) q[b] = B[C::yi(0, 0, k, b * M + a)];
+        for (int b = 0; b < M; ++b) q[b] = B[C::yi(cl, 0, k, b * M + a)];
         eo_qsplit<M>(q, qe, qo);
         eo_bwd<N, M, MIR, 1, Mr::NE, Mr::NO, false>(tb.bBy, qe, qo, jx);
 #pragma unroll
-        for (int b = 0; b < M; ++b) q[b] = B[C::yi(0, 1, k, b * M + a)];
+        for (int b = 0; b < M; ++b) q[b] = B[C::yi(cl, 1, k, b * M + a)];
         eo_qsplit<M>(q, qe, qo);
         eo_bwd<N, M, MIR, -1, Mr::NO, Mr::NE, false>(tb.bDy, qe, qo, jyz);
       }
 #pragma unroll
-      for (int b = 0; b < M; ++b) q[b] = B[C::yi(0, 2, k, b * M + a)];
+      for (int b = 0; b < M; ++b) q[b] = B[C::yi(cl, 2, k, b * M + a)];
       eo_qsplit<M>(q, qe, qo);
       if (GRAD)
         eo_bwd<N, M, MIR, 1, Mr::NE, Mr::NO, true>(tb.bBy, qe, qo, jyz);
@@ -208,11 +212,11 @@ __device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Ge
       }
     }
     group_sync<WPE>(gid);
-    // x' stage: item (k, j), contract over a, RED into the lattice
-    for (int w = t; w < N * N; w += C::T) {
+    // x' stage: item (comp, k, j), contract over a, RED into the lattice
+    for (int w = t; w < NC * N * N; w += C::T) {
       int ck, j;
       C::item_x(w, ck, j);
-      const int k = ck;
+      const int comp = c0 + ck / N, k = ck % N;
       double acc[N];
       double q[M], qe[HP], qo[H];
       if (GRAD) {

@@ -276,7 +276,8 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
     element_eo_or_plain<N, M, typename LargeShape<N, M>::type>(c, mode, tb, a);
     return;
   } else {
-    element_shape<N, M, typename DefaultShape<N, M>::type>(c, mode, tb, a);
+    // small P: all three components per stage (more pencils per warp), even-odd
+    element_eo_or_plain<N, M, typename DefaultShape<N, M>::type>(c, mode, tb, a);
   }
 }
 
