@@ -27,8 +27,8 @@ OMAT = of.Material(1.0e7, 0.3, 1.0e3)
 TOL = 1e-12
 
 
-def gpu_problem(tag, P, m, div, L, dr=None, origin=(0.0, 0.0, 0.0)):
-    return GpuFemProblem(BoxMesh(div, L, origin), build_basis(P, BasisKind(tag)), MAT, gauss_rule(m), dr)
+def gpu_problem(tag, P, m, div, L, dr=None, origin=(0.0, 0.0, 0.0), mat=None):
+    return GpuFemProblem(BoxMesh(div, L, origin), build_basis(P, BasisKind(tag)), mat or MAT, gauss_rule(m), dr)
 
 
 @pytest.mark.parametrize("case", element_cases(), ids=lambda c: f"{c[1]}-P{c[2]}-m{c[3]}-{c[0]}")
@@ -229,3 +229,109 @@ def test_explicit_consistent_mass_vs_reference():
     assert len(ref) == len(got) and max(abs(a - b) for a, b in zip(ref, got)) <= 1
     assert max_rel_err(traj.state.u, g["u"]) <= 1e-9
     assert max_rel_err(traj.state.v, g["v"]) <= 1e-9
+
+
+# ------------------------------------------------------------------------------
+# Property tests mirroring the reference suite (test_femcore.py, test_acceptance.py
+# criterion 7, test_dynamics.py), run on the GPU path.
+
+KINDS5 = ("LagrangeGLL", "ModalJacobi", "SDME_M", "SDME_K", "SDME_H")
+RMAT = NeoHookean.from_engineering(1000.0, 0.3, 1.0)  # test_femcore.py:13
+
+
+@pytest.mark.parametrize("tag", KINDS5)
+def test_rigid_translation_zero_force(tag):
+    """test_femcore.py:30-34: a rigid translation produces no internal force."""
+    pb = gpu_problem(tag, 3, 4, (2, 2, 2), (1.0, 1.0, 1.0), mat=RMAT)
+    u = pb.constant_field([0.2, -0.1, 0.3])
+    assert np.abs(pb.internal_force(u)).max() <= 1e-9
+    assert np.abs(pb.internal_force(np.zeros(pb.n_free))).max() <= 1e-14
+
+
+@pytest.mark.parametrize("tag", KINDS5)
+def test_constant_stress_divergence_theorem(tag):
+    """test_femcore.py:37-51: homogeneous stretch F = diag(1.1, 1, 1); the
+    internal force equals the surface load of the constant first PK stress."""
+    P = 3
+    pb = gpu_problem(tag, P, P + 1, (2, 2, 2), (1.0, 1.0, 1.0), mat=RMAT)
+    # u = (F - I) X is linear and exact in every basis: X = (X0 + h/2) 1 + (h/2) xi
+    from paper_2104_13466_b200.basis import constant_coeffs, gll_rule
+    if pb.basis.kind.is_nodal:
+        nodes = gll_rule(P + 1).points
+        lin = np.concatenate(([nodes[0], nodes[-1]], nodes[1:-1]))
+    else:
+        lin = np.linalg.solve(pb.basis.transform.T, np.array([-1.0, 1.0] + [0.0] * (P - 1)))
+    const = constant_coeffs(pb.basis)
+    reorder = lambda c: np.concatenate(([c[0]], c[2:], [c[1]]))  # function -> lattice-local order
+    xs = np.empty(P * pb.mesh.divisions[0] + 1)
+    h = pb.mesh.h[0]
+    for e in range(pb.mesh.divisions[0]):
+        xs[P * e:P * e + P + 1] = (e * h + 0.5 * h) * reorder(const) + 0.5 * h * reorder(lin)
+    ones = [np.tile(reorder(const)[:P], pb.mesh.divisions[d]).tolist() + [const[1]] for d in (1, 2)]
+    lat = np.zeros(pb.lattice_shape)
+    lat[0] = 0.1 * np.einsum("z,y,x->zyx", ones[1], ones[0], xs)
+    u = pb.to_free(lat)
+    r = pb.internal_force(u)
+    mu, lam = RMAT.mu, RMAT.lambda_lame
+    Fh = np.diag([1.1, 1.0, 1.0])
+    C = Fh.T @ Fh
+    Ci = np.linalg.inv(C)
+    S = mu * (np.eye(3) - Ci) + lam * 0.5 * np.log(np.linalg.det(C)) * Ci
+    P1 = Fh @ S
+    surf = np.zeros(pb.n_free)
+    for tagf, nrm in (("xmin", [-1, 0, 0]), ("xmax", [1, 0, 0]), ("ymin", [0, -1, 0]), ("ymax", [0, 1, 0]),
+                      ("zmin", [0, 0, -1]), ("zmax", [0, 0, 1])):
+        surf += pb.traction_vector(tagf, P1 @ np.array(nrm, dtype=float))
+    assert np.abs(r - surf).max() <= 1e-8 * np.abs(r).max()
+
+
+@pytest.mark.parametrize("tag", KINDS5)
+@pytest.mark.parametrize("P", [2, 4])
+def test_global_fd_tangent_consistency(tag, P):
+    """test_acceptance.py:196-221 (criterion 7): central FD of f_int along a
+    random direction vs the matrix-free K_T, <= 1e-5 relative, Dirichlet."""
+    pb = gpu_problem(tag, P, P + 1, (2, 2, 2), (1.0, 1.0, 1.0), [("xmin", (0, 1, 2))], mat=RMAT)
+    rng = np.random.default_rng(4)
+    u0 = 0.01 * rng.uniform(-1, 1, pb.n_free) / P
+    du = rng.standard_normal(pb.n_free)
+    du /= np.linalg.norm(du)
+    eps = 1e-6
+    fd = (pb.internal_force(u0 + eps * du) - pb.internal_force(u0 - eps * du)) / (2 * eps)
+    kd = pb.apply_tangent(u0, du)
+    assert np.linalg.norm(fd - kd) <= 1e-5 * np.linalg.norm(kd)
+
+
+@pytest.mark.parametrize("tag", KINDS5)
+def test_tangent_symmetry_and_mass_conservation(tag):
+    """test_femcore.py:92-108: K_T symmetric (q.Kp = p.Kq); c.M c = rho * volume
+    for the constant field c (one component)."""
+    pb = gpu_problem(tag, 3, 4, (2, 3, 2), (1.0, 1.5, 1.0), [("xmin", (0, 1, 2))], mat=RMAT)
+    rng = np.random.default_rng(9)
+    u = 1e-3 * rng.uniform(-1, 1, pb.n_free)
+    p, q = rng.standard_normal(pb.n_free), rng.standard_normal(pb.n_free)
+    a, b = q @ pb.apply_tangent(u, p), p @ pb.apply_tangent(u, q)
+    assert abs(a - b) <= 1e-10 * max(abs(a), abs(b))
+    pb2 = gpu_problem(tag, 3, 4, (2, 3, 2), (1.0, 1.5, 1.0), mat=RMAT)
+    c = pb2.constant_field([1.0, 0.0, 0.0])
+    assert c @ pb2.mass_apply(c) == pytest.approx(RMAT.rho0 * 1.5, rel=1e-12)
+
+
+def test_newmark_rest_state_stays_at_rest():
+    """test_dynamics.py:113-118: zero load, zero state -> zero Newton iterations."""
+    pb = gpu_problem("SDME_M", 2, 3, (2, 2, 2), (1.0, 1.0, 1.0), mat=RMAT)
+    traj = newmark_run(pb, lambda t: np.zeros(pb.n_free), 1e-3, 5)
+    assert np.abs(traj.state.u).max() <= 1e-14 and traj.newton_iters == [0] * 5
+
+
+def test_explicit_momentum_conservation():
+    """test_dynamics.py:62-81: uniform initial velocity, no force, lumped mass:
+    momentum conserved to 1e-10 and the motion is exactly u(T) = T v0."""
+    from paper_2104_13466_b200.dynamics import ScaledLoad
+    pb = gpu_problem("SDME_M", 3, 4, (2, 2, 2), (1.0, 1.0, 1.0), mat=RMAT)
+    v0 = pb.constant_field([0.0, 0.3, 0.0])
+    ey = pb.constant_field([0.0, 1.0, 0.0])
+    traj = explicit_run(pb, ScaledLoad(np.zeros(pb.n_free), lambda t: 0.0), 1e-3, 100, v0=v0)
+    p0, p1 = ey @ pb.mass_apply(v0), ey @ pb.mass_apply(traj.state.v)
+    assert abs(p1 - p0) <= 1e-10 * abs(p0)
+    ut = traj.state.t * v0
+    assert np.abs(traj.state.u - ut).max() <= 1e-8 * np.abs(ut).max()
