@@ -11,10 +11,16 @@
 
 struct sdme_ctx;
 
+// meshes with at most this many elements use E-vector mode (sdme_ctx::ev_mode)
+constexpr long long kEvMaxElements = 8192;
+
 // Operator entry points of one (P, m) instantiation.
 struct SdmeOps {
   void (*element)(sdme_ctx*, int mode, const double* u, const double* p, double* y, double ck, double cm);
   void (*diag)(sdme_ctx*, const double* u, double* d, double ck, double cm);
+  // small-mesh PCG iteration tail after an E-vector element launch (pcg_small.cuh)
+  void (*pcg_small)(sdme_ctx*, double* x, double* r, double* p, double* ap, const double* dinv,
+                    cudaGraphConditionalHandle cond);
 };
 
 struct sdme_ctx {
@@ -32,7 +38,8 @@ struct sdme_ctx {
   double* d_partial = nullptr;
   double* d_scal = nullptr;
   double* h_scal = nullptr;         // pinned
-  unsigned long long* d_flag = nullptr;
+  unsigned long long* d_flag = nullptr;   // [0] element inversion, [1] non-positive diagonal
+  unsigned long long* d_dflag = nullptr;  // d_flag + 1
   unsigned long long* h_flag = nullptr;
   double* d_gaps = nullptr;
   long long gaps_cap = 0;
@@ -50,6 +57,22 @@ struct sdme_ctx {
   int* d_status = nullptr;  // PCG status word (device) and its pinned mirror
   int* h_status = nullptr;
   const int* cur_skip = nullptr;  // element kernels exit early when *cur_skip != 0 (PCG graph)
+  // E-vector mode (small meshes): one launch over all elements writing their
+  // boxes to d_ev, then a deterministic gather -- instead of 8 colour passes
+  bool ev_mode = false;
+  bool ev_no_gather = false;
+  int pcg_warm = 0;  // operator kinds whose launch setup ran (sdme_pcg)
+  // instantiated PCG graph, reused while the solve's operands are the same
+  cudaGraph_t pcg_graph = nullptr;
+  cudaGraphExec_t pcg_exec = nullptr;
+  struct PcgKey {
+    const double* u = nullptr;
+    const double* x = nullptr;
+    double ck = 0.0, cm = 0.0;
+    bool operator==(const PcgKey& o) const { return u == o.u && x == o.x && ck == o.ck && cm == o.cm; }
+  } pcg_key;
+  long long pcg_per_iter = 0;  // element launch leaves A p in d_ev (small PCG path gathers)
+  double* d_ev = nullptr;
 };
 
 // per-order operator tables (ops.cu, one object file per P)

@@ -134,7 +134,8 @@ __device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo
 
 template <int N, int M, int WPE, int NC, bool GRAD, bool VAL, int MIR>
 __device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Geo& g, double* __restrict__ dst,
-                                            int X0, int Y0, int Z0, double* A, double* B, int t, int gid) {
+                                            int X0, int Y0, int Z0, double* A, double* B, int t, int gid,
+                                            double* evb = nullptr) {
   using C = V3<N, M, WPE, NC>;
   using Mr = Mir<N, MIR>;
   constexpr int HP = Half<M>::HP, H = Half<M>::H > 0 ? Half<M>::H : 1;
@@ -232,6 +233,12 @@ __device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Ge
         eo_bwd<N, M, MIR, 1, Mr::NE, Mr::NO, true>(tb.bBx, qe, qo, acc);
       else
         eo_bwd<N, M, MIR, 1, Mr::NE, Mr::NO, false>(tb.bBx, qe, qo, acc);
+      if (evb) {
+        double* er = evb + ((comp * N + k) * N + j) * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) er[i] = acc[i];
+        continue;
+      }
       const int Z = Z0 + k, Y = Y0 + j;
       const bool chk = touches_dirichlet(g, comp, X0, Y0, Z0, N);
       double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Lx + X0;

@@ -50,6 +50,7 @@ struct OpArgs {
   int colour;         // bit0: i parity, bit1: j parity, bit2: k parity
   unsigned long long* inv_flag;  // atomicMin(elem*nq + qp) on det F <= 0
   const int* skip = nullptr;     // if set and non-zero: return at once (stopped PCG graph)
+  double* ev = nullptr;          // E-vector mode (colour < 0): element boxes stored, not scattered
 };
 
 __device__ __forceinline__ bool constrained(const Geo& g, int comp, int X, int Y, int Z) {
@@ -68,8 +69,18 @@ __device__ __forceinline__ bool touches_dirichlet(const Geo& g, int comp, int X0
 }
 
 // Element of this block slot, for the given colour pass.  Returns false past the end.
+// colour >= 0: the elements of one parity class (8-colour passes);
+// colour < 0: every element in lexicographic order (E-vector mode).
 __device__ __forceinline__ bool colour_element(const Geo& g, int colour, long long idx,
                                                int& ei, int& ej, int& ek) {
+  if (colour < 0) {
+    if (idx >= (long long)g.nx * g.ny * g.nz) return false;
+    ei = (int)(idx % g.nx);
+    const long long r = idx / g.nx;
+    ej = (int)(r % g.ny);
+    ek = (int)(r / g.ny);
+    return true;
+  }
   const int cx = colour & 1, cy = (colour >> 1) & 1, cz = (colour >> 2) & 1;
   const int nex = (g.nx - cx + 1) >> 1, ney = (g.ny - cy + 1) >> 1, nez = (g.nz - cz + 1) >> 1;
   if (nex <= 0 || ney <= 0 || nez <= 0) return false;
@@ -85,6 +96,7 @@ __device__ __forceinline__ bool colour_element(const Geo& g, int colour, long lo
 }
 
 __host__ __device__ inline long long colour_count(const Geo& g, int colour) {
+  if (colour < 0) return (long long)g.nx * g.ny * g.nz;
   const int cx = colour & 1, cy = (colour >> 1) & 1, cz = (colour >> 2) & 1;
   const long long nex = (g.nx - cx + 1) >> 1, ney = (g.ny - cy + 1) >> 1, nez = (g.nz - cz + 1) >> 1;
   if (nex <= 0 || ney <= 0 || nez <= 0) return 0;
@@ -736,12 +748,65 @@ __global__ void __launch_bounds__(128) element_diag(const __grid_constant__ Tab<
       const int k = it / N, j = it % N;
       double* s = smem + el * L::per_elem;
       const int Z = base[el][2] + k, Y = base[el][1] + j;
+      if (args.ev) {
+        double* er = args.ev + (eid[el] * 3 + comp) * (N * N * N) + it * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) er[i] = s[L::kX1 + it * N + i];
+        continue;
+      }
       double* row = args.y + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Lx + base[el][0];
 #pragma unroll
       for (int i = 0; i < N; ++i)
         if (!constrained(g, comp, base[el][0] + i, Y, Z)) row[i] += s[L::kX1 + it * N + i];
     }
     __syncthreads();
+  }
+}
+
+// E-vector mode: y += sum of the element boxes covering each lattice point.
+// Along each axis a point lies in one element (interior offset) or two (a
+// shared plane: offset P in the left element, 0 in the right one); the up to
+// 8 contributions are summed in a fixed (z, y, x, ascending element) order,
+// so results are bit-reproducible.  Constrained points are left untouched.
+__device__ __forceinline__ int ev_cands(int X, int P, int n, int (&e)[2], int (&o)[2]) {
+  const int q = X / P, r = X - q * P;
+  if (r != 0) { e[0] = q; o[0] = r; return 1; }
+  if (q == 0) { e[0] = 0; o[0] = 0; return 1; }
+  if (q == n) { e[0] = n - 1; o[0] = P; return 1; }
+  e[0] = q - 1; o[0] = P; e[1] = q; o[1] = 0;
+  return 2;
+}
+
+// gathered value of lattice entry idx (comp-major); false on constrained points
+template <int N>
+__device__ __forceinline__ bool ev_point(const double* __restrict__ ev, const Geo& g, long long idx, double& s) {
+  constexpr int P = N - 1, B = N * N * N;
+  const int comp = (int)(idx / g.Ns);
+  const long long r = idx - comp * g.Ns;
+  const int X = (int)(r % g.Lx), Y = (int)((r / g.Lx) % g.Ly), Z = (int)(r / ((long long)g.Lx * g.Ly));
+  if (constrained(g, comp, X, Y, Z)) return false;
+  int ex[2], ox[2], ey[2], oy[2], ez[2], oz[2];
+  const int nx = ev_cands(X, P, g.nx, ex, ox), ny = ev_cands(Y, P, g.ny, ey, oy),
+            nz = ev_cands(Z, P, g.nz, ez, oz);
+  s = 0.0;
+  for (int a = 0; a < nz; ++a)
+    for (int b = 0; b < ny; ++b)
+      for (int c = 0; c < nx; ++c) {
+        const long long e = ((long long)ez[a] * g.ny + ey[b]) * g.nx + ex[c];
+        s += ev[(e * 3 + comp) * B + (oz[a] * N + oy[b]) * N + ox[c]];
+      }
+  return true;
+}
+
+template <int N>
+__global__ void __launch_bounds__(256) k_ev_gather(double* __restrict__ y, const double* __restrict__ ev,
+                                                   const __grid_constant__ Geo g, const int* skip) {
+  if (skip && *(volatile const int*)skip) return;
+  const long long total = 3 * g.Ns;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    double s;
+    if (ev_point<N>(ev, g, idx, s)) y[idx] += s;
   }
 }
 

@@ -286,9 +286,12 @@ __device__ __forceinline__ void v3_forward(const Tab3<N, M>& tb, const Geo& g, c
   }
 }
 
+// evb != nullptr (E-vector mode): the element's box goes to evb[comp][k][j][i]
+// instead of being scattered with RED into the lattice.
 template <int N, int M, int WPE, int NC, bool GRAD, bool VAL>
 __device__ __forceinline__ void v3_backward(const Tab3<N, M>& tb, const Geo& g, double* __restrict__ dst,
-                                            int X0, int Y0, int Z0, double* A, double* B, int t, int gid) {
+                                            int X0, int Y0, int Z0, double* A, double* B, int t, int gid,
+                                            double* evb = nullptr) {
   using C = V3<N, M, WPE, NC>;
   constexpr int NX = NC * N * N, NY = NC * N * M, NZ = NC * M * M;
 #pragma unroll 1
@@ -389,7 +392,8 @@ __device__ __forceinline__ void v3_backward(const Tab3<N, M>& tb, const Geo& g, 
             if (GRAD) acc = fma(tb.bDx[a][i], jx[a], acc);
             acc = fma(tb.bBx[a][i], jyz[a], acc);
           }
-          if (!chk || !constrained(g, comp, X0 + i, Y, Z)) red_add(row + i, acc);
+          if (evb) evb[((comp * N + k) * N + j) * N + i] = acc;
+          else if (!chk || !constrained(g, comp, X0 + i, Y, Z)) red_add(row + i, acc);
         }
       }
     }
@@ -546,12 +550,13 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
       }
     }
     group_sync<WPE>(gid);
+    double* evb = args.ev ? args.ev + (((long long)ek * g.ny + ej) * g.nx + ei) * 3 * (N * N * N) : nullptr;
     if (MODE == MODE_MASS)
-      v3_backward<N, M, WPE, NC, false, true>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid);
+      v3_backward<N, M, WPE, NC, false, true>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb);
     else if (MODE == MODE_FINT)
-      v3_backward<N, M, WPE, NC, true, false>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid);
+      v3_backward<N, M, WPE, NC, true, false>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb);
     else
-      v3_backward<N, M, WPE, NC, true, VAL>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid);
+      v3_backward<N, M, WPE, NC, true, VAL>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb);
   }
 }
 

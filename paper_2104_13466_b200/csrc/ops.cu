@@ -12,6 +12,7 @@
 #include "element_kernels.cuh"
 #include "element_v3.cuh"
 #include "element_v4.cuh"
+#include "pcg_small.cuh"
 
 #ifndef SDME_ORDER
 #error "compile with -DSDME_ORDER=P"
@@ -81,6 +82,16 @@ struct DefaultShape {
   using type = Shape<N, M, WPE, 3, (WPE == 1 ? 2 : 1), 1>;
 };
 
+// E-vector mode: y += gathered element boxes (after the single element launch)
+template <int N>
+void ev_gather(sdme_ctx* c, const OpArgs& a) {
+  ++c->launches;  // the element launch
+  const long long n = 3 * c->geo.Ns;
+  const unsigned grid = (unsigned)std::min<long long>((n + 255) / 256, 148LL * 8);
+  k_ev_gather<N><<<grid, 256, 0, c->st>>>(a.y, c->d_ev, c->geo, a.skip);
+  ++c->launches;
+}
+
 template <int N, int M, class S, int MODE, bool VAL, class TB = Tab3<N, M>>
 void launch_v3(sdme_ctx* c, const TB& tb, OpArgs a) {
   constexpr bool VALS = VAL || MODE == MODE_MASS;
@@ -94,6 +105,15 @@ void launch_v3(sdme_ctx* c, const TB& tb, OpArgs a) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     max_blocks = std::max(1, nb) * sms;
+  }
+  if (c->ev_mode) {
+    a.colour = -1;
+    a.ev = c->d_ev;
+    const long long need = (colour_count(c->geo, -1) + S::EPB - 1) / S::EPB;
+    kern<<<(unsigned)std::min<long long>(need, max_blocks), S::EPB * S::WPE * 32, smem, c->st>>>(tb, c->geo, a);
+    if (c->ev_no_gather) ++c->launches;
+    else ev_gather<N>(c, a);
+    return;
   }
   for (int col = 0; col < 8; ++col) {
     const long long cnt = colour_count(c->geo, col);
@@ -256,6 +276,14 @@ template <int N, int M>
 void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, double* y, double ck, double cm) {
   const Tab3<N, M> tb = make_tab3<N, M>(c);
   OpArgs a{u, p, y, ck, cm, 0, c->d_flag, c->cur_skip};
+  if constexpr (N <= 5) {
+    // E-vector mode (small meshes, one launch over all elements): latency
+    // shape, four warps per element, all three components per stage
+    if (c->ev_mode && c->variant != 6) {
+      element_eo_or_plain<N, M, Shape<N, M, 4, 3, 1, 1>>(c, mode, tb, a);
+      return;
+    }
+  }
   if constexpr (N == 5 && M == 5) {
     // P = 4, m = 5 (BASELINE config 2); schedule history in profiles/variants_r01.txt.
     // SDME_VARIANT: 3 = 3-component shape (8 warps/SM), 2 = component-serial,
@@ -264,7 +292,7 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
       element_shape<N, M, Shape<N, M, 1, 3, 2, 4>>(c, mode, tb, a);
       return;
     }
-    if (c->variant == 4) { element_v4_modes<N, M, 8, false>(c, mode, tb, a); return; }
+    if (c->variant == 4 && !c->ev_mode) { element_v4_modes<N, M, 8, false>(c, mode, tb, a); return; }
     if (c->variant == 2) { element_shape<N, M, Shape<N, M, 1, 1, 1, 12>>(c, mode, tb, a); return; }
     using SK = Shape<N, M, 1, 1, 1, 11, true>;
     if (c->variant == 5) { element_shape<N, M, SK>(c, mode, tb, a); return; }
@@ -292,6 +320,14 @@ void diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm) {
   }
   const Tab<N, M> tb = make_tab<N, M>(c);
   OpArgs a{u, nullptr, d, ck, cm, 0, c->d_flag};
+  if (c->ev_mode) {
+    a.colour = -1;
+    a.ev = c->d_ev;
+    const long long cnt = colour_count(c->geo, -1);
+    element_diag<N, M, EB><<<(unsigned)((cnt + EB - 1) / EB), 128, smem, c->st>>>(tb, c->geo, a);
+    ev_gather<N>(c, a);
+    return;
+  }
   for (int col = 0; col < 8; ++col) {
     const long long cnt = colour_count(c->geo, col);
     if (cnt == 0) continue;
@@ -301,9 +337,17 @@ void diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm) {
   }
 }
 
+template <int N>
+void pcg_small_impl(sdme_ctx* c, double* x, double* r, double* p, double* ap, const double* dinv,
+                    cudaGraphConditionalHandle cond) {
+  k_pcg_small<N><<<kSmallCta, kSmallThreads, 0, c->st>>>(x, r, p, ap, dinv, c->d_ev, c->geo, c->d_scal,
+                                                         c->d_status, cond);
+  ++c->launches;
+}
+
 template <int N, int M>
 const Ops* ops_for() {
-  static const Ops o{&element_impl<N, M>, &diag_impl<N, M>};
+  static const Ops o{&element_impl<N, M>, &diag_impl<N, M>, &pcg_small_impl<N>};
   return &o;
 }
 

@@ -15,6 +15,7 @@
 #include "contact_kernels.cuh"
 #include "element_kernels.cuh"
 #include "vector_kernels.cuh"
+#include "pcg_small.cuh"
 
 #include "ctx.cuh"
 
@@ -136,10 +137,7 @@ int reset_flag(sdme_ctx* ctx) {
   return SDME_OK;
 }
 
-int check_flag(sdme_ctx* ctx) {
-  CK(cudaMemcpyAsync(ctx->h_flag, ctx->d_flag, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->st));
-  CK(cudaStreamSynchronize(ctx->st));
-  const unsigned long long f = *ctx->h_flag;
+int flag_error(sdme_ctx* ctx, unsigned long long f) {
   if (f != kNoFlag) {
     const long long nq = (long long)ctx->m * ctx->m * ctx->m;
     const int64_t e = (int64_t)(f / nq);
@@ -149,6 +147,12 @@ int check_flag(sdme_ctx* ctx) {
     return set_err(ctx, SDME_INVERSION, buf, e, q);
   }
   return SDME_OK;
+}
+
+int check_flag(sdme_ctx* ctx) {
+  CK(cudaMemcpyAsync(ctx->h_flag, ctx->d_flag, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return flag_error(ctx, ctx->h_flag[0]);
 }
 
 // y = A p  with A = c_k K(u) + c_m M (y zeroed first)
@@ -162,6 +166,72 @@ int apply_raw(sdme_ctx* ctx, const double* u, const double* p, double* y, double
 }
 
 }  // namespace
+
+// The whole PCG solve as one CUDA graph: a conditional while-node whose body
+// is one iteration; the iteration's last kernel clears the condition once the
+// status word is set, so the host waits once per solve.  Small meshes
+// (E-vector mode) run the iteration as one element launch + one cluster
+// kernel (pcg_small.cuh); others as the 7-kernel sequence.
+int build_pcg_graph(sdme_ctx* ctx, const double* pu, double* px, double* r, double* p, double* ap, double* dinv,
+                  double c_k, double c_m) {
+  const bool small = ctx->ev_mode && ctx->nvec <= kSmallPcgMax && ctx->ops->pcg_small;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  CK(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle cond;
+  CK(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = cond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t loop;
+  CK(cudaGraphAddNode(&loop, graph, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  const long long l0 = ctx->launches;
+  CK(cudaStreamBeginCaptureToGraph(ctx->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  ctx->cur_skip = ctx->d_status;
+  if (small) {
+    // E-vector element launch, then one cluster kernel for the rest
+    ctx->ev_no_gather = true;
+    if (c_k != 0.0)
+      ctx->ops->element(ctx, MODE_APPLY, pu, p, ap, c_k, c_m);
+    else
+      ctx->ops->element(ctx, MODE_MASS, nullptr, p, ap, 0.0, c_m);
+    ctx->ev_no_gather = false;
+    ctx->ops->pcg_small(ctx, px, r, p, ap, dinv, cond);
+  } else {
+    k_zero<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(ap, ctx->nvec, ctx->d_status);
+    if (c_k != 0.0)
+      ctx->ops->element(ctx, MODE_APPLY, pu, p, ap, c_k, c_m);
+    else
+      ctx->ops->element(ctx, MODE_MASS, nullptr, p, ap, 0.0, c_m);
+    k_pcg_pap<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(p, ap, ctx->nvec, ctx->d_partial, ctx->d_status);
+    k_pcg_alpha<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, ctx->d_status);
+    k_pcg_update<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(px, r, p, ap, dinv, ctx->d_scal, ctx->nvec,
+                                                          ctx->d_partial, ctx->d_status);
+    k_pcg_check<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, ctx->d_status);
+    k_pcg_p<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, r, dinv, ctx->d_scal, ctx->nvec, ctx->d_status,
+                                                       cond);
+    ctx->launches += 6;
+  }
+  ctx->cur_skip = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(ctx->st, &body);
+  const long long per_iter = ctx->launches - l0;
+  ctx->launches = l0;
+  if (ce != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    return set_err(ctx, SDME_CUDA_ERROR, std::string("graph capture: ") + cudaGetErrorString(ce));
+  }
+  if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    return set_err(ctx, SDME_CUDA_ERROR, "graph instantiate failed");
+  }
+  ctx->pcg_graph = graph;
+  ctx->pcg_exec = exec;
+  ctx->pcg_per_iter = per_iter;
+  return SDME_OK;
+}
 
 // =========================================================================
 extern "C" {
@@ -212,8 +282,19 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   if (cudaMalloc(&ctx->d_partial, kRedBlocks * 4 * sizeof(double)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
   if (cudaMalloc(&ctx->d_scal, 16 * sizeof(double)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
   if (cudaMallocHost(&ctx->h_scal, 16 * sizeof(double)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
-  if (cudaMalloc(&ctx->d_flag, sizeof(unsigned long long)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
-  if (cudaMallocHost(&ctx->h_flag, sizeof(unsigned long long)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+  if (cudaMalloc(&ctx->d_flag, 2 * sizeof(unsigned long long)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+  ctx->d_dflag = ctx->d_flag + 1;
+  // E-vector mode for meshes too small to fill the GPU with 8 colour passes
+  // (each pass would hold < 1 element per SM slot); SDME_EV=0/1 forces it.
+  {
+    const long long ne = (long long)g.nx * g.ny * g.nz;
+    ctx->ev_mode = ne <= kEvMaxElements;
+    if (const char* v = getenv("SDME_EV")) ctx->ev_mode = atoi(v) != 0;
+    if (ctx->ev_mode &&
+        cudaMalloc(&ctx->d_ev, (size_t)ne * 3 * n * n * n * sizeof(double)) != cudaSuccess)
+      return fail(SDME_CUDA_ERROR);
+  }
+  if (cudaMallocHost(&ctx->h_flag, 2 * sizeof(unsigned long long)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
   if (cudaMalloc(&ctx->d_status, sizeof(int)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
   if (cudaMallocHost(&ctx->h_status, sizeof(int)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
   // free mask from the Dirichlet planes
@@ -252,6 +333,9 @@ int sdme_destroy(sdme_ctx* ctx) {
     if (p) cudaFree(p);
   cudaFree(ctx->d_perm);
   cudaFree(ctx->d_free);
+  cudaFree(ctx->d_ev);
+  if (ctx->pcg_exec) cudaGraphExecDestroy(ctx->pcg_exec);
+  if (ctx->pcg_graph) cudaGraphDestroy(ctx->pcg_graph);
   cudaFree(ctx->d_fbuf);
   cudaFree(ctx->d_partial);
   cudaFree(ctx->d_scal);
@@ -467,86 +551,66 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
   double* dinv = vec(ctx, ctx->v_dinv);
   if (iters) *iters = 0;
   if (relres) *relres = 0.0;
-  // preconditioner (solver.py:102-126): built before the ||b|| short-circuit
-  if (precond == 1) {
-    if ((rc = sdme_diag(ctx, u_lin, c_k, c_m, ctx->v_ap))) return rc;
-    if ((rc = sdme_vec_reciprocal(ctx, ctx->v_dinv, ctx->v_ap))) return rc;
-  } else if (precond == 0) {
-    k_fill_masked<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(dinv, ctx->d_free, 1.0, ctx->nvec);
-    ++ctx->launches;
-  } else {
+  if (precond != 0 && precond != 1)
     return set_err(ctx, SDME_BAD_ARGUMENT, "unknown preconditioner (out of scope: sgs)");
+  // Everything up to the end of the iterations is queued without a host
+  // wait; the outcomes (element inversion in the diagonal, non-positive
+  // diagonal, ||b|| = 0, converged / indefinite / maxit) are read back once
+  // and reported in the reference's order (solver.py:102-170).
+  if ((rc = reset_flag(ctx))) return rc;
+  CK(cudaMemcpyAsync(ctx->d_dflag, &kNoFlag, sizeof(kNoFlag), cudaMemcpyHostToDevice, ctx->st));
+  if (precond == 1) {
+    CK(cudaMemsetAsync(ap, 0, ctx->nvec * sizeof(double), ctx->st));
+    ctx->ops->diag(ctx, pu, ap, c_k, c_m);
+    k_invert_diag<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(dinv, ap, ctx->d_free, ctx->nvec, ctx->d_dflag);
+  } else {
+    k_fill_masked<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(dinv, ctx->d_free, 1.0, ctx->nvec);
   }
-  // ||b||
-  if ((rc = dot_into(ctx, pb, pb, S_SCRATCH)) || (rc = read_scalars(ctx))) return rc;
-  const double nb = std::sqrt(ctx->h_scal[S_SCRATCH]);
+  ++ctx->launches;
+  // ||b||, scalar state and status word on the device; r = b ; p = z = dinv r ; rz = r.z
+  if ((rc = dot_into(ctx, pb, pb, S_SCRATCH))) return rc;
+  k_pcg_init<<<1, 32, 0, ctx->st>>>(ctx->d_scal, tol, (double)maxit, ctx->d_status, ctx->d_flag);
+  ++ctx->launches;
   CK(cudaMemsetAsync(px, 0, ctx->nvec * sizeof(double), ctx->st));
-  if (nb == 0.0) {
-    CK(cudaStreamSynchronize(ctx->st));
-    return SDME_OK;
-  }
-  // r = b ; p = z = dinv r ; rz = r.z
   CK(cudaMemcpyAsync(r, pb, ctx->nvec * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
   k_mul<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, dinv, r, ctx->nvec);
   ++ctx->launches;
   if ((rc = dot_into(ctx, r, p, S_RZ0))) return rc;
+  if (maxit > 0) {
+    // warm the operator's one-time launch setup (function attributes,
+    // occupancy queries) outside the capture, once per operator kind
+    const int kind = (c_k != 0.0 ? 1 : 0) | (c_m != 0.0 ? 2 : 0);
+    if (!(ctx->pcg_warm & (1 << kind))) {
+      if ((rc = apply_raw(ctx, pu, p, ap, c_k, c_m))) return rc;
+      ctx->pcg_warm |= 1 << kind;
+    }
+    // one graph launch per solve (build_pcg_graph); the instantiated graph is
+    // reused while the operands are the same (every Newton step of a run)
+    const sdme_ctx::PcgKey key{pu, px, c_k, c_m};
+    if (!ctx->pcg_exec || !(key == ctx->pcg_key)) {
+      if (ctx->pcg_exec) cudaGraphExecDestroy(ctx->pcg_exec);
+      if (ctx->pcg_graph) cudaGraphDestroy(ctx->pcg_graph);
+      ctx->pcg_exec = nullptr;
+      ctx->pcg_graph = nullptr;
+      if ((rc = build_pcg_graph(ctx, pu, px, r, p, ap, dinv, c_k, c_m))) return rc;
+      ctx->pcg_key = key;
+    }
+    CK(cudaGraphLaunch(ctx->pcg_exec, ctx->st));
+  }
+  CK(cudaMemcpyAsync(ctx->h_flag, ctx->d_flag, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+  if ((rc = read_scalars(ctx)) || (rc = check_launch(ctx))) return rc;
+  if (c_k != 0.0 && (rc = flag_error(ctx, ctx->h_flag[0]))) return rc;
+  if (precond == 1 && ctx->h_flag[1] != kNoFlag)
+    return set_err(ctx, SDME_BAD_DIAGONAL, "diagonal preconditioner needs positive diagonal entries",
+                   (int64_t)ctx->h_flag[1], -1);
+  const double nb = ctx->h_scal[S_NB];
+  if (nb == 0.0) return SDME_OK;
   int status = PCG_MAXIT;
   if (maxit > 0) {
-    // device scalar state
-    double init[S_COUNT];
-    CK(cudaMemcpyAsync(init, ctx->d_scal, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
-    CK(cudaStreamSynchronize(ctx->st));
-    init[S_NB] = nb;
-    init[S_TOL] = tol;
-    init[S_RELPREV] = 1.0;
-    init[S_ITER] = 0.0;
-    init[S_MAXIT] = (double)maxit;
-    CK(cudaMemcpyAsync(ctx->d_scal, init, S_COUNT * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
-    CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int), ctx->st));
-    // warm the operator's one-time launch setup outside the capture
-    if ((rc = apply_raw(ctx, pu, p, ap, c_k, c_m))) return rc;
-    // one iteration as a CUDA graph; every kernel exits early once stopped
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    const long long l0 = ctx->launches;
-    CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
-    ctx->cur_skip = ctx->d_status;
-    k_zero<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(ap, ctx->nvec, ctx->d_status);
-    if (c_k != 0.0)
-      ctx->ops->element(ctx, MODE_APPLY, pu, p, ap, c_k, c_m);
-    else
-      ctx->ops->element(ctx, MODE_MASS, nullptr, p, ap, 0.0, c_m);
-    k_pcg_pap<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(p, ap, ctx->nvec, ctx->d_partial, ctx->d_status);
-    k_pcg_alpha<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, ctx->d_status);
-    k_pcg_update<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(px, r, p, ap, dinv, ctx->d_scal, ctx->nvec,
-                                                          ctx->d_partial, ctx->d_status);
-    k_pcg_check<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, ctx->d_status);
-    k_pcg_p<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, r, dinv, ctx->d_scal, ctx->nvec, ctx->d_status);
-    ctx->cur_skip = nullptr;
-    const cudaError_t ce = cudaStreamEndCapture(ctx->st, &graph);
-    const long long per_iter = ctx->launches - l0 + 6;
-    ctx->launches = l0;
-    if (ce != cudaSuccess) return set_err(ctx, SDME_CUDA_ERROR, std::string("graph capture: ") + cudaGetErrorString(ce));
-    if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
-      cudaGraphDestroy(graph);
-      return set_err(ctx, SDME_CUDA_ERROR, "graph instantiate failed");
-    }
-    long long launched = 0;
-    int chunk = 2;
-    for (;;) {
-      for (int g = 0; g < chunk; ++g) cudaGraphLaunch(exec, ctx->st);
-      launched += chunk;
-      ctx->launches += chunk * per_iter;
-      CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
-      CK(cudaStreamSynchronize(ctx->st));
-      if (*ctx->h_status != PCG_RUNNING || launched > (long long)maxit + 64) break;
-      chunk = std::min(chunk * 2, 16);
-    }
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
-    if ((rc = check_launch(ctx)) || (rc = read_scalars(ctx))) return rc;
     status = *ctx->h_status;
     const int it = (int)ctx->h_scal[S_ITER];
+    ctx->launches += ctx->pcg_per_iter * it;
     if (status == PCG_CONVERGED) {
       if (iters) *iters = it;
       if (relres) *relres = ctx->h_scal[S_STOPREL];

@@ -9,16 +9,9 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "pcg_state.cuh"
+
 namespace sdme {
-
-constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed -> deterministic partials
-constexpr int kRedThreads = 256;
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  return v;
-}
 
 // Block-wide sum of NV values in fixed order; result valid in thread 0.
 template <int NV>
@@ -110,24 +103,6 @@ __global__ void k_lincomb(LinComb lc, double* y, long long n) {
 // several iterations between checks without changing the result.  The order
 // of checks is the reference's: pAp <= 0 -> error (residual of the previous
 // iterate), then the recursive-residual test, then maxit.
-enum {
-  S_RZ0 = 0,   // r.z of the previous iterate, ping-pong by iteration parity
-  S_RZ1,
-  S_PAP,
-  S_ALPHA,
-  S_BETA,
-  S_NB,        // ||b||
-  S_TOL,
-  S_RELPREV,   // relative residual of the previous iterate (PCGError stats)
-  S_ITER,      // iterations completed
-  S_STOPREL,   // relative residual at stop
-  S_MAXIT,
-  S_SCRATCH,   // generic dot result
-  S_COUNT
-};
-enum { PCG_RUNNING = 0, PCG_CONVERGED = 1, PCG_INDEFINITE = 2, PCG_MAXIT = 3 };
-
-__device__ __forceinline__ bool pcg_done(const int* status) { return status && *(volatile const int*)status != 0; }
 
 // partial p.ap (skips once stopped)
 __global__ void __launch_bounds__(kRedThreads) k_pcg_pap(const double* __restrict__ p, const double* __restrict__ ap,
@@ -140,6 +115,26 @@ __global__ void __launch_bounds__(kRedThreads) k_pcg_pap(const double* __restric
   double out[1];
   block_sum<1>(acc, out);
   if (threadIdx.x == 0) partial[blockIdx.x] = out[0];
+}
+
+// scalar state of a new solve from ||b||^2 in S_SCRATCH; ||b|| = 0 stops at
+// once, and so does a raised flag (inverted element or non-positive diagonal
+// while building the preconditioner: reported by the host, nothing to iterate)
+__global__ void k_pcg_init(double* s, double tol, double maxit, int* status, const unsigned long long* flags) {
+  if (threadIdx.x == 0) {
+    if (flags[0] != ~0ull || flags[1] != ~0ull) {
+      *status = PCG_STOPPED;
+      return;
+    }
+    const double nb = sqrt(s[S_SCRATCH]);
+    s[S_NB] = nb;
+    s[S_TOL] = tol;
+    s[S_RELPREV] = 1.0;
+    s[S_ITER] = 0.0;
+    s[S_STOPREL] = 0.0;
+    s[S_MAXIT] = maxit;
+    *status = nb == 0.0 ? PCG_CONVERGED : PCG_RUNNING;
+  }
 }
 
 // pap, indefinite test, alpha = rz / pap
@@ -219,10 +214,14 @@ __global__ void __launch_bounds__(kRedThreads) k_pcg_check(const double* partial
   }
 }
 
-// p = dinv r + beta p
+// p = dinv r + beta p ; last kernel of an iteration: ends the graph's while loop once stopped
 __global__ void k_pcg_p(double* __restrict__ p, const double* __restrict__ r, const double* __restrict__ dinv,
-                        const double* __restrict__ s, long long n, const int* status) {
-  if (pcg_done(status)) return;
+                        const double* __restrict__ s, long long n, const int* status,
+                        cudaGraphConditionalHandle cond) {
+  if (pcg_done(status)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+    return;
+  }
   const double beta = s[S_BETA];
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)

@@ -335,3 +335,25 @@ def test_explicit_momentum_conservation():
     assert abs(p1 - p0) <= 1e-10 * abs(p0)
     ut = traj.state.t * v0
     assert np.abs(traj.state.u - ut).max() <= 1e-8 * np.abs(ut).max()
+
+
+@pytest.mark.parametrize("tag,P,m", [("SDME_M", 4, 6), ("LagrangeGLL", 3, 4), ("ModalJacobi", 2, 3),
+                                     ("SDME_H", 6, 7)])
+def test_evector_mode_matches_colour_passes(tag, P, m, monkeypatch):
+    """Small meshes use one launch + deterministic gather (E-vector mode);
+    large ones 8 colour passes with RED.  Both orders of summation agree to
+    rounding, and each is bit-reproducible."""
+    out = {}
+    rng = np.random.default_rng(3)
+    for mode in ("0", "1"):
+        monkeypatch.setenv("SDME_EV", mode)
+        pb = gpu_problem(tag, P, m, (3, 2, 2), (1.5, 1.0, 1.0), [("xmin", (0, 1, 2))])
+        if mode == "0":
+            u = 1e-3 * rng.uniform(-1, 1, pb.n_free)
+            p = rng.standard_normal(pb.n_free)
+        out[mode] = [pb.internal_force(u), pb.apply_tangent(u, p, c_m=3.0e4), pb.mass_apply(p),
+                     pb.tangent_diagonal(u, c_m=3.0e4)]
+        again = pb.apply_tangent(u, p, c_m=3.0e4)
+        assert np.array_equal(again, out[mode][1])
+    for a, b in zip(out["0"], out["1"]):
+        assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
