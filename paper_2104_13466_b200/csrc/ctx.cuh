@@ -20,7 +20,7 @@ struct SdmeOps {
   void (*diag)(sdme_ctx*, const double* u, double* d, double ck, double cm);
   // small-mesh PCG iteration tail after an E-vector element launch (pcg_small.cuh)
   void (*pcg_small)(sdme_ctx*, double* x, double* r, double* p, double* ap, const double* dinv,
-                    cudaGraphConditionalHandle cond);
+                    cudaGraphConditionalHandle cond, int has_cond);
 };
 
 struct sdme_ctx {
@@ -71,7 +71,8 @@ struct sdme_ctx {
     double ck = 0.0, cm = 0.0;
     bool operator==(const PcgKey& o) const { return u == o.u && x == o.x && ck == o.ck && cm == o.cm; }
   } pcg_key;
-  long long pcg_per_iter = 0;  // element launch leaves A p in d_ev (small PCG path gathers)
+  long long pcg_per_iter = 0;
+  bool pcg_direct = false;  // SDME_PCG_DIRECT: no graph (profiling aid)  // element launch leaves A p in d_ev (small PCG path gathers)
   double* d_ev = nullptr;
 };
 

@@ -778,23 +778,37 @@ __device__ __forceinline__ int ev_cands(int X, int P, int n, int (&e)[2], int (&
 }
 
 // gathered value of lattice entry idx (comp-major); false on constrained points
+// (E-vector mode only: meshes of <= kEvMaxElements elements, so 32-bit index math)
 template <int N>
-__device__ __forceinline__ bool ev_point(const double* __restrict__ ev, const Geo& g, long long idx, double& s) {
+__device__ __forceinline__ bool ev_point(const double* __restrict__ ev, const Geo& g, long long idx_, double& s) {
   constexpr int P = N - 1, B = N * N * N;
-  const int comp = (int)(idx / g.Ns);
-  const long long r = idx - comp * g.Ns;
-  const int X = (int)(r % g.Lx), Y = (int)((r / g.Lx) % g.Ly), Z = (int)(r / ((long long)g.Lx * g.Ly));
+  const int idx = (int)idx_, ns = (int)g.Ns;
+  const int comp = idx / ns;
+  const int r = idx - comp * ns;
+  const int rxy = r / g.Lx, X = r - rxy * g.Lx;
+  const int Z = rxy / g.Ly, Y = rxy - Z * g.Ly;
   if (constrained(g, comp, X, Y, Z)) return false;
   int ex[2], ox[2], ey[2], oy[2], ez[2], oz[2];
   const int nx = ev_cands(X, P, g.nx, ex, ox), ny = ev_cands(Y, P, g.ny, ey, oy),
             nz = ev_cands(Z, P, g.nz, ez, oz);
-  s = 0.0;
-  for (int a = 0; a < nz; ++a)
-    for (int b = 0; b < ny; ++b)
-      for (int c = 0; c < nx; ++c) {
-        const long long e = ((long long)ez[a] * g.ny + ey[b]) * g.nx + ex[c];
-        s += ev[(e * 3 + comp) * B + (oz[a] * N + oy[b]) * N + ox[c]];
+  // all (up to 8) loads issued before the fixed-order sum
+  double v[8];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const bool ok = a < nz && b < ny && c < nx;
+        const int e = (ez[a & (nz - 1)] * g.ny + ey[b & (ny - 1)]) * g.nx + ex[c & (nx - 1)];
+        v[(a * 2 + b) * 2 + c] =
+            ok ? ev[(long long)(e * 3 + comp) * B + (oz[a & (nz - 1)] * N + oy[b & (ny - 1)]) * N +
+                    ox[c & (nx - 1)]]
+               : 0.0;
       }
+  s = 0.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) s += v[t];
   return true;
 }
 

@@ -339,9 +339,25 @@ void diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm) {
 
 template <int N>
 void pcg_small_impl(sdme_ctx* c, double* x, double* r, double* p, double* ap, const double* dinv,
-                    cudaGraphConditionalHandle cond) {
-  k_pcg_small<N><<<kSmallCta, kSmallThreads, 0, c->st>>>(x, r, p, ap, dinv, c->d_ev, c->geo, c->d_scal,
-                                                         c->d_status, cond);
+                    cudaGraphConditionalHandle cond, int has_cond) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_pcg_small<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kSmallCta);
+  cfg.blockDim = dim3(kSmallThreads);
+  cfg.stream = c->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kSmallCta;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_pcg_small<N>, x, r, p, ap, dinv, (const double*)c->d_ev, c->geo, c->d_scal,
+                     c->d_status, cond, has_cond);
   ++c->launches;
 }
 

@@ -20,13 +20,18 @@
 
 namespace sdme {
 
-constexpr int kSmallCta = 8;
+constexpr int kSmallCta = 16;  // non-portable cluster size (attribute set at launch)
 constexpr int kSmallThreads = 1024;
 constexpr long long kSmallPcgMax = 1LL << 18;  // lattice entries (3 Ns) for this path
 
-// CTA-wide fixed-order sum of NV values into out[NV] (shared), visible to all threads
+// Cluster-wide sum of NV values: warp trees -> CTA tree (warp 0) -> the
+// kSmallCta CTA partials read from distributed shared memory by lanes 0..7 of
+// warp 0 and combined by the same fixed tree, so every CTA obtains the same
+// bit-identical totals in tot[] (shared).  part[] must not be rewritten
+// until every CTA has passed a later cluster barrier.
 template <int NV>
-__device__ __forceinline__ void cta_sum(double (&v)[NV], double (*red)[kSmallThreads / 32], double* out) {
+__device__ __forceinline__ void cluster_sum(cooperative_groups::cluster_group& cl, double (&v)[NV],
+                                            double (*red)[kSmallThreads / 32], double* part, double* tot) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
@@ -34,22 +39,34 @@ __device__ __forceinline__ void cta_sum(double (&v)[NV], double (*red)[kSmallThr
     if (lane == 0) red[k][wid] = s;
   }
   __syncthreads();
-  if (threadIdx.x < NV) {
-    double s = 0.0;
-    for (int w = 0; w < kSmallThreads / 32; ++w) s += red[threadIdx.x][w];
-    out[threadIdx.x] = s;
+  if (wid == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double s = warp_sum(red[k][lane]);
+      if (lane == 0) part[k] = s;
+    }
   }
+  cl.sync();
+  if (wid == 0) {
+    const double* rp = cl.map_shared_rank(part, lane < kSmallCta ? lane : 0);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double s = warp_sum(lane < kSmallCta ? rp[k] : 0.0);
+      if (lane == 0) tot[k] = s;
+    }
+  }
+  __syncthreads();
 }
 
 template <int N>
-__global__ void __cluster_dims__(kSmallCta, 1, 1) __launch_bounds__(kSmallThreads)
+__global__ void __launch_bounds__(kSmallThreads)
     k_pcg_small(double* __restrict__ x, double* __restrict__ r, double* __restrict__ p, double* __restrict__ ap,
                 const double* __restrict__ dinv, const double* __restrict__ ev, const __grid_constant__ Geo g,
-                double* s, int* status, cudaGraphConditionalHandle cond) {
+                double* s, int* status, cudaGraphConditionalHandle cond, int has_cond) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   __shared__ double red[2][kSmallThreads / 32];
-  __shared__ double part[3];
+  __shared__ double part[3], tot[3];
   const bool lead = cl.block_rank() == 0 && threadIdx.x == 0;
   // every read of the scalar state happens before any write (first cluster barrier)
   const bool done = pcg_done(status);
@@ -58,7 +75,7 @@ __global__ void __cluster_dims__(kSmallCta, 1, 1) __launch_bounds__(kSmallThread
                relprev = s[S_RELPREV];
   cl.sync();
   if (done) {
-    if (lead) cudaGraphSetConditional(cond, 0);
+    if (lead) set_cond(cond, has_cond);
     return;
   }
   const long long n = 3 * g.Ns;
@@ -72,17 +89,15 @@ __global__ void __cluster_dims__(kSmallCta, 1, 1) __launch_bounds__(kSmallThread
     ap[i] = v;
     a1[0] = fma(p[i], v, a1[0]);
   }
-  cta_sum<1>(a1, red, part);
-  cl.sync();
-  double pap = 0.0;
-  for (int q = 0; q < kSmallCta; ++q) pap += cl.map_shared_rank(part, q)[0];
+  cluster_sum<1>(cl, a1, red, part, tot);
+  const double pap = tot[0];
   if (!(pap > 0.0)) {
     if (lead) {
       s[S_PAP] = pap;
       s[S_ITER] = (double)k;
       s[S_STOPREL] = relprev;
       *status = PCG_INDEFINITE;
-      cudaGraphSetConditional(cond, 0);
+      set_cond(cond, has_cond);
     }
     cl.sync();
     return;
@@ -101,15 +116,8 @@ __global__ void __cluster_dims__(kSmallCta, 1, 1) __launch_bounds__(kSmallThread
     a2[0] = fma(ri, ri, a2[0]);
     a2[1] = fma(ri, dinv[i] * ri, a2[1]);
   }
-  __syncthreads();  // red[] reuse
-  cta_sum<2>(a2, red, part + 1);
-  cl.sync();
-  double rr = 0.0, rz = 0.0;
-  for (int q = 0; q < kSmallCta; ++q) {
-    const double* pq = cl.map_shared_rank(part, q);
-    rr += pq[1];
-    rz += pq[2];
-  }
+  cluster_sum<2>(cl, a2, red, part + 1, tot + 1);
+  const double rr = tot[1], rz = tot[2];
   cl.sync();  // remote reads done before any CTA exits
   const double rel = sqrt(rr) / nb;
   if (rel <= tol || (double)k >= maxit) {
@@ -117,7 +125,7 @@ __global__ void __cluster_dims__(kSmallCta, 1, 1) __launch_bounds__(kSmallThread
       s[S_ITER] = (double)k;
       s[S_STOPREL] = rel;
       *status = rel <= tol ? PCG_CONVERGED : PCG_MAXIT;
-      cudaGraphSetConditional(cond, 0);
+      set_cond(cond, has_cond);
     }
     return;
   }

@@ -36,4 +36,9 @@ enum { PCG_RUNNING = 0, PCG_CONVERGED = 1, PCG_INDEFINITE = 2, PCG_MAXIT = 3, PC
 
 __device__ __forceinline__ bool pcg_done(const int* status) { return status && *(volatile const int*)status != 0; }
 
+// end the enclosing conditional while-node (no-op outside a graph)
+__device__ __forceinline__ void set_cond(cudaGraphConditionalHandle cond, int has_cond) {
+  if (has_cond) cudaGraphSetConditional(cond, 0);
+}
+
 }  // namespace sdme

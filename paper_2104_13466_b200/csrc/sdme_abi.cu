@@ -167,6 +167,40 @@ int apply_raw(sdme_ctx* ctx, const double* u, const double* p, double* y, double
 
 }  // namespace
 
+// One PCG iteration on ctx->st: E-vector element launch + one cluster kernel
+// (small meshes) or the 7-kernel sequence.  Every kernel returns at once when
+// the status word is set; the last one clears the graph's loop condition.
+void enqueue_pcg_iteration(sdme_ctx* ctx, const double* pu, double* px, double* r, double* p, double* ap,
+                           double* dinv, double c_k, double c_m, cudaGraphConditionalHandle cond, int has_cond) {
+  const bool small = ctx->ev_mode && ctx->nvec <= kSmallPcgMax && ctx->ops->pcg_small;
+  ctx->cur_skip = ctx->d_status;
+  if (small) {
+    // E-vector element launch, then one cluster kernel for the rest
+    ctx->ev_no_gather = true;
+    if (c_k != 0.0)
+      ctx->ops->element(ctx, MODE_APPLY, pu, p, ap, c_k, c_m);
+    else
+      ctx->ops->element(ctx, MODE_MASS, nullptr, p, ap, 0.0, c_m);
+    ctx->ev_no_gather = false;
+    ctx->ops->pcg_small(ctx, px, r, p, ap, dinv, cond, has_cond);
+  } else {
+    k_zero<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(ap, ctx->nvec, ctx->d_status);
+    if (c_k != 0.0)
+      ctx->ops->element(ctx, MODE_APPLY, pu, p, ap, c_k, c_m);
+    else
+      ctx->ops->element(ctx, MODE_MASS, nullptr, p, ap, 0.0, c_m);
+    k_pcg_pap<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(p, ap, ctx->nvec, ctx->d_partial, ctx->d_status);
+    k_pcg_alpha<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, ctx->d_status);
+    k_pcg_update<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(px, r, p, ap, dinv, ctx->d_scal, ctx->nvec,
+                                                          ctx->d_partial, ctx->d_status);
+    k_pcg_check<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, ctx->d_status);
+    k_pcg_p<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, r, dinv, ctx->d_scal, ctx->nvec, ctx->d_status,
+                                                       cond, has_cond);
+    ctx->launches += 6;
+  }
+  ctx->cur_skip = nullptr;
+}
+
 // The whole PCG solve as one CUDA graph: a conditional while-node whose body
 // is one iteration; the iteration's last kernel clears the condition once the
 // status word is set, so the host waits once per solve.  Small meshes
@@ -174,7 +208,6 @@ int apply_raw(sdme_ctx* ctx, const double* u, const double* p, double* y, double
 // kernel (pcg_small.cuh); others as the 7-kernel sequence.
 int build_pcg_graph(sdme_ctx* ctx, const double* pu, double* px, double* r, double* p, double* ap, double* dinv,
                   double c_k, double c_m) {
-  const bool small = ctx->ev_mode && ctx->nvec <= kSmallPcgMax && ctx->ops->pcg_small;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   CK(cudaGraphCreate(&graph, 0));
@@ -190,32 +223,7 @@ int build_pcg_graph(sdme_ctx* ctx, const double* pu, double* px, double* r, doub
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   const long long l0 = ctx->launches;
   CK(cudaStreamBeginCaptureToGraph(ctx->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  ctx->cur_skip = ctx->d_status;
-  if (small) {
-    // E-vector element launch, then one cluster kernel for the rest
-    ctx->ev_no_gather = true;
-    if (c_k != 0.0)
-      ctx->ops->element(ctx, MODE_APPLY, pu, p, ap, c_k, c_m);
-    else
-      ctx->ops->element(ctx, MODE_MASS, nullptr, p, ap, 0.0, c_m);
-    ctx->ev_no_gather = false;
-    ctx->ops->pcg_small(ctx, px, r, p, ap, dinv, cond);
-  } else {
-    k_zero<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(ap, ctx->nvec, ctx->d_status);
-    if (c_k != 0.0)
-      ctx->ops->element(ctx, MODE_APPLY, pu, p, ap, c_k, c_m);
-    else
-      ctx->ops->element(ctx, MODE_MASS, nullptr, p, ap, 0.0, c_m);
-    k_pcg_pap<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(p, ap, ctx->nvec, ctx->d_partial, ctx->d_status);
-    k_pcg_alpha<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, ctx->d_status);
-    k_pcg_update<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(px, r, p, ap, dinv, ctx->d_scal, ctx->nvec,
-                                                          ctx->d_partial, ctx->d_status);
-    k_pcg_check<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, ctx->d_status);
-    k_pcg_p<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, r, dinv, ctx->d_scal, ctx->nvec, ctx->d_status,
-                                                       cond);
-    ctx->launches += 6;
-  }
-  ctx->cur_skip = nullptr;
+  enqueue_pcg_iteration(ctx, pu, px, r, p, ap, dinv, c_k, c_m, cond, 1);
   const cudaError_t ce = cudaStreamEndCapture(ctx->st, &body);
   const long long per_iter = ctx->launches - l0;
   ctx->launches = l0;
@@ -246,6 +254,7 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   sdme_ctx* ctx = new sdme_ctx();
   ctx->ops = ops;
   if (const char* v = getenv("SDME_VARIANT")) ctx->variant = atoi(v);
+  if (const char* v = getenv("SDME_PCG_DIRECT")) ctx->pcg_direct = atoi(v) != 0;
   ctx->P = d->P;
   ctx->m = d->m;
   ctx->n = d->P + 1;
@@ -587,7 +596,17 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
     // one graph launch per solve (build_pcg_graph); the instantiated graph is
     // reused while the operands are the same (every Newton step of a run)
     const sdme_ctx::PcgKey key{pu, px, c_k, c_m};
-    if (!ctx->pcg_exec || !(key == ctx->pcg_key)) {
+    if (ctx->pcg_direct) {
+      // profiling aid (SDME_PCG_DIRECT=1): plain launches, one host check per
+      // iteration, so per-kernel tools see every launch
+      for (int it = 0; it <= maxit; ++it) {
+        enqueue_pcg_iteration(ctx, pu, px, r, p, ap, dinv, c_k, c_m, 0, 0);
+        CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        if (*ctx->h_status != PCG_RUNNING) break;
+      }
+      ctx->pcg_per_iter = 0;
+    } else if (!ctx->pcg_exec || !(key == ctx->pcg_key)) {
       if (ctx->pcg_exec) cudaGraphExecDestroy(ctx->pcg_exec);
       if (ctx->pcg_graph) cudaGraphDestroy(ctx->pcg_graph);
       ctx->pcg_exec = nullptr;
@@ -595,7 +614,7 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
       if ((rc = build_pcg_graph(ctx, pu, px, r, p, ap, dinv, c_k, c_m))) return rc;
       ctx->pcg_key = key;
     }
-    CK(cudaGraphLaunch(ctx->pcg_exec, ctx->st));
+    if (!ctx->pcg_direct) CK(cudaGraphLaunch(ctx->pcg_exec, ctx->st));
   }
   CK(cudaMemcpyAsync(ctx->h_flag, ctx->d_flag, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));

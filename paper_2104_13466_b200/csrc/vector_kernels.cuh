@@ -217,9 +217,9 @@ __global__ void __launch_bounds__(kRedThreads) k_pcg_check(const double* partial
 // p = dinv r + beta p ; last kernel of an iteration: ends the graph's while loop once stopped
 __global__ void k_pcg_p(double* __restrict__ p, const double* __restrict__ r, const double* __restrict__ dinv,
                         const double* __restrict__ s, long long n, const int* status,
-                        cudaGraphConditionalHandle cond) {
+                        cudaGraphConditionalHandle cond, int has_cond) {
   if (pcg_done(status)) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(cond, has_cond);
     return;
   }
   const double beta = s[S_BETA];
