@@ -142,28 +142,12 @@ __device__ __forceinline__ void eo_qsplit(const double (&q)[M], double (&qe)[Hal
   if (M % 2) qe[H] = q[H];
 }
 
-// y = T^T q for a B-type (F = +1) or D-type (F = -1) operator, y accumulated (ACC) or set
-template <int N, int M, int MIR, int F, int WE, int WO, bool ACC>
-__device__ __forceinline__ void eo_bwd(const EoBwd<M, WE, WO>& t, const double (&qe)[Half<M>::HP],
-                                       const double (&qo)[Half<M>::H > 0 ? Half<M>::H : 1], double (&y)[N]) {
+// Reconstruction of y = T^T q from the even / odd partial sums YE (WE) and
+// YO (WO) of a B-type (F = +1) or D-type (F = -1) operator; y accumulated
+// (ACC) or set.  For D-type the mirror sign is -s, so the fixed sets swap.
+template <int N, int MIR, int F, int WE, int WO, bool ACC>
+__device__ __forceinline__ void eo_recon(const double* YE, const double* YO, double (&y)[N]) {
   using Mr = Mir<N, MIR>;
-  constexpr int H = Half<M>::H, HP = Half<M>::HP;
-  double YE[WE > 0 ? WE : 1], YO[WO > 0 ? WO : 1];
-#pragma unroll
-  for (int e = 0; e < WE; ++e) {
-    double s = 0.0;
-#pragma unroll
-    for (int a = 0; a < HP; ++a) s = fma(t.E[e][a], qe[a], s);
-    YE[e] = s;
-  }
-#pragma unroll
-  for (int o = 0; o < WO; ++o) {
-    double s = 0.0;
-#pragma unroll
-    for (int a = 0; a < H; ++a) s = fma(t.O[o][a], qo[a], s);
-    YO[o] = s;
-  }
-  // reconstruction; for D-type the mirror sign is -s, so fixed sets swap
 #pragma unroll
   for (int p = 0; p < Mr::NP; ++p) {
     const int l = Mr::nth(0, p), r = Mr::sig(l);
@@ -191,6 +175,29 @@ __device__ __forceinline__ void eo_bwd(const EoBwd<M, WE, WO>& t, const double (
     if (ACC) y[l] += YO[Mr::NP + f];
     else y[l] = YO[Mr::NP + f];
   }
+}
+
+// y = T^T q for a B-type (F = +1) or D-type (F = -1) operator, y accumulated (ACC) or set
+template <int N, int M, int MIR, int F, int WE, int WO, bool ACC>
+__device__ __forceinline__ void eo_bwd(const EoBwd<M, WE, WO>& t, const double (&qe)[Half<M>::HP],
+                                       const double (&qo)[Half<M>::H > 0 ? Half<M>::H : 1], double (&y)[N]) {
+  constexpr int H = Half<M>::H, HP = Half<M>::HP;
+  double YE[WE > 0 ? WE : 1], YO[WO > 0 ? WO : 1];
+#pragma unroll
+  for (int e = 0; e < WE; ++e) {
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < HP; ++a) s = fma(t.E[e][a], qe[a], s);
+    YE[e] = s;
+  }
+#pragma unroll
+  for (int o = 0; o < WO; ++o) {
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < H; ++a) s = fma(t.O[o][a], qo[a], s);
+    YO[o] = s;
+  }
+  eo_recon<N, MIR, F, WE, WO, ACC>(YE, YO, y);
 }
 
 }  // namespace sdme

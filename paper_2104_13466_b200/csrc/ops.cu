@@ -12,7 +12,12 @@
 #include "element_kernels.cuh"
 #include "element_v3.cuh"
 #include "element_v4.cuh"
+#include "element_v5.cuh"
 #include "pcg_small.cuh"
+
+#ifndef SDME_V5_MINB
+#define SDME_V5_MINB 8
+#endif
 
 #ifndef SDME_ORDER
 #error "compile with -DSDME_ORDER=P"
@@ -272,6 +277,45 @@ void element_eo_or_plain(sdme_ctx* c, int mode, const Tab3<N, M>& tb, OpArgs a) 
     element_shape<N, M, S>(c, mode, tb, a);
 }
 
+// v5 (element_v5.cuh): K.p with the p-side z stage, point work and z'
+// stage fused per quadrature column in registers
+template <int N, int M, int MINB, bool VAL, int MIR>
+void launch_v5(sdme_ctx* c, const TabEO<N, M, MIR>& tb, OpArgs a) {
+  using C = V3<N, M, 1, 1, false>;
+  constexpr int smem = (C::PER + 2 * N * N * N) * 8;
+  auto kern = element_v5<N, M, MINB, VAL, MIR>;
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    max_blocks = std::max(1, nb) * sms;
+  }
+  if (c->ev_mode) {
+    a.colour = -1;
+    a.ev = c->d_ev;
+    kern<<<(unsigned)std::min<long long>(colour_count(c->geo, -1), max_blocks), 32, smem, c->st>>>(tb, c->geo, a);
+    if (c->ev_no_gather) ++c->launches;
+    else ev_gather<N>(c, a);
+    return;
+  }
+  for (int col = 0; col < 8; ++col) {
+    const long long cnt = colour_count(c->geo, col);
+    if (cnt == 0) continue;
+    a.colour = col;
+    kern<<<(unsigned)std::min<long long>(cnt, max_blocks), 32, smem, c->st>>>(tb, c->geo, a);
+    ++c->launches;
+  }
+}
+
+template <int N, int M, int MIR>
+void apply_v5(sdme_ctx* c, const TabEO<N, M, MIR>& tb, OpArgs a) {
+  if (a.c_m != 0.0) launch_v5<N, M, SDME_V5_MINB, true, MIR>(c, tb, a);
+  else launch_v5<N, M, SDME_V5_MINB, false, MIR>(c, tb, a);
+}
+
 template <int N, int M>
 void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, double* y, double ck, double cm) {
   const Tab3<N, M> tb = make_tab3<N, M>(c);
@@ -296,6 +340,13 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
     if (c->variant == 2) { element_shape<N, M, Shape<N, M, 1, 1, 1, 12>>(c, mode, tb, a); return; }
     using SK = Shape<N, M, 1, 1, 1, 11, true>;
     if (c->variant == 5) { element_shape<N, M, SK>(c, mode, tb, a); return; }
+    if (mode == MODE_APPLY && c->variant == 8 && c->mir >= 0) {
+      // column-fused v5 (element_v5.cuh): 255 registers, 8 warps/SM; measured
+      // 2.87 ms vs 2.50 ms for the default below (profiles/variants_r01.txt)
+      if (c->mir == 0) apply_v5<N, M, 0>(c, make_tabeo<N, M, 0>(c), a);
+      else apply_v5<N, M, 1>(c, make_tabeo<N, M, 1>(c), a);
+      return;
+    }
     // default for every mode: component-serial, cp.async-staged rows,
     // even-odd contractions, 11 warps/SM (K.p 2.47 ms, f_int 1.60 ms, mass 1.27 ms)
     element_eo_or_plain<N, M, SK>(c, mode, tb, a);
