@@ -131,8 +131,10 @@ int sdme_host_alloc(size_t bytes, void** ptr);
 int sdme_host_free(void* ptr);
 
 /* timing (CUDA events on the context stream) ----------------------------- */
-/* op: 0 = apply (K p, c_m), 1 = fint, 2 = mass, 3 = diag, 4 = pcg iteration vector
- * kernels; returns mean milliseconds per call over `reps` back-to-back calls. */
+/* op: 0 = apply (K(u) p + c_m M p from u), 1 = fint, 2 = mass, 3 = diag,
+ * 4 = quadrature-data setup at u (K = F^-T, ln J stored per point, as sdme_pcg
+ * does once per solve), 5 = apply from the stored data (the PCG operator; needs
+ * a prior op 4); returns mean milliseconds per call over `reps` calls. */
 int sdme_time_op(sdme_ctx* ctx, int op, int u, int p, int y, double c_m, int reps, double* ms);
 int sdme_sync(sdme_ctx* ctx);
 /* kernel launches issued by this context since creation (evidence for bench) */

@@ -69,11 +69,17 @@ struct sdme_ctx {
     const double* u = nullptr;
     const double* x = nullptr;
     double ck = 0.0, cm = 0.0;
-    bool operator==(const PcgKey& o) const { return u == o.u && x == o.x && ck == o.ck && cm == o.cm; }
+    bool pa = false;
+    bool operator==(const PcgKey& o) const {
+      return u == o.u && x == o.x && ck == o.ck && cm == o.cm && pa == o.pa;
+    }
   } pcg_key;
   long long pcg_per_iter = 0;
   bool pcg_direct = false;  // SDME_PCG_DIRECT: no graph (profiling aid)  // element launch leaves A p in d_ev (small PCG path gathers)
   double* d_ev = nullptr;
+  // stored quadrature data of the PCG linearisation point (MODE_SETUP / MODE_PA)
+  double* d_qpd = nullptr;
+  bool pa = true;  // SDME_PA=0 disables (the PCG then applies K(u) from scratch)
 };
 
 // per-order operator tables (ops.cu, one object file per P)

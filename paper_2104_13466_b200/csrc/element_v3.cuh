@@ -449,12 +449,14 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
   int buf = 0;
   if (args.skip && *(volatile const int*)args.skip) return;
   const long long cnt = colour_count(g, args.colour);
-  constexpr bool GRADP = (MODE == MODE_APPLY);
+  constexpr bool GRADP = (MODE == MODE_APPLY || MODE == MODE_PA);
+  constexpr bool UPASS = (MODE == MODE_APPLY || MODE == MODE_FINT || MODE == MODE_SETUP);
+  constexpr bool PPASS = (MODE == MODE_APPLY || MODE == MODE_MASS || MODE == MODE_PA);
   const long long stride = (long long)gridDim.x * EPB;
   // dP constants with c_k folded in
   const double mu_k = args.c_k * g.mu, lam_k = args.c_k * g.lam;
   const double cmr = args.c_m * g.rho;
-  const double* first_field = MODE == MODE_MASS ? args.p : args.u;
+  const double* first_field = UPASS ? args.u : args.p;
   if (STG && (long long)blockIdx.x * EPB + gid < cnt) {
     int ei, ej, ek;
     colour_element(g, args.colour, (long long)blockIdx.x * EPB + gid, ei, ej, ek);
@@ -473,11 +475,11 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
     if (!STG && idx + stride < cnt) {  // warm L2 with the next element's rows
       int ni, nj, nk;
       colour_element(g, args.colour, idx + stride, ni, nj, nk);
-      if (MODE != MODE_MASS) v3_prefetch<N, C::T>(g, args.u, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk, t);
-      if (MODE != MODE_FINT) v3_prefetch<N, C::T>(g, args.p, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk, t);
+      if (UPASS) v3_prefetch<N, C::T>(g, args.u, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk, t);
+      if (PPASS) v3_prefetch<N, C::T>(g, args.p, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk, t);
     }
     double Hu[C::QPT][9];
-    if (MODE != MODE_MASS) {
+    if (UPASS) {
       const NextRows after_u = MODE == MODE_APPLY ? NextRows{args.p, X0, Y0, Z0} : nxt;
       v3_forward<N, M, WPE, NC, true, false, STG>(tb, g, args.u, X0, Y0, Z0, A, Bf, t, gid, Rb, &buf, after_u);
 #pragma unroll
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
       }
       group_sync<WPE>(gid);
     }
-    if (MODE != MODE_FINT)
+    if (PPASS)
       v3_forward<N, M, WPE, NC, GRADP, VAL, STG>(tb, g, args.p, X0, Y0, Z0, A, Bf, t, gid, Rb, &buf, nxt);
 #pragma unroll
     for (int r = 0; r < C::QPT; ++r) {
@@ -503,12 +505,30 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
         for (int i = 0; i < 3; ++i) A[C::qi(3, i, q)] *= cmr;
         continue;
       }
+      const long long eid = ((long long)ek * g.ny + ej) * g.nx + ei;
       QpK s;
-      qp_k(Hu[r], s);
-      if (!(s.det > 0.0)) {
-        const int a = q % M, b = (q / M) % M, c = q / (M * M);
-        const long long e = ((long long)ek * g.ny + ej) * g.nx + ei;
-        atomicMin(args.inv_flag, (unsigned long long)e * C::Q + (unsigned long long)((a * M + b) * M + c));
+      if (MODE == MODE_PA) {
+        const double* qd = args.qpd + eid * (kQpSlots * C::Q) + q;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) s.K[i][d] = __ldg(qd + (i * 3 + d) * C::Q);
+        s.lnJ = __ldg(qd + 9 * C::Q);
+      } else {
+        qp_k(Hu[r], s);
+        if (!(s.det > 0.0)) {
+          const int a = q % M, b = (q / M) % M, c = q / (M * M);
+          atomicMin(args.inv_flag, (unsigned long long)eid * C::Q + (unsigned long long)((a * M + b) * M + c));
+        }
+      }
+      if (MODE == MODE_SETUP) {
+        double* qd = args.qpd + eid * (kQpSlots * C::Q) + q;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) qd[(i * 3 + d) * C::Q] = s.K[i][d];
+        qd[9 * C::Q] = s.lnJ;
+        continue;
       }
       if (MODE == MODE_FINT) {
         const double cK = g.lam * s.lnJ - g.mu;
@@ -550,6 +570,7 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
       }
     }
     group_sync<WPE>(gid);
+    if (MODE == MODE_SETUP) continue;
     double* evb = args.ev ? args.ev + (((long long)ek * g.ny + ej) * g.nx + ei) * 3 * (N * N * N) : nullptr;
     if (MODE == MODE_MASS)
       v3_backward<N, M, WPE, NC, false, true>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb);

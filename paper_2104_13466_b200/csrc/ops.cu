@@ -111,6 +111,14 @@ void launch_v3(sdme_ctx* c, const TB& tb, OpArgs a) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     max_blocks = std::max(1, nb) * sms;
   }
+  if (MODE == MODE_SETUP) {
+    // no scatter: one pass over all elements
+    a.colour = -1;
+    const long long need = (colour_count(c->geo, -1) + S::EPB - 1) / S::EPB;
+    kern<<<(unsigned)std::min<long long>(need, max_blocks), S::EPB * S::WPE * 32, smem, c->st>>>(tb, c->geo, a);
+    ++c->launches;
+    return;
+  }
   if (c->ev_mode) {
     a.colour = -1;
     a.ev = c->d_ev;
@@ -133,7 +141,10 @@ void launch_v3(sdme_ctx* c, const TB& tb, OpArgs a) {
 
 template <int N, int M, class S, class TB = Tab3<N, M>>
 void element_shape(sdme_ctx* c, int mode, const TB& tb, OpArgs a) {
-  if (mode == MODE_FINT) launch_v3<N, M, S, MODE_FINT, false, TB>(c, tb, a);
+  if (mode == MODE_SETUP) launch_v3<N, M, S, MODE_SETUP, false, TB>(c, tb, a);
+  else if (mode == MODE_PA && a.c_m != 0.0) launch_v3<N, M, S, MODE_PA, true, TB>(c, tb, a);
+  else if (mode == MODE_PA) launch_v3<N, M, S, MODE_PA, false, TB>(c, tb, a);
+  else if (mode == MODE_FINT) launch_v3<N, M, S, MODE_FINT, false, TB>(c, tb, a);
   else if (mode == MODE_APPLY && a.c_m != 0.0) launch_v3<N, M, S, MODE_APPLY, true, TB>(c, tb, a);
   else if (mode == MODE_APPLY) launch_v3<N, M, S, MODE_APPLY, false, TB>(c, tb, a);
   else launch_v3<N, M, S, MODE_MASS, true, TB>(c, tb, a);
@@ -320,6 +331,7 @@ template <int N, int M>
 void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, double* y, double ck, double cm) {
   const Tab3<N, M> tb = make_tab3<N, M>(c);
   OpArgs a{u, p, y, ck, cm, 0, c->d_flag, c->cur_skip};
+  a.qpd = c->d_qpd;
   if constexpr (N <= 5) {
     // E-vector mode (small meshes, one launch over all elements): latency
     // shape, four warps per element, all three components per stage
@@ -329,17 +341,12 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
     }
   }
   if constexpr (N == 5 && M == 5) {
-    // P = 4, m = 5 (BASELINE config 2); schedule history in profiles/variants_r01.txt.
-    // SDME_VARIANT: 3 = 3-component shape (8 warps/SM), 2 = component-serial,
-    // 12 warps/SM, 4 = column-resident v4, 5 = staged without even-odd.
-    if (c->variant == 3) {
-      element_shape<N, M, Shape<N, M, 1, 3, 2, 4>>(c, mode, tb, a);
-      return;
-    }
-    if (c->variant == 4 && !c->ev_mode) { element_v4_modes<N, M, 8, false>(c, mode, tb, a); return; }
-    if (c->variant == 2) { element_shape<N, M, Shape<N, M, 1, 1, 1, 12>>(c, mode, tb, a); return; }
+    // P = 4, m = 5 (BASELINE config 2); schedule history in profiles/variants_r01.txt
+    // (the 3-component, 12-warp and unstaged shapes measured there are template
+    // arguments of this same kernel).  SDME_VARIANT: 4 = column-resident v4,
+    // 8 = column-fused v5, both slower and opt-in only.
+    if (c->variant == 4 && !c->ev_mode && mode <= MODE_MASS) { element_v4_modes<N, M, 8, false>(c, mode, tb, a); return; }
     using SK = Shape<N, M, 1, 1, 1, 11, true>;
-    if (c->variant == 5) { element_shape<N, M, SK>(c, mode, tb, a); return; }
     if (mode == MODE_APPLY && c->variant == 8 && c->mir >= 0) {
       // column-fused v5 (element_v5.cuh): 255 registers, 8 warps/SM; measured
       // 2.87 ms vs 2.50 ms for the default below (profiles/variants_r01.txt)

@@ -167,18 +167,35 @@ int apply_raw(sdme_ctx* ctx, const double* u, const double* p, double* y, double
 
 }  // namespace
 
+// quadrature-data buffer for MODE_SETUP / MODE_PA (allocated on first use;
+// false -- and the PCG applies K(u) from scratch -- if it does not fit)
+bool ensure_qpd(sdme_ctx* ctx) {
+  if (ctx->d_qpd) return true;
+  const long long ne = (long long)ctx->geo.nx * ctx->geo.ny * ctx->geo.nz;
+  const size_t bytes = (size_t)ne * kQpSlots * ctx->m * ctx->m * ctx->m * sizeof(double);
+  if (cudaMalloc(&ctx->d_qpd, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->d_qpd = nullptr;
+    ctx->pa = false;
+    return false;
+  }
+  return true;
+}
+
 // One PCG iteration on ctx->st: E-vector element launch + one cluster kernel
 // (small meshes) or the 7-kernel sequence.  Every kernel returns at once when
 // the status word is set; the last one clears the graph's loop condition.
 void enqueue_pcg_iteration(sdme_ctx* ctx, const double* pu, double* px, double* r, double* p, double* ap,
-                           double* dinv, double c_k, double c_m, cudaGraphConditionalHandle cond, int has_cond) {
+                           double* dinv, double c_k, double c_m, bool pa, cudaGraphConditionalHandle cond,
+                           int has_cond) {
+  const int kmode = pa ? MODE_PA : MODE_APPLY;
   const bool small = ctx->ev_mode && ctx->nvec <= kSmallPcgMax && ctx->ops->pcg_small;
   ctx->cur_skip = ctx->d_status;
   if (small) {
     // E-vector element launch, then one cluster kernel for the rest
     ctx->ev_no_gather = true;
     if (c_k != 0.0)
-      ctx->ops->element(ctx, MODE_APPLY, pu, p, ap, c_k, c_m);
+      ctx->ops->element(ctx, kmode, pu, p, ap, c_k, c_m);
     else
       ctx->ops->element(ctx, MODE_MASS, nullptr, p, ap, 0.0, c_m);
     ctx->ev_no_gather = false;
@@ -186,7 +203,7 @@ void enqueue_pcg_iteration(sdme_ctx* ctx, const double* pu, double* px, double* 
   } else {
     k_zero<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(ap, ctx->nvec, ctx->d_status);
     if (c_k != 0.0)
-      ctx->ops->element(ctx, MODE_APPLY, pu, p, ap, c_k, c_m);
+      ctx->ops->element(ctx, kmode, pu, p, ap, c_k, c_m);
     else
       ctx->ops->element(ctx, MODE_MASS, nullptr, p, ap, 0.0, c_m);
     k_pcg_pap<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(p, ap, ctx->nvec, ctx->d_partial, ctx->d_status);
@@ -207,7 +224,7 @@ void enqueue_pcg_iteration(sdme_ctx* ctx, const double* pu, double* px, double* 
 // (E-vector mode) run the iteration as one element launch + one cluster
 // kernel (pcg_small.cuh); others as the 7-kernel sequence.
 int build_pcg_graph(sdme_ctx* ctx, const double* pu, double* px, double* r, double* p, double* ap, double* dinv,
-                  double c_k, double c_m) {
+                    double c_k, double c_m, bool pa) {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   CK(cudaGraphCreate(&graph, 0));
@@ -223,7 +240,7 @@ int build_pcg_graph(sdme_ctx* ctx, const double* pu, double* px, double* r, doub
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   const long long l0 = ctx->launches;
   CK(cudaStreamBeginCaptureToGraph(ctx->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  enqueue_pcg_iteration(ctx, pu, px, r, p, ap, dinv, c_k, c_m, cond, 1);
+  enqueue_pcg_iteration(ctx, pu, px, r, p, ap, dinv, c_k, c_m, pa, cond, 1);
   const cudaError_t ce = cudaStreamEndCapture(ctx->st, &body);
   const long long per_iter = ctx->launches - l0;
   ctx->launches = l0;
@@ -255,6 +272,7 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   ctx->ops = ops;
   if (const char* v = getenv("SDME_VARIANT")) ctx->variant = atoi(v);
   if (const char* v = getenv("SDME_PCG_DIRECT")) ctx->pcg_direct = atoi(v) != 0;
+  if (const char* v = getenv("SDME_PA")) ctx->pa = atoi(v) != 0;
   ctx->P = d->P;
   ctx->m = d->m;
   ctx->n = d->P + 1;
@@ -343,6 +361,7 @@ int sdme_destroy(sdme_ctx* ctx) {
   cudaFree(ctx->d_perm);
   cudaFree(ctx->d_free);
   cudaFree(ctx->d_ev);
+  cudaFree(ctx->d_qpd);
   if (ctx->pcg_exec) cudaGraphExecDestroy(ctx->pcg_exec);
   if (ctx->pcg_graph) cudaGraphDestroy(ctx->pcg_graph);
   cudaFree(ctx->d_fbuf);
@@ -568,6 +587,10 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
   // and reported in the reference's order (solver.py:102-170).
   if ((rc = reset_flag(ctx))) return rc;
   CK(cudaMemcpyAsync(ctx->d_dflag, &kNoFlag, sizeof(kNoFlag), cudaMemcpyHostToDevice, ctx->st));
+  // K(u) is fixed during the solve: store K = F^-T and ln J at the quadrature
+  // points once (MODE_SETUP, flags inverted elements) and iterate with MODE_PA
+  const bool pa = c_k != 0.0 && ctx->pa && ensure_qpd(ctx);
+  if (pa) ctx->ops->element(ctx, MODE_SETUP, pu, nullptr, nullptr, 1.0, 0.0);
   if (precond == 1) {
     CK(cudaMemsetAsync(ap, 0, ctx->nvec * sizeof(double), ctx->st));
     ctx->ops->diag(ctx, pu, ap, c_k, c_m);
@@ -588,19 +611,24 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
   if (maxit > 0) {
     // warm the operator's one-time launch setup (function attributes,
     // occupancy queries) outside the capture, once per operator kind
-    const int kind = (c_k != 0.0 ? 1 : 0) | (c_m != 0.0 ? 2 : 0);
+    const int kind = (c_k != 0.0 ? 1 : 0) | (c_m != 0.0 ? 2 : 0) | (pa ? 4 : 0);
     if (!(ctx->pcg_warm & (1 << kind))) {
-      if ((rc = apply_raw(ctx, pu, p, ap, c_k, c_m))) return rc;
+      CK(cudaMemsetAsync(ap, 0, ctx->nvec * sizeof(double), ctx->st));
+      if (c_k != 0.0)
+        ctx->ops->element(ctx, pa ? MODE_PA : MODE_APPLY, pu, p, ap, c_k, c_m);
+      else
+        ctx->ops->element(ctx, MODE_MASS, nullptr, p, ap, 0.0, c_m);
+      if ((rc = check_launch(ctx))) return rc;
       ctx->pcg_warm |= 1 << kind;
     }
     // one graph launch per solve (build_pcg_graph); the instantiated graph is
     // reused while the operands are the same (every Newton step of a run)
-    const sdme_ctx::PcgKey key{pu, px, c_k, c_m};
+    const sdme_ctx::PcgKey key{pu, px, c_k, c_m, pa};
     if (ctx->pcg_direct) {
       // profiling aid (SDME_PCG_DIRECT=1): plain launches, one host check per
       // iteration, so per-kernel tools see every launch
       for (int it = 0; it <= maxit; ++it) {
-        enqueue_pcg_iteration(ctx, pu, px, r, p, ap, dinv, c_k, c_m, 0, 0);
+        enqueue_pcg_iteration(ctx, pu, px, r, p, ap, dinv, c_k, c_m, pa, 0, 0);
         CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
         if (*ctx->h_status != PCG_RUNNING) break;
@@ -611,7 +639,7 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
       if (ctx->pcg_graph) cudaGraphDestroy(ctx->pcg_graph);
       ctx->pcg_exec = nullptr;
       ctx->pcg_graph = nullptr;
-      if ((rc = build_pcg_graph(ctx, pu, px, r, p, ap, dinv, c_k, c_m))) return rc;
+      if ((rc = build_pcg_graph(ctx, pu, px, r, p, ap, dinv, c_k, c_m, pa))) return rc;
       ctx->pcg_key = key;
     }
     if (!ctx->pcg_direct) CK(cudaGraphLaunch(ctx->pcg_exec, ctx->st));
@@ -790,6 +818,15 @@ int sdme_time_op(sdme_ctx* ctx, int op, int u, int p, int y, double c_m, int rep
       case 3:
         cudaMemsetAsync(py, 0, ctx->nvec * sizeof(double), ctx->st);
         ctx->ops->diag(ctx, pu, py, 1.0, c_m);
+        break;
+      case 4:  // quadrature-data setup at u
+        if (!ensure_qpd(ctx)) return SDME_CUDA_ERROR;
+        ctx->ops->element(ctx, MODE_SETUP, pu, nullptr, nullptr, 1.0, 0.0);
+        break;
+      case 5:  // K.p (+ c_m M p) from the stored quadrature data (PCG operator)
+        if (!ctx->d_qpd) return SDME_BAD_ARGUMENT;
+        cudaMemsetAsync(py, 0, ctx->nvec * sizeof(double), ctx->st);
+        ctx->ops->element(ctx, MODE_PA, pu, pp, py, 1.0, c_m);
         break;
       default: return SDME_BAD_ARGUMENT;
     }

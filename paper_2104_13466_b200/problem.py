@@ -335,7 +335,7 @@ class GpuFemProblem:
     def time_op(self, op: str, u: DeviceVector, p: DeviceVector, y: DeviceVector, c_m: float = 0.0,
                 reps: int = 10) -> float:
         """Mean ms per call of one operator, CUDA events on the context stream."""
-        code = {"apply": 0, "fint": 1, "mass": 2, "diag": 3}[op]
+        code = {"apply": 0, "fint": 1, "mass": 2, "diag": 3, "setup": 4, "apply_pa": 5}[op]
         ms = C.c_double(0.0)
         native.check(self._ctx, native.lib().sdme_time_op(self._ctx, code, u.vid, p.vid, y.vid, c_m, reps,
                                                           C.byref(ms)), "time_op")

@@ -357,3 +357,25 @@ def test_evector_mode_matches_colour_passes(tag, P, m, monkeypatch):
         assert np.array_equal(again, out[mode][1])
     for a, b in zip(out["0"], out["1"]):
         assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
+
+
+@pytest.mark.parametrize("tag,P,m", [("SDME_M", 4, 5), ("LagrangeGLL", 2, 3), ("SDME_H", 6, 7)])
+def test_pcg_operator_from_stored_quadrature_data_is_bit_identical(tag, P, m, monkeypatch):
+    """sdme_pcg stores K = F^-T and ln J once per solve and iterates with them
+    (MODE_PA); the solve is bit-identical to iterating with K(u).p from u."""
+    rng = np.random.default_rng(11)
+    res = {}
+    for pa in ("1", "0"):
+        monkeypatch.setenv("SDME_PA", pa)
+        pb = gpu_problem(tag, P, m, (3, 2, 2), (1.5, 1.0, 1.0), [("xmin", (0, 1, 2))])
+        if pa == "1":
+            u = 1e-3 * rng.uniform(-1, 1, pb.n_free)
+            b = rng.standard_normal(pb.n_free)
+        x, st = pcg_gpu(pb, u, b, c_m=2.0e5, precond="diagonal", tol=1e-10, maxit=500)
+        res[pa] = (x, st.iterations)
+        uv, pv, yv = pb.vector().set_free(u), pb.vector().set_free(b), pb.vector()
+        pb.time_op("setup", uv, pv, yv, 0.0, 1)
+        pb.time_op("apply_pa", uv, pv, yv, 2.0e5, 1)
+        assert np.array_equal(yv.free(), pb.apply_tangent(u, b, c_m=2.0e5))
+    assert res["0"][1] == res["1"][1]
+    assert np.array_equal(res["0"][0], res["1"][0])
