@@ -126,6 +126,16 @@ int sdme_contact(sdme_ctx* ctx, int u, int side, int qf, const double* Bf, const
 /* number of face points of a side for the given qf */
 int sdme_contact_points(const sdme_ctx* ctx, int side, int qf, int64_t* n);
 
+/* implicit contact (contact.py:120-140 stiffness, dynamics.py:268-284): with
+ * the active set (g < 0) of the last sdme_contact call,
+ * y += K_c p,  K_c = eps sum_{q active} warea N_f N_g n n^T  (matrix-free) */
+int sdme_contact_apply(sdme_ctx* ctx, int p, int y);
+/* d += diag(K_c) */
+int sdme_contact_diag(sdme_ctx* ctx, int d);
+/* on != 0: sdme_pcg solves with A + K_c (and its diagonal in the Jacobi
+ * preconditioner), the operator of newmark_run with contact (dynamics.py:241) */
+int sdme_pcg_contact(sdme_ctx* ctx, int on);
+
 /* page-locked host buffers (fast H2D/D2H for the free-order vector calls) */
 int sdme_host_alloc(size_t bytes, void** ptr);
 int sdme_host_free(void* ptr);

@@ -345,17 +345,67 @@ class Problem:
 
 
 class Contact:
-    """PenaltyContact force evaluation (contact.py:72-151) without the
-    stiffness matrix (explicit path only needs forces)."""
+    """PenaltyContact (contact.py:72-176): forces, assembled stiffness, the
+    pressure-settled test and the per-step penalty update."""
 
-    def __init__(self, problem: Problem, point, normal, eps, tag, quad_order=None):
+    def __init__(self, problem: Problem, point, normal, eps, tag, quad_order=None, deps=0.0, gap_tol=1e-3,
+                 stress_tol=1e-2):
         self.pb = problem
         self.point = np.asarray(point, dtype=float)
         n = np.asarray(normal, dtype=float)
         self.normal = n / np.linalg.norm(n)
         self.eps = eps
+        self.deps, self.gap_tol, self.stress_tol = deps, gap_tol, stress_tol
         q = quad_order if quad_order is not None else problem.basis.P + 1
         self.faces = problem.face_tables(tag, q)
+        self.last_pressures = None
+        self.history = []
+
+    def stiffness(self, u):
+        """contact.py:129-140: eps sum_{q active} warea N_f N_g (n n^T), CSR."""
+        rows, cols, vals = [], [], []
+        nn = np.outer(self.normal, self.normal)
+        for (e, x, fv, warea, _), g in zip(self.faces, self.gaps(u)):
+            act = g < 0.0
+            if not act.any():
+                continue
+            fv = np.where(np.abs(fv).max(axis=0) > 1e-13, fv, 0.0)  # face support (contact.py:121-123)
+            kf = np.einsum("q,qf,qg->fg", self.eps * warea * act, fv, fv)
+            kc = np.einsum("fg,ce->fcge", kf, nn).reshape(kf.shape[0] * 3, kf.shape[0] * 3)
+            d = self.pb._edofs[e]
+            ok = d >= 0
+            rows.append(np.repeat(d[ok], ok.sum()))
+            cols.append(np.tile(d[ok], ok.sum()))
+            vals.append(kc[np.ix_(ok, ok)].ravel())
+        n = self.pb.n_free
+        if not rows:
+            return None
+        return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(n, n))
+
+    def pressures(self, u):
+        return np.concatenate([np.where(g < 0.0, -self.eps * g, 0.0) for g in self.gaps(u)])
+
+    def settled(self, p):
+        """contact.py:153-160 (and records p as the iteration's pressures)."""
+        prev = self.last_pressures
+        self.last_pressures = p
+        if prev is None or prev.shape != p.shape:
+            return not p.any()
+        scale = max(np.abs(p).max(), np.abs(prev).max())
+        if scale == 0.0:
+            return True
+        return float(np.abs(p - prev).max()) / scale <= self.stress_tol
+
+    def accept_step(self, u):
+        """contact.py:162-176."""
+        gs = np.concatenate(self.gaps(u))
+        pen = max(float(-gs.min()), 0.0)
+        act = gs < 0.0
+        tn = np.where(act, -self.eps * gs, 0.0)
+        self.history.append((self.eps, pen, float(tn[act].min()) if act.any() else 0.0, int(act.sum())))
+        if pen > self.gap_tol and self.deps > 0.0:
+            self.eps += self.deps
+        self.last_pressures = None
 
     def gaps(self, u):
         return [(x + vals @ self.pb.gather(e, u) - self.point) @ self.normal
@@ -368,6 +418,7 @@ class Contact:
             tn = np.where(g < 0.0, -self.eps * g, 0.0)
             if not np.any(g < 0.0):
                 continue
+            vals = np.where(np.abs(vals).max(axis=0) > 1e-13, vals, 0.0)  # face support (contact.py:121-123)
             r = np.einsum("q,qf,c->fc", warea * tn, vals, self.normal)
             self.pb.scatter(out, e, r.reshape(-1))
         return out, gs

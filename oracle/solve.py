@@ -59,8 +59,10 @@ def pcg(a, b, precond="diagonal", tol=1e-8, maxit=10000):
 
 
 def newmark(problem, load, dt, n_steps, newton_tol=1e-8, newton_maxit=25, pcg_tol=1e-10,
-            gamma=0.5, beta=0.25, u0=None, v0=None, maxit=200000):
-    """dynamics.py:173-257 (no contact), condense=False, Jacobi-PCG.
+            gamma=0.5, beta=0.25, u0=None, v0=None, maxit=200000, contact=None):
+    """dynamics.py:173-257, condense=False, Jacobi-PCG, optional penalty
+    contact (residual + fc, Newton waits for settled pressures, operator
+    + K_c of the iteration's active set, accept_step per step).
 
     Returns dict(u, v, a, newton_iters, pcg_iters) with pcg_iters a list of
     (step, newton_iter, iterations)."""
@@ -71,7 +73,16 @@ def newmark(problem, load, dt, n_steps, newton_tol=1e-8, newton_maxit=25, pcg_to
     u = np.zeros(n) if u0 is None else np.array(u0, float)
     v = np.zeros(n) if v0 is None else np.array(v0, float)
     mass = problem.mass()
-    psi0 = load(0.0) - problem.internal_force(u)
+
+    def residual(uk, atr, tt):
+        psi = load(tt) - problem.internal_force(uk) - mass @ atr
+        if contact is None:
+            return psi, True, None
+        fc, _ = contact.force(uk)
+        ok = contact.settled(contact.pressures(uk))
+        return psi + fc, ok, contact.stiffness(uk)
+
+    psi0, _, _ = residual(u, np.zeros(n), 0.0)
     a, _, _ = pcg(mass, psi0, "diagonal", pcg_tol, maxit)
     t = 0.0
     newton_iters, pcg_iters = [], []
@@ -82,15 +93,17 @@ def newmark(problem, load, dt, n_steps, newton_tol=1e-8, newton_maxit=25, pcg_to
         cnt = 0
         for k in range(newton_maxit):
             atr = b1 * (uk - u) - b2 * v - b3 * a
-            psi = load(tn) - problem.internal_force(uk) - mass @ atr
+            psi, ok, kc = residual(uk, atr, tn)
             rn = np.linalg.norm(psi)
             if ref is None:
                 ref = rn
-            if ref == 0.0 or rn <= newton_tol * ref:
+            if ref == 0.0 or (rn <= newton_tol * ref and ok):
                 break
             if k == newton_maxit - 1:
                 raise RuntimeError("Newton did not converge")
             eff = problem.assemble(uk, 1.0, b1)
+            if kc is not None:
+                eff = (eff + kc).tocsr()
             du, its, _ = pcg(eff, psi, "diagonal", pcg_tol, maxit)
             pcg_iters.append((step, k, its))
             uk = uk + du
@@ -99,6 +112,8 @@ def newmark(problem, load, dt, n_steps, newton_tol=1e-8, newton_maxit=25, pcg_to
         an = b1 * (uk - u) - b2 * v - b3 * a
         v = v + dt * ((1.0 - gamma) * a + gamma * an)
         u, a, t = uk, an, tn
+        if contact is not None:
+            contact.accept_step(u)
     return dict(u=u, v=v, a=a, newton_iters=newton_iters, pcg_iters=pcg_iters)
 
 

@@ -4,8 +4,10 @@ Mirrors ``sdmefem.contact`` (``contact.py:25-204``): :class:`RigidObstacle`,
 :class:`ContactParams`, and :class:`GpuPenaltyContact` with
 ``evaluate_forces`` (force, pressures, gaps, active set, settled flag),
 ``accept_step`` (penalty stepping + history) and ``penalty_energy``.  The
-contact *stiffness* matrix (implicit contact) is the next row (SURVEY F3);
-``evaluate_forces`` returns ``stiffness=None``.
+contact stiffness (implicit contact, ``contact.py:120-140``) is a matrix-free
+operator on the device: ``ContactForces.stiffness`` is a :class:`ContactStiffness`
+(``@`` and ``diagonal()``) over the active set of that evaluation, and
+``newmark_run(..., contact=...)`` adds it to the PCG operator.
 """
 
 from __future__ import annotations
@@ -20,7 +22,7 @@ from .basis import gauss_rule
 from .lattice import FACE_TAGS
 from .problem import DeviceVector, GpuFemProblem
 
-__all__ = ["RigidObstacle", "ContactParams", "ContactForces", "GpuPenaltyContact", "gap"]
+__all__ = ["RigidObstacle", "ContactParams", "ContactForces", "ContactStiffness", "GpuPenaltyContact", "gap"]
 
 
 @dataclass(frozen=True)
@@ -70,6 +72,36 @@ class ContactForces:
     settled: bool
 
 
+class ContactStiffness:
+    """K_c = eps sum_{q active} warea N_f N_g (n n^T) of one force evaluation
+    (``contact.py:129-140``), applied matrix-free on the device.  Valid until
+    the next evaluation of the same contact (the active set lives on the device)."""
+
+    def __init__(self, contact: "GpuPenaltyContact", serial: int):
+        self.contact = contact
+        self.serial = serial
+        self.shape = (contact.problem.n_free, contact.problem.n_free)
+
+    def _check(self):
+        if self.serial != self.contact._serial:
+            raise RuntimeError("contact stiffness of an older evaluation (the active set has changed)")
+
+    def __matmul__(self, p: np.ndarray) -> np.ndarray:
+        self._check()
+        pb = self.contact.problem
+        pv = pb._scratch("kc_p").set_free(np.asarray(p, dtype=float))
+        y = pb._scratch("kc_y").fill(0.0)
+        native.check(pb._ctx, native.lib().sdme_contact_apply(pb._ctx, pv.vid, y.vid), "contact_apply")
+        return y.free()
+
+    def diagonal(self) -> np.ndarray:
+        self._check()
+        pb = self.contact.problem
+        d = pb._scratch("kc_y").fill(0.0)
+        native.check(pb._ctx, native.lib().sdme_contact_diag(pb._ctx, d.vid), "contact_diag")
+        return d.free()
+
+
 class GpuPenaltyContact:
     """Penalty contact of one box side against a rigid plane (``contact.py:72-204``)."""
 
@@ -95,11 +127,13 @@ class GpuPenaltyContact:
         self.history = []
         self._fc = None
         self._u = None
+        self._serial = 0  # bumped by every device evaluation (active set)
 
     def forces_(self, u: DeviceVector, fc: DeviceVector, record: bool = False):
         """Device path: fc = contact nodal force at u (no host traffic unless
         ``record`` asks for the gap statistics)."""
         pb = self.problem
+        self._serial += 1
         gaps = np.empty(self.n_points) if record else None
         stats = np.zeros(3) if record else None
         rc = native.lib().sdme_contact(
@@ -113,6 +147,7 @@ class GpuPenaltyContact:
         return gaps
 
     def _gaps(self, u: DeviceVector, fc: DeviceVector):
+        self._serial += 1
         gaps = np.empty(self.n_points)
         rc = native.lib().sdme_contact(
             self.problem._ctx, u.vid, self.side, self.qf, native.dptr(self.Bf), native.dptr(self.xf),
@@ -136,7 +171,19 @@ class GpuPenaltyContact:
         pressures = np.where(act, -self.params.eps_n * g, 0.0)
         settled = self._pressure_settled(pressures)
         self._last_pressures = pressures
-        return ContactForces(fc.free(), None, pressures, g, act, settled)
+        kc = ContactStiffness(self, self._serial) if act.any() else None
+        return ContactForces(fc.free(), kc, pressures, g, act, settled)
+
+    def evaluate_(self, u: DeviceVector, fc: DeviceVector):
+        """Device form of :meth:`evaluate_forces` for the Newton loop: fc on
+        the device, returns (settled, any_active); the gaps (one value per face
+        point) are the only host traffic."""
+        g = self._gaps(u, fc)
+        act = g < 0.0
+        pressures = np.where(act, -self.params.eps_n * g, 0.0)
+        settled = self._pressure_settled(pressures)
+        self._last_pressures = pressures
+        return settled, bool(act.any())
 
     def _pressure_settled(self, pressures):
         """``contact.py:153-160``."""
@@ -152,6 +199,10 @@ class GpuPenaltyContact:
         """``contact.py:162-176``: history row and penalty stepping."""
         u, fc = self._scratch()
         u.set_free(u_free)
+        self.accept_step_(u, fc)
+
+    def accept_step_(self, u: DeviceVector, fc: DeviceVector):
+        """:meth:`accept_step` on a device vector (fc is scratch)."""
         g = self._gaps(u, fc)
         pen = max(float(-g.min()), 0.0) if g.size else 0.0
         act = g < 0.0

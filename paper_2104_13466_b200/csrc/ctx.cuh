@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 
+#include "contact_types.cuh"
 #include "element_kernels.cuh"
 
 struct sdme_ctx;
@@ -70,12 +71,21 @@ struct sdme_ctx {
     const double* x = nullptr;
     double ck = 0.0, cm = 0.0;
     bool pa = false;
+    bool contact = false;
+    double eps = 0.0;
     bool operator==(const PcgKey& o) const {
-      return u == o.u && x == o.x && ck == o.ck && cm == o.cm && pa == o.pa;
+      return u == o.u && x == o.x && ck == o.ck && cm == o.cm && pa == o.pa && contact == o.contact &&
+             eps == o.eps;
     }
   } pcg_key;
   long long pcg_per_iter = 0;
-  bool pcg_direct = false;  // SDME_PCG_DIRECT: no graph (profiling aid)  // element launch leaves A p in d_ev (small PCG path gathers)
+  bool pcg_direct = false;  // SDME_PCG_DIRECT: no graph (profiling aid)
+  // implicit contact: face tables / parameters of the last sdme_contact call
+  // (its gaps in d_gaps define the active set of the contact stiffness)
+  sdme::FaceTab c_ft{};
+  sdme::ContactArgs c_ca{};
+  bool c_ready = false;
+  bool pcg_contact = false;  // sdme_pcg adds K_c (and its diagonal)  // element launch leaves A p in d_ev (small PCG path gathers)
   double* d_ev = nullptr;
   // stored quadrature data of the PCG linearisation point (MODE_SETUP / MODE_PA)
   double* d_qpd = nullptr;

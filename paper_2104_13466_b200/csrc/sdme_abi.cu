@@ -167,6 +167,30 @@ int apply_raw(sdme_ctx* ctx, const double* u, const double* p, double* y, double
 
 }  // namespace
 
+// the 4 in-plane colour passes of one contact evaluation / apply / diagonal
+void launch_contact(sdme_ctx* ctx, ContactArgs ca) {
+  const int ne[3] = {ctx->geo.nx, ctx->geo.ny, ctx->geo.nz};
+  const int d1 = ca.axis == 0 ? 1 : 0, d2 = ca.axis == 2 ? 1 : 2;
+  for (int col = 0; col < 4; ++col) {
+    const int m1 = (ne[d1] - (col & 1) + 1) >> 1, m2 = (ne[d2] - ((col >> 1) & 1) + 1) >> 1;
+    if (m1 <= 0 || m2 <= 0) continue;
+    ca.colour = col;
+    k_contact<<<m1 * m2, 128, 0, ctx->st>>>(ctx->c_ft, ctx->geo, ca);
+    ++ctx->launches;
+  }
+}
+
+// y += K_c p (CONTACT_APPLY) or y += diag(K_c) (CONTACT_DIAG), active set of
+// the last sdme_contact evaluation
+void contact_op(sdme_ctx* ctx, int mode, const double* p, double* y, const int* skip) {
+  ContactArgs ca = ctx->c_ca;
+  ca.mode = mode;
+  ca.u = p;
+  ca.fc = y;
+  ca.skip = skip;
+  launch_contact(ctx, ca);
+}
+
 // quadrature-data buffer for MODE_SETUP / MODE_PA (allocated on first use;
 // false -- and the PCG applies K(u) from scratch -- if it does not fit)
 bool ensure_qpd(sdme_ctx* ctx) {
@@ -186,10 +210,11 @@ bool ensure_qpd(sdme_ctx* ctx) {
 // (small meshes) or the 7-kernel sequence.  Every kernel returns at once when
 // the status word is set; the last one clears the graph's loop condition.
 void enqueue_pcg_iteration(sdme_ctx* ctx, const double* pu, double* px, double* r, double* p, double* ap,
-                           double* dinv, double c_k, double c_m, bool pa, cudaGraphConditionalHandle cond,
-                           int has_cond) {
+                           double* dinv, double c_k, double c_m, bool pa, bool withc,
+                           cudaGraphConditionalHandle cond, int has_cond) {
   const int kmode = pa ? MODE_PA : MODE_APPLY;
-  const bool small = ctx->ev_mode && ctx->nvec <= kSmallPcgMax && ctx->ops->pcg_small;
+  // (the cluster tail gathers A p itself, so K_c p needs the general sequence)
+  const bool small = ctx->ev_mode && ctx->nvec <= kSmallPcgMax && ctx->ops->pcg_small && !withc;
   ctx->cur_skip = ctx->d_status;
   if (small) {
     // E-vector element launch, then one cluster kernel for the rest
@@ -206,6 +231,7 @@ void enqueue_pcg_iteration(sdme_ctx* ctx, const double* pu, double* px, double* 
       ctx->ops->element(ctx, kmode, pu, p, ap, c_k, c_m);
     else
       ctx->ops->element(ctx, MODE_MASS, nullptr, p, ap, 0.0, c_m);
+    if (withc) contact_op(ctx, CONTACT_APPLY, p, ap, ctx->d_status);
     k_pcg_pap<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(p, ap, ctx->nvec, ctx->d_partial, ctx->d_status);
     k_pcg_alpha<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, ctx->d_status);
     k_pcg_update<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(px, r, p, ap, dinv, ctx->d_scal, ctx->nvec,
@@ -224,7 +250,7 @@ void enqueue_pcg_iteration(sdme_ctx* ctx, const double* pu, double* px, double* 
 // (E-vector mode) run the iteration as one element launch + one cluster
 // kernel (pcg_small.cuh); others as the 7-kernel sequence.
 int build_pcg_graph(sdme_ctx* ctx, const double* pu, double* px, double* r, double* p, double* ap, double* dinv,
-                    double c_k, double c_m, bool pa) {
+                    double c_k, double c_m, bool pa, bool withc) {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   CK(cudaGraphCreate(&graph, 0));
@@ -240,7 +266,7 @@ int build_pcg_graph(sdme_ctx* ctx, const double* pu, double* px, double* r, doub
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   const long long l0 = ctx->launches;
   CK(cudaStreamBeginCaptureToGraph(ctx->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  enqueue_pcg_iteration(ctx, pu, px, r, p, ap, dinv, c_k, c_m, pa, cond, 1);
+  enqueue_pcg_iteration(ctx, pu, px, r, p, ap, dinv, c_k, c_m, pa, withc, cond, 1);
   const cudaError_t ce = cudaStreamEndCapture(ctx->st, &body);
   const long long per_iter = ctx->launches - l0;
   ctx->launches = l0;
@@ -590,10 +616,12 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
   // K(u) is fixed during the solve: store K = F^-T and ln J at the quadrature
   // points once (MODE_SETUP, flags inverted elements) and iterate with MODE_PA
   const bool pa = c_k != 0.0 && ctx->pa && ensure_qpd(ctx);
+  const bool withc = c_k != 0.0 && ctx->pcg_contact && ctx->c_ready;
   if (pa) ctx->ops->element(ctx, MODE_SETUP, pu, nullptr, nullptr, 1.0, 0.0);
   if (precond == 1) {
     CK(cudaMemsetAsync(ap, 0, ctx->nvec * sizeof(double), ctx->st));
     ctx->ops->diag(ctx, pu, ap, c_k, c_m);
+    if (withc) contact_op(ctx, CONTACT_DIAG, nullptr, ap, nullptr);
     k_invert_diag<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(dinv, ap, ctx->d_free, ctx->nvec, ctx->d_dflag);
   } else {
     k_fill_masked<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(dinv, ctx->d_free, 1.0, ctx->nvec);
@@ -623,12 +651,12 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
     }
     // one graph launch per solve (build_pcg_graph); the instantiated graph is
     // reused while the operands are the same (every Newton step of a run)
-    const sdme_ctx::PcgKey key{pu, px, c_k, c_m, pa};
+    const sdme_ctx::PcgKey key{pu, px, c_k, c_m, pa, withc, withc ? ctx->c_ca.eps : 0.0};
     if (ctx->pcg_direct) {
       // profiling aid (SDME_PCG_DIRECT=1): plain launches, one host check per
       // iteration, so per-kernel tools see every launch
       for (int it = 0; it <= maxit; ++it) {
-        enqueue_pcg_iteration(ctx, pu, px, r, p, ap, dinv, c_k, c_m, pa, 0, 0);
+        enqueue_pcg_iteration(ctx, pu, px, r, p, ap, dinv, c_k, c_m, pa, withc, 0, 0);
         CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
         if (*ctx->h_status != PCG_RUNNING) break;
@@ -639,7 +667,7 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
       if (ctx->pcg_graph) cudaGraphDestroy(ctx->pcg_graph);
       ctx->pcg_exec = nullptr;
       ctx->pcg_graph = nullptr;
-      if ((rc = build_pcg_graph(ctx, pu, px, r, p, ap, dinv, c_k, c_m, pa))) return rc;
+      if ((rc = build_pcg_graph(ctx, pu, px, r, p, ap, dinv, c_k, c_m, pa, withc))) return rc;
       ctx->pcg_key = key;
     }
     if (!ctx->pcg_direct) CK(cudaGraphLaunch(ctx->pcg_exec, ctx->st));
@@ -760,16 +788,14 @@ int sdme_contact(sdme_ctx* ctx, int u, int side, int qf, const double* Bf, const
   ca.u = pu;
   ca.fc = pf;
   ca.gaps = ctx->d_gaps;
+  ca.mode = CONTACT_FORCE;
+  ctx->c_ft = ft;
+  ctx->c_ca = ca;
+  ctx->c_ready = true;
   CK(cudaMemsetAsync(pf, 0, ctx->nvec * sizeof(double), ctx->st));
   const int ne[3] = {ctx->geo.nx, ctx->geo.ny, ctx->geo.nz};
   const int d1 = ca.axis == 0 ? 1 : 0, d2 = ca.axis == 2 ? 1 : 2;
-  for (int col = 0; col < 4; ++col) {
-    const int m1 = (ne[d1] - (col & 1) + 1) >> 1, m2 = (ne[d2] - ((col >> 1) & 1) + 1) >> 1;
-    if (m1 <= 0 || m2 <= 0) continue;
-    ca.colour = col;
-    k_contact<<<m1 * m2, 128, 0, ctx->st>>>(ft, ctx->geo, ca);
-    ++ctx->launches;
-  }
+  launch_contact(ctx, ca);
   int rc = check_launch(ctx);
   if (rc) return rc;
   if (gaps_host || stats) {
@@ -795,6 +821,29 @@ int sdme_contact(sdme_ctx* ctx, int u, int side, int qf, const double* Bf, const
       stats[2] = (double)act;
     }
   }
+  return SDME_OK;
+}
+
+int sdme_contact_apply(sdme_ctx* ctx, int p, int y) {
+  double* pp = ctx ? vec(ctx, p) : nullptr;
+  double* py = ctx ? vec(ctx, y) : nullptr;
+  if (!pp || !py || pp == py) return SDME_BAD_ARGUMENT;
+  if (!ctx->c_ready) return set_err(ctx, SDME_BAD_ARGUMENT, "no contact evaluation yet (sdme_contact)");
+  contact_op(ctx, CONTACT_APPLY, pp, py, nullptr);
+  return check_launch(ctx);
+}
+
+int sdme_contact_diag(sdme_ctx* ctx, int d) {
+  double* pd = ctx ? vec(ctx, d) : nullptr;
+  if (!pd) return SDME_BAD_ARGUMENT;
+  if (!ctx->c_ready) return set_err(ctx, SDME_BAD_ARGUMENT, "no contact evaluation yet (sdme_contact)");
+  contact_op(ctx, CONTACT_DIAG, nullptr, pd, nullptr);
+  return check_launch(ctx);
+}
+
+int sdme_pcg_contact(sdme_ctx* ctx, int on) {
+  if (!ctx) return SDME_BAD_ARGUMENT;
+  ctx->pcg_contact = on != 0;
   return SDME_OK;
 }
 

@@ -4,7 +4,11 @@
 step for step -- trial acceleration, residual psi = P - R(u) - M a, Newton
 stop relative to the first ||psi|| of the step, effective operator
 K_T + b1 M, Newmark v/a update -- with every vector operation on the GPU and
-the linear solves done by matrix-free Jacobi-PCG.
+the linear solves done by matrix-free Jacobi-PCG.  With
+``contact=`` the residual carries the penalty force, Newton also waits for the
+contact pressures to settle, the operator adds the contact stiffness of the
+current active set (matrix-free, sdme_pcg_contact) and every accepted step
+runs ``accept_step`` -- ``dynamics.py:196-255`` / ``contact.py:103-176``.
 
 ``explicit_run`` is the central-difference scheme of ``dynamics.py:130-170``
 with the row-sum lumped mass and penalty contact against a rigid plane
@@ -18,6 +22,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import native
 from .errors import NewtonDivergenceError
 from .problem import DeviceVector, GpuFemProblem
 from .solver import SolverConfig, StatsLog, pcg_gpu
@@ -128,9 +133,6 @@ def newmark_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
                 cfg: SolverConfig | None = None, gamma: float = 0.5, beta: float = 0.25,
                 contact=None, snapshot_stride: int = 0, track_energy: bool = False) -> Trajectory:
     """Implicit Newmark with Newton-Raphson (``dynamics.py:173-257``)."""
-    if contact is not None:
-        raise NotImplementedError("implicit penalty contact (contact stiffness) is the next row "
-                                  "(SURVEY F3); use explicit_run(..., contact=...)")
     if track_energy:
         raise NotImplementedError("energy tracking is not on the GPU path")
     cfg = cfg or SolverConfig(precond="diagonal", tol=1e-10, condense=False)
@@ -142,12 +144,20 @@ def newmark_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
     load = _Load(pb, external_load)
     traj = Trajectory()
     uk, atr, psi, tmp, du, a = (DeviceVector(pb) for _ in range(6))
+    fcv = DeviceVector(pb) if contact is not None else None
+    lib = native.lib()
 
     def residual(uk_, atr_, t_next):
-        # psi = P(t) - R(uk) - M a_trial   (dynamics.py:197-203)
+        """psi = P(t) - R(uk) - M a_trial (+ f_c(uk))  (dynamics.py:197-203);
+        returns (contact settled, any contact point active)."""
         pb.fint_(uk_, tmp)
         pb.mass_(atr_, psi)
-        return psi.assign(1.0, load.at(t_next), -1.0, tmp, -1.0, psi)
+        if contact is None:
+            psi.assign(1.0, load.at(t_next), -1.0, tmp, -1.0, psi)
+            return True, False
+        settled, active = contact.evaluate_(uk_, fcv)
+        psi.assign(1.0, load.at(t_next), -1.0, tmp, -1.0, psi, 1.0, fcv)
+        return settled, active
 
     # a0 = M^-1 psi0 (mass-only PCG, short-circuits for psi0 = 0)
     atr.fill(0.0)
@@ -166,20 +176,28 @@ def newmark_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
             # a_trial = b1 (uk - u) - b2 v - b3 a  (difference first, as dynamics.py:219)
             tmp.assign(1.0, uk, -1.0, u)
             atr.assign(nm.b1, tmp, -nm.b2, v, -nm.b3, a)
-            residual(uk, atr, t_next)
+            contact_ok, active = residual(uk, atr, t_next)
             rnorm = psi.norm()
             if psi_ref is None:
                 psi_ref = rnorm
             if psi_ref == 0.0:
                 break
-            if rnorm <= newton_tol * psi_ref:
+            if rnorm <= newton_tol * psi_ref and contact_ok:
                 break
             if k == newton_maxit - 1:
                 raise NewtonDivergenceError(
                     f"Newton did not converge in {newton_maxit} iterations at t={t_next:.6g} "
                     f"(residual {rnorm / psi_ref:.3e} relative)", rnorm)
-            _, st = pcg_gpu(pb, uk, psi, c_m=nm.b1, precond=cfg.precond, tol=cfg.tol,
-                            maxit=cfg.maxit, x=du)
+            # effective operator K_T + b1 M (+ K_c on the active set of this
+            # residual, dynamics.py:235-241)
+            if active:
+                lib.sdme_pcg_contact(pb._ctx, 1)
+            try:
+                _, st = pcg_gpu(pb, uk, psi, c_m=nm.b1, precond=cfg.precond, tol=cfg.tol,
+                                maxit=cfg.maxit, x=du)
+            finally:
+                if active:
+                    lib.sdme_pcg_contact(pb._ctx, 0)
             traj.stats.add(step, k, "newmark", st)
             uk.assign(1.0, uk, 1.0, du)
             n_newton += 1
@@ -191,6 +209,8 @@ def newmark_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
         a.copy_from(atr)
         u.copy_from(uk)
         t = t_next
+        if contact is not None:
+            contact.accept_step_(u, fcv)
         if snapshot_stride and (step + 1) % snapshot_stride == 0:
             traj.times.append(t)
             traj.snapshots.append(u.free())
@@ -204,8 +224,6 @@ def lumped_mass(problem: GpuFemProblem) -> tuple[DeviceVector, DeviceVector]:
     ones = DeviceVector(problem).fill(1.0)
     ml = problem.mass_(ones, DeviceVector(problem))
     inv = DeviceVector(problem)
-    from . import native
-
     native.check(problem._ctx, native.lib().sdme_vec_reciprocal(problem._ctx, inv.vid, ml.vid),
                  "lumped mass")
     return ml, inv

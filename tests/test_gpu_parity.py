@@ -87,7 +87,7 @@ def test_contact_force_vs_reference():
     pb = gpu_problem("SDME_M", 3, 4, (3, 2, 2), (0.3, 0.2, 0.2))
     c = GpuPenaltyContact(pb, RigidObstacle([-1e-3, 0, 0], [1, 0, 0]), ContactParams(1e10), "xmin")
     fc = c.evaluate_forces(g["u"])
-    assert fc.stiffness is None
+    assert fc.stiffness is not None  # active points -> contact stiffness operator
     assert max_rel_err(fc.force, g["force"]) <= TOL
     assert max_rel_err(fc.gaps, g["gaps"]) <= TOL
     assert fc.active.any()
@@ -379,3 +379,77 @@ def test_pcg_operator_from_stored_quadrature_data_is_bit_identical(tag, P, m, mo
         assert np.array_equal(yv.free(), pb.apply_tangent(u, b, c_m=2.0e5))
     assert res["0"][1] == res["1"][1]
     assert np.array_equal(res["0"][0], res["1"][0])
+
+
+# ------------------------------------------------------------------------------
+# Implicit penalty contact: contact stiffness operator and
+# newmark_run(contact=...) against the reference.
+
+def _block(P, gap0=0.0):
+    """test_contact.py:14-20: unit block gap0 above the y = 0 plane."""
+    return GpuFemProblem(BoxMesh((1, 1, 1), (1.0, 1.0, 1.0), (0.0, gap0, 0.0)), build_basis(P, BasisKind("SDME_M")),
+                         NeoHookean.from_engineering(100.0, 0.3, 1.0), gauss_rule(P + 1))
+
+
+def test_contact_stiffness_is_force_jacobian_psd_and_matches_oracle():
+    """test_contact.py:69-94: K_c is the negative force gradient (FD 1e-5),
+    symmetric PSD; its action and diagonal equal the assembled oracle K_c."""
+    pb = _block(3)
+    plane = RigidObstacle(np.zeros(3), np.array([0.0, 1.0, 0.0]))
+    c = GpuPenaltyContact(pb, plane, ContactParams(1e4), "ymin")
+    rng = np.random.default_rng(0)
+    u0 = pb.constant_field([0.0, -2e-3, 0.0]) + 1e-4 * rng.uniform(-1, 1, pb.n_free)
+    du = rng.standard_normal(pb.n_free)
+    du /= np.linalg.norm(du)
+    fc = c.evaluate_forces(u0)
+    kd = fc.stiffness @ du
+    dg = fc.stiffness.diagonal()
+    q = rng.standard_normal(pb.n_free)
+    qk, dk = q @ (fc.stiffness @ du), du @ (fc.stiffness @ q)
+    assert abs(qk - dk) <= 1e-12 * max(abs(qk), abs(dk))
+    assert du @ kd >= 0.0
+    h = 1e-7
+    fd = (c.evaluate_forces(u0 + h * du).force - c.evaluate_forces(u0 - h * du).force) / (2 * h)
+    assert np.abs(fd + kd).max() <= 1e-5 * np.abs(fd).max()
+    opb = of.Problem(of.Mesh((1, 1, 1), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0)), ob.Basis("SDME_M", 3),
+                     of.Material(100.0, 0.3, 1.0), 4)
+    oc = of.Contact(opb, [0.0, 0.0, 0.0], [0.0, 1.0, 0.0], 1e4, "ymin")
+    ks = oc.stiffness(u0)
+    assert max_rel_err(kd, ks @ du) <= TOL
+    assert max_rel_err(dg, ks.diagonal()) <= TOL
+
+
+def test_contact_stiffness_absent_without_penetration():
+    """test_contact.py:45-51."""
+    pb = _block(2, gap0=0.1)
+    c = GpuPenaltyContact(pb, RigidObstacle(np.zeros(3), np.array([0.0, 1.0, 0.0])), ContactParams(1e4), "ymin")
+    fc = c.evaluate_forces(np.zeros(pb.n_free))
+    assert fc.stiffness is None and not fc.active.any() and fc.settled
+    assert np.abs(fc.force).max() == 0.0
+
+
+def test_implicit_contact_newmark_vs_reference():
+    """Reference newmark_run with penalty contact (bar impact, shortened):
+    Newton counts equal, PCG counts +-1, penalty stepping history equal,
+    final u, v, a within 1e-9."""
+    from paper_2104_13466_b200.dynamics import ScaledLoad
+
+    g = load_golden("impact")
+    pb = GpuFemProblem(BoxMesh((1, 2, 1), (0.05, 0.1, 0.05), (-0.025, 0.0005, -0.025)),
+                       build_basis(3, BasisKind("SDME_H")), NeoHookean.from_engineering(100.0, 0.3, 1.0),
+                       gauss_rule(4))
+    c = GpuPenaltyContact(pb, RigidObstacle(np.zeros(3), np.array([0.0, 1.0, 0.0])),
+                          ContactParams(1e4, deps_n=1e3, gap_tol=3e-5, stress_tol=1e-2), "ymin")
+    cfg = SolverConfig(precond="diagonal", tol=1e-12, maxit=100000, condense=False)
+    traj = newmark_run(pb, ScaledLoad(np.zeros(pb.n_free), lambda t: 0.0), float(g["dt"]), int(g["steps"]),
+                       newton_tol=1e-10, v0=g["v0"], cfg=cfg, contact=c)
+    assert traj.newton_iters == list(g["newton_iters"])
+    its = np.array([r["iterations"] for r in traj.stats.rows if r["step"] >= 0])
+    assert np.all(np.abs(its - g["pcg_rows"][1:, 2]) <= 1)
+    hist = np.array(c.history)
+    assert np.array_equal(hist[:, 0], g["history"][:, 0])
+    assert np.array_equal(hist[:, 3], g["history"][:, 3])
+    assert max_rel_err(hist[:, 1], g["history"][:, 1]) <= 1e-8
+    assert max_rel_err(traj.state.u, g["u"]) <= 1e-9
+    assert max_rel_err(traj.state.v, g["v"]) <= 1e-9
+    assert max_rel_err(traj.state.a, g["a"]) <= 1e-9

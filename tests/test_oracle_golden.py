@@ -126,3 +126,27 @@ def test_oracle_config1_newmark():
     assert len(its) == len(ref_its)
     assert max(abs(a - b) for a, b in zip(its, ref_its)) <= 1
     assert max_rel_err(out["u"], g["u"]) <= 1e-9
+
+
+def _impact_problem():
+    return of.Problem(of.Mesh((1, 2, 1), (0.05, 0.1, 0.05), (-0.025, 0.0005, -0.025)), ob.Basis("SDME_H", 3),
+                      of.Material(100.0, 0.3, 1.0), 4)
+
+
+def test_oracle_implicit_contact_newmark():
+    """reference newmark_run with penalty contact (bar impact,
+    scenarios.py:92-113, shortened): Newton counts, penalty history, state."""
+    g = load_golden("impact")
+    pb = _impact_problem()
+    c = of.Contact(pb, [0.0, 0.0, 0.0], [0.0, 1.0, 0.0], 1e4, "ymin", deps=1e3, gap_tol=3e-5, stress_tol=1e-2)
+    out = osv.newmark(pb, lambda t: np.zeros(pb.n_free), float(g["dt"]), int(g["steps"]), newton_tol=1e-10,
+                      pcg_tol=1e-12, v0=g["v0"], contact=c)
+    assert out["newton_iters"] == list(g["newton_iters"])
+    its = [r[2] for r in out["pcg_iters"]]
+    assert np.all(np.abs(np.array(its) - g["pcg_rows"][1:, 2]) <= 1)
+    hist = np.array(c.history)
+    assert np.array_equal(hist[:, 0], g["history"][:, 0])  # penalty stepping
+    assert np.array_equal(hist[:, 3], g["history"][:, 3])  # active counts
+    assert max_rel_err(hist[:, 1], g["history"][:, 1]) <= 1e-8
+    for k in ("u", "v", "a"):
+        assert max_rel_err(out[k], g[k]) <= 1e-9, k
