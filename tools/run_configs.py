@@ -11,7 +11,8 @@ c3: P in {2,3,4,6,8} x {LagrangeGLL, ModalJacobi, SDME_M}, N = round(256/P)
 c4: explicit impact, bar 80x16x16 P=3 SDME_M, v0 = -10 m/s, rigid wall at
     x = -1e-3, eps = 1e10, lumped mass, dt = 0.5 * 2/sqrt(lambda_max) (D6, D7).
 c5: cantilever 64x8x8 P=6, 3 bases, 50 Newmark steps dt=1e-3, tip traction
-    in -z ramped over the run (D8): PCG iterations per Newton step, s/step.
+    -1.3e6 in z ramped over the run (D8; calibrated to ~30% tip deflection of
+    the 4 m length): PCG iterations per Newton step, s/step.
 """
 
 from __future__ import annotations
@@ -110,9 +111,9 @@ def c4(quick=False, steps=2000):
           "final_mean_vx": float(traj.state.v[0::3].mean()), "history_every50": hist[:8]})
 
 
-def c5(quick=False, traction=-1.0e4):
+def c5(quick=False, traction=-1.3e6, tags=("LagrangeGLL", "ModalJacobi", "SDME_H")):
     out = []
-    for tag in ("LagrangeGLL", "ModalJacobi", "SDME_H"):
+    for tag in tags:
         div = (64, 8, 8) if not quick else (16, 2, 2)
         kind = BasisKind(tag)
         pb = GpuFemProblem(BoxMesh(div, (4.0, 0.5, 0.5)), build_basis(6, kind), MAT, gauss_rule(7),
@@ -126,15 +127,21 @@ def c5(quick=False, traction=-1.0e4):
         wall = time.perf_counter() - t0
         its = [r["iterations"] for r in traj.stats.rows if r["step"] >= 0]
         lat = pb.to_lattice(traj.state.u)
-        tip = float(lat[2, ::6, ::6, -1].mean())  # vertex points of the tip face (values)
+        # vertex coefficients are point values in every basis (internal modes vanish there)
+        tip = float(lat[2, ::6, ::6, -1].mean())
         emit({"config": "c5", "basis": tag, "n_free": pb.n_free, "steps": n_steps, "s_per_step": wall / n_steps,
               "newton_iters_mean": float(np.mean(traj.newton_iters)), "pcg_iters_mean": float(np.mean(its)),
-              "pcg_iters_max": int(max(its)), "tip_uz_mean_coeff": tip, "traction": traction})
+              "pcg_iters_max": int(max(its)), "tip_uz_mean": tip, "tip_deflection_over_length": -tip / 4.0,
+              "traction": traction})
 
 
 if __name__ == "__main__":
     quick = "--quick" in sys.argv
     for a in sys.argv[1:]:
         if a.startswith("--"):
+            continue
+        if a.startswith("c5:"):  # c5:<traction>[:<basis>] calibration runs
+            parts = a.split(":")
+            c5(quick, float(parts[1]), tuple(parts[2:]) or ("SDME_H",))
             continue
         {"c1": c1, "c3": lambda: c3(quick), "c4": lambda: c4(quick), "c5": lambda: c5(quick)}[a]()
