@@ -13,7 +13,7 @@
 struct sdme_ctx;
 
 // meshes with at most this many elements use E-vector mode (sdme_ctx::ev_mode)
-constexpr long long kEvMaxElements = 8192;
+constexpr long long kEvMaxElements = 4096;  // tools/ev_crossover.py
 
 // Operator entry points of one (P, m) instantiation.
 struct SdmeOps {

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "ctx.cuh"
+#include "element_diag.cuh"
 #include "element_eo.cuh"
 #include "element_kernels.cuh"
 #include "element_v3.cuh"
@@ -27,25 +28,6 @@ using namespace sdme;
 using Ops = SdmeOps;
 
 namespace {
-
-template <int N, int M>
-struct Conf {
-  static constexpr int bytes = Smem<N, M>::per_elem * 8;
-  static constexpr int EB = bytes > 100000 ? 1 : (100000 / bytes > 8 ? 8 : 100000 / bytes);
-};
-
-template <int N, int M>
-Tab<N, M> make_tab(const sdme_ctx* c) {
-  Tab<N, M> t;
-  for (int a = 0; a < M; ++a) {
-    for (int l = 0; l < N; ++l) {
-      t.B[a][l] = c->Bl[a * N + l];
-      t.D[a][l] = c->Dl[a * N + l];
-    }
-    t.W[a] = c->w[a];
-  }
-  return t;
-}
 
 // v3 tables: weights, det J and dxi/dX folded per axis (element_v3.cuh)
 template <int N, int M>
@@ -367,22 +349,49 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
   }
 }
 
+// squared 1D tables of the diagonal kernel (element_diag.cuh): per axis
+// w B^2, w B D (2/h), w D^2 (2/h)^2, det J folded into z
+template <int N, int M>
+TabD<N, M> make_tabd(const sdme_ctx* c) {
+  TabD<N, M> t;
+  const Geo& g = c->geo;
+  for (int a = 0; a < M; ++a)
+    for (int l = 0; l < N; ++l) {
+      const double b = c->Bl[a * N + l], d = c->Dl[a * N + l], w = c->w[a];
+      for (int ax = 0; ax < 3; ++ax) {
+        const double s = g.s[ax], jz = ax == 2 ? g.detJ : 1.0;
+        double(&T)[3][M][N] = ax == 0 ? t.x : (ax == 1 ? t.y : t.z);
+        T[0][a][l] = w * b * b * jz;
+        T[1][a][l] = w * b * d * s * jz;
+        T[2][a][l] = w * d * d * s * s * jz;
+      }
+    }
+  return t;
+}
+
 template <int N, int M>
 void diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm) {
-  constexpr int EB = Conf<N, M>::EB;
-  constexpr int smem = Conf<N, M>::bytes * EB;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(element_diag<N, M, EB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_done = true;
+  constexpr int bytes = DiagLay<N, M, 1>::PER * 8;
+  constexpr int WPE = bytes <= 40960 ? 1 : (bytes <= 65536 ? 4 : 8);
+  constexpr int smem = DiagLay<N, M, WPE>::PER * 8;
+  auto kern = element_diag3<N, M, WPE, 1, 1>;
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, WPE * 32, smem);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    max_blocks = std::max(1, nb) * sms;
   }
-  const Tab<N, M> tb = make_tab<N, M>(c);
+  const Tab3<N, M> tb = make_tab3<N, M>(c);
+  const TabD<N, M> td = make_tabd<N, M>(c);
   OpArgs a{u, nullptr, d, ck, cm, 0, c->d_flag};
   if (c->ev_mode) {
     a.colour = -1;
     a.ev = c->d_ev;
-    const long long cnt = colour_count(c->geo, -1);
-    element_diag<N, M, EB><<<(unsigned)((cnt + EB - 1) / EB), 128, smem, c->st>>>(tb, c->geo, a);
+    kern<<<(unsigned)std::min<long long>(colour_count(c->geo, -1), max_blocks), WPE * 32, smem, c->st>>>(
+        tb, td, c->geo, a);
     ev_gather<N>(c, a);
     return;
   }
@@ -390,7 +399,7 @@ void diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm) {
     const long long cnt = colour_count(c->geo, col);
     if (cnt == 0) continue;
     a.colour = col;
-    element_diag<N, M, EB><<<(unsigned)((cnt + EB - 1) / EB), 128, smem, c->st>>>(tb, c->geo, a);
+    kern<<<(unsigned)std::min<long long>(cnt, max_blocks), WPE * 32, smem, c->st>>>(tb, td, c->geo, a);
     ++c->launches;
   }
 }
