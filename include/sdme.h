@@ -97,6 +97,10 @@ int sdme_fint(sdme_ctx* ctx, int u, int r);
 int sdme_apply(sdme_ctx* ctx, int u, int p, int y, double c_k, double c_m);
 /* y = M a -- mass_full @ a_trial (dynamics.py:198) */
 int sdme_mass(sdme_ctx* ctx, int a, int y);
+/* total strain energy sum_e sum_q w det J psi(F) (femcore.py:374-378, material.py:80);
+ * fixed-order reduction */
+int sdme_strain_energy(sdme_ctx* ctx, int u, double* out);
+
 /* d = diag(c_k K_T(u) + c_m M) on free points -- a.diagonal() (solver.py:106) */
 int sdme_diag(sdme_ctx* ctx, int u, double c_k, double c_m, int d);
 

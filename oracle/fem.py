@@ -204,6 +204,14 @@ def elem_fint(mat, grad, wdet, ue, e=-1):
     return np.einsum("q,qfd,qcd->fc", wdet, grad, p1).reshape(-1)
 
 
+def elem_energy(mat, grad, wdet, ue, e=-1):
+    """strain_energy (femcore.py:109-113, material.py:80)."""
+    f, _, lnj = _state(grad, ue, e)
+    trc = np.einsum("qij,qij->q", f, f)
+    psi = 0.5 * mat.mu * (trc - 3.0) - mat.mu * lnj + 0.5 * mat.lam * lnj ** 2
+    return float(wdet @ psi)
+
+
 _VOIGT = ((0, 0), (1, 1), (2, 2), (0, 1), (1, 2), (0, 2))
 
 
@@ -264,6 +272,11 @@ class Problem:
         d = self._edofs[e]
         ok = d >= 0
         np.add.at(out, d[ok], r[ok])
+
+    def total_strain_energy(self, u):
+        """femcore.py:374-378."""
+        return sum(elem_energy(self.mat, self.tab.per_elem[e][1], self.tab.per_elem[e][2], self.gather(e, u), e)
+                   for e in range(self.mesh.ne))
 
     def internal_force(self, u):
         out = np.zeros(self.n_free)
@@ -422,6 +435,11 @@ class Contact:
             r = np.einsum("q,qf,c->fc", warea * tn, vals, self.normal)
             self.pb.scatter(out, e, r.reshape(-1))
         return out, gs
+
+    def penalty_energy(self, u):
+        """contact.py:178-184."""
+        return sum(0.5 * self.eps * float(warea @ np.minimum(g, 0.0) ** 2)
+                   for (_, _, _, warea, _), g in zip(self.faces, self.gaps(u)))
 
     def penetration(self, u):
         return max(0.0, max(float(-g.min()) for g in self.gaps(u)))

@@ -59,7 +59,7 @@ def pcg(a, b, precond="diagonal", tol=1e-8, maxit=10000):
 
 
 def newmark(problem, load, dt, n_steps, newton_tol=1e-8, newton_maxit=25, pcg_tol=1e-10,
-            gamma=0.5, beta=0.25, u0=None, v0=None, maxit=200000, contact=None):
+            gamma=0.5, beta=0.25, u0=None, v0=None, maxit=200000, contact=None, track_energy=False):
     """dynamics.py:173-257, condense=False, Jacobi-PCG, optional penalty
     contact (residual + fc, Newton waits for settled pressures, operator
     + K_c of the iteration's active set, accept_step per step).
@@ -85,7 +85,14 @@ def newmark(problem, load, dt, n_steps, newton_tol=1e-8, newton_maxit=25, pcg_to
     psi0, _, _ = residual(u, np.zeros(n), 0.0)
     a, _, _ = pcg(mass, psi0, "diagonal", pcg_tol, maxit)
     t = 0.0
-    newton_iters, pcg_iters = [], []
+    newton_iters, pcg_iters, energy = [], [], []
+
+    def energy_row(tt):  # dynamics.py:260-265
+        pen = contact.penalty_energy(u) if contact is not None else 0.0
+        energy.append((tt, 0.5 * float(v @ (mass @ v)), problem.total_strain_energy(u), pen))
+
+    if track_energy:
+        energy_row(t)
     for step in range(n_steps):
         tn = t + dt
         uk = u.copy()
@@ -114,7 +121,9 @@ def newmark(problem, load, dt, n_steps, newton_tol=1e-8, newton_maxit=25, pcg_to
         u, a, t = uk, an, tn
         if contact is not None:
             contact.accept_step(u)
-    return dict(u=u, v=v, a=a, newton_iters=newton_iters, pcg_iters=pcg_iters)
+        if track_energy:
+            energy_row(t)
+    return dict(u=u, v=v, a=a, newton_iters=newton_iters, pcg_iters=pcg_iters, energy=energy)
 
 
 def explicit_lumped(problem, load, dt, n_steps, u0=None, v0=None, contact=None):

@@ -217,6 +217,10 @@ class GpuPenaltyContact:
         """``contact.py:178-184``: sum over points of eps/2 warea min(g,0)^2."""
         u, fc = self._scratch()
         u.set_free(u_free)
+        return self.penalty_energy_(u, fc)
+
+    def penalty_energy_(self, u: DeviceVector, fc: DeviceVector) -> float:
+        """:meth:`penalty_energy` at a device vector (fc is scratch)."""
         g = self._gaps(u, fc).reshape(-1, self.qf, self.qf)
         ax = self.side // 2
         d1, d2 = [d for d in range(3) if d != ax]

@@ -89,6 +89,7 @@ struct sdme_ctx {
   double* d_ev = nullptr;
   // stored quadrature data of the PCG linearisation point (MODE_SETUP / MODE_PA)
   double* d_qpd = nullptr;
+  double* d_energy = nullptr;  // per-element strain energy (sdme_strain_energy)
   bool pa = true;  // SDME_PA=0 disables (the PCG then applies K(u) from scratch)
 };
 

@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
   if (args.skip && *(volatile const int*)args.skip) return;
   const long long cnt = colour_count(g, args.colour);
   constexpr bool GRADP = (MODE == MODE_APPLY || MODE == MODE_PA);
-  constexpr bool UPASS = (MODE == MODE_APPLY || MODE == MODE_FINT || MODE == MODE_SETUP);
+  constexpr bool UPASS = (MODE == MODE_APPLY || MODE == MODE_FINT || MODE == MODE_SETUP || MODE == MODE_ENERGY);
   constexpr bool PPASS = (MODE == MODE_APPLY || MODE == MODE_MASS || MODE == MODE_PA);
   const long long stride = (long long)gridDim.x * EPB;
   // dP constants with c_k folded in
@@ -521,6 +521,18 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
           atomicMin(args.inv_flag, (unsigned long long)eid * C::Q + (unsigned long long)((a * M + b) * M + c));
         }
       }
+      if (MODE == MODE_ENERGY) {
+        // psi = mu/2 (tr C - 3) - mu ln J + lam/2 ln J^2 (material.py:80), weighted
+        double trc = 0.0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) trc = fma(s.F[i][d], s.F[i][d], trc);
+        const double psi = 0.5 * g.mu * (trc - 3.0) - g.mu * s.lnJ + 0.5 * g.lam * s.lnJ * s.lnJ;
+        const int a = q % M, b = (q / M) % M, c = q / (M * M);
+        A[C::qi(0, 0, q)] = args.wq[a] * args.wq[b] * args.wq[c] * g.detJ * psi;
+        continue;
+      }
       if (MODE == MODE_SETUP) {
         double* qd = args.qpd + eid * (kQpSlots * C::Q) + q;
 #pragma unroll
@@ -571,6 +583,16 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
     }
     group_sync<WPE>(gid);
     if (MODE == MODE_SETUP) continue;
+    if (MODE == MODE_ENERGY) {
+      // fixed-order element sum (one thread), then the next element may reuse A
+      if (t == 0) {
+        double e = 0.0;
+        for (int q = 0; q < C::Q; ++q) e += A[C::qi(0, 0, q)];
+        args.qpd[((long long)ek * g.ny + ej) * g.nx + ei] = e;
+      }
+      group_sync<WPE>(gid);
+      continue;
+    }
     double* evb = args.ev ? args.ev + (((long long)ek * g.ny + ej) * g.nx + ei) * 3 * (N * N * N) : nullptr;
     if (MODE == MODE_MASS)
       v3_backward<N, M, WPE, NC, false, true>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb);

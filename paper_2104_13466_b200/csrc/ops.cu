@@ -93,7 +93,7 @@ void launch_v3(sdme_ctx* c, const TB& tb, OpArgs a) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     max_blocks = std::max(1, nb) * sms;
   }
-  if (MODE == MODE_SETUP) {
+  if (MODE == MODE_SETUP || MODE == MODE_ENERGY) {
     // no scatter: one pass over all elements
     a.colour = -1;
     const long long need = (colour_count(c->geo, -1) + S::EPB - 1) / S::EPB;
@@ -124,6 +124,7 @@ void launch_v3(sdme_ctx* c, const TB& tb, OpArgs a) {
 template <int N, int M, class S, class TB = Tab3<N, M>>
 void element_shape(sdme_ctx* c, int mode, const TB& tb, OpArgs a) {
   if (mode == MODE_SETUP) launch_v3<N, M, S, MODE_SETUP, false, TB>(c, tb, a);
+  else if (mode == MODE_ENERGY) launch_v3<N, M, S, MODE_ENERGY, false, TB>(c, tb, a);
   else if (mode == MODE_PA && a.c_m != 0.0) launch_v3<N, M, S, MODE_PA, true, TB>(c, tb, a);
   else if (mode == MODE_PA) launch_v3<N, M, S, MODE_PA, false, TB>(c, tb, a);
   else if (mode == MODE_FINT) launch_v3<N, M, S, MODE_FINT, false, TB>(c, tb, a);
@@ -313,7 +314,8 @@ template <int N, int M>
 void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, double* y, double ck, double cm) {
   const Tab3<N, M> tb = make_tab3<N, M>(c);
   OpArgs a{u, p, y, ck, cm, 0, c->d_flag, c->cur_skip};
-  a.qpd = c->d_qpd;
+  a.qpd = mode == MODE_ENERGY ? y : c->d_qpd;  // MODE_ENERGY: y is the per-element energy buffer
+  for (int q = 0; q < M && q < 12; ++q) a.wq[q] = c->w[q];
   if constexpr (N <= 5) {
     // E-vector mode (small meshes, one launch over all elements): latency
     // shape, four warps per element, all three components per stage

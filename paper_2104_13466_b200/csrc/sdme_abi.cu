@@ -388,6 +388,7 @@ int sdme_destroy(sdme_ctx* ctx) {
   cudaFree(ctx->d_free);
   cudaFree(ctx->d_ev);
   cudaFree(ctx->d_qpd);
+  cudaFree(ctx->d_energy);
   if (ctx->pcg_exec) cudaGraphExecDestroy(ctx->pcg_exec);
   if (ctx->pcg_graph) cudaGraphDestroy(ctx->pcg_graph);
   cudaFree(ctx->d_fbuf);
@@ -822,6 +823,22 @@ int sdme_contact(sdme_ctx* ctx, int u, int side, int qf, const double* Bf, const
     }
   }
   return SDME_OK;
+}
+
+int sdme_strain_energy(sdme_ctx* ctx, int u, double* out) {
+  double* pu = ctx ? vec(ctx, u) : nullptr;
+  if (!pu || !out) return SDME_BAD_ARGUMENT;
+  const long long ne = (long long)ctx->geo.nx * ctx->geo.ny * ctx->geo.nz;
+  if (!ctx->d_energy) CK(cudaMalloc(&ctx->d_energy, ne * sizeof(double)));
+  int rc = reset_flag(ctx);
+  if (rc) return rc;
+  ctx->ops->element(ctx, MODE_ENERGY, pu, nullptr, ctx->d_energy, 1.0, 0.0);
+  k_sum<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(ctx->d_energy, ne, ctx->d_partial);
+  k_finish<1><<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal + S_SCRATCH);
+  ctx->launches += 2;
+  if ((rc = check_flag(ctx)) || (rc = read_scalars(ctx))) return rc;
+  *out = ctx->h_scal[S_SCRATCH];
+  return check_launch(ctx);
 }
 
 int sdme_contact_apply(sdme_ctx* ctx, int p, int y) {

@@ -61,6 +61,17 @@ __global__ void __launch_bounds__(kRedThreads) k_dots(const DotArgs<NV> da, long
   }
 }
 
+// partial[blk] = sum of a (fixed grid and tree)
+__global__ void __launch_bounds__(kRedThreads) k_sum(const double* __restrict__ a, long long n, double* partial) {
+  double acc[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    acc[0] += a[i];
+  double out[1];
+  block_sum<1>(acc, out);
+  if (threadIdx.x == 0) partial[blockIdx.x] = out[0];
+}
+
 // Sum kRedBlocks partials (fixed order) into res[k].
 template <int NV>
 __global__ void __launch_bounds__(kRedThreads) k_finish(const double* partial, double* res) {

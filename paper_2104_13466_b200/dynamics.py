@@ -133,8 +133,6 @@ def newmark_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
                 cfg: SolverConfig | None = None, gamma: float = 0.5, beta: float = 0.25,
                 contact=None, snapshot_stride: int = 0, track_energy: bool = False) -> Trajectory:
     """Implicit Newmark with Newton-Raphson (``dynamics.py:173-257``)."""
-    if track_energy:
-        raise NotImplementedError("energy tracking is not on the GPU path")
     cfg = cfg or SolverConfig(precond="diagonal", tol=1e-10, condense=False)
     cfg.validate()
     nm = NewmarkCoeffs(dt, gamma, beta)
@@ -167,6 +165,15 @@ def newmark_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
     traj.stats.add(-1, 0, "newmark-init", st)
 
     t = 0.0
+
+    def energy_row(tt):
+        # (t, kinetic 1/2 v.Mv, strain, penalty) -- dynamics.py:260-265
+        kin = 0.5 * v.dot(pb.mass_(v, tmp))
+        pen = contact.penalty_energy_(u, fcv) if contact is not None else 0.0
+        traj.energy.append((tt, kin, pb.strain_energy_(u), pen))
+
+    if track_energy:
+        energy_row(t)
     for step in range(n_steps):
         t_next = t + dt
         uk.copy_from(u)
@@ -211,6 +218,8 @@ def newmark_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
         t = t_next
         if contact is not None:
             contact.accept_step_(u, fcv)
+        if track_energy:
+            energy_row(t)
         if snapshot_stride and (step + 1) % snapshot_stride == 0:
             traj.times.append(t)
             traj.snapshots.append(u.free())

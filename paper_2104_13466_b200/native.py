@@ -67,6 +67,7 @@ SIGNATURES = {
     "sdme_contact_apply": [C.c_void_p, C.c_int, C.c_int],
     "sdme_contact_diag": [C.c_void_p, C.c_int],
     "sdme_pcg_contact": [C.c_void_p, C.c_int],
+    "sdme_strain_energy": [C.c_void_p, C.c_int, C.POINTER(C.c_double)],
     "sdme_time_op": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, _dp],
     "sdme_host_alloc": [C.c_size_t, C.POINTER(C.c_void_p)],
     "sdme_host_free": [C.c_void_p],

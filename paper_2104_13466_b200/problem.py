@@ -264,6 +264,16 @@ class GpuFemProblem:
         u = self._scratch("u").set_free(u_free)
         return self.diag_(u, self._scratch("y"), 1.0, c_m).free()
 
+    def strain_energy_(self, u: DeviceVector) -> float:
+        """Total strain energy at a device vector (femcore.py:374-378)."""
+        out = C.c_double(0.0)
+        native.check(self._ctx, native.lib().sdme_strain_energy(self._ctx, u.vid, C.byref(out)), "strain energy")
+        return out.value
+
+    def total_strain_energy(self, u_free: np.ndarray) -> float:
+        """``FemProblem.total_strain_energy`` (femcore.py:374-378)."""
+        return self.strain_energy_(self._scratch("u").set_free(u_free))
+
     def mass_apply(self, a_free: np.ndarray) -> np.ndarray:
         """``mass() @ a`` (femcore.py:367-372, dynamics.py:198)."""
         a = self._scratch("p").set_free(a_free)

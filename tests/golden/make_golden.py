@@ -246,10 +246,37 @@ def gen_impact():
     print("impact", traj.newton_iters, cont.history[-3:])
 
 
+def gen_impact_energy():
+    """The full bar-impact scenario (scenarios.py:92-113: 200 steps, contact at
+    ~83 steps, rebound) with energy tracking -- acceptance criterion 9
+    (test_acceptance.py:249-264) -- Jacobi-PCG and tight tolerances."""
+    mat = NeoHookean.from_engineering(100.0, 0.3, 1.0)
+    mesh = gen_box_mesh((1, 2, 1), (0.05, 0.1, 0.05), (-0.025, 0.005, -0.025))
+    el = TensorElement.create(3, build_basis(3, BasisKind("SDME_H")))
+    prob = FemProblem(mesh, el, build_dofmap(mesh, el, None), mat, rule=gauss_rule(4))
+    v0 = prob.l2_project(lambda x: np.tile([0.0, -0.06, 0.0], (len(x), 1)))
+    cont = PenaltyContact(prob, RigidObstacle(np.zeros(3), np.array([0.0, 1.0, 0.0])),
+                          ContactParams(1e4, deps_n=1e3, gap_tol=1e-3, stress_tol=1e-2), "ymin")
+    cfg = SolverConfig(precond="diagonal", tol=1e-12, maxit=100000, condense=False)
+    zero = np.zeros(prob.n_free)
+    traj = newmark_run(prob, lambda t: zero, 1e-3, 200, newton_tol=1e-10, v0=v0, cfg=cfg, contact=cont,
+                       track_energy=True)
+    en = np.array(traj.energy)
+    total = en[:, 1] + en[:, 2] + en[:, 3]
+    ey = prob.l2_project(lambda x: np.tile([0.0, 1.0, 0.0], (len(x), 1)))
+    vy = float(ey @ (prob.mass() @ traj.state.v)) / (0.05 * 0.1 * 0.05)
+    np.savez_compressed(os.path.join(HERE, "impact_energy.npz"), u=traj.state.u, v=traj.state.v, v0=v0,
+                        energy=en, history=np.array(cont.history), newton_iters=np.array(traj.newton_iters),
+                        vy=np.array(vy))
+    print("impact_energy drift", float(np.abs(total - total[0]).max() / total[0]), "vy", vy,
+          "pen", max(h[1] for h in cont.history))
+
+
 if __name__ == "__main__":
     import sys
 
-    which = sys.argv[1:] or ["basis", "elements", "global", "contact", "explicit", "impact", "config1"]
+    which = sys.argv[1:] or ["basis", "elements", "global", "contact", "explicit", "impact", "impact_energy",
+                             "config1"]
     for w in which:
         t = time.perf_counter()
         globals()["gen_" + w]()

@@ -453,3 +453,39 @@ def test_implicit_contact_newmark_vs_reference():
     assert max_rel_err(traj.state.u, g["u"]) <= 1e-9
     assert max_rel_err(traj.state.v, g["v"]) <= 1e-9
     assert max_rel_err(traj.state.a, g["a"]) <= 1e-9
+
+
+def test_bar_impact_energy_criterion9_vs_reference():
+    """Full bar-impact scenario (scenarios.py:92-113) on the GPU with energy
+    tracking: energy rows, penalty history and final state vs the reference
+    run; acceptance criterion 9 (test_acceptance.py:249-264) holds."""
+    g = load_golden("impact_energy")
+    pb = GpuFemProblem(BoxMesh((1, 2, 1), (0.05, 0.1, 0.05), (-0.025, 0.005, -0.025)),
+                       build_basis(3, BasisKind("SDME_H")), NeoHookean.from_engineering(100.0, 0.3, 1.0),
+                       gauss_rule(4))
+    c = GpuPenaltyContact(pb, RigidObstacle(np.zeros(3), np.array([0.0, 1.0, 0.0])),
+                          ContactParams(1e4, deps_n=1e3, gap_tol=1e-3, stress_tol=1e-2), "ymin")
+    cfg = SolverConfig(precond="diagonal", tol=1e-12, maxit=100000, condense=False)
+    traj = newmark_run(pb, ScaledLoad(np.zeros(pb.n_free), lambda t: 0.0), 1e-3, 200, newton_tol=1e-10,
+                       v0=g["v0"], cfg=cfg, contact=c, track_energy=True)
+    assert traj.newton_iters == list(g["newton_iters"])
+    en = np.array(traj.energy)
+    assert max_rel_err(en, g["energy"]) <= 1e-8
+    assert np.array_equal(np.array(c.history)[:, 0], g["history"][:, 0])
+    assert max_rel_err(traj.state.u, g["u"]) <= 1e-9
+    total = en[:, 1] + en[:, 2] + en[:, 3]
+    drift = float(np.abs(total - total[0]).max() / total[0])
+    ey = pb.constant_field([0.0, 1.0, 0.0])
+    vy = float(ey @ pb.mass_apply(traj.state.v)) / (0.05 * 0.1 * 0.05)
+    pen = max(h[1] for h in c.history)
+    assert pen <= 1e-3 and min(h[2] for h in c.history) >= 0.0 and drift <= 0.02 and vy > 0.0
+    assert vy == pytest.approx(float(g["vy"]), rel=1e-8)
+
+
+def test_strain_energy_vs_oracle():
+    """total_strain_energy (femcore.py:374-378) at a seeded admissible state."""
+    pb = gpu_problem("SDME_K", 3, 4, (3, 2, 2), (1.5, 1.0, 1.0), [("xmin", (0, 1, 2))])
+    rng = np.random.default_rng(21)
+    u = 1e-3 * rng.uniform(-1, 1, pb.n_free)
+    opb = of.Problem(of.Mesh((3, 2, 2), (1.5, 1.0, 1.0)), ob.Basis("SDME_K", 3), OMAT, 4, [("xmin", (0, 1, 2))])
+    assert pb.total_strain_energy(u) == pytest.approx(opb.total_strain_energy(u), rel=1e-12)

@@ -150,3 +150,19 @@ def test_oracle_implicit_contact_newmark():
     assert max_rel_err(hist[:, 1], g["history"][:, 1]) <= 1e-8
     for k in ("u", "v", "a"):
         assert max_rel_err(out[k], g[k]) <= 1e-9, k
+
+
+def test_oracle_bar_impact_energy_criterion9():
+    """Acceptance criterion 9 (test_acceptance.py:249-264) on the full
+    bar-impact scenario: energy rows, penalty history and final state."""
+    g = load_golden("impact_energy")
+    pb = of.Problem(of.Mesh((1, 2, 1), (0.05, 0.1, 0.05), (-0.025, 0.005, -0.025)), ob.Basis("SDME_H", 3),
+                    of.Material(100.0, 0.3, 1.0), 4)
+    c = of.Contact(pb, [0.0, 0.0, 0.0], [0.0, 1.0, 0.0], 1e4, "ymin", deps=1e3, gap_tol=1e-3, stress_tol=1e-2)
+    out = osv.newmark(pb, lambda t: np.zeros(pb.n_free), 1e-3, 200, newton_tol=1e-10, pcg_tol=1e-12,
+                      v0=g["v0"], contact=c, track_energy=True)
+    assert out["newton_iters"] == list(g["newton_iters"])
+    en = np.array(out["energy"])
+    assert max_rel_err(en, g["energy"]) <= 1e-8
+    assert np.array_equal(np.array(c.history)[:, 0], g["history"][:, 0])
+    assert max_rel_err(out["u"], g["u"]) <= 1e-9
