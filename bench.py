@@ -265,6 +265,43 @@ def run_reference(args):
     return 0
 
 
+def config1_time_step(cpu: bool) -> dict:
+    """The second half of BASELINE's metric: s/time-step at P = 4 on config 1
+    (4^3 SDME_M, (P+2)^3 Gauss, Newmark + Newton + Jacobi-PCG 1e-10, traction
+    1e5 ramped over 10 dt), wall clock per step through newmark_run; beside it
+    one step of the oracle restatement of the reference on the host (cpu)."""
+    from paper_2104_13466_b200 import (BoxMesh, GpuFemProblem, NeoHookean, ScaledLoad, SolverConfig,
+                                       build_basis, newmark_run)
+    from paper_2104_13466_b200.basis import BasisKind, gauss_rule
+
+    mat = NeoHookean.from_engineering(E_MOD, NU, RHO)
+    pb = GpuFemProblem(BoxMesh((4, 4, 4), (1.0, 1.0, 1.0)), build_basis(4, BasisKind("SDME_M")), mat,
+                       gauss_rule(6), [("xmin", (0, 1, 2))])
+    base = pb.traction_vector("xmax", [0.0, 0.0, 1.0e5])
+    load = ScaledLoad(base, lambda t: min(t / 1e-3, 1.0))
+    cfg = SolverConfig(precond="diagonal", tol=1e-10, condense=False)
+    newmark_run(pb, load, 1e-4, 1, cfg=cfg)  # warm-up (context, graphs)
+    t0 = time.perf_counter()
+    traj = newmark_run(pb, load, 1e-4, 10, newton_tol=1e-8, cfg=cfg)
+    gpu = (time.perf_counter() - t0) / 10
+    out = {"config": "config1: 4^3 hex P=4 SDME_M, m=6, 10 Newmark steps, Newton 1e-8, Jacobi-PCG 1e-10",
+           "ms_per_step": gpu * 1e3, "newton_iters": traj.newton_iters,
+           "pcg_iters": [r["iterations"] for r in traj.stats.rows if r["step"] >= 0]}
+    if cpu:
+        from oracle import basis as ob
+        from oracle import fem as of
+        from oracle import solve as osv
+
+        opb = of.Problem(of.Mesh((4, 4, 4), (1.0, 1.0, 1.0)), ob.Basis("SDME_M", 4), of.Material(E_MOD, NU, RHO), 6,
+                         [("xmin", (0, 1, 2))])
+        obase = opb.traction_vector("xmax", [0.0, 0.0, 1.0e5])
+        t0 = time.perf_counter()
+        osv.newmark(opb, lambda t: obase * min(t / 1e-3, 1.0), 1e-4, 1, newton_tol=1e-8, pcg_tol=1e-10)
+        out["cpu_s_per_step"] = time.perf_counter() - t0
+        out["cpu_kind"] = "port (oracle/solve.py newmark: assembled CSR tangent + Jacobi-PCG, numpy/scipy), 1 step"
+    return out
+
+
 def run_ours(args):
     ws, rank, local = dist_env()
     if ws > 1:
@@ -348,6 +385,7 @@ def run_ours(args):
            "api": "GpuFemProblem.apply_tangent(u_free, p_free) -> ndarray"}
     del out
 
+    tstep = config1_time_step(rank == 0 and not args.no_cpu) if rank == 0 else None
     cpu = None
     if rank == 0 and not args.no_cpu:
         s, cores, ns = cpu_sample_kp(None, None)
@@ -366,6 +404,7 @@ def run_ours(args):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "fint_ms": t_fint * 1e3,
             "fint_gdofs": n_dof / t_fint / 1e9,
+            "time_step": tstep,
             "pcg_operator": {"setup_ms": t_setup * 1e3, "kp_ms": t_pa * 1e3, "kp_gdofs": n_dof / t_pa / 1e9,
                              "note": "K.p inside sdme_pcg: K = F^-T and ln J stored per quadrature point "
                                      "once per solve (setup), bit-identical to the from-u K.p"},

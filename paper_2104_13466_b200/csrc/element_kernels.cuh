@@ -41,7 +41,8 @@ struct Geo {
 // MODE_SETUP stores K = F^-T and ln J at every quadrature point (OpArgs::qpd);
 // MODE_PA is K.p from those stored values (the PCG operator: u is fixed
 // during a solve, so the u pass and the point inverse/log are done once).
-// MODE_ENERGY writes the element strain energy sum_q w_q det J psi(F) to qpd[e].
+// MODE_ENERGY writes the element strain energy sum_q w_q det J psi(F) to qpd[e]
+// (p carries the 1D rule weights in that mode).
 enum Mode { MODE_FINT = 0, MODE_APPLY = 1, MODE_MASS = 2, MODE_PA = 3, MODE_SETUP = 4, MODE_ENERGY = 5 };
 constexpr int kQpSlots = 10;  // K (9) + ln J per point, [elem][slot][q]
 
@@ -55,7 +56,6 @@ struct OpArgs {
   const int* skip = nullptr;     // if set and non-zero: return at once (stopped PCG graph)
   double* ev = nullptr;          // E-vector mode (colour < 0): element boxes stored, not scattered
   double* qpd = nullptr;         // quadrature data (MODE_SETUP writes, MODE_PA reads)
-  double wq[12] = {};            // 1D rule weights (MODE_ENERGY)
 };
 
 __device__ __forceinline__ bool constrained(const Geo& g, int comp, int X, int Y, int Z) {

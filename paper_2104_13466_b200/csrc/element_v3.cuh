@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
           for (int d = 0; d < 3; ++d) trc = fma(s.F[i][d], s.F[i][d], trc);
         const double psi = 0.5 * g.mu * (trc - 3.0) - g.mu * s.lnJ + 0.5 * g.lam * s.lnJ * s.lnJ;
         const int a = q % M, b = (q / M) % M, c = q / (M * M);
-        A[C::qi(0, 0, q)] = args.wq[a] * args.wq[b] * args.wq[c] * g.detJ * psi;
+        A[C::qi(0, 0, q)] = __ldg(args.p + a) * __ldg(args.p + b) * __ldg(args.p + c) * g.detJ * psi;
         continue;
       }
       if (MODE == MODE_SETUP) {

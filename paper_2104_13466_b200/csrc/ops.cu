@@ -315,7 +315,6 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
   const Tab3<N, M> tb = make_tab3<N, M>(c);
   OpArgs a{u, p, y, ck, cm, 0, c->d_flag, c->cur_skip};
   a.qpd = mode == MODE_ENERGY ? y : c->d_qpd;  // MODE_ENERGY: y is the per-element energy buffer
-  for (int q = 0; q < M && q < 12; ++q) a.wq[q] = c->w[q];
   if constexpr (N <= 5) {
     // E-vector mode (small meshes, one launch over all elements): latency
     // shape, four warps per element, all three components per stage

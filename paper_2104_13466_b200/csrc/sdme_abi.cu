@@ -829,10 +829,14 @@ int sdme_strain_energy(sdme_ctx* ctx, int u, double* out) {
   double* pu = ctx ? vec(ctx, u) : nullptr;
   if (!pu || !out) return SDME_BAD_ARGUMENT;
   const long long ne = (long long)ctx->geo.nx * ctx->geo.ny * ctx->geo.nz;
-  if (!ctx->d_energy) CK(cudaMalloc(&ctx->d_energy, ne * sizeof(double)));
+  if (!ctx->d_energy) {
+    // per-element energies, then the m rule weights (read by the kernel through p)
+    CK(cudaMalloc(&ctx->d_energy, (ne + ctx->m) * sizeof(double)));
+    CK(cudaMemcpy(ctx->d_energy + ne, ctx->w.data(), ctx->m * sizeof(double), cudaMemcpyHostToDevice));
+  }
   int rc = reset_flag(ctx);
   if (rc) return rc;
-  ctx->ops->element(ctx, MODE_ENERGY, pu, nullptr, ctx->d_energy, 1.0, 0.0);
+  ctx->ops->element(ctx, MODE_ENERGY, pu, ctx->d_energy + ne, ctx->d_energy, 1.0, 0.0);
   k_sum<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(ctx->d_energy, ne, ctx->d_partial);
   k_finish<1><<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal + S_SCRATCH);
   ctx->launches += 2;
