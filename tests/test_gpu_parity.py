@@ -159,6 +159,14 @@ def test_inversion_error_reports_first_element_and_point():
     with pytest.raises(ElementInversionError) as err:
         pb.internal_force(u)
     assert (err.value.elem_id, err.value.qp) == (ref.value.elem_id, ref.value.qp) == (4, ref.value.qp)
+    # the same state as a PCG linearisation point (stored-quadrature setup and
+    # diagonal both see it) and through the K.p and diagonal entry points
+    b = np.ones(pb.n_free)
+    for call in (lambda: pcg_gpu(pb, u, b, c_m=1e5), lambda: pb.apply_tangent(u, b),
+                 lambda: pb.tangent_diagonal(u, c_m=1e5)):
+        with pytest.raises(ElementInversionError) as err2:
+            call()
+        assert (err2.value.elem_id, err2.value.qp) == (ref.value.elem_id, ref.value.qp)
 
 
 def test_pcg_error_contract():
