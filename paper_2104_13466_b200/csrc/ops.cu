@@ -12,7 +12,6 @@
 #include "element_eo.cuh"
 #include "element_kernels.cuh"
 #include "element_v3.cuh"
-#include "element_v4.cuh"
 #include "element_v5.cuh"
 #include "pcg_small.cuh"
 
@@ -218,37 +217,6 @@ TabEO<N, M, MIR> make_tabeo(const sdme_ctx* c) {
 }
 
 
-template <int N, int M, int MINB, int MODE, bool VAL, bool ASYNC, bool GUS = false>
-void launch_v4(sdme_ctx* c, const Tab3<N, M>& tb, OpArgs a) {
-  constexpr int smem =
-      (V4<N, M>::PER + (ASYNC ? 4 * 3 * N * N * N : 0) + (GUS && MODE == MODE_APPLY ? 9 * M * 32 : 0)) * 8;
-  auto kern = element_v4<N, M, MINB, MODE, VAL, ASYNC, GUS>;
-  static int max_blocks = -1;
-  if (max_blocks < 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    max_blocks = std::max(1, nb) * sms;
-  }
-  for (int col = 0; col < 8; ++col) {
-    const long long cnt = colour_count(c->geo, col);
-    if (cnt == 0) continue;
-    a.colour = col;
-    const unsigned grid = (unsigned)std::min<long long>(cnt, max_blocks);
-    kern<<<grid, 32, smem, c->st>>>(tb, c->geo, a);
-    ++c->launches;
-  }
-}
-
-template <int N, int M, int MINB, bool ASYNC, bool GUS = false>
-void element_v4_modes(sdme_ctx* c, int mode, const Tab3<N, M>& tb, OpArgs a) {
-  if (mode == MODE_FINT) launch_v4<N, M, MINB, MODE_FINT, false, ASYNC, GUS>(c, tb, a);
-  else if (mode == MODE_APPLY && a.c_m != 0.0) launch_v4<N, M, MINB, MODE_APPLY, true, ASYNC, GUS>(c, tb, a);
-  else if (mode == MODE_APPLY) launch_v4<N, M, MINB, MODE_APPLY, false, ASYNC, GUS>(c, tb, a);
-  else launch_v4<N, M, MINB, MODE_MASS, true, ASYNC, GUS>(c, tb, a);
-}
 
 // Component-serial staged shape for P >= 5: enough warps per element that the
 // element's shared memory (points, stage scratch, staged rows) is shared by
@@ -326,9 +294,8 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
   if constexpr (N == 5 && M == 5) {
     // P = 4, m = 5 (BASELINE config 2); schedule history in profiles/variants_r01.txt
     // (the 3-component, 12-warp and unstaged shapes measured there are template
-    // arguments of this same kernel).  SDME_VARIANT: 4 = column-resident v4,
-    // 8 = column-fused v5, both slower and opt-in only.
-    if (c->variant == 4 && !c->ev_mode && mode <= MODE_MASS) { element_v4_modes<N, M, 8, false>(c, mode, tb, a); return; }
+    // arguments of this same kernel).  SDME_VARIANT=8: column-fused v5, slower,
+    // opt-in only (the column-resident v4 of that history was removed).
     using SK = Shape<N, M, 1, 1, 1, 11, true>;
     if (mode == MODE_APPLY && c->variant == 8 && c->mir >= 0) {
       // column-fused v5 (element_v5.cuh): 255 registers, 8 warps/SM; measured
