@@ -46,7 +46,7 @@ struct Lay {
   template <> struct Lay<NN, MM, NCC> { static constexpr int xo = XO, yo = YO, sx = SX, sy = SY, sq = SQ; };
 SDME_LAY(2, 2, 3, 0, 0, 5, 6, 20)
 SDME_LAY(2, 3, 3, 0, 0, 6, 9, 41)
-SDME_LAY(3, 3, 3, 0, 0, 9, 13, 41)
+SDME_LAY(3, 3, 3, 0, 1, 9, 19, 41)
 SDME_LAY(3, 4, 3, 0, 1, 25, 19, 64)
 SDME_LAY(4, 4, 3, 0, 0, 19, 20, 64)
 SDME_LAY(4, 5, 3, 0, 2, 20, 28, 137)

@@ -65,7 +65,10 @@ template <int N, int M>
 struct DefaultShape {
   static constexpr int bytes = V3<N, M, 1, 3>::PER * 8;
   static constexpr int WPE = bytes <= 40960 ? 1 : (bytes <= 65536 ? 4 : 8);
-  using type = Shape<N, M, WPE, 3, (WPE == 1 ? 2 : 1), 1>;
+  // resident 2-warp blocks per SM for P = 2, 3 at m = P + 1 (register cap
+  // 128 / 168: 16 / 12 warps per SM; tools/prof_c3.py), else unconstrained
+  static constexpr int MINB = (N == 3 && M == 3) ? 8 : ((N == 4 && M == 4) ? 6 : 1);
+  using type = Shape<N, M, WPE, 3, (WPE == 1 ? 2 : 1), MINB>;
 };
 
 // E-vector mode: y += gathered element boxes (after the single element launch)
