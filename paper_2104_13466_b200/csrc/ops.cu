@@ -226,8 +226,8 @@ TabEO<N, M, MIR> make_tabeo(const sdme_ctx* c) {
 // 4 or 8 warps.
 template <int N, int M>
 struct LargeShape {
-  static constexpr int bytes = (V3<N, M, 1, 1>::PER + 2 * N * N * N) * 8;
-  static constexpr int WPE = bytes <= 40960 ? 1 : (bytes <= 65536 ? 4 : 8);
+  // enough warps that one round covers a stage's M^2 (or N M) pencils
+  static constexpr int WPE = (M * M + 31) / 32 > 8 ? 8 : (M * M + 31) / 32;
   using type = Shape<N, M, WPE, 1, 1, 1, true>;
 };
 
@@ -342,8 +342,7 @@ TabD<N, M> make_tabd(const sdme_ctx* c) {
 
 template <int N, int M>
 void diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm) {
-  constexpr int bytes = DiagLay<N, M, 1>::PER * 8;
-  constexpr int WPE = bytes <= 40960 ? 1 : (bytes <= 65536 ? 4 : 8);
+  constexpr int WPE = LargeShape<N, M>::WPE;  // one round per stage
   constexpr int smem = DiagLay<N, M, WPE>::PER * 8;
   auto kern = element_diag3<N, M, WPE, 1, 1>;
   static int max_blocks = -1;
