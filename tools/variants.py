@@ -1,5 +1,10 @@
 """Time the P=4 schedule variants (SDME_VARIANT) on config 2 and check they
-agree with variant 0.  Usage: python tools/variants.py 0 1 2 3"""
+agree with variant 0.  Usage: python tools/variants.py 0 8
+
+Current variants: 0 = default (component-serial, staged, even-odd), 8 =
+column-fused v5.  The earlier variants in profiles/variants_r01.txt (1-5) were
+template arguments of the v3 kernel and the removed column-resident v4; they are
+recorded there, not selectable any more."""
 import json
 import os
 import subprocess
