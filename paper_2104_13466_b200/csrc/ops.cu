@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "ctx.cuh"
+#include "element_col.cuh"
 #include "element_diag.cuh"
 #include "element_eo.cuh"
 #include "element_kernels.cuh"
@@ -135,33 +136,22 @@ void element_shape(sdme_ctx* c, int mode, const TB& tb, OpArgs a) {
   else launch_v3<N, M, S, MODE_MASS, true, TB>(c, tb, a);
 }
 
-// Even-odd tables (eo.cuh) from the lattice-order 1D tables, with the same
-// folding of weights, det J and 2/h as make_tab3.
+// Even-odd forward / backward tables of one 1D operator T (m x n, rows =
+// points, columns = lattice-local functions) with the mirror structure
+// Mir<n, MIR>: pairs first, then the fixed points whose sign (F * s) is + (even
+// set) or - (odd set); F = +1 for B-type, -1 for D-type operators.  Folded by
+// 1/2 so the reconstruction is one add / subtract (eo.cuh).
 template <int N, int M, int MIR>
-TabEO<N, M, MIR> make_tabeo(const sdme_ctx* c) {
+struct EoBuild {
   using Mr = Mir<N, MIR>;
-  constexpr int H = M / 2, HP = (M + 1) / 2;
-  const Geo& g = c->geo;
-  double Bv[M][N], Dv[3][M][N], bB[3][M][N], bD[3][M][N];
-  for (int a = 0; a < M; ++a)
-    for (int l = 0; l < N; ++l) {
-      const double b = c->Bl[a * N + l], d = c->Dl[a * N + l], w = c->w[a];
-      Bv[a][l] = b;
-      for (int ax = 0; ax < 3; ++ax) {
-        const double jz = ax == 2 ? g.detJ : 1.0;
-        Dv[ax][a][l] = d * g.s[ax];
-        bB[ax][a][l] = b * w * jz;
-        bD[ax][a][l] = d * w * g.s[ax] * jz;
-      }
-    }
-  // column / row sets of a type-F operator: pairs first, then the fixed points
-  // whose sign (F * s) is + (even set) or - (odd set)
-  auto set_of = [](int F, bool even, int idx) {
+  static constexpr int H = M / 2, HP = (M + 1) / 2;
+  static int set_of(int F, bool even, int idx) {
     if (idx < Mr::NP) return Mr::nth(0, idx);
     const int kind = (F > 0) == even ? 1 : 2;
     return Mr::nth(kind, idx - Mr::NP);
-  };
-  auto fwd = [&](auto& dst, const double (&T)[M][N], int F) {
+  }
+  template <class Dst>
+  static void fwd(Dst& dst, const double (&T)[M][N], int F) {
     constexpr int WS = sizeof(dst.S[0]) / sizeof(double), WT = sizeof(dst.T[0]) / sizeof(double);
     const int nS = F > 0 ? Mr::NE : Mr::NO, nT = F > 0 ? Mr::NO : Mr::NE;
     for (int a = 0; a < HP; ++a)
@@ -182,8 +172,9 @@ TabEO<N, M, MIR> make_tabeo(const sdme_ctx* c) {
         }
         dst.T[a][o] = v;
       }
-  };
-  auto bwd = [&](auto& dst, const double (&T)[M][N], int F) {
+  }
+  template <class Dst>
+  static void bwd(Dst& dst, const double (&T)[M][N], int F) {
     constexpr int WE = sizeof(dst.E) / sizeof(dst.E[0]), WO = sizeof(dst.O) / sizeof(dst.O[0]);
     const int nE = F > 0 ? Mr::NE : Mr::NO, nO = F > 0 ? Mr::NO : Mr::NE;
     for (int e = 0; e < WE; ++e)
@@ -204,7 +195,29 @@ TabEO<N, M, MIR> make_tabeo(const sdme_ctx* c) {
         }
         dst.O[o][a] = v;
       }
-  };
+  }
+};
+
+// Even-odd tables (eo.cuh) from the lattice-order 1D tables, with the same
+// folding of weights, det J and 2/h as make_tab3.
+template <int N, int M, int MIR>
+TabEO<N, M, MIR> make_tabeo(const sdme_ctx* c) {
+  const Geo& g = c->geo;
+  double Bv[M][N], Dv[3][M][N], bB[3][M][N], bD[3][M][N];
+  for (int a = 0; a < M; ++a)
+    for (int l = 0; l < N; ++l) {
+      const double b = c->Bl[a * N + l], d = c->Dl[a * N + l], w = c->w[a];
+      Bv[a][l] = b;
+      for (int ax = 0; ax < 3; ++ax) {
+        const double jz = ax == 2 ? g.detJ : 1.0;
+        Dv[ax][a][l] = d * g.s[ax];
+        bB[ax][a][l] = b * w * jz;
+        bD[ax][a][l] = d * w * g.s[ax] * jz;
+      }
+    }
+  using EB = EoBuild<N, M, MIR>;
+  auto fwd = [](auto& dst, const double (&T)[M][N], int F) { EB::fwd(dst, T, F); };
+  auto bwd = [](auto& dst, const double (&T)[M][N], int F) { EB::bwd(dst, T, F); };
   TabEO<N, M, MIR> t;
   fwd(t.B, Bv, 1);
   fwd(t.Dx, Dv[0], -1);
@@ -281,6 +294,9 @@ void apply_v5(sdme_ctx* c, const TabEO<N, M, MIR>& tb, OpArgs a) {
   else launch_v5<N, M, SDME_V5_MINB, false, MIR>(c, tb, a);
 }
 
+template <int N, int MIR>
+void col_modes(sdme_ctx* c, int mode, OpArgs a);
+
 template <int N, int M>
 void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, double* y, double ck, double cm) {
   const Tab3<N, M> tb = make_tab3<N, M>(c);
@@ -307,8 +323,15 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
       else apply_v5<N, M, 1>(c, make_tabeo<N, M, 1>(c), a);
       return;
     }
-    // default for every mode: component-serial, cp.async-staged rows,
-    // even-odd contractions, 11 warps/SM (K.p 2.47 ms, f_int 1.60 ms, mass 1.27 ms)
+    // f_int and K.p: collocated sum factorisation (element_col.cuh) unless
+    // SDME_VARIANT=10; other modes and non-mirrored tables: component-serial,
+    // cp.async-staged rows, even-odd contractions, 11 warps/SM
+    if ((mode == MODE_FINT || mode == MODE_APPLY || mode == MODE_PA || mode == MODE_SETUP) && c->variant != 10 &&
+        c->mir >= 0) {
+      if (c->mir == 0) col_modes<N, 0>(c, mode, a);
+      else col_modes<N, 1>(c, mode, a);
+      return;
+    }
     element_eo_or_plain<N, M, SK>(c, mode, tb, a);
     return;
   } else if constexpr (N >= 6) {
@@ -338,6 +361,98 @@ TabD<N, M> make_tabd(const sdme_ctx* c) {
       }
     }
   return t;
+}
+
+// collocated tables (element_col.cuh, m = n): B, D^ = D B^-1 per axis (x 2/h)
+template <int N, int MIR>
+TabC<N, MIR> make_tabc(const sdme_ctx* c) {
+  const Geo& g = c->geo;
+  double Bv[N][N], Dv[N][N], inv[N][N], a[N][2 * N];
+  for (int r = 0; r < N; ++r)
+    for (int l = 0; l < N; ++l) {
+      Bv[r][l] = c->Bl[r * N + l];
+      Dv[r][l] = c->Dl[r * N + l];
+    }
+  // B^-1 by Gauss-Jordan with partial pivoting (n <= 9, cond(B) <= 34)
+  for (int r = 0; r < N; ++r)
+    for (int l = 0; l < 2 * N; ++l) a[r][l] = l < N ? Bv[r][l] : (l - N == r ? 1.0 : 0.0);
+  for (int col = 0; col < N; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < N; ++r)
+      if (std::fabs(a[r][col]) > std::fabs(a[piv][col])) piv = r;
+    for (int l = 0; l < 2 * N; ++l) std::swap(a[col][l], a[piv][l]);
+    const double d = a[col][col];
+    for (int l = 0; l < 2 * N; ++l) a[col][l] /= d;
+    for (int r = 0; r < N; ++r)
+      if (r != col) {
+        const double f = a[r][col];
+        for (int l = 0; l < 2 * N; ++l) a[r][l] -= f * a[col][l];
+      }
+  }
+  for (int r = 0; r < N; ++r)
+    for (int l = 0; l < N; ++l) inv[r][l] = a[r][N + l];
+  double Dh[3][N][N];
+  for (int r = 0; r < N; ++r)
+    for (int q = 0; q < N; ++q) {
+      double s = 0.0;
+      for (int l = 0; l < N; ++l) s += Dv[r][l] * inv[l][q];
+      for (int ax = 0; ax < 3; ++ax) Dh[ax][r][q] = s * g.s[ax];
+    }
+  TabC<N, MIR> t;
+  EoBuild<N, N, MIR>::fwd(t.B, Bv, 1);
+  EoBuild<N, N, MIR>::bwd(t.bB, Bv, 1);
+  EoBuild<N, N, 0>::fwd(t.Dx, Dh[0], -1);
+  EoBuild<N, N, 0>::fwd(t.Dy, Dh[1], -1);
+  EoBuild<N, N, 0>::fwd(t.Dz, Dh[2], -1);
+  EoBuild<N, N, 0>::bwd(t.bDx, Dh[0], -1);
+  EoBuild<N, N, 0>::bwd(t.bDy, Dh[1], -1);
+  EoBuild<N, N, 0>::bwd(t.bDz, Dh[2], -1);
+  for (int q = 0; q < N; ++q) t.wq[q] = c->w[q];
+  t.detJ = g.detJ;
+  return t;
+}
+
+template <int N, int MODE, bool VAL, int MIR>
+void launch_col(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
+  constexpr int smem = ColLay<N, VAL>::PER * 8;
+  auto kern = element_col<N, 11, MODE, VAL, MIR>;
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    max_blocks = std::max(1, nb) * sms;
+  }
+  if (MODE == MODE_SETUP || c->ev_mode) {
+    // setup: no scatter, one pass over all elements; E-vector mode: boxes + gather
+    a.colour = -1;
+    if (MODE != MODE_SETUP) a.ev = c->d_ev;
+    kern<<<(unsigned)std::min<long long>(colour_count(c->geo, -1), max_blocks), 32, smem, c->st>>>(tb, c->geo, a);
+    if (MODE == MODE_SETUP || c->ev_no_gather) ++c->launches;
+    else ev_gather<N>(c, a);
+    return;
+  }
+  for (int col = 0; col < 8; ++col) {
+    const long long cnt = colour_count(c->geo, col);
+    if (cnt == 0) continue;
+    a.colour = col;
+    kern<<<(unsigned)std::min<long long>(cnt, max_blocks), 32, smem, c->st>>>(tb, c->geo, a);
+    ++c->launches;
+  }
+}
+
+// collocated path: f_int, K.p (from u or from stored quadrature data)
+template <int N, int MIR>
+void col_modes(sdme_ctx* c, int mode, OpArgs a) {
+  const TabC<N, MIR> tb = make_tabc<N, MIR>(c);
+  if (mode == MODE_FINT) launch_col<N, MODE_FINT, false, MIR>(c, tb, a);
+  else if (mode == MODE_SETUP) launch_col<N, MODE_SETUP, false, MIR>(c, tb, a);
+  else if (mode == MODE_APPLY && a.c_m != 0.0) launch_col<N, MODE_APPLY, true, MIR>(c, tb, a);
+  else if (mode == MODE_APPLY) launch_col<N, MODE_APPLY, false, MIR>(c, tb, a);
+  else if (mode == MODE_PA && a.c_m != 0.0) launch_col<N, MODE_PA, true, MIR>(c, tb, a);
+  else launch_col<N, MODE_PA, false, MIR>(c, tb, a);
 }
 
 template <int N, int M>

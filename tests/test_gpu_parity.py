@@ -497,3 +497,31 @@ def test_strain_energy_vs_oracle():
     u = 1e-3 * rng.uniform(-1, 1, pb.n_free)
     opb = of.Problem(of.Mesh((3, 2, 2), (1.5, 1.0, 1.0)), ob.Basis("SDME_K", 3), OMAT, 4, [("xmin", (0, 1, 2))])
     assert pb.total_strain_energy(u) == pytest.approx(opb.total_strain_energy(u), rel=1e-12)
+
+
+@pytest.mark.parametrize("tag", KINDS5)
+def test_collocated_path_vs_oracle(tag, monkeypatch):
+    """P = 4, m = 5 on colour passes runs the collocated kernels
+    (element_col.cuh) for f_int, K.p (+ c_m M p) and the PCG operator; all
+    agree with the oracle to 1e-12, and with the v3 kernels (SDME_VARIANT=10)."""
+    monkeypatch.setenv("SDME_EV", "0")
+    div, L = (3, 2, 2), (1.5, 1.0, 1.0)
+    opb = of.Problem(of.Mesh(div, L), ob.Basis(tag, 4), OMAT, 5, [("xmin", (0, 1, 2))])
+    rng = np.random.default_rng(17)
+    u = 1e-3 * rng.uniform(-1, 1, opb.n_free)
+    p = rng.standard_normal(opb.n_free)
+    ref_f = opb.internal_force(u)
+    ref_kp = opb.assemble(u, 1.0, 2.0e5) @ p
+    out = {}
+    for variant in ("0", "10"):
+        monkeypatch.setenv("SDME_VARIANT", variant)
+        pb = gpu_problem(tag, 4, 5, div, L, [("xmin", (0, 1, 2))])
+        f, kp = pb.internal_force(u), pb.apply_tangent(u, p, c_m=2.0e5)
+        assert max_rel_err(f, ref_f) <= TOL
+        assert max_rel_err(kp, ref_kp) <= TOL
+        uv, pv, yv = pb.vector().set_free(u), pb.vector().set_free(p), pb.vector()
+        pb.time_op("setup", uv, pv, yv, 0.0, 1)
+        pb.time_op("apply_pa", uv, pv, yv, 2.0e5, 1)
+        assert np.array_equal(yv.free(), kp)
+        out[variant] = kp
+    assert max_rel_err(out["0"], out["10"]) <= 1e-13
