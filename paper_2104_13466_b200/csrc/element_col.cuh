@@ -35,7 +35,9 @@ struct TabC {
 
 // shared layout of one element (component-serial): point slots [d][comp][q]
 // (V3 qi), x-stage output [k][j][a], y-stage output [k][b][a], point values /
-// backward accumulator U[c][b][a], the weight table W[q] = w_a w_b w_c det J
+// backward accumulator U[c][b][a], the weight table W[q] = w_a w_b w_c det J,
+// the staged rows and the table of lattice offsets of the N^3 box entries
+// (so a staged copy costs one shared load and an add, no index arithmetic)
 template <int N, bool VALS>
 struct ColLay {
   using C = V3<N, N, 1, 1, VALS>;
@@ -46,9 +48,18 @@ struct ColLay {
   static constexpr int PTS = (VALS ? 12 : 9) * SQ;
   static constexpr int X = PTS, Y = X + N * SX, U = Y + N * SY, W = U + N * SU;
   static constexpr int R = W + N * N * N;                   // staged rows [2][N^3]
-  static constexpr int PER = R + 2 * N * N * N;
+  static constexpr int TAB = R + 2 * N * N * N;             // int lattice offsets of the box entries
+  static constexpr int PER = TAB + (N * N * N + 1) / 2;
   __device__ static int qi(int d, int comp, int q) { return (d * 3 + comp) * SQ + q; }
 };
+
+template <int N>
+__device__ __forceinline__ void col_stage(const Geo& g, const double* __restrict__ field, int comp, int X0, int Y0,
+                                          int Z0, double* rows, int t, const int* tab) {
+  const double* base = field + comp * g.Ns + ((long long)Z0 * g.Ly + Y0) * g.Lx + X0;
+  for (int w = t; w < N * N * N; w += 32) cp_async8(rows + w, base + tab[w]);
+  cp_async_commit();
+}
 
 template <int N, int MIR, bool VAL, bool VALS>
 __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g, const double* __restrict__ src,
@@ -60,15 +71,16 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
   constexpr int NE = Mr::NE > 0 ? Mr::NE : 1, NO = Mr::NO > 0 ? Mr::NO : 1;
   constexpr int PE = Mp::NE, PO = Mp::NO > 0 ? Mp::NO : 1;
   double* R = S + L::R;
+  const int* tab = reinterpret_cast<const int*>(S + L::TAB);
 #pragma unroll 1
   for (int comp = 0; comp < 3; ++comp) {
     {
       double* nb = R + (*buf ^ 1) * N * N * N;
       if (comp + 1 < 3) {
-        v3_stage_rows<N, 32>(g, src, comp + 1, X0, Y0, Z0, nb, t);
+        col_stage<N>(g, src, comp + 1, X0, Y0, Z0, nb, t, tab);
         cp_async_wait<1>();
       } else if (next.field) {
-        v3_stage_rows<N, 32>(g, next.field, 0, next.X0, next.Y0, next.Z0, nb, t);
+        col_stage<N>(g, next.field, 0, next.X0, next.Y0, next.Z0, nb, t, tab);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
@@ -265,13 +277,17 @@ __global__ void __launch_bounds__(32, MINB) element_col(const __grid_constant__ 
   const double mu_k = args.c_k * g.mu, lam_k = args.c_k * g.lam;
   const double cmr = args.c_m * g.rho;
   const double* first_field = UPASS ? args.u : args.p;
-  // weight table W[q] = w_a w_b w_c det J
-  for (int q = t; q < Q; q += 32)
+  // weight table W[q] = w_a w_b w_c det J and the box-offset table
+  int* tab = reinterpret_cast<int*>(S + L::TAB);
+  for (int q = t; q < Q; q += 32) {
     S[L::W + q] = tb.wq[q % N] * tb.wq[(q / N) % N] * tb.wq[q / (N * N)] * tb.detJ;
+    tab[q] = ((q / (N * N)) * g.Ly + (q / N) % N) * g.Lx + q % N;
+  }
+  __syncwarp();
   if ((long long)blockIdx.x < cnt) {
     int ei, ej, ek;
     colour_element(g, args.colour, blockIdx.x, ei, ej, ek);
-    v3_stage_rows<N, 32>(g, first_field, 0, (N - 1) * ei, (N - 1) * ej, (N - 1) * ek, S + L::R, t);
+    col_stage<N>(g, first_field, 0, (N - 1) * ei, (N - 1) * ej, (N - 1) * ek, S + L::R, t, tab);
   }
   for (long long idx = blockIdx.x; idx < cnt; idx += stride) {
     int ei, ej, ek;
