@@ -53,15 +53,15 @@ struct ColLay {
   __device__ static int qi(int d, int comp, int q) { return (d * 3 + comp) * SQ + q; }
 };
 
-template <int N>
+template <int N, int T>
 __device__ __forceinline__ void col_stage(const Geo& g, const double* __restrict__ field, int comp, int X0, int Y0,
                                           int Z0, double* rows, int t, const int* tab) {
   const double* base = field + comp * g.Ns + ((long long)Z0 * g.Ly + Y0) * g.Lx + X0;
-  for (int w = t; w < N * N * N; w += 32) cp_async8(rows + w, base + tab[w]);
+  for (int w = t; w < N * N * N; w += T) cp_async8(rows + w, base + tab[w]);
   cp_async_commit();
 }
 
-template <int N, int MIR, bool VAL, bool VALS>
+template <int N, int WPE, int MIR, bool VAL, bool VALS>
 __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g, const double* __restrict__ src,
                                             int X0, int Y0, int Z0, double* S, int t, int* buf, NextRows next,
                                             bool grad) {
@@ -77,18 +77,18 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
     {
       double* nb = R + (*buf ^ 1) * N * N * N;
       if (comp + 1 < 3) {
-        col_stage<N>(g, src, comp + 1, X0, Y0, Z0, nb, t, tab);
+        col_stage<N, 32 * WPE>(g, src, comp + 1, X0, Y0, Z0, nb, t, tab);
         cp_async_wait<1>();
       } else if (next.field) {
-        col_stage<N>(g, next.field, 0, next.X0, next.Y0, next.Z0, nb, t, tab);
+        col_stage<N, 32 * WPE>(g, next.field, 0, next.X0, next.Y0, next.Z0, nb, t, tab);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
-      __syncwarp();
+      group_sync<WPE>(0);
     }
     // x stage: item (k, j) -> values at a
-    for (int w = t; w < N * N; w += 32) {
+    for (int w = t; w < N * N; w += 32 * WPE) {
       const double* row = R + *buf * N * N * N + w * N;
       double v[N], E[NE], O[NO], o[N];
 #pragma unroll
@@ -98,9 +98,9 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
 #pragma unroll
       for (int a = 0; a < N; ++a) S[L::X + (w / N) * L::SX + (w % N) * N + a] = o[a];
     }
-    __syncwarp();
+    group_sync<WPE>(0);
     // y stage: item (k, a) -> values at b
-    for (int w = t; w < N * N; w += 32) {
+    for (int w = t; w < N * N; w += 32 * WPE) {
       const int k = w / N, a = w % N;
       double v[N], E[NE], O[NO], o[N];
 #pragma unroll
@@ -110,9 +110,9 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
 #pragma unroll
       for (int b = 0; b < N; ++b) S[L::Y + k * L::SY + b * N + a] = o[b];
     }
-    __syncwarp();
+    group_sync<WPE>(0);
     // z stage: column (b, a) -> values U at c, and d/dz at the points
-    for (int w = t; w < N * N; w += 32) {
+    for (int w = t; w < N * N; w += 32 * WPE) {
       double v[N], E[NE], O[NO], u[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) v[k] = S[L::Y + k * L::SY + w];
@@ -132,10 +132,10 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
         for (int c = 0; c < N; ++c) S[L::qi(2, comp, c * N * N + w)] = gz[c];
       }
     }
-    __syncwarp();
+    group_sync<WPE>(0);
     if (grad) {
       // x pencils (c, b) and y pencils (c, a) of the point values
-      for (int w = t; w < N * N; w += 32) {
+      for (int w = t; w < N * N; w += 32 * WPE) {
         const int c = w / N, r = w % N;
         double v[N], pe[PE], po[PO], gx[N], gy[N];
 #pragma unroll
@@ -151,7 +151,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
 #pragma unroll
         for (int b = 0; b < N; ++b) S[L::qi(1, comp, c * N * N + b * N + r)] = gy[b];
       }
-      __syncwarp();
+      group_sync<WPE>(0);
     }
     *buf ^= 1;
   }
@@ -159,7 +159,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
 
 // backward: per component, the weighted flux slots 0..2 (and the weighted
 // value slot 3 when VAL) -> y += B^T (x) B^T (x) B^T (sum_d D^_d^T F_d [+ V])
-template <int N, int MIR, bool VAL, bool VALS>
+template <int N, int WPE, int MIR, bool VAL, bool VALS>
 __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& g, double* __restrict__ dst, int X0,
                                              int Y0, int Z0, double* S, int t, double* evb, bool grad) {
   using L = ColLay<N, VALS>;
@@ -170,7 +170,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
   for (int comp = 0; comp < 3; ++comp) {
     if (grad) {
       // x' pencils (c, b): U = D^_x^T F_x
-      for (int w = t; w < N * N; w += 32) {
+      for (int w = t; w < N * N; w += 32 * WPE) {
         const int c = w / N, b = w % N;
         double q[N], qe[HP], qo[H], y[N];
 #pragma unroll
@@ -180,9 +180,9 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
 #pragma unroll
         for (int a = 0; a < N; ++a) S[L::U + c * L::SU + b * N + a] = y[a];
       }
-      __syncwarp();
+      group_sync<WPE>(0);
       // y' pencils (c, a): U += D^_y^T F_y
-      for (int w = t; w < N * N; w += 32) {
+      for (int w = t; w < N * N; w += 32 * WPE) {
         const int c = w / N, a = w % N;
         double q[N], qe[HP], qo[H], y[N];
 #pragma unroll
@@ -195,10 +195,10 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
 #pragma unroll
         for (int b = 0; b < N; ++b) S[L::U + c * L::SU + b * N + a] = y[b];
       }
-      __syncwarp();
+      group_sync<WPE>(0);
     }
     // z' columns (b, a): V = U + D^_z^T F_z (+ value term), then B^T along z
-    for (int w = t; w < N * N; w += 32) {
+    for (int w = t; w < N * N; w += 32 * WPE) {
       double v[N], q[N], qe[HP], qo[H], h[N];
 #pragma unroll
       for (int c = 0; c < N; ++c) v[c] = grad ? S[L::U + c * L::SU + w] : 0.0;
@@ -217,9 +217,9 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
 #pragma unroll
       for (int k = 0; k < N; ++k) S[L::Y + k * L::SY + w] = h[k];
     }
-    __syncwarp();
+    group_sync<WPE>(0);
     // y' items (k, a): B^T along y
-    for (int w = t; w < N * N; w += 32) {
+    for (int w = t; w < N * N; w += 32 * WPE) {
       const int k = w / N, a = w % N;
       double v[N], qe[HP], qo[H], h[N];
 #pragma unroll
@@ -229,9 +229,9 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
 #pragma unroll
       for (int j = 0; j < N; ++j) S[L::X + k * L::SX + j * N + a] = h[j];
     }
-    __syncwarp();
+    group_sync<WPE>(0);
     // x' items (k, j): B^T along x, scatter
-    for (int w = t; w < N * N; w += 32) {
+    for (int w = t; w < N * N; w += 32 * WPE) {
       const int k = w / N, j = w % N;
       double v[N], qe[HP], qo[H], acc[N];
 #pragma unroll
@@ -251,7 +251,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
       for (int i = 0; i < N; ++i)
         if (!chk || !constrained(g, comp, X0 + i, Y, Z)) red_add(row + i, acc[i]);
     }
-    __syncwarp();
+    group_sync<WPE>(0);
   }
 }
 
@@ -259,12 +259,13 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
 // stored quadrature data (MODE_PA), and that data (MODE_SETUP, from the same
 // collocated grad u, so MODE_PA is bit-identical to MODE_APPLY); one warp per
 // element, persistent.
-template <int N, int MINB, int MODE, bool VAL, int MIR>
-__global__ void __launch_bounds__(32, MINB) element_col(const __grid_constant__ TabC<N, MIR> tb,
+template <int N, int WPE, int MINB, int MODE, bool VAL, int MIR>
+__global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_constant__ TabC<N, MIR> tb,
                                                         const __grid_constant__ Geo g, OpArgs args) {
   constexpr bool VALS = VAL;
   using L = ColLay<N, VALS>;
-  constexpr int Q = N * N * N, QPT = (Q + 31) / 32;
+  constexpr int T = 32 * WPE;
+  constexpr int Q = N * N * N, QPT = (Q + T - 1) / T;
   extern __shared__ double smem[];
   double* S = smem;
   const int t = threadIdx.x;
@@ -279,15 +280,15 @@ __global__ void __launch_bounds__(32, MINB) element_col(const __grid_constant__ 
   const double* first_field = UPASS ? args.u : args.p;
   // weight table W[q] = w_a w_b w_c det J and the box-offset table
   int* tab = reinterpret_cast<int*>(S + L::TAB);
-  for (int q = t; q < Q; q += 32) {
+  for (int q = t; q < Q; q += T) {
     S[L::W + q] = tb.wq[q % N] * tb.wq[(q / N) % N] * tb.wq[q / (N * N)] * tb.detJ;
     tab[q] = ((q / (N * N)) * g.Ly + (q / N) % N) * g.Lx + q % N;
   }
-  __syncwarp();
+  group_sync<WPE>(0);
   if ((long long)blockIdx.x < cnt) {
     int ei, ej, ek;
     colour_element(g, args.colour, blockIdx.x, ei, ej, ek);
-    col_stage<N>(g, first_field, 0, (N - 1) * ei, (N - 1) * ej, (N - 1) * ek, S + L::R, t, tab);
+    col_stage<N, 32 * WPE>(g, first_field, 0, (N - 1) * ei, (N - 1) * ej, (N - 1) * ek, S + L::R, t, tab);
   }
   for (long long idx = blockIdx.x; idx < cnt; idx += stride) {
     int ei, ej, ek;
@@ -303,10 +304,10 @@ __global__ void __launch_bounds__(32, MINB) element_col(const __grid_constant__ 
     double Hu[QPT][9];
     if (UPASS) {
       const NextRows after_u = MODE == MODE_APPLY ? NextRows{args.p, X0, Y0, Z0} : nxt;
-      col_forward<N, MIR, false, VALS>(tb, g, args.u, X0, Y0, Z0, S, t, &buf, after_u, true);
+      col_forward<N, WPE, MIR, false, VALS>(tb, g, args.u, X0, Y0, Z0, S, t, &buf, after_u, true);
 #pragma unroll
       for (int r = 0; r < QPT; ++r) {
-        const int q = t + r * 32;
+        const int q = t + r * T;
         if (q < Q) {
 #pragma unroll
           for (int i = 0; i < 3; ++i)
@@ -314,12 +315,12 @@ __global__ void __launch_bounds__(32, MINB) element_col(const __grid_constant__ 
             for (int d = 0; d < 3; ++d) Hu[r][i * 3 + d] = S[L::qi(d, i, q)];
         }
       }
-      __syncwarp();
+      group_sync<WPE>(0);
     }
-    if (PPASS) col_forward<N, MIR, VAL, VALS>(tb, g, args.p, X0, Y0, Z0, S, t, &buf, nxt, true);
+    if (PPASS) col_forward<N, WPE, MIR, VAL, VALS>(tb, g, args.p, X0, Y0, Z0, S, t, &buf, nxt, true);
 #pragma unroll
     for (int r = 0; r < QPT; ++r) {
-      const int q = t + r * 32;
+      const int q = t + r * T;
       if (q >= Q) continue;
       const double wdet = S[L::W + q];
       QpK s;
@@ -384,10 +385,10 @@ __global__ void __launch_bounds__(32, MINB) element_col(const __grid_constant__ 
         }
       }
     }
-    __syncwarp();
+    group_sync<WPE>(0);
     if (MODE == MODE_SETUP) continue;
     double* evb = args.ev ? args.ev + eid * 3 * Q : nullptr;
-    col_backward<N, MIR, VAL, VALS>(tb, g, args.y, X0, Y0, Z0, S, t, evb, true);
+    col_backward<N, WPE, MIR, VAL, VALS>(tb, g, args.y, X0, Y0, Z0, S, t, evb, true);
   }
 }
 

@@ -335,6 +335,14 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
     element_eo_or_plain<N, M, SK>(c, mode, tb, a);
     return;
   } else if constexpr (N >= 6) {
+    if constexpr (N == M) {
+      if ((mode == MODE_FINT || mode == MODE_APPLY || mode == MODE_PA || mode == MODE_SETUP) && c->variant != 10 &&
+          c->mir >= 0) {
+        if (c->mir == 0) col_modes<N, 0>(c, mode, a);
+        else col_modes<N, 1>(c, mode, a);
+        return;
+      }
+    }
     element_eo_or_plain<N, M, typename LargeShape<N, M>::type>(c, mode, tb, a);
     return;
   } else {
@@ -414,13 +422,15 @@ TabC<N, MIR> make_tabc(const sdme_ctx* c) {
 
 template <int N, int MODE, bool VAL, int MIR>
 void launch_col(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
+  constexpr int WPE = LargeShape<N, N>::WPE;  // one round per stage
+  constexpr int T = 32 * WPE;
   constexpr int smem = ColLay<N, VAL>::PER * 8;
-  auto kern = element_col<N, 11, MODE, VAL, MIR>;
+  auto kern = element_col<N, WPE, (WPE == 1 ? 11 : 1), MODE, VAL, MIR>;
   static int max_blocks = -1;
   if (max_blocks < 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T, smem);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     max_blocks = std::max(1, nb) * sms;
@@ -429,7 +439,7 @@ void launch_col(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
     // setup: no scatter, one pass over all elements; E-vector mode: boxes + gather
     a.colour = -1;
     if (MODE != MODE_SETUP) a.ev = c->d_ev;
-    kern<<<(unsigned)std::min<long long>(colour_count(c->geo, -1), max_blocks), 32, smem, c->st>>>(tb, c->geo, a);
+    kern<<<(unsigned)std::min<long long>(colour_count(c->geo, -1), max_blocks), T, smem, c->st>>>(tb, c->geo, a);
     if (MODE == MODE_SETUP || c->ev_no_gather) ++c->launches;
     else ev_gather<N>(c, a);
     return;
@@ -438,7 +448,7 @@ void launch_col(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
     const long long cnt = colour_count(c->geo, col);
     if (cnt == 0) continue;
     a.colour = col;
-    kern<<<(unsigned)std::min<long long>(cnt, max_blocks), 32, smem, c->st>>>(tb, c->geo, a);
+    kern<<<(unsigned)std::min<long long>(cnt, max_blocks), T, smem, c->st>>>(tb, c->geo, a);
     ++c->launches;
   }
 }
