@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(128) k_contact(const __grid_constant__ FaceTab
     c[axis] = plane;
     c[d1] = P * f1 + l1;
     c[d2] = P * f2 + l2;
-    su[comp][r] = ca.u[comp * g.Ns + ((long long)c[2] * g.Ly + c[1]) * g.Lx + c[0]];
+    su[comp][r] = ca.u[comp * g.Ns + ((long long)c[2] * g.Ly + c[1]) * g.Px + c[0]];
   }
   __syncthreads();
   // points: gap and pressure (force), or eps warea (n . N p) on the active set (apply),
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(128) k_contact(const __grid_constant__ FaceTab
     c[axis] = plane;
     c[d1] = P * f1 + l1;
     c[d2] = P * f2 + l2;
-    const long long off = ((long long)c[2] * g.Ly + c[1]) * g.Lx + c[0];
+    const long long off = ((long long)c[2] * g.Ly + c[1]) * g.Px + c[0];
 #pragma unroll
     for (int comp = 0; comp < 3; ++comp) {
       if (ca.normal[comp] != 0.0 && !constrained(g, comp, c[0], c[1], c[2]))

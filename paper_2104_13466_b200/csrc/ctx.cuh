@@ -30,8 +30,10 @@ struct sdme_ctx {
   double h[3]{}, origin[3]{};
   std::vector<double> Bl, Dl, w;  // lattice-local order, m x n
   cudaStream_t st = nullptr;
-  long long nvec = 0;             // 3 * Ns
+  long long nvec = 0;             // 3 * Ns (device vector length, pitched rows)
+  long long nlat = 0;             // 3 * Lx * Ly * Lz (dense host lattice arrays)
   std::vector<double*> vecs;
+  std::vector<void*> vec_tmaps;  // device CUtensorMap per vector (element box TMA), parallel to vecs
   int* d_perm = nullptr;
   int64_t n_free = 0;
   unsigned char* d_free = nullptr;  // 1 on free lattice dofs
@@ -92,6 +94,9 @@ struct sdme_ctx {
   double* d_energy = nullptr;  // per-element strain energy (sdme_strain_energy)
   bool pa = true;  // SDME_PA=0 disables (the PCG then applies K(u) from scratch)
 };
+
+// TMA tensor map (device address) of a context vector, nullptr if none
+const void* sdme_tmap_of(const sdme_ctx* c, const double* v);
 
 // per-order operator tables (ops.cu, one object file per P)
 const SdmeOps* sdme_ops_p1(int m);

@@ -18,6 +18,7 @@
 // (parity tests at 1e-12 against the reference).
 #pragma once
 #include "element_eo.cuh"
+#include "tma.cuh"
 
 namespace sdme {
 
@@ -36,9 +37,12 @@ struct TabC {
 // shared layout of one element (component-serial): point slots [d][comp][q]
 // (V3 qi), x-stage output [k][j][a], y-stage output [k][b][a], point values /
 // backward accumulator U[c][b][a], the weight table W[q] = w_a w_b w_c det J,
-// the staged rows and the table of lattice offsets of the N^3 box entries
-// (so a staged copy costs one shared load and an add, no index arithmetic)
-template <int N, bool VALS>
+// then either (TM = false) the cp.async-staged rows [2][N^3] and the table of
+// lattice offsets of the N^3 box entries (a staged copy costs one shared load
+// and an add), or (TM = true) three TMA boxes [k][j][RP] (two staging buffers
+// and the output box of the bulk reduce-add; RP = row pitch, N rounded up to
+// even so that box rows are 16-byte multiples) and their two mbarriers.
+template <int N, bool VALS, bool TM = false>
 struct ColLay {
   using C = V3<N, N, 1, 1, VALS>;
   static constexpr int SQ = C::Ly::sq;
@@ -47,25 +51,36 @@ struct ColLay {
   static constexpr int SU = N * N;                          // point values, c stride
   static constexpr int PTS = (VALS ? 12 : 9) * SQ;
   static constexpr int X = PTS, Y = X + N * SX, U = Y + N * SY, W = U + N * SU;
-  static constexpr int R = W + N * N * N;                   // staged rows [2][N^3]
-  static constexpr int TAB = R + 2 * N * N * N;             // int lattice offsets of the box entries
-  static constexpr int PER = TAB + (N * N * N + 1) / 2;
+  static constexpr int RP = TM ? N + (N & 1) : N;           // staged row pitch
+  static constexpr int RB = TM ? (N * N * RP + 15) / 16 * 16 : N * N * N;  // one staging buffer (128-B multiple)
+  static constexpr int R = TM ? (W + N * N * N + 15) / 16 * 16 : W + N * N * N;
+  static constexpr int O = R + 2 * RB;                      // TM: output box of the reduce-add
+  static constexpr int TAB = R + 2 * RB;                    // !TM: int lattice offsets of the box entries
+  static constexpr int BAR = O + RB;                        // TM: two mbarriers
+  static constexpr int PER = TM ? BAR + 2 : TAB + (N * N * N + 1) / 2;
   __device__ static int qi(int d, int comp, int q) { return (d * 3 + comp) * SQ + q; }
+};
+
+// what to stage after the last component of a forward pass (TMA path)
+struct NextBox {
+  const CUtensorMap* map;  // nullptr: nothing
+  int X0, Y0, Z0;
 };
 
 template <int N, int T>
 __device__ __forceinline__ void col_stage(const Geo& g, const double* __restrict__ field, int comp, int X0, int Y0,
                                           int Z0, double* rows, int t, const int* tab) {
-  const double* base = field + comp * g.Ns + ((long long)Z0 * g.Ly + Y0) * g.Lx + X0;
+  const double* base = field + comp * g.Ns + ((long long)Z0 * g.Ly + Y0) * g.Px + X0;
   for (int w = t; w < N * N * N; w += T) cp_async8(rows + w, base + tab[w]);
   cp_async_commit();
 }
 
-template <int N, int WPE, int MIR, bool VAL, bool VALS>
+template <int N, int WPE, int MIR, bool VAL, bool VALS, bool TM = false>
 __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g, const double* __restrict__ src,
                                             int X0, int Y0, int Z0, double* S, int t, int* buf, NextRows next,
-                                            bool grad) {
-  using L = ColLay<N, VALS>;
+                                            bool grad, const CUtensorMap* smap = nullptr, NextBox nbox = {},
+                                            unsigned* ph = nullptr) {
+  using L = ColLay<N, VALS, TM>;
   using Mr = Mir<N, MIR>;
   using Mp = Mir<N, 0>;
   constexpr int NE = Mr::NE > 0 ? Mr::NE : 1, NO = Mr::NO > 0 ? Mr::NO : 1;
@@ -74,7 +89,23 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
   const int* tab = reinterpret_cast<const int*>(S + L::TAB);
 #pragma unroll 1
   for (int comp = 0; comp < 3; ++comp) {
-    {
+    if (TM) {
+      // one lane issues the next box (this field's next component, or the
+      // next field / element), then every lane waits for the current box
+      const int nbi = *buf ^ 1;
+      unsigned long long* bars = reinterpret_cast<unsigned long long*>(S + L::BAR);
+      if (t == 0) {
+        if (comp + 1 < 3) {
+          mbar_expect_tx(bars + nbi, N * N * L::RP * 8);
+          tma_load_box(R + nbi * L::RB, smap, X0, Y0, Z0, comp + 1, bars + nbi);
+        } else if (nbox.map) {
+          mbar_expect_tx(bars + nbi, N * N * L::RP * 8);
+          tma_load_box(R + nbi * L::RB, nbox.map, nbox.X0, nbox.Y0, nbox.Z0, 0, bars + nbi);
+        }
+      }
+      mbar_wait(bars + *buf, (*ph >> *buf) & 1u);
+      *ph ^= 1u << *buf;
+    } else {
       double* nb = R + (*buf ^ 1) * N * N * N;
       if (comp + 1 < 3) {
         col_stage<N, 32 * WPE>(g, src, comp + 1, X0, Y0, Z0, nb, t, tab);
@@ -89,10 +120,21 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
     }
     // x stage: item (k, j) -> values at a
     for (int w = t; w < N * N; w += 32 * WPE) {
-      const double* row = R + *buf * N * N * N + w * N;
       double v[N], E[NE], O[NO], o[N];
+      if (TM) {
+        // 16-byte loads of the pitched box row (conflict-free for RP = 6)
+        const double2* row = reinterpret_cast<const double2*>(R + *buf * L::RB + w * L::RP);
 #pragma unroll
-      for (int i = 0; i < N; ++i) v[i] = row[i];
+        for (int i = 0; i < L::RP / 2; ++i) {
+          const double2 d = row[i];
+          v[2 * i] = d.x;
+          if (2 * i + 1 < N) v[2 * i + 1] = d.y;
+        }
+      } else {
+        const double* row = R + *buf * N * N * N + w * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] = row[i];
+      }
       eo_split<N, MIR>(v, E, O);
       eo_fwd<N, Mr::NE, Mr::NO>(tb.B, E, O, o);
 #pragma unroll
@@ -159,10 +201,11 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
 
 // backward: per component, the weighted flux slots 0..2 (and the weighted
 // value slot 3 when VAL) -> y += B^T (x) B^T (x) B^T (sum_d D^_d^T F_d [+ V])
-template <int N, int WPE, int MIR, bool VAL, bool VALS>
+template <int N, int WPE, int MIR, bool VAL, bool VALS, bool TM = false>
 __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& g, double* __restrict__ dst, int X0,
-                                             int Y0, int Z0, double* S, int t, double* evb, bool grad) {
-  using L = ColLay<N, VALS>;
+                                             int Y0, int Z0, double* S, int t, double* evb, bool grad,
+                                             const CUtensorMap* ymap = nullptr) {
+  using L = ColLay<N, VALS, TM>;
   using Mr = Mir<N, MIR>;
   using Mp = Mir<N, 0>;
   constexpr int HP = Half<N>::HP, H = Half<N>::H > 0 ? Half<N>::H : 1;
@@ -231,6 +274,11 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
     }
     group_sync<WPE>(0);
     // x' items (k, j): B^T along x, scatter
+    if (TM) {
+      // the output box of the previous component's reduce-add has been read
+      if (t == 0) bulk_wait_read();
+      group_sync<WPE>(0);
+    }
     for (int w = t; w < N * N; w += 32 * WPE) {
       const int k = w / N, j = w % N;
       double v[N], qe[HP], qo[H], acc[N];
@@ -238,6 +286,22 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
       for (int a = 0; a < N; ++a) v[a] = S[L::X + k * L::SX + j * N + a];
       eo_qsplit<N>(v, qe, qo);
       eo_bwd<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.bB, qe, qo, acc);
+      if (TM) {
+        // row of the output box; constrained points and the pitch slot get 0
+        // (the reduce-add of +0.0 outside the element touches only points no
+        // other element of this colour pass owns, or is dropped at the edge)
+        const int Z = Z0 + k, Y = Y0 + j;
+        if (touches_dirichlet(g, comp, X0, Y0, Z0, N)) {
+#pragma unroll
+          for (int i = 0; i < N; ++i)
+            if (constrained(g, comp, X0 + i, Y, Z)) acc[i] = 0.0;
+        }
+        double2* orow = reinterpret_cast<double2*>(S + L::O + w * L::RP);
+#pragma unroll
+        for (int i = 0; i < L::RP / 2; ++i)
+          orow[i] = make_double2(acc[2 * i], 2 * i + 1 < N ? acc[2 * i + 1] : 0.0);
+        continue;
+      }
       if (evb) {
         double* er = evb + ((comp * N + k) * N + j) * N;
 #pragma unroll
@@ -246,12 +310,14 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
       }
       const int Z = Z0 + k, Y = Y0 + j;
       const bool chk = touches_dirichlet(g, comp, X0, Y0, Z0, N);
-      double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Lx + X0;
+      double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Px + X0;
 #pragma unroll
       for (int i = 0; i < N; ++i)
         if (!chk || !constrained(g, comp, X0 + i, Y, Z)) red_add(row + i, acc[i]);
     }
+    if (TM) fence_proxy_async_smem();
     group_sync<WPE>(0);
+    if (TM && t == 0) tma_reduce_add_box(ymap, S + L::O, X0, Y0, Z0, comp);
   }
 }
 
@@ -259,14 +325,14 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
 // stored quadrature data (MODE_PA), and that data (MODE_SETUP, from the same
 // collocated grad u, so MODE_PA is bit-identical to MODE_APPLY); one warp per
 // element, persistent.
-template <int N, int WPE, int MINB, int MODE, bool VAL, int MIR>
+template <int N, int WPE, int MINB, int MODE, bool VAL, int MIR, bool TM = false>
 __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_constant__ TabC<N, MIR> tb,
                                                         const __grid_constant__ Geo g, OpArgs args) {
   constexpr bool VALS = VAL;
-  using L = ColLay<N, VALS>;
+  using L = ColLay<N, VALS, TM>;
   constexpr int T = 32 * WPE;
   constexpr int Q = N * N * N, QPT = (Q + T - 1) / T;
-  extern __shared__ double smem[];
+  extern __shared__ __align__(128) double smem[];
   double* S = smem;
   const int t = threadIdx.x;
   int buf = 0;
@@ -278,17 +344,35 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
   const double mu_k = args.c_k * g.mu, lam_k = args.c_k * g.lam;
   const double cmr = args.c_m * g.rho;
   const double* first_field = UPASS ? args.u : args.p;
+  const CUtensorMap* umap = static_cast<const CUtensorMap*>(args.tu);
+  const CUtensorMap* pmap = static_cast<const CUtensorMap*>(args.tp);
+  const CUtensorMap* first_map = UPASS ? umap : pmap;
+  unsigned ph = 0;  // TM: mbarrier phase bit per staging buffer
   // weight table W[q] = w_a w_b w_c det J and the box-offset table
   int* tab = reinterpret_cast<int*>(S + L::TAB);
   for (int q = t; q < Q; q += T) {
     S[L::W + q] = tb.wq[q % N] * tb.wq[(q / N) % N] * tb.wq[q / (N * N)] * tb.detJ;
-    tab[q] = ((q / (N * N)) * g.Ly + (q / N) % N) * g.Lx + q % N;
+    if (!TM) tab[q] = ((q / (N * N)) * g.Ly + (q / N) % N) * g.Px + q % N;
+  }
+  if (TM && t == 0) {
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(S + L::BAR);
+    mbar_init(bars, 1);
+    mbar_init(bars + 1, 1);
+    mbar_fence_init();
   }
   group_sync<WPE>(0);
   if ((long long)blockIdx.x < cnt) {
     int ei, ej, ek;
     colour_element(g, args.colour, blockIdx.x, ei, ej, ek);
-    col_stage<N, 32 * WPE>(g, first_field, 0, (N - 1) * ei, (N - 1) * ej, (N - 1) * ek, S + L::R, t, tab);
+    if (TM) {
+      if (t == 0) {
+        unsigned long long* bars = reinterpret_cast<unsigned long long*>(S + L::BAR);
+        mbar_expect_tx(bars, N * N * L::RP * 8);
+        tma_load_box(S + L::R, first_map, (N - 1) * ei, (N - 1) * ej, (N - 1) * ek, 0, bars);
+      }
+    } else {
+      col_stage<N, 32 * WPE>(g, first_field, 0, (N - 1) * ei, (N - 1) * ej, (N - 1) * ek, S + L::R, t, tab);
+    }
   }
   for (long long idx = blockIdx.x; idx < cnt; idx += stride) {
     int ei, ej, ek;
@@ -296,15 +380,19 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
     const int X0 = (N - 1) * ei, Y0 = (N - 1) * ej, Z0 = (N - 1) * ek;
     const long long eid = ((long long)ek * g.ny + ej) * g.nx + ei;
     NextRows nxt{nullptr, 0, 0, 0};
+    NextBox nxb{nullptr, 0, 0, 0};
     if (idx + stride < cnt) {
       int ni, nj, nk;
       colour_element(g, args.colour, idx + stride, ni, nj, nk);
-      nxt = NextRows{first_field, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
+      if (TM) nxb = NextBox{first_map, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
+      else nxt = NextRows{first_field, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
     }
     double Hu[QPT][9];
     if (UPASS) {
       const NextRows after_u = MODE == MODE_APPLY ? NextRows{args.p, X0, Y0, Z0} : nxt;
-      col_forward<N, WPE, MIR, false, VALS>(tb, g, args.u, X0, Y0, Z0, S, t, &buf, after_u, true);
+      const NextBox after_ub = MODE == MODE_APPLY ? NextBox{pmap, X0, Y0, Z0} : nxb;
+      col_forward<N, WPE, MIR, false, VALS, TM>(tb, g, args.u, X0, Y0, Z0, S, t, &buf, after_u, true, umap,
+                                                after_ub, &ph);
 #pragma unroll
       for (int r = 0; r < QPT; ++r) {
         const int q = t + r * T;
@@ -317,7 +405,8 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
       }
       group_sync<WPE>(0);
     }
-    if (PPASS) col_forward<N, WPE, MIR, VAL, VALS>(tb, g, args.p, X0, Y0, Z0, S, t, &buf, nxt, true);
+    if (PPASS)
+      col_forward<N, WPE, MIR, VAL, VALS, TM>(tb, g, args.p, X0, Y0, Z0, S, t, &buf, nxt, true, pmap, nxb, &ph);
 #pragma unroll
     for (int r = 0; r < QPT; ++r) {
       const int q = t + r * T;
@@ -388,8 +477,11 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
     group_sync<WPE>(0);
     if (MODE == MODE_SETUP) continue;
     double* evb = args.ev ? args.ev + eid * 3 * Q : nullptr;
-    col_backward<N, WPE, MIR, VAL, VALS>(tb, g, args.y, X0, Y0, Z0, S, t, evb, true);
+    col_backward<N, WPE, MIR, VAL, VALS, TM>(tb, g, args.y, X0, Y0, Z0, S, t, evb, true,
+                                             static_cast<const CUtensorMap*>(args.ty));
   }
+  // the reduce-adds have completed before the CTA (and its shared memory) retires
+  if (TM && t == 0) bulk_wait_all();
 }
 
 }  // namespace sdme

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_diag3(const __gr
           continue;
         }
         const int Z = Z0 + k, Y = Y0 + j;
-        double* row = args.y + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Lx + X0;
+        double* row = args.y + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Px + X0;
 #pragma unroll
         for (int i = 0; i < N; ++i)
           if (!constrained(g, comp, X0 + i, Y, Z)) red_add(row + i, acc[r][i]);

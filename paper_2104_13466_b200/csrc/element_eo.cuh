@@ -45,7 +45,7 @@ __device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo
 #pragma unroll
         for (int i = 0; i < N; ++i) v[i] = row[i];
       } else {
-        const double* row = src + comp * g.Ns + ((long long)(Z0 + k) * g.Ly + (Y0 + j)) * g.Lx + X0;
+        const double* row = src + comp * g.Ns + ((long long)(Z0 + k) * g.Ly + (Y0 + j)) * g.Px + X0;
 #pragma unroll
         for (int i = 0; i < N; ++i) v[i] = __ldg(row + i);
       }
@@ -241,7 +241,7 @@ __device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Ge
       }
       const int Z = Z0 + k, Y = Y0 + j;
       const bool chk = touches_dirichlet(g, comp, X0, Y0, Z0, N);
-      double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Lx + X0;
+      double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Px + X0;
 #pragma unroll
       for (int i = 0; i < N; ++i)
         if (!chk || !constrained(g, comp, X0 + i, Y, Z)) red_add(row + i, acc[i]);

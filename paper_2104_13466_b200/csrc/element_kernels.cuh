@@ -11,7 +11,9 @@
 // (element_v3.cuh, element_eo.cuh, element_diag.cuh).
 //
 // Data layout: every global vector is a lattice of
-// Lx*Ly*Lz points per displacement component, component-major, x fastest.
+// Lx*Ly*Lz points per displacement component, component-major, x fastest,
+// rows padded to the even pitch Px (the pad column is held at 0 like a
+// Dirichlet point; host-side lattice arrays stay dense, Lx per row).
 // Element (i,j,k) owns the (P+1)^3 box starting at (P*i, P*j, P*k).  The 1D
 // tables arrive permuted to *lattice-local* order (column l = lattice offset l),
 // so an element gather is a strided box with no index table.
@@ -31,6 +33,7 @@ namespace sdme {
 struct Geo {
   int nx, ny, nz;     // elements per axis
   int Lx, Ly, Lz;     // lattice points per axis (P*n+1)
+  int Px;             // x pitch of the device lattice (Lx rounded up to even: 16-byte rows for TMA)
   long long Ns;       // points per component plane
   double s[3];        // dxi/dX = 2/h per axis
   double detJ;        // h_x h_y h_z / 8
@@ -56,6 +59,11 @@ struct OpArgs {
   const int* skip = nullptr;     // if set and non-zero: return at once (stopped PCG graph)
   double* ev = nullptr;          // E-vector mode (colour < 0): element boxes stored, not scattered
   double* qpd = nullptr;         // quadrature data (MODE_SETUP writes, MODE_PA reads)
+  // TMA tensor maps (CUtensorMap in global memory) of u, p, y for the
+  // box-load / reduce-add element kernels; nullptr: per-lane staging and RED
+  const void* tu = nullptr;
+  const void* tp = nullptr;
+  const void* ty = nullptr;
 };
 
 __device__ __forceinline__ bool constrained(const Geo& g, int comp, int X, int Y, int Z) {
@@ -178,7 +186,8 @@ __device__ __forceinline__ bool ev_point(const double* __restrict__ ev, const Ge
   const int idx = (int)idx_, ns = (int)g.Ns;
   const int comp = idx / ns;
   const int r = idx - comp * ns;
-  const int rxy = r / g.Lx, X = r - rxy * g.Lx;
+  const int rxy = r / g.Px, X = r - rxy * g.Px;
+  if (X >= g.Lx) return false;  // pitch padding
   const int Z = rxy / g.Ly, Y = rxy - Z * g.Ly;
   if (constrained(g, comp, X, Y, Z)) return false;
   int ex[2], ox[2], ey[2], oy[2], ez[2], oz[2];

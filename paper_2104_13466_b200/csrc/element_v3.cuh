@@ -129,7 +129,7 @@ __device__ __forceinline__ void v3_stage_rows(const Geo& g, const double* __rest
   for (int w = t; w < N * N * N; w += T) {
     const int kj = w / N, i = w % N;
     const int k = kj / N, j = kj % N;
-    cp_async8(rows + w, field + comp * g.Ns + ((long long)(Z0 + k) * g.Ly + (Y0 + j)) * g.Lx + X0 + i);
+    cp_async8(rows + w, field + comp * g.Ns + ((long long)(Z0 + k) * g.Ly + (Y0 + j)) * g.Px + X0 + i);
   }
   cp_async_commit();
 }
@@ -145,7 +145,7 @@ __device__ __forceinline__ void v3_prefetch(const Geo& g, const double* __restri
                                             int t) {
   for (int w = t; w < 3 * N * N; w += T) {
     const int comp = w / (N * N), kj = w % (N * N);
-    const double* row = src + comp * g.Ns + ((long long)(Z0 + kj / N) * g.Ly + (Y0 + kj % N)) * g.Lx + X0;
+    const double* row = src + comp * g.Ns + ((long long)(Z0 + kj / N) * g.Ly + (Y0 + kj % N)) * g.Px + X0;
     prefetch_l2(row);
     prefetch_l2(row + N - 1);
   }
@@ -193,7 +193,7 @@ __device__ __forceinline__ void v3_forward(const Tab3<N, M>& tb, const Geo& g, c
 #pragma unroll
           for (int i = 0; i < N; ++i) v[i] = row[i];
         } else {
-          const double* row = src + comp * g.Ns + ((long long)(Z0 + k) * g.Ly + (Y0 + j)) * g.Lx + X0;
+          const double* row = src + comp * g.Ns + ((long long)(Z0 + k) * g.Ly + (Y0 + j)) * g.Px + X0;
 #pragma unroll
           for (int i = 0; i < N; ++i) v[i] = __ldg(row + i);
         }
@@ -383,7 +383,7 @@ __device__ __forceinline__ void v3_backward(const Tab3<N, M>& tb, const Geo& g, 
         }
         const int Z = Z0 + k, Y = Y0 + j;
         const bool chk = touches_dirichlet(g, comp, X0, Y0, Z0, N);
-        double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Lx + X0;
+        double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Px + X0;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
           double acc = 0.0;

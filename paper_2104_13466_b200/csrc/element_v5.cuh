@@ -296,7 +296,7 @@ __device__ __forceinline__ void v5_backward_yx(const TabEO<N, M, MIR>& tb, const
       }
       const int Z = Z0 + k, Y = Y0 + j;
       const bool chk = touches_dirichlet(g, comp, X0, Y0, Z0, N);
-      double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Lx + X0;
+      double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Px + X0;
 #pragma unroll
       for (int i = 0; i < N; ++i)
         if (!chk || !constrained(g, comp, X0 + i, Y, Z)) red_add(row + i, acc[i]);

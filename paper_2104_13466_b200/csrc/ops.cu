@@ -302,6 +302,9 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
   const Tab3<N, M> tb = make_tab3<N, M>(c);
   OpArgs a{u, p, y, ck, cm, 0, c->d_flag, c->cur_skip};
   a.qpd = mode == MODE_ENERGY ? y : c->d_qpd;  // MODE_ENERGY: y is the per-element energy buffer
+  a.tu = sdme_tmap_of(c, u);
+  a.tp = sdme_tmap_of(c, p);
+  a.ty = mode == MODE_ENERGY ? nullptr : sdme_tmap_of(c, y);
   if constexpr (N <= 5) {
     // E-vector mode (small meshes, one launch over all elements): latency
     // shape, four warps per element, all three components per stage
@@ -420,12 +423,12 @@ TabC<N, MIR> make_tabc(const sdme_ctx* c) {
   return t;
 }
 
-template <int N, int MODE, bool VAL, int MIR>
-void launch_col(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
+template <int N, int MODE, bool VAL, int MIR, bool TM>
+void launch_col_k(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
   constexpr int WPE = LargeShape<N, N>::WPE;  // one round per stage
   constexpr int T = 32 * WPE;
-  constexpr int smem = ColLay<N, VAL>::PER * 8;
-  auto kern = element_col<N, WPE, (WPE == 1 ? 11 : 1), MODE, VAL, MIR>;
+  constexpr int smem = ColLay<N, VAL, TM>::PER * 8;
+  auto kern = element_col<N, WPE, (WPE == 1 ? 11 : 1), MODE, VAL, MIR, TM>;
   static int max_blocks = -1;
   if (max_blocks < 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -451,6 +454,24 @@ void launch_col(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
     kern<<<(unsigned)std::min<long long>(cnt, max_blocks), T, smem, c->st>>>(tb, c->geo, a);
     ++c->launches;
   }
+}
+
+// TMA box loads / bulk reduce-add (tma.cuh) when every vector of the mode has
+// a tensor map and the colour passes scatter (not E-vector mode), for even P
+// only: element boxes start at x = P i, and an FP64 box whose start is not
+// 16-byte aligned faults (tools/micro/tma_f64.cu).  SDME_VARIANT=11 keeps the
+// cp.async / RED kernel (A/B only).
+template <int N, int MODE, bool VAL, int MIR>
+void launch_col(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
+  if constexpr (N % 2 == 1) {
+    const bool maps = MODE == MODE_SETUP ? a.tu != nullptr
+                                         : (a.ty && (MODE == MODE_PA || a.tu) && (MODE == MODE_FINT || a.tp));
+    if (maps && !c->ev_mode && c->variant != 11) {
+      launch_col_k<N, MODE, VAL, MIR, true>(c, tb, a);
+      return;
+    }
+  }
+  launch_col_k<N, MODE, VAL, MIR, false>(c, tb, a);
 }
 
 // collocated path: f_int, K.p (from u or from stored quadrature data)

@@ -1,6 +1,8 @@
 // C-ABI implementation: context, device vectors, operator dispatch over (P, m),
 // the Jacobi-PCG driver (solver.py:129-170), explicit step and contact.
 // Build: see paper_2104_13466_b200/build.py (nvcc -gencode arch=compute_100a,code=sm_100a).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -97,17 +99,60 @@ double* vec(sdme_ctx* c, int id) {
   return c->vecs[id];
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)f;
+  }();
+  return fn;
+}
+
+// Tensor map of one lattice vector for the element box TMA (tma.cuh): 4D
+// (x, y, z, component) FP64, pitched rows (Px), box (RP, n, n, 1) with RP = n
+// rounded up to even (16-byte box rows); elements outside (Lx, Ly, Lz) are
+// zero-filled on load and dropped on reduce.  nullptr if unavailable.
+void* make_tmap(sdme_ctx* ctx, double* p) {
+  if (getenv("SDME_NO_TMA")) return nullptr;
+  auto enc = tmap_encoder();
+  if (!enc) return nullptr;
+  const Geo& g = ctx->geo;
+  const int n = ctx->n, rp = n + (n & 1);
+  CUtensorMap m;
+  cuuint64_t dims[4] = {(cuuint64_t)g.Lx, (cuuint64_t)g.Ly, (cuuint64_t)g.Lz, 3};
+  cuuint64_t strides[3] = {(cuuint64_t)g.Px * 8, (cuuint64_t)g.Px * g.Ly * 8, (cuuint64_t)g.Ns * 8};
+  cuuint32_t box[4] = {(cuuint32_t)rp, (cuuint32_t)n, (cuuint32_t)n, 1}, es[4] = {1, 1, 1, 1};
+  if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return nullptr;
+  void* d = nullptr;
+  if (cudaMalloc(&d, sizeof(CUtensorMap)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, &m, sizeof(CUtensorMap), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  return d;
+}
+
 int alloc_vec(sdme_ctx* ctx, int* id) {
   double* p = nullptr;
   CK(cudaMalloc(&p, ctx->nvec * sizeof(double)));
   CK(cudaMemsetAsync(p, 0, ctx->nvec * sizeof(double), ctx->st));
+  void* tm = make_tmap(ctx, p);
   for (size_t i = 0; i < ctx->vecs.size(); ++i)
     if (!ctx->vecs[i]) {
       ctx->vecs[i] = p;
+      ctx->vec_tmaps[i] = tm;
       *id = (int)i;
       return SDME_OK;
     }
   ctx->vecs.push_back(p);
+  ctx->vec_tmaps.push_back(tm);
   *id = (int)ctx->vecs.size() - 1;
   return SDME_OK;
 }
@@ -285,6 +330,13 @@ int build_pcg_graph(sdme_ctx* ctx, const double* pu, double* px, double* r, doub
 }
 
 // =========================================================================
+const void* sdme_tmap_of(const sdme_ctx* c, const double* v) {
+  if (!v) return nullptr;
+  for (size_t i = 0; i < c->vecs.size(); ++i)
+    if (c->vecs[i] == v) return c->vec_tmaps[i];
+  return nullptr;
+}
+
 extern "C" {
 
 int sdme_create(const sdme_desc* d, sdme_ctx** out) {
@@ -317,7 +369,8 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   Geo& g = ctx->geo;
   g.nx = d->nx; g.ny = d->ny; g.nz = d->nz;
   g.Lx = P * d->nx + 1; g.Ly = P * d->ny + 1; g.Lz = P * d->nz + 1;
-  g.Ns = (long long)g.Lx * g.Ly * g.Lz;
+  g.Px = (g.Lx + 1) & ~1;  // even pitch: 16-byte aligned rows (TMA tensor maps)
+  g.Ns = (long long)g.Px * g.Ly * g.Lz;
   g.s[0] = 2.0 / d->hx; g.s[1] = 2.0 / d->hy; g.s[2] = 2.0 / d->hz;
   g.detJ = d->hx * d->hy * d->hz / 8.0;
   g.mu = d->mu; g.lam = d->lambda_lame; g.rho = d->rho0;
@@ -325,6 +378,7 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   ctx->h[0] = d->hx; ctx->h[1] = d->hy; ctx->h[2] = d->hz;
   for (int c = 0; c < 3; ++c) ctx->origin[c] = d->origin[c];
   ctx->nvec = 3 * g.Ns;
+  ctx->nlat = 3LL * g.Lx * g.Ly * g.Lz;
   ctx->n_free = d->n_free;
 
   auto fail = [&](int code) {
@@ -353,6 +407,9 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   // free mask from the Dirichlet planes
   {
     std::vector<unsigned char> fm(ctx->nvec, 1);
+    if (g.Px > g.Lx)  // pitch padding is never free
+      for (long long r = 0; r < 3LL * g.Ly * g.Lz; ++r)
+        for (int X = g.Lx; X < g.Px; ++X) fm[r * g.Px + X] = 0;
     for (int c = 0; c < 3; ++c) {
       const int mk = g.dmask[c];
       if (!mk) continue;
@@ -361,7 +418,7 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
           for (int X = 0; X < g.Lx; ++X) {
             const bool cons = ((mk & 1) && X == 0) || ((mk & 2) && X == g.Lx - 1) || ((mk & 4) && Y == 0) ||
                               ((mk & 8) && Y == g.Ly - 1) || ((mk & 16) && Z == 0) || ((mk & 32) && Z == g.Lz - 1);
-            if (cons) fm[c * g.Ns + ((long long)Z * g.Ly + Y) * g.Lx + X] = 0;
+            if (cons) fm[c * g.Ns + ((long long)Z * g.Ly + Y) * g.Px + X] = 0;
           }
     }
     if (cudaMalloc(&ctx->d_free, ctx->nvec) != cudaSuccess) return fail(SDME_CUDA_ERROR);
@@ -370,8 +427,12 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   }
   if (d->perm) {
     if (d->n_free <= 0) return fail(SDME_BAD_ARGUMENT);
+    // dense host permutation (Lx per row) -> pitched device rows, -1 on the padding
+    std::vector<int> pp(ctx->nvec, -1);
+    for (long long r = 0; r < 3LL * g.Ly * g.Lz; ++r)
+      for (int X = 0; X < g.Lx; ++X) pp[r * g.Px + X] = d->perm[r * g.Lx + X];
     if (cudaMalloc(&ctx->d_perm, ctx->nvec * sizeof(int)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
-    if (cudaMemcpy(ctx->d_perm, d->perm, ctx->nvec * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
+    if (cudaMemcpy(ctx->d_perm, pp.data(), ctx->nvec * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
       return fail(SDME_CUDA_ERROR);
     if (cudaMalloc(&ctx->d_fbuf, d->n_free * sizeof(double)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
   }
@@ -383,6 +444,8 @@ int sdme_destroy(sdme_ctx* ctx) {
   if (!ctx) return SDME_OK;
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   for (double* p : ctx->vecs)
+    if (p) cudaFree(p);
+  for (void* p : ctx->vec_tmaps)
     if (p) cudaFree(p);
   cudaFree(ctx->d_perm);
   cudaFree(ctx->d_free);
@@ -408,7 +471,7 @@ int sdme_destroy(sdme_ctx* ctx) {
 
 int sdme_lattice_size(const sdme_ctx* ctx, int64_t* n) {
   if (!ctx || !n) return SDME_BAD_ARGUMENT;
-  *n = ctx->nvec;
+  *n = ctx->nlat;
   return SDME_OK;
 }
 
@@ -434,13 +497,18 @@ int sdme_vec_free(sdme_ctx* ctx, int id) {
   CK(cudaStreamSynchronize(ctx->st));
   cudaFree(p);
   ctx->vecs[id] = nullptr;
+  if (ctx->vec_tmaps[id]) cudaFree(ctx->vec_tmaps[id]);
+  ctx->vec_tmaps[id] = nullptr;
   return SDME_OK;
 }
 
 int sdme_vec_upload(sdme_ctx* ctx, int id, const double* host) {
   double* p = ctx ? vec(ctx, id) : nullptr;
   if (!p || !host) return SDME_BAD_ARGUMENT;
-  CK(cudaMemcpyAsync(p, host, ctx->nvec * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  // dense host rows (Lx doubles) -> pitched device rows (Px doubles)
+  const Geo& g = ctx->geo;
+  CK(cudaMemcpy2DAsync(p, g.Px * sizeof(double), host, g.Lx * sizeof(double), g.Lx * sizeof(double),
+                       3LL * g.Ly * g.Lz, cudaMemcpyHostToDevice, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
   return SDME_OK;
 }
@@ -448,7 +516,9 @@ int sdme_vec_upload(sdme_ctx* ctx, int id, const double* host) {
 int sdme_vec_download(sdme_ctx* ctx, int id, double* host) {
   double* p = ctx ? vec(ctx, id) : nullptr;
   if (!p || !host) return SDME_BAD_ARGUMENT;
-  CK(cudaMemcpyAsync(host, p, ctx->nvec * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+  const Geo& g = ctx->geo;
+  CK(cudaMemcpy2DAsync(host, g.Lx * sizeof(double), p, g.Px * sizeof(double), g.Lx * sizeof(double),
+                       3LL * g.Ly * g.Lz, cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
   return SDME_OK;
 }

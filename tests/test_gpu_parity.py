@@ -525,3 +525,40 @@ def test_collocated_path_vs_oracle(tag, monkeypatch):
         assert np.array_equal(yv.free(), kp)
         out[variant] = kp
     assert max_rel_err(out["0"], out["10"]) <= 1e-13
+
+
+@pytest.mark.parametrize("tag,P,div", [("SDME_M", 4, (3, 2, 2)), ("LagrangeGLL", 4, (2, 3, 1)),
+                                       ("ModalJacobi", 5, (3, 1, 2)), ("SDME_H", 6, (2, 2, 1)),
+                                       ("SDME_M", 7, (1, 2, 1)), ("SDME_K", 8, (2, 1, 1))])
+def test_tma_box_path_vs_oracle(tag, P, div, monkeypatch):
+    """Colour passes of the collocated kernels load each element box with a
+    TMA tensor copy and add the result back with a bulk tensor reduce-add
+    (tma.cuh; pitched lattice rows) for even P; odd P (box starts off a
+    16-byte boundary) keeps the cp.async / RED kernel.  Dirichlet planes on three faces (the
+    output box zeroes them), odd and even element counts (the pitch slot of
+    the last element is dropped at the lattice edge): f_int and K.p + c_m M p
+    agree with the oracle to 1e-12, with the per-lane cp.async / RED kernel
+    (SDME_VARIANT=11) to 1e-13, and reruns are bit-identical."""
+    monkeypatch.setenv("SDME_EV", "0")
+    L = tuple(0.5 * d for d in div)
+    dr = [("xmin", (0, 1, 2)), ("xmax", (0,)), ("ymax", (1, 2))]
+    opb = of.Problem(of.Mesh(div, L), ob.Basis(tag, P), OMAT, P + 1, dr)
+    rng = np.random.default_rng(29)
+    u = 1e-3 * rng.uniform(-1, 1, opb.n_free)
+    p = rng.standard_normal(opb.n_free)
+    ref_f = opb.internal_force(u)
+    ref_kp = opb.assemble(u, 1.0, 2.0e5) @ p
+    out = {}
+    for variant in ("0", "11"):
+        monkeypatch.setenv("SDME_VARIANT", variant)
+        pb = gpu_problem(tag, P, P + 1, div, L, dr)
+        f, kp = pb.internal_force(u), pb.apply_tangent(u, p, c_m=2.0e5)
+        assert max_rel_err(f, ref_f) <= TOL
+        assert max_rel_err(kp, ref_kp) <= TOL
+        assert np.array_equal(pb.apply_tangent(u, p, c_m=2.0e5).view(np.int64), kp.view(np.int64))
+        x, st = pcg_gpu(pb, u, f, c_m=2.0e5, tol=1e-10)
+        out[variant] = (f, kp, x, st.iterations)
+    for a, b in zip(out["0"][:2], out["11"][:2]):
+        assert max_rel_err(a, b) <= 1e-13
+    assert abs(out["0"][3] - out["11"][3]) <= 1
+    assert max_rel_err(out["0"][2], out["11"][2]) <= 1e-9
