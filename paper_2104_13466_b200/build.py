@@ -52,22 +52,30 @@ def _compile(args):
     return obj
 
 
-def build(force: bool = False, verbose: bool = True, jobs: int | None = None) -> str:
+def build(force: bool = False, verbose: bool = True, jobs: int | None = None, only=None, defs=()) -> str:
+    """Compile every translation unit (or, with ``only``, just those orders'
+    operator units -- a development shortcut that relinks the other existing
+    objects) and link libsdme.so.  ``defs``: extra -D flags for the operator units."""
     if not force and up_to_date():
         return LIB
     os.makedirs(OBJDIR, exist_ok=True)
     units = [(os.path.join(CSRC, "sdme_abi.cu"), os.path.join(OBJDIR, "sdme_abi.o"), [])]
-    units += [(os.path.join(CSRC, "ops.cu"), os.path.join(OBJDIR, f"ops_p{p}.o"), [f"-DSDME_ORDER={p}"])
+    units += [(os.path.join(CSRC, "ops.cu"), os.path.join(OBJDIR, f"ops_p{p}.o"), [f"-DSDME_ORDER={p}", *defs])
               for p in ORDERS]
+    objs_all = [u[1] for u in units]
+    if only is not None:
+        units = [u for u in units[1:] if int(u[1].rsplit("_p", 1)[1][:-2]) in only]
     if verbose:
         print(f"nvcc {' '.join(NVCC_FLAGS)} : {len(units)} translation units", flush=True)
     with ThreadPoolExecutor(max_workers=jobs or min(len(units), os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(_compile, units))
-    cmd = [nvcc(), *ARCH, "-shared", "-o", LIB + ".tmp", *objs]
+        list(ex.map(_compile, units))
+    cmd = [nvcc(), *ARCH, "-shared", "-o", LIB + ".tmp", *objs_all]
     subprocess.run(cmd, check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    only = [int(a.split("=", 1)[1]) for a in sys.argv if a.startswith("--only=")]
+    defs = [a for a in sys.argv if a.startswith("-D")]
+    build(force="--force" in sys.argv or bool(only) or bool(defs), only=only or None, defs=defs)

@@ -45,12 +45,20 @@ struct TabC {
 template <int N, bool VALS, bool TM = false>
 struct ColLay {
   using C = V3<N, N, 1, 1, VALS>;
-  static constexpr int SQ = C::Ly::sq;
+  static constexpr int SQ = TM ? N * N * N : C::Ly::sq;    // point slot stride (no cross-slot accesses)
   static constexpr int SX = N * N;                          // x output, k stride
   static constexpr int SY = C::Ly::sy;                      // y output, k stride
   static constexpr int SU = N * N;                          // point values, c stride
   static constexpr int PTS = (VALS ? 12 : 9) * SQ;
-  static constexpr int X = PTS, Y = X + N * SX, U = Y + N * SY, W = U + N * SU;
+  // x-stage output X(k, j, a) = k XK + j XJ + a XA: TM layout (XK, XJ, XA) =
+  // (N, 1, N^2 rounded up to 1 mod 16), bank-conflict free for both the x-stage
+  // rows (lanes (k, j)) and the y-stage columns (lanes (k, a)) -- tools/col_layout.py;
+  // else rows [k][j][a]
+  static constexpr int XK = TM ? N : SX, XJ = TM ? 1 : N;
+  static constexpr int XA = TM ? (N * N + 14) / 16 * 16 + 1 : 1;
+  static constexpr int XSPAN = TM ? (N - 1) * (XK + XJ + XA) + 1 : N * SX;
+  __device__ static int xo(int k, int j, int a) { return k * XK + j * XJ + a * XA; }
+  static constexpr int X = PTS, Y = X + XSPAN, U = Y + N * SY, W = U + N * SU;
   static constexpr int RP = TM ? N + (N & 1) : N;           // staged row pitch
   static constexpr int RB = TM ? (N * N * RP + 15) / 16 * 16 : N * N * N;  // one staging buffer (128-B multiple)
   static constexpr int R = TM ? (W + N * N * N + 15) / 16 * 16 : W + N * N * N;
@@ -138,7 +146,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
       eo_split<N, MIR>(v, E, O);
       eo_fwd<N, Mr::NE, Mr::NO>(tb.B, E, O, o);
 #pragma unroll
-      for (int a = 0; a < N; ++a) S[L::X + (w / N) * L::SX + (w % N) * N + a] = o[a];
+      for (int a = 0; a < N; ++a) S[L::X + L::xo(w / N, w % N, a)] = o[a];
     }
     group_sync<WPE>(0);
     // y stage: item (k, a) -> values at b
@@ -146,7 +154,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
       const int k = w / N, a = w % N;
       double v[N], E[NE], O[NO], o[N];
 #pragma unroll
-      for (int j = 0; j < N; ++j) v[j] = S[L::X + k * L::SX + j * N + a];
+      for (int j = 0; j < N; ++j) v[j] = S[L::X + L::xo(k, j, a)];
       eo_split<N, MIR>(v, E, O);
       eo_fwd<N, Mr::NE, Mr::NO>(tb.B, E, O, o);
 #pragma unroll
@@ -270,7 +278,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
       eo_qsplit<N>(v, qe, qo);
       eo_bwd<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.bB, qe, qo, h);
 #pragma unroll
-      for (int j = 0; j < N; ++j) S[L::X + k * L::SX + j * N + a] = h[j];
+      for (int j = 0; j < N; ++j) S[L::X + L::xo(k, j, a)] = h[j];
     }
     group_sync<WPE>(0);
     // x' items (k, j): B^T along x, scatter
@@ -283,7 +291,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
       const int k = w / N, j = w % N;
       double v[N], qe[HP], qo[H], acc[N];
 #pragma unroll
-      for (int a = 0; a < N; ++a) v[a] = S[L::X + k * L::SX + j * N + a];
+      for (int a = 0; a < N; ++a) v[a] = S[L::X + L::xo(k, j, a)];
       eo_qsplit<N>(v, qe, qo);
       eo_bwd<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.bB, qe, qo, acc);
       if (TM) {

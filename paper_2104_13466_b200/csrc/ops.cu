@@ -16,6 +16,10 @@
 #include "element_v5.cuh"
 #include "pcg_small.cuh"
 
+#ifndef SDME_COL_MINB
+#define SDME_COL_MINB 11  // resident 1-warp blocks per SM for the P = 4 collocated kernels
+#endif
+
 #ifndef SDME_V5_MINB
 #define SDME_V5_MINB 8
 #endif
@@ -428,7 +432,7 @@ void launch_col_k(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
   constexpr int WPE = LargeShape<N, N>::WPE;  // one round per stage
   constexpr int T = 32 * WPE;
   constexpr int smem = ColLay<N, VAL, TM>::PER * 8;
-  auto kern = element_col<N, WPE, (WPE == 1 ? 11 : 1), MODE, VAL, MIR, TM>;
+  auto kern = element_col<N, WPE, (WPE == 1 ? SDME_COL_MINB : 1), MODE, VAL, MIR, TM>;
   static int max_blocks = -1;
   if (max_blocks < 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -7,6 +7,7 @@ extracted from the built object (`cuobjdump -xelf all build_obj/ops_p4.o`).  Row
 are joined by instruction order within the function (nvdisasm -g line info)."""
 import collections
 import csv
+import os
 import re
 import subprocess
 import sys
@@ -29,14 +30,23 @@ def main(csv_path, cubin, fn, top=40):
         if re.match(r"\s*/\*[0-9a-f]{4,}\*/", l):
             lines.append(cur)
     n = min(len(lines), len(R))
-    samp, inst = collections.Counter(), collections.Counter()
+    iW, iX = h.index("L1 Wavefronts Shared"), h.index("L1 Wavefronts Shared Excessive")
+    samp, inst, wf, wx = (collections.Counter() for _ in range(4))
+
+    def num(x):
+        return float(x.replace(",", "")) if x not in ("", "-") else 0.0
+
     for k in range(n):
         samp[lines[k]] += int(R[k][iS])
         inst[lines[k]] += int(R[k][iI])
+        wf[lines[k]] += num(R[k][iW])
+        wx[lines[k]] += num(R[k][iX])
     tot = sum(samp.values())
-    print(f"instructions matched {n} of {len(R)} (sass {len(lines)}); samples {tot}")
-    for loc, s in samp.most_common(top):
-        print(f"{100 * s / tot:5.1f}%  inst {inst[loc]:10d}  {loc}")
+    print(f"instructions matched {n} of {len(R)} (sass {len(lines)}); samples {tot}; "
+          f"shared wavefronts {sum(wf.values()):.0f} (excessive {sum(wx.values()):.0f})")
+    key = wf if os.environ.get("BY_WAVEFRONTS") else samp
+    for loc, _ in key.most_common(top):
+        print(f"{100 * samp[loc] / tot:5.1f}%  inst {inst[loc]:10d}  smem wf {wf[loc]:10.0f} exc {wx[loc]:9.0f}  {loc}")
 
 
 if __name__ == "__main__":
