@@ -1,3 +1,6 @@
+# Round evidence on one B200: GPU tests, smoke, bench (ours + reference arm),
+# the bench's ncu launch list, per-launch DRAM traffic of K.p / mass / f_int,
+# and one ncu --set full capture of the K.p kernel.  Outputs in gpurun_out/.
 set -x
 mkdir -p gpurun_out
 cd $GRAFT_REPO_ROOT
@@ -7,4 +10,5 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_launch.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 24 --csv --log-file gpurun_out/traffic.csv python tools/prof_variant.py > gpurun_out/ncu_traffic.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:element_col -c 1 -o gpurun_out/kp -f python tools/prof_apply.py > gpurun_out/ncu_full.log 2>&1
