@@ -12,8 +12,12 @@
 
 struct sdme_ctx;
 
-// meshes with at most this many elements use E-vector mode (sdme_ctx::ev_mode)
-constexpr long long kEvMaxElements = 4096;  // tools/ev_crossover.py
+// meshes with at most this many element points (elements x (P+1)^3) use
+// E-vector mode (sdme_ctx::ev_mode): 4096 elements at P = 4; measured with the
+// TMA colour passes, tools/ev_crossover.py: P = 4 16^3 EV 79 vs 103 us, 24^3
+// 237 vs 188 us; P = 6 64x8x8 (4096 elements) EV 197 vs 187 us
+constexpr long long kEvMaxPoints = 4096LL * 125;
+constexpr long long kEvMaxElements = kEvMaxPoints / 8;  // bound for the 32-bit index math (P = 1)
 
 // Operator entry points of one (P, m) instantiation.
 struct SdmeOps {

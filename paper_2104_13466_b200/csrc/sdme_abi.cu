@@ -395,7 +395,7 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   // (each pass would hold < 1 element per SM slot); SDME_EV=0/1 forces it.
   {
     const long long ne = (long long)g.nx * g.ny * g.nz;
-    ctx->ev_mode = ne <= kEvMaxElements;
+    ctx->ev_mode = ne * n * n * n <= kEvMaxPoints;
     if (const char* v = getenv("SDME_EV")) ctx->ev_mode = atoi(v) != 0;
     if (ctx->ev_mode &&
         cudaMalloc(&ctx->d_ev, (size_t)ne * 3 * n * n * n * sizeof(double)) != cudaSuccess)
