@@ -24,7 +24,7 @@ from sdmefem.dynamics import SolverConfig, newmark_run
 from sdmefem.femcore import (FemProblem, build_face_tables, element_internal_force,
                              element_mass, element_tangent)
 from sdmefem.material import NeoHookean
-from sdmefem.meshdof import build_dofmap, gen_box_mesh
+from sdmefem.meshdof import Mesh, build_dofmap, gen_box_mesh
 from sdmefem.quadrature import gauss_rule
 from sdmefem.solver import pcg
 from sdmefem.tensorelem import TensorElement
@@ -270,6 +270,127 @@ def gen_impact_energy():
                         vy=np.array(vy))
     print("impact_energy drift", float(np.abs(total - total[0]).max() / total[0]), "vy", vy,
           "pen", max(h[1] for h in cont.history))
+
+
+# ---------------------------------------------------------------------------
+# general hexahedral meshes: twisted / renumbered / perturbed
+
+_BITS = ((0, 0, 0), (1, 0, 0), (1, 1, 0), (0, 1, 0), (0, 0, 1), (1, 0, 1), (1, 1, 1), (0, 1, 1))
+
+
+def _rotations():
+    """The 24 orientation-preserving maps of the unit cube's corner bits,
+    as (perm, flips): local bit d -> physical axis perm[d], reversed if flips[d]."""
+    import itertools
+    out = []
+    for perm in itertools.permutations(range(3)):
+        for flips in itertools.product((0, 1), repeat=3):
+            m = np.zeros((3, 3))
+            for d in range(3):
+                m[perm[d], d] = -1.0 if flips[d] else 1.0
+            if np.linalg.det(m) > 0:
+                out.append((perm, flips))
+    return out
+
+
+def _relabel(conn, rot):
+    """Connectivity of the same hexahedron with its local axes rotated."""
+    perm, flips = rot
+    phys = {b: conn[i] for i, b in enumerate(_BITS)}
+    new = []
+    for b in _BITS:
+        x = [0, 0, 0]
+        for d in range(3):
+            x[perm[d]] = 1 - b[d] if flips[d] else b[d]
+        new.append(phys[tuple(x)])
+    return new
+
+
+def general_mesh(kind, seed):
+    """Seeded general meshes: 'twist' = two unit hexes, the second with rotated
+    local axes; 'box' = a 3x2x2 box with shuffled vertex ids, every element's
+    local axes rotated at random and interior vertices displaced."""
+    rng = np.random.default_rng(seed)
+    rots = _rotations()
+    if kind == "twist":
+        base = gen_box_mesh((2, 1, 1), (2.0, 1.0, 1.0))
+        elems = [list(base.elems[0]), _relabel(list(base.elems[1]), rots[seed % len(rots)])]
+        return Mesh(3, base.coords.copy(), np.array(elems), {})
+    base = gen_box_mesh((3, 2, 2), (1.5, 1.0, 1.0))
+    coords = base.coords.copy()
+    inner = np.all((coords > 1e-12) & (coords < np.array([1.5, 1.0, 1.0]) - 1e-12), axis=1)
+    coords[inner] += 0.08 * rng.uniform(-1, 1, (int(inner.sum()), 3))
+    # shift boundary-face vertices within their face so faces stay planar
+    for ax, hi in ((0, 1.5), (1, 1.0), (2, 1.0)):
+        on = (np.abs(coords[:, ax]) < 1e-12) | (np.abs(coords[:, ax] - hi) < 1e-12)
+        for other in range(3):
+            if other == ax:
+                continue
+            top = 1.5 if other == 0 else 1.0
+            movable = on & (coords[:, other] > 1e-12) & (coords[:, other] < top - 1e-12)
+            coords[movable, other] += 0.05 * rng.uniform(-1, 1, int(movable.sum()))
+    newid = rng.permutation(len(coords))
+    coords2 = np.empty_like(coords)
+    coords2[newid] = coords
+    elems = [_relabel([int(newid[v]) for v in conn], rots[int(rng.integers(len(rots)))]) for conn in base.elems]
+    order = rng.permutation(len(elems))
+    elems = [elems[i] for i in order]
+    boundary = {tag: [tuple(int(newid[v]) for v in quad) for quad in quads] for tag, quads in base.boundary.items()}
+    return Mesh(3, coords2, np.array(elems), boundary)
+
+
+GENERAL_CASES = [  # (mesh kind, seed, basis, P, dirichlet)
+    ("twist", 5, "ModalJacobi", 3, None),
+    ("twist", 17, "LagrangeGLL", 4, None),
+    ("twist", 22, "SDME_M", 4, None),
+    ("box", 1, "SDME_M", 4, [("xmin", (0, 1, 2)), ("zmax", (2,))]),
+    ("box", 2, "LagrangeGLL", 2, [("xmin", (0, 1, 2))]),
+    ("box", 3, "SDME_H", 3, [("ymin", (1,)), ("xmax", (0, 1, 2))]),
+    ("box", 4, "SDME_K", 6, [("xmin", (0, 1, 2))]),
+]
+
+
+def gen_meshes():
+    out = {}
+    for ci, (kind, seed, tag, P, dr) in enumerate(GENERAL_CASES):
+        mesh = general_mesh(kind, seed)
+        el = TensorElement.create(3, build_basis(P, BasisKind(tag)))
+        dm = build_dofmap(mesh, el, dr)
+        prob = FemProblem(mesh, el, dm, MAT)
+        rng = np.random.default_rng(100 + ci)
+        u = 2e-3 * rng.uniform(-1, 1, prob.n_free)
+        p = rng.standard_normal(prob.n_free)
+        c_m = 3.0e4
+        kt = prob.tangent(u)
+        mass = prob.mass()
+        eff = kt + c_m * mass
+        key = f"m{ci}"
+        out[key + "_coords"] = mesh.coords
+        out[key + "_elems"] = mesh.elems
+        tags = sorted(mesh.boundary)
+        out[key + "_btags"] = np.array(tags)
+        for t in tags:
+            out[key + "_b_" + t] = np.array(mesh.boundary[t])
+        out[key + "_meta"] = np.array([KINDS.index(tag), P])
+        out[key + "_dir"] = np.array([[["xmin", "xmax", "ymin", "ymax", "zmin", "zmax"].index(t), c]
+                                      for t, cs in (dr or []) for c in cs]).reshape(-1, 2)
+        out[key + "_gdof"] = dm.gdof
+        out[key + "_gsign"] = dm.gsign
+        out[key + "_free_map"] = dm.free_map
+        out[key + "_u"] = u
+        out[key + "_p"] = p
+        out[key + "_cm"] = np.array(c_m)
+        out[key + "_fint"] = prob.internal_force(u)
+        out[key + "_kp"] = kt @ p
+        out[key + "_mp"] = mass @ p
+        out[key + "_diag"] = eff.diagonal()
+        b = prob.internal_force(u) + 1e3 * p
+        x, st = pcg(eff, b, precond="diagonal", tol=1e-10, maxit=100000)
+        out[key + "_pcg_b"] = b
+        out[key + "_pcg_x"] = x
+        out[key + "_pcg_iters"] = np.array(st.iterations)
+        print(key, kind, tag, P, prob.n_free, "pcg", st.iterations, "signs", int((dm.gsign < 0).sum()))
+    np.savez_compressed(os.path.join(HERE, "meshes.npz"), **out)
 
 
 if __name__ == "__main__":
