@@ -61,8 +61,35 @@ typedef struct {
   int64_t n_free;        /* reference free-DOF count (required with perm)   */
 } sdme_desc;
 
+/* General hexahedral mesh descriptor: FemProblem(mesh, element,
+ * dmap, mat, rule) on any conforming hex mesh (meshdof.py:41-136) with
+ * trilinear geometry (meshdof.py:269-296, femcore.py:73-81) and the
+ * reference's oriented mode numbering (build_dofmap, meshdof.py:404-472).
+ * Vectors of such a context are plain free-DOF arrays (length n_free, the
+ * reference order); m must be P + 1 (the reference default rule).  The host
+ * builds the tables (paper_2104_13466_b200/mesh.py); kernel point / function
+ * order is [comp][z][y][x] over lattice-local 1D offsets (0 = left vertex,
+ * P = right vertex, 1..P-1 = internal functions 2..P). */
+typedef struct {
+  int P;                 /* polynomial order, 2..8                                   */
+  int m;                 /* Gauss points per direction: P + 1                        */
+  int64_t n_elems;
+  const double* B;       /* m x (P+1) values, reference function order               */
+  const double* D;       /* m x (P+1) derivatives                                    */
+  const double* w;       /* m weights                                                */
+  double mu, lambda_lame, rho0;
+  int64_t n_free;
+  const int32_t* dof;    /* n_elems x 3 x (P+1)^3: 2*free + (sign < 0), or -1        */
+  const int64_t* asm_ptr;   /* n_free + 1: CSR of element-vector slots per free DOF  */
+  const int32_t* asm_slot;  /* asm_ptr[n_free]: 2*slot + (sign < 0), element order  */
+  const double* geom;    /* n_elems x 10 x m^3: J^-1[d][c] (slot 3d + c), w det J    */
+} sdme_mesh_desc;
+
 /* lifecycle ------------------------------------------------------------- */
 int sdme_create(const sdme_desc* desc, sdme_ctx** out);
+/* general mesh context: the same vector / operator / PCG entry points work on
+ * it (sdme_contact*, sdme_strain_energy and lattice-order uploads excepted). */
+int sdme_create_mesh(const sdme_mesh_desc* desc, sdme_ctx** out);
 int sdme_destroy(sdme_ctx* ctx);
 /* 3*Lx*Ly*Lz (lattice vector length) */
 int sdme_lattice_size(const sdme_ctx* ctx, int64_t* n);

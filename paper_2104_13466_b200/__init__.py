@@ -13,6 +13,8 @@ from .problem import DeviceVector, GpuFemProblem, NeoHookean
 from .solver import GpuLinearSolver, SolverConfig, SolveStats, StatsLog, make_solver, pcg_gpu
 from .dynamics import ScaledLoad, cfl_dt, explicit_run, newmark_run
 from .contact import ContactParams, GpuPenaltyContact, RigidObstacle
+from .mesh import HexMesh, MeshError, read_mesh, write_mesh
+from .mesh_problem import GpuMeshProblem
 
 __all__ = [
     "Basis1D", "BasisKind", "build_basis", "gauss_rule", "gll_rule",
@@ -22,4 +24,5 @@ __all__ = [
     "GpuLinearSolver", "SolverConfig", "SolveStats", "StatsLog", "make_solver", "pcg_gpu",
     "ScaledLoad", "cfl_dt", "explicit_run", "newmark_run",
     "ContactParams", "GpuPenaltyContact", "RigidObstacle",
+    "HexMesh", "MeshError", "read_mesh", "write_mesh", "GpuMeshProblem",
 ]

@@ -97,6 +97,15 @@ struct sdme_ctx {
   double* d_qpd = nullptr;
   double* d_energy = nullptr;  // per-element strain energy (sdme_strain_energy)
   bool pa = true;  // SDME_PA=0 disables (the PCG then applies K(u) from scratch)
+  // general mesh (sdme_create_mesh): vectors in the reference free order,
+  // elements gathered / assembled through index tables (element_gen.cuh)
+  bool gen = false;
+  int* d_dof = nullptr;           // [elem][comp][Q] 2*free + neg, or -1
+  long long* d_aptr = nullptr;    // assembly CSR over free DOFs
+  int* d_aslot = nullptr;
+  double* d_geom = nullptr;       // [elem][10][Q] J^-1, w det J
+  double* d_evu = nullptr;        // gathered element boxes of u and p
+  double* d_evp = nullptr;
 };
 
 // TMA tensor map (device address) of a context vector, nullptr if none
@@ -111,3 +120,12 @@ const SdmeOps* sdme_ops_p5(int m);
 const SdmeOps* sdme_ops_p6(int m);
 const SdmeOps* sdme_ops_p7(int m);
 const SdmeOps* sdme_ops_p8(int m);
+// general-mesh operator tables (ops.cu; m = P + 1, P >= 2)
+const SdmeOps* sdme_ops_gen_p1(int m);
+const SdmeOps* sdme_ops_gen_p2(int m);
+const SdmeOps* sdme_ops_gen_p3(int m);
+const SdmeOps* sdme_ops_gen_p4(int m);
+const SdmeOps* sdme_ops_gen_p5(int m);
+const SdmeOps* sdme_ops_gen_p6(int m);
+const SdmeOps* sdme_ops_gen_p7(int m);
+const SdmeOps* sdme_ops_gen_p8(int m);

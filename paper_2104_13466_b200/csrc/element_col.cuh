@@ -333,7 +333,30 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
 // stored quadrature data (MODE_PA), and that data (MODE_SETUP, from the same
 // collocated grad u, so MODE_PA is bit-identical to MODE_APPLY); one warp per
 // element, persistent.
-template <int N, int WPE, int MINB, int MODE, bool VAL, int MIR, bool TM = false>
+// general meshes (GEN): 1D tables without 2/h or det J (reference-coordinate
+// gradients), per-point J^-1 and w det J from args.geo, element boxes read
+// from / written to E-vector buffers (element_gen.cuh gathers and assembles)
+template <int N>
+__device__ __forceinline__ void gen_jinv(const double* __restrict__ geo, long long eid, int q, double J[3][3]) {
+  constexpr int Q = N * N * N;
+  const double* gp = geo + eid * (10 * Q) + q;
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) J[d][c] = __ldg(gp + (d * 3 + c) * Q);
+}
+
+// H[i][c] <- sum_d H[i][d] J^-1[d][c]  (reference -> material gradient)
+__device__ __forceinline__ void gen_to_phys(double* H, const double J[3][3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double h0 = H[i * 3], h1 = H[i * 3 + 1], h2 = H[i * 3 + 2];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) H[i * 3 + c] = fma(h0, J[0][c], fma(h1, J[1][c], h2 * J[2][c]));
+  }
+}
+
+template <int N, int WPE, int MINB, int MODE, bool VAL, int MIR, bool TM = false, bool GEN = false>
 __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_constant__ TabC<N, MIR> tb,
                                                         const __grid_constant__ Geo g, OpArgs args) {
   constexpr bool VALS = VAL;
@@ -369,7 +392,9 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
     mbar_fence_init();
   }
   group_sync<WPE>(0);
-  if ((long long)blockIdx.x < cnt) {
+  if (GEN && (long long)blockIdx.x < cnt) {
+    col_stage<N, 32 * WPE>(g, first_field + (long long)blockIdx.x * 3 * Q, 0, 0, 0, 0, S + L::R, t, tab);
+  } else if ((long long)blockIdx.x < cnt) {
     int ei, ej, ek;
     colour_element(g, args.colour, blockIdx.x, ei, ej, ek);
     if (TM) {
@@ -383,23 +408,33 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
     }
   }
   for (long long idx = blockIdx.x; idx < cnt; idx += stride) {
-    int ei, ej, ek;
-    colour_element(g, args.colour, idx, ei, ej, ek);
-    const int X0 = (N - 1) * ei, Y0 = (N - 1) * ej, Z0 = (N - 1) * ek;
-    const long long eid = ((long long)ek * g.ny + ej) * g.nx + ei;
+    int X0 = 0, Y0 = 0, Z0 = 0;
+    long long eid = idx, eoff = 0;  // GEN: E-vector box offset of this element
+    if (GEN) {
+      eoff = idx * 3 * Q;
+    } else {
+      int ei, ej, ek;
+      colour_element(g, args.colour, idx, ei, ej, ek);
+      X0 = (N - 1) * ei, Y0 = (N - 1) * ej, Z0 = (N - 1) * ek;
+      eid = ((long long)ek * g.ny + ej) * g.nx + ei;
+    }
     NextRows nxt{nullptr, 0, 0, 0};
     NextBox nxb{nullptr, 0, 0, 0};
     if (idx + stride < cnt) {
-      int ni, nj, nk;
-      colour_element(g, args.colour, idx + stride, ni, nj, nk);
-      if (TM) nxb = NextBox{first_map, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
-      else nxt = NextRows{first_field, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
+      if (GEN) {
+        nxt = NextRows{first_field + (idx + stride) * 3 * Q, 0, 0, 0};
+      } else {
+        int ni, nj, nk;
+        colour_element(g, args.colour, idx + stride, ni, nj, nk);
+        if (TM) nxb = NextBox{first_map, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
+        else nxt = NextRows{first_field, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
+      }
     }
     double Hu[QPT][9];
     if (UPASS) {
-      const NextRows after_u = MODE == MODE_APPLY ? NextRows{args.p, X0, Y0, Z0} : nxt;
+      const NextRows after_u = MODE == MODE_APPLY ? NextRows{args.p + eoff, X0, Y0, Z0} : nxt;
       const NextBox after_ub = MODE == MODE_APPLY ? NextBox{pmap, X0, Y0, Z0} : nxb;
-      col_forward<N, WPE, MIR, false, VALS, TM>(tb, g, args.u, X0, Y0, Z0, S, t, &buf, after_u, true, umap,
+      col_forward<N, WPE, MIR, false, VALS, TM>(tb, g, args.u + eoff, X0, Y0, Z0, S, t, &buf, after_u, true, umap,
                                                 after_ub, &ph);
 #pragma unroll
       for (int r = 0; r < QPT; ++r) {
@@ -409,17 +444,23 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
           for (int i = 0; i < 3; ++i)
 #pragma unroll
             for (int d = 0; d < 3; ++d) Hu[r][i * 3 + d] = S[L::qi(d, i, q)];
+          if constexpr (GEN) {
+            double J[3][3];
+            gen_jinv<N>(args.geo, eid, q, J);
+            gen_to_phys(Hu[r], J);
+          }
         }
       }
       group_sync<WPE>(0);
     }
     if (PPASS)
-      col_forward<N, WPE, MIR, VAL, VALS, TM>(tb, g, args.p, X0, Y0, Z0, S, t, &buf, nxt, true, pmap, nxb, &ph);
+      col_forward<N, WPE, MIR, VAL, VALS, TM>(tb, g, args.p + eoff, X0, Y0, Z0, S, t, &buf, nxt, true, pmap, nxb,
+                                              &ph);
 #pragma unroll
     for (int r = 0; r < QPT; ++r) {
       const int q = t + r * T;
       if (q >= Q) continue;
-      const double wdet = S[L::W + q];
+      const double wdet = GEN ? __ldg(args.geo + eid * (10 * Q) + 9 * Q + q) : S[L::W + q];
       QpK s;
       if (MODE == MODE_PA) {
         const double* qd = args.qpd + eid * (kQpSlots * Q) + q;
@@ -444,7 +485,20 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
         qd[9 * Q] = s.lnJ;
         continue;
       }
-      if (MODE == MODE_FINT) {
+      if (MODE == MODE_FINT && GEN) {
+        // flux back to the reference axes: wdet * P J^-T
+        const double cK = g.lam * s.lnJ - g.mu;
+        double J[3][3];
+        gen_jinv<N>(args.geo, eid, q, J);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          double Pi[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) Pi[c] = fma(g.mu, s.F[i][c], cK * s.K[i][c]);
+#pragma unroll
+          for (int d = 0; d < 3; ++d) S[L::qi(d, i, q)] = wdet * fma(Pi[0], J[d][0], fma(Pi[1], J[d][1], Pi[2] * J[d][2]));
+        }
+      } else if (MODE == MODE_FINT) {
         const double cK = g.lam * s.lnJ - g.mu;
 #pragma unroll
         for (int i = 0; i < 3; ++i)
@@ -456,6 +510,11 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
         for (int i = 0; i < 3; ++i)
 #pragma unroll
           for (int d = 0; d < 3; ++d) Hp[i][d] = S[L::qi(d, i, q)];
+        double Jg[3][3];
+        if constexpr (GEN) {
+          gen_jinv<N>(args.geo, eid, q, Jg);
+          gen_to_phys(&Hp[0][0], Jg);
+        }
         double tr = 0.0;
 #pragma unroll
         for (int i = 0; i < 3; ++i)
@@ -469,13 +528,28 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
             M1[i][j] = fma(s.K[i][0], Hp[j][0], fma(s.K[i][1], Hp[j][1], s.K[i][2] * Hp[j][2]));
         const double cc = mu_k - lam_k * s.lnJ;
         const double lt = lam_k * tr;
+        if constexpr (GEN) {
 #pragma unroll
-        for (int i = 0; i < 3; ++i)
+          for (int i = 0; i < 3; ++i) {
+            double Pi[3];
 #pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            const double m2 = fma(M1[i][0], s.K[0][d], fma(M1[i][1], s.K[1][d], M1[i][2] * s.K[2][d]));
-            S[L::qi(d, i, q)] = wdet * fma(cc, m2, fma(lt, s.K[i][d], mu_k * Hp[i][d]));
+            for (int c = 0; c < 3; ++c) {
+              const double m2 = fma(M1[i][0], s.K[0][c], fma(M1[i][1], s.K[1][c], M1[i][2] * s.K[2][c]));
+              Pi[c] = fma(cc, m2, fma(lt, s.K[i][c], mu_k * Hp[i][c]));
+            }
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+              S[L::qi(d, i, q)] = wdet * fma(Pi[0], Jg[d][0], fma(Pi[1], Jg[d][1], Pi[2] * Jg[d][2]));
           }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              const double m2 = fma(M1[i][0], s.K[0][d], fma(M1[i][1], s.K[1][d], M1[i][2] * s.K[2][d]));
+              S[L::qi(d, i, q)] = wdet * fma(cc, m2, fma(lt, s.K[i][d], mu_k * Hp[i][d]));
+            }
+        }
         if (VAL) {
 #pragma unroll
           for (int i = 0; i < 3; ++i) S[L::qi(3, i, q)] *= cmr * wdet;

@@ -64,6 +64,9 @@ struct OpArgs {
   const void* tu = nullptr;
   const void* tp = nullptr;
   const void* ty = nullptr;
+  // general meshes (element_gen.cuh): per element and point J^-1 (9 slots) and
+  // w det J ([elem][10][Q]); u / p are then E-vector boxes [elem][comp][Q]
+  const double* geo = nullptr;
 };
 
 __device__ __forceinline__ bool constrained(const Geo& g, int comp, int X, int Y, int Z) {

@@ -11,6 +11,7 @@
 #include "element_col.cuh"
 #include "element_diag.cuh"
 #include "element_eo.cuh"
+#include "element_gen.cuh"
 #include "element_kernels.cuh"
 #include "element_v3.cuh"
 #include "element_v5.cuh"
@@ -548,6 +549,131 @@ void pcg_small_impl(sdme_ctx* c, double* x, double* r, double* p, double* ap, co
   ++c->launches;
 }
 
+// ------------------------------------------------ general meshes (F4)
+// element_gen.cuh: gather -> element_col<..., GEN> -> deterministic assembly
+
+template <int N, int MODE, bool VAL, int MIR>
+void launch_col_gen(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
+  constexpr int WPE = LargeShape<N, N>::WPE;
+  constexpr int T = 32 * WPE;
+  constexpr int smem = ColLay<N, VAL>::PER * 8;
+  auto kern = element_col<N, WPE, 1, MODE, VAL, MIR, false, true>;
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T, smem);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    max_blocks = std::max(1, nb) * sms;
+  }
+  a.colour = -1;
+  kern<<<(unsigned)std::min<long long>(colour_count(c->geo, -1), max_blocks), T, smem, c->st>>>(tb, c->geo, a);
+  ++c->launches;
+}
+
+template <int N, int MIR>
+void gen_modes(sdme_ctx* c, int mode, OpArgs a) {
+  const TabC<N, MIR> tb = make_tabc<N, MIR>(c);  // geo.s = 1, det J = 1: reference-coordinate tables
+  if (mode == MODE_FINT) launch_col_gen<N, MODE_FINT, false, MIR>(c, tb, a);
+  else if (mode == MODE_SETUP) launch_col_gen<N, MODE_SETUP, false, MIR>(c, tb, a);
+  else if (mode == MODE_APPLY && a.c_m != 0.0) launch_col_gen<N, MODE_APPLY, true, MIR>(c, tb, a);
+  else if (mode == MODE_APPLY) launch_col_gen<N, MODE_APPLY, false, MIR>(c, tb, a);
+  else if (mode == MODE_PA && a.c_m != 0.0) launch_col_gen<N, MODE_PA, true, MIR>(c, tb, a);
+  else launch_col_gen<N, MODE_PA, false, MIR>(c, tb, a);
+}
+
+inline unsigned gen_grid(long long n) { return (unsigned)std::min<long long>((n + 255) / 256, 148LL * 16); }
+
+template <int N>
+void gen_element_impl(sdme_ctx* c, int mode, const double* u, const double* p, double* y, double ck, double cm) {
+  constexpr int Q = N * N * N;
+  const long long ns = (long long)c->geo.nx * 3 * Q;
+  const int* skip = c->cur_skip;
+  OpArgs a{c->d_evu, c->d_evp, y, ck, cm, -1, c->d_flag, skip};
+  a.geo = c->d_geom;
+  a.qpd = c->d_qpd;
+  a.ev = c->d_ev;
+  if (mode == MODE_MASS) {
+    // c_m M p: the K.p kernel with c_k = 0 on a zero u (F = I)
+    mode = MODE_APPLY;
+    a.c_k = 0.0;
+    cudaMemsetAsync(c->d_evu, 0, ns * sizeof(double), c->st);
+  } else if (mode == MODE_FINT || mode == MODE_APPLY || mode == MODE_SETUP) {
+    k_gen_gather<<<gen_grid(ns), 256, 0, c->st>>>(c->d_evu, u, c->d_dof, ns, skip);
+    ++c->launches;
+  }
+  if (mode == MODE_APPLY || mode == MODE_PA) {
+    k_gen_gather<<<gen_grid(ns), 256, 0, c->st>>>(c->d_evp, p, c->d_dof, ns, skip);
+    ++c->launches;
+  }
+  if (c->mir == 0) gen_modes<N, 0>(c, mode, a);
+  else gen_modes<N, 1>(c, mode, a);
+  if (mode != MODE_SETUP) {
+    k_gen_assemble<<<gen_grid(c->nvec), 256, 0, c->st>>>(y, c->d_ev, c->d_aptr, c->d_aslot, c->nvec, skip);
+    ++c->launches;
+  }
+}
+
+// squared 1D tables without weights (w det J is per point on general meshes)
+template <int N>
+TabD<N, N> make_tabd_gen(const sdme_ctx* c) {
+  TabD<N, N> t;
+  for (int a = 0; a < N; ++a)
+    for (int l = 0; l < N; ++l) {
+      const double b = c->Bl[a * N + l], d = c->Dl[a * N + l];
+      for (int ax = 0; ax < 3; ++ax) {
+        double(&T)[3][N][N] = ax == 0 ? t.x : (ax == 1 ? t.y : t.z);
+        T[0][a][l] = b * b;
+        T[1][a][l] = b * d;
+        T[2][a][l] = d * d;
+      }
+    }
+  return t;
+}
+
+template <int N, int MIR>
+void gen_diag_launch(sdme_ctx* c, OpArgs a) {
+  constexpr int WPE = LargeShape<N, N>::WPE;
+  constexpr int smem = DiagGenLay<N, WPE, MIR>::PER * 8;
+  auto kern = element_diag_gen<N, WPE, MIR>;
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * WPE, smem);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    max_blocks = std::max(1, nb) * sms;
+  }
+  kern<<<(unsigned)std::min<long long>(colour_count(c->geo, -1), max_blocks), 32 * WPE, smem, c->st>>>(
+      make_tabc<N, MIR>(c), make_tabd_gen<N>(c), c->geo, a);
+  ++c->launches;
+}
+
+template <int N>
+void gen_diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm) {
+  constexpr int Q = N * N * N;
+  const long long ns = (long long)c->geo.nx * 3 * Q;
+  OpArgs a{c->d_evu, nullptr, d, ck, cm, -1, c->d_flag};
+  a.geo = c->d_geom;
+  a.ev = c->d_ev;
+  if (ck != 0.0) {
+    k_gen_gather<<<gen_grid(ns), 256, 0, c->st>>>(c->d_evu, u, c->d_dof, ns, nullptr);
+    ++c->launches;
+  }
+  if (c->mir == 0) gen_diag_launch<N, 0>(c, a);
+  else gen_diag_launch<N, 1>(c, a);
+  k_gen_assemble<<<gen_grid(c->nvec), 256, 0, c->st>>>(d, c->d_ev, c->d_aptr, c->d_aslot, c->nvec, nullptr);
+  ++c->launches;
+}
+
+template <int N>
+const Ops* gen_ops_for() {
+  static const Ops o{&gen_element_impl<N>, &gen_diag_impl<N>, nullptr};
+  return &o;
+}
+
 template <int N, int M>
 const Ops* ops_for() {
   static const Ops o{&element_impl<N, M>, &diag_impl<N, M>, &pcg_small_impl<N>};
@@ -561,5 +687,14 @@ const Ops* ops_for() {
 const SdmeOps* SDME_CAT(sdme_ops_p, SDME_ORDER)(int m) {
   if (m == SDME_ORDER + 1) return ops_for<SDME_ORDER + 1, SDME_ORDER + 1>();
   if (m == SDME_ORDER + 2) return ops_for<SDME_ORDER + 1, SDME_ORDER + 2>();
+  return nullptr;
+}
+
+// general meshes: m = P + 1 (collocated kernels), P >= 2
+const SdmeOps* SDME_CAT(sdme_ops_gen_p, SDME_ORDER)(int m) {
+#if SDME_ORDER >= 2
+  if (m == SDME_ORDER + 1) return gen_ops_for<SDME_ORDER + 1>();
+#endif
+  (void)m;
   return nullptr;
 }

@@ -117,7 +117,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 // rounded up to even (16-byte box rows); elements outside (Lx, Ly, Lz) are
 // zero-filled on load and dropped on reduce.  nullptr if unavailable.
 void* make_tmap(sdme_ctx* ctx, double* p) {
-  if (getenv("SDME_NO_TMA")) return nullptr;
+  if (ctx->gen || getenv("SDME_NO_TMA")) return nullptr;
   auto enc = tmap_encoder();
   if (!enc) return nullptr;
   const Geo& g = ctx->geo;
@@ -440,6 +440,93 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   return SDME_OK;
 }
 
+// general hexahedral mesh context (element_gen.cuh)
+int sdme_create_mesh(const sdme_mesh_desc* d, sdme_ctx** out) {
+  if (!d || !out) return SDME_BAD_ARGUMENT;
+  *out = nullptr;
+  if (d->P < 2 || d->P > 8 || d->m != d->P + 1 || d->n_elems < 1 || d->n_free < 1 || !d->B || !d->D || !d->w ||
+      !d->dof || !d->asm_ptr || !d->asm_slot || !d->geom)
+    return SDME_BAD_ARGUMENT;
+  const Ops* ops = nullptr;
+  switch (d->P) {
+    case 2: ops = sdme_ops_gen_p2(d->m); break;
+    case 3: ops = sdme_ops_gen_p3(d->m); break;
+    case 4: ops = sdme_ops_gen_p4(d->m); break;
+    case 5: ops = sdme_ops_gen_p5(d->m); break;
+    case 6: ops = sdme_ops_gen_p6(d->m); break;
+    case 7: ops = sdme_ops_gen_p7(d->m); break;
+    case 8: ops = sdme_ops_gen_p8(d->m); break;
+    default: break;
+  }
+  if (!ops) return SDME_BAD_ARGUMENT;
+  sdme_ctx* ctx = new sdme_ctx();
+  ctx->ops = ops;
+  ctx->gen = true;
+  if (const char* v = getenv("SDME_PCG_DIRECT")) ctx->pcg_direct = atoi(v) != 0;
+  if (const char* v = getenv("SDME_PA")) ctx->pa = atoi(v) != 0;
+  const int P = d->P, n = P + 1, m = d->m;
+  ctx->P = P;
+  ctx->m = m;
+  ctx->n = n;
+  auto func_of = [&](int l) { return l == 0 ? 0 : (l == P ? 1 : l + 1); };
+  ctx->Bl.resize(m * n);
+  ctx->Dl.resize(m * n);
+  ctx->w.assign(d->w, d->w + m);
+  for (int a = 0; a < m; ++a)
+    for (int l = 0; l < n; ++l) {
+      ctx->Bl[a * n + l] = d->B[a * n + func_of(l)];
+      ctx->Dl[a * n + l] = d->D[a * n + func_of(l)];
+    }
+  ctx->mir = detect_mirror(ctx);
+  auto fail = [&](int code) {
+    sdme_destroy(ctx);
+    return code;
+  };
+  if (ctx->mir < 0) return fail(SDME_BAD_ARGUMENT);  // every reference basis mirrors
+  Geo& g = ctx->geo;
+  // elements as a row; one element box is a dense n^3 "lattice" (the staged
+  // copies of element_col read E-vector boxes through the same code)
+  g.nx = (int)d->n_elems; g.ny = 1; g.nz = 1;
+  g.Lx = g.Ly = g.Lz = n; g.Px = n;
+  g.Ns = (long long)n * n * n;
+  g.s[0] = g.s[1] = g.s[2] = 1.0;
+  g.detJ = 1.0;
+  g.mu = d->mu; g.lam = d->lambda_lame; g.rho = d->rho0;
+  ctx->nvec = d->n_free;
+  ctx->nlat = d->n_free;
+  ctx->n_free = d->n_free;
+  const long long ns = d->n_elems * 3 * g.Ns;
+  const long long nnz = d->asm_ptr[d->n_free];
+  if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+  bool ok = cudaMalloc(&ctx->d_partial, kRedBlocks * 4 * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_scal, 16 * sizeof(double)) == cudaSuccess &&
+            cudaMallocHost(&ctx->h_scal, 16 * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_flag, 2 * sizeof(unsigned long long)) == cudaSuccess &&
+            cudaMallocHost(&ctx->h_flag, 2 * sizeof(unsigned long long)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_status, sizeof(int)) == cudaSuccess &&
+            cudaMallocHost(&ctx->h_status, sizeof(int)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_free, ctx->nvec) == cudaSuccess &&
+            cudaMalloc(&ctx->d_ev, ns * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_evu, ns * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_evp, ns * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_dof, ns * sizeof(int)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_aptr, (d->n_free + 1) * sizeof(long long)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_aslot, std::max<long long>(nnz, 1) * sizeof(int)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_geom, d->n_elems * 10 * g.Ns * sizeof(double)) == cudaSuccess;
+  if (!ok) return fail(SDME_CUDA_ERROR);
+  ctx->d_dflag = ctx->d_flag + 1;
+  ok = cudaMemset(ctx->d_free, 1, ctx->nvec) == cudaSuccess &&
+       cudaMemcpy(ctx->d_dof, d->dof, ns * sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
+       cudaMemcpy(ctx->d_aptr, d->asm_ptr, (d->n_free + 1) * sizeof(long long), cudaMemcpyHostToDevice) ==
+           cudaSuccess &&
+       cudaMemcpy(ctx->d_aslot, d->asm_slot, nnz * sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
+       cudaMemcpy(ctx->d_geom, d->geom, d->n_elems * 10 * g.Ns * sizeof(double), cudaMemcpyHostToDevice) ==
+           cudaSuccess;
+  if (!ok) return fail(SDME_CUDA_ERROR);
+  *out = ctx;
+  return SDME_OK;
+}
+
 int sdme_destroy(sdme_ctx* ctx) {
   if (!ctx) return SDME_OK;
   if (ctx->st) cudaStreamSynchronize(ctx->st);
@@ -449,6 +536,12 @@ int sdme_destroy(sdme_ctx* ctx) {
     if (p) cudaFree(p);
   cudaFree(ctx->d_perm);
   cudaFree(ctx->d_free);
+  cudaFree(ctx->d_dof);
+  cudaFree(ctx->d_aptr);
+  cudaFree(ctx->d_aslot);
+  cudaFree(ctx->d_geom);
+  cudaFree(ctx->d_evu);
+  cudaFree(ctx->d_evp);
   cudaFree(ctx->d_ev);
   cudaFree(ctx->d_qpd);
   cudaFree(ctx->d_energy);
@@ -507,8 +600,11 @@ int sdme_vec_upload(sdme_ctx* ctx, int id, const double* host) {
   if (!p || !host) return SDME_BAD_ARGUMENT;
   // dense host rows (Lx doubles) -> pitched device rows (Px doubles)
   const Geo& g = ctx->geo;
-  CK(cudaMemcpy2DAsync(p, g.Px * sizeof(double), host, g.Lx * sizeof(double), g.Lx * sizeof(double),
-                       3LL * g.Ly * g.Lz, cudaMemcpyHostToDevice, ctx->st));
+  if (ctx->gen)  // general mesh: free-DOF arrays
+    CK(cudaMemcpyAsync(p, host, ctx->nvec * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  else
+    CK(cudaMemcpy2DAsync(p, g.Px * sizeof(double), host, g.Lx * sizeof(double), g.Lx * sizeof(double),
+                         3LL * g.Ly * g.Lz, cudaMemcpyHostToDevice, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
   return SDME_OK;
 }
@@ -517,13 +613,17 @@ int sdme_vec_download(sdme_ctx* ctx, int id, double* host) {
   double* p = ctx ? vec(ctx, id) : nullptr;
   if (!p || !host) return SDME_BAD_ARGUMENT;
   const Geo& g = ctx->geo;
-  CK(cudaMemcpy2DAsync(host, g.Lx * sizeof(double), p, g.Px * sizeof(double), g.Lx * sizeof(double),
-                       3LL * g.Ly * g.Lz, cudaMemcpyDeviceToHost, ctx->st));
+  if (ctx->gen)
+    CK(cudaMemcpyAsync(host, p, ctx->nvec * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+  else
+    CK(cudaMemcpy2DAsync(host, g.Lx * sizeof(double), p, g.Px * sizeof(double), g.Lx * sizeof(double),
+                         3LL * g.Ly * g.Lz, cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
   return SDME_OK;
 }
 
 int sdme_vec_upload_free(sdme_ctx* ctx, int id, const double* host) {
+  if (ctx && ctx->gen) return sdme_vec_upload(ctx, id, host);
   double* p = ctx ? vec(ctx, id) : nullptr;
   if (!p || !host || !ctx->d_perm) return set_err(ctx, SDME_BAD_ARGUMENT, "no permutation / bad vector");
   CK(cudaMemcpyAsync(ctx->d_fbuf, host, ctx->n_free * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
@@ -534,6 +634,7 @@ int sdme_vec_upload_free(sdme_ctx* ctx, int id, const double* host) {
 }
 
 int sdme_vec_download_free(sdme_ctx* ctx, int id, double* host) {
+  if (ctx && ctx->gen) return sdme_vec_download(ctx, id, host);
   double* p = ctx ? vec(ctx, id) : nullptr;
   if (!p || !host || !ctx->d_perm) return set_err(ctx, SDME_BAD_ARGUMENT, "no permutation / bad vector");
   k_lattice_to_free<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(ctx->d_fbuf, p, ctx->d_perm, ctx->nvec);
@@ -809,7 +910,7 @@ int sdme_explicit_step(sdme_ctx* ctx, int u, int u_prev, int v, int load, double
 }
 
 int sdme_contact_points(const sdme_ctx* ctx, int side, int qf, int64_t* n) {
-  if (!ctx || side < 0 || side > 5 || qf < 1 || !n) return SDME_BAD_ARGUMENT;
+  if (!ctx || ctx->gen || side < 0 || side > 5 || qf < 1 || !n) return SDME_BAD_ARGUMENT;
   const int axis = side / 2;
   const int ne[3] = {ctx->geo.nx, ctx->geo.ny, ctx->geo.nz};
   const int d1 = axis == 0 ? 1 : 0, d2 = axis == 2 ? 1 : 2;
@@ -821,6 +922,7 @@ int sdme_contact(sdme_ctx* ctx, int u, int side, int qf, const double* Bf, const
                  const double* point, const double* normal, double eps, int fc, double* gaps_host,
                  double* stats) {
   if (!ctx) return SDME_BAD_ARGUMENT;
+  if (ctx->gen) return set_err(ctx, SDME_BAD_ARGUMENT, "contact needs a box-mesh context");
   double* pu = vec(ctx, u);
   double* pf = vec(ctx, fc);
   if (!pu || !pf || side < 0 || side > 5 || qf < 1 || qf > kMaxQF || ctx->n > kMaxN || !Bf || !xf || !wf ||
@@ -898,6 +1000,7 @@ int sdme_contact(sdme_ctx* ctx, int u, int side, int qf, const double* Bf, const
 int sdme_strain_energy(sdme_ctx* ctx, int u, double* out) {
   double* pu = ctx ? vec(ctx, u) : nullptr;
   if (!pu || !out) return SDME_BAD_ARGUMENT;
+  if (ctx->gen) return set_err(ctx, SDME_BAD_ARGUMENT, "strain energy needs a box-mesh context");
   const long long ne = (long long)ctx->geo.nx * ctx->geo.ny * ctx->geo.nz;
   if (!ctx->d_energy) {
     // per-element energies, then the m rule weights (read by the kernel through p)

@@ -35,9 +35,20 @@ class Desc(C.Structure):
                 ("dirichlet_mask", C.c_int * 3), ("perm", _i32p), ("n_free", C.c_int64)]
 
 
+_i64p = C.POINTER(C.c_int64)
+
+
+class MeshDesc(C.Structure):
+    """``sdme_mesh_desc`` (include/sdme.h): general hexahedral mesh context."""
+    _fields_ = [("P", C.c_int), ("m", C.c_int), ("n_elems", C.c_int64), ("B", _dp), ("D", _dp), ("w", _dp),
+                ("mu", C.c_double), ("lambda_lame", C.c_double), ("rho0", C.c_double), ("n_free", C.c_int64),
+                ("dof", _i32p), ("asm_ptr", _i64p), ("asm_slot", _i32p), ("geom", _dp)]
+
+
 # name -> argtypes (restype c_int for all)
 SIGNATURES = {
     "sdme_create": [C.POINTER(Desc), C.POINTER(C.c_void_p)],
+    "sdme_create_mesh": [C.POINTER(MeshDesc), C.POINTER(C.c_void_p)],
     "sdme_destroy": [C.c_void_p],
     "sdme_lattice_size": [C.c_void_p, C.POINTER(C.c_int64)],
     "sdme_last_error": [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int), C.c_char_p, C.c_size_t],
