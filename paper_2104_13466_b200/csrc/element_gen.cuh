@@ -33,10 +33,12 @@ static __global__ void __launch_bounds__(256) k_gen_gather(double* __restrict__ 
   }
 }
 
-// y[f] += sum_k sign_k ev[slot_k] over the CSR entries of f (increasing element)
+// y[f] += sum_k sign_k ev[slot_k] over the CSR entries of f (increasing element);
+// unsigned for a diagonal (sign_k^2 = 1)
 static __global__ void __launch_bounds__(256) k_gen_assemble(double* __restrict__ y, const double* __restrict__ ev,
                                                       const long long* __restrict__ ptr,
-                                                      const int* __restrict__ slot, long long n, const int* skip) {
+                                                      const int* __restrict__ slot, long long n, const int* skip,
+                                                      bool diagonal = false) {
   if (skip && *(volatile const int*)skip) return;
   for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < n;
        f += (long long)gridDim.x * blockDim.x) {
@@ -44,7 +46,7 @@ static __global__ void __launch_bounds__(256) k_gen_assemble(double* __restrict_
     for (long long k = __ldg(ptr + f), e = __ldg(ptr + f + 1); k < e; ++k) {
       const int sl = __ldg(slot + k);
       const double v = __ldg(ev + (sl >> 1));
-      s += (sl & 1) ? -v : v;
+      s += ((sl & 1) && !diagonal) ? -v : v;
     }
     y[f] += s;
   }

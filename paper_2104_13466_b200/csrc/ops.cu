@@ -664,7 +664,8 @@ void gen_diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm
   }
   if (c->mir == 0) gen_diag_launch<N, 0>(c, a);
   else gen_diag_launch<N, 1>(c, a);
-  k_gen_assemble<<<gen_grid(c->nvec), 256, 0, c->st>>>(d, c->d_ev, c->d_aptr, c->d_aslot, c->nvec, nullptr);
+  k_gen_assemble<<<gen_grid(c->nvec), 256, 0, c->st>>>(d, c->d_ev, c->d_aptr, c->d_aslot, c->nvec, nullptr,
+                                                       true);
   ++c->launches;
 }
 
