@@ -393,6 +393,25 @@ def gen_meshes():
     np.savez_compressed(os.path.join(HERE, "meshes.npz"), **out)
 
 
+def gen_mesh_newmark():
+    """Implicit Newmark (dynamics.py:173-257) on a general (renumbered,
+    rotated, perturbed) mesh with a traction on xmax."""
+    mesh = general_mesh("box", 3)
+    el = TensorElement.create(3, build_basis(3, BasisKind("SDME_H")))
+    dm = build_dofmap(mesh, el, [("xmin", (0, 1, 2))])
+    prob = FemProblem(mesh, el, dm, MAT)
+    faces = build_face_tables(prob.mesh, prob.element, "xmax", prob.rule)
+    base = prob.traction_vector(faces, lambda f: np.tile([0.0, 2.0e5, 1.0e5], (len(f.pts), 1)))
+    dt = 1e-4
+    load = lambda t: base * min(t / (5 * dt), 1.0)
+    cfg = SolverConfig(precond="diagonal", tol=1e-10, maxit=200000, condense=False)
+    traj = newmark_run(prob, load, dt, 5, newton_tol=1e-8, cfg=cfg)
+    rows = [(r["step"], r["newton_iter"], r["iterations"]) for r in traj.stats.rows]
+    np.savez_compressed(os.path.join(HERE, "mesh_newmark.npz"), u=traj.state.u, v=traj.state.v, a=traj.state.a,
+                        load=base, newton_iters=np.array(traj.newton_iters), pcg_rows=np.array(rows))
+    print("mesh_newmark", traj.newton_iters, [r[2] for r in rows])
+
+
 if __name__ == "__main__":
     import sys
 

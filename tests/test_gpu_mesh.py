@@ -77,3 +77,29 @@ def test_inversion_reports_element():
     with pytest.raises(ElementInversionError) as ei:
         pb.internal_force(u)
     assert 0 <= ei.value.elem_id < pb.mesh.n_elems
+
+
+def test_newmark_on_general_mesh_vs_reference():
+    """newmark_run (dynamics.py:173-257) on a renumbered, rotated, perturbed
+    mesh with a traction on xmax: the load vector (femcore.py:215-259,
+    391-397), Newton counts, PCG counts +-1 and the final state."""
+    from paper_2104_13466_b200 import BasisKind, ScaledLoad, SolverConfig, build_basis, newmark_run
+    from conftest import load_golden
+    from test_mesh import mesh_from
+    gm = load_golden("meshes")
+    g = load_golden("mesh_newmark")
+    # the same mesh as golden case m5 ('box', seed 3)
+    mesh = mesh_from(gm, "m5")
+    pb = GpuMeshProblem(mesh, build_basis(3, BasisKind("SDME_H")), MAT, dirichlet=[("xmin", (0, 1, 2))])
+    base = pb.traction_vector("xmax", [0.0, 2.0e5, 1.0e5])
+    assert max_rel_err(base, g["load"]) <= TOL
+    dt = 1e-4
+    load = ScaledLoad(base, lambda t: min(t / (5 * dt), 1.0))
+    cfg = SolverConfig(precond="diagonal", tol=1e-10, maxit=200000, condense=False)
+    traj = newmark_run(pb, load, dt, 5, newton_tol=1e-8, cfg=cfg)
+    assert list(traj.newton_iters) == list(g["newton_iters"])
+    its = [r["iterations"] for r in traj.stats.rows]
+    assert len(its) == len(g["pcg_rows"])
+    assert all(abs(a - b) <= 1 for a, b in zip(its, g["pcg_rows"][:, 2]))
+    assert max_rel_err(traj.state.u, g["u"]) <= 1e-9
+    assert max_rel_err(traj.state.v, g["v"]) <= 1e-8
