@@ -12,7 +12,8 @@ namespace sdme {
 template <int N, int M, int WPE, int NC, bool GRAD, bool VAL, bool STAGED = false, int MIR>
 __device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo& g, const double* __restrict__ src,
                                            int X0, int Y0, int Z0, double* A, double* B, int t, int gid,
-                                           double* R = nullptr, int* buf = nullptr, NextRows next = {}) {
+                                           double* R = nullptr, int* buf = nullptr, NextRows next = {},
+                                           BoxIO bx = {}) {
   static_assert(!STAGED || NC == 1, "row staging is per component");
   using C = V3<N, M, WPE, NC>;
   using Mr = Mir<N, MIR>;
@@ -42,6 +43,10 @@ __device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo
       double v[N];
       if (STAGED) {
         const double* row = R + *buf * N * N * N + (k * N + j) * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] = row[i];
+      } else if (bx.in) {
+        const double* row = bx.in + comp * BoxW<N>::CB + (k * N + j) * BoxW<N>::BW + bx.shift;
 #pragma unroll
         for (int i = 0; i < N; ++i) v[i] = row[i];
       } else {
@@ -135,10 +140,11 @@ __device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo
 template <int N, int M, int WPE, int NC, bool GRAD, bool VAL, int MIR>
 __device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Geo& g, double* __restrict__ dst,
                                             int X0, int Y0, int Z0, double* A, double* B, int t, int gid,
-                                            double* evb = nullptr) {
+                                            double* evb = nullptr, BoxIO bx = {}) {
   using C = V3<N, M, WPE, NC>;
   using Mr = Mir<N, MIR>;
   constexpr int HP = Half<M>::HP, H = Half<M>::H > 0 ? Half<M>::H : 1;
+  constexpr int BW = BoxW<N>::BW;
 #pragma unroll 1
   for (int c0 = 0; c0 < 3; c0 += NC) {
     double* const X = (NC == 3) ? A : B + C::YO;
@@ -214,6 +220,11 @@ __device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Ge
     }
     group_sync<WPE>(gid);
     // x' stage: item (comp, k, j), contract over a, RED into the lattice
+    // (or into the output box of the TMA reduce-add)
+    if (bx.out) {
+      if (t == 0) bulk_wait_read();  // the previous element's reduce-adds have read the box
+      group_sync<WPE>(gid);
+    }
     for (int w = t; w < NC * N * N; w += C::T) {
       int ck, j;
       C::item_x(w, ck, j);
@@ -241,10 +252,34 @@ __device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Ge
       }
       const int Z = Z0 + k, Y = Y0 + j;
       const bool chk = touches_dirichlet(g, comp, X0, Y0, Z0, N);
+      if (bx.out) {
+        // output box row: the element's N values at `shift`, zeros elsewhere
+        // (slots outside the element belong to elements of other colours)
+        double* orow = bx.out + comp * BoxW<N>::CB + (k * N + j) * BW;
+#pragma unroll
+        for (int i = 0; i < N; ++i) orow[bx.shift + i] = (chk && constrained(g, comp, X0 + i, Y, Z)) ? 0.0 : acc[i];
+        if (BW - N == 1) {
+          orow[N] = 0.0;
+        } else {
+          orow[N + 1] = 0.0;
+          orow[bx.shift ? 0 : N] = 0.0;
+        }
+        continue;
+      }
       double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Px + X0;
 #pragma unroll
       for (int i = 0; i < N; ++i)
         if (!chk || !constrained(g, comp, X0 + i, Y, Z)) red_add(row + i, acc[i]);
+    }
+    if (bx.out) {
+      fence_proxy_async_smem();
+      group_sync<WPE>(gid);
+      if (t == 0) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          tma_reduce_add_box(static_cast<const CUtensorMap*>(bx.ymap), bx.out + c * BoxW<N>::CB, bx.xs, bx.Y0,
+                             bx.Z0, c);
+      }
     }
     group_sync<WPE>(gid);
   }

@@ -22,6 +22,7 @@
 //     tools/bank_model.py (half-warp 64-bit bank model, matches ncu counts).
 // Next element's input rows are prefetched into L2 while the current one runs.
 #pragma once
+#include "tma.cuh"
 #include "element_kernels.cuh"
 
 namespace sdme {
@@ -140,6 +141,23 @@ struct NextRows {
   int X0, Y0, Z0;
 };
 
+// TMA element boxes of the NC = 3 kernels (element_v3 TMB): the x stage reads
+// rows from a shared box [comp][k][j][BW] (rows start at `shift`, the box's x
+// start is the even lattice x at or below X0), the x' stage writes the output
+// box that one lane then adds back with bulk tensor reduce-adds (tma.cuh).
+template <int N>
+struct BoxW {
+  static constexpr int BW = (N + 2) & ~1;  // even box width covering [X0, X0 + N) from an even start
+  static constexpr int CB = (N * N * BW + 15) / 16 * 16;  // one component's box (TMA: 128-B aligned)
+};
+struct BoxIO {
+  const double* in = nullptr;   // forward: shared input box
+  double* out = nullptr;        // backward: shared output box
+  int shift = 0;                // X0 - (box x start)
+  const void* ymap = nullptr;   // backward: tensor map of the output vector
+  int xs = 0, Y0 = 0, Z0 = 0;   // box start
+};
+
 template <int N, int T>
 __device__ __forceinline__ void v3_prefetch(const Geo& g, const double* __restrict__ src, int X0, int Y0, int Z0,
                                             int t) {
@@ -159,7 +177,8 @@ __device__ __forceinline__ void v3_prefetch(const Geo& g, const double* __restri
 template <int N, int M, int WPE, int NC, bool GRAD, bool VAL, bool STAGED = false>
 __device__ __forceinline__ void v3_forward(const Tab3<N, M>& tb, const Geo& g, const double* __restrict__ src,
                                            int X0, int Y0, int Z0, double* A, double* B, int t, int gid,
-                                           double* R = nullptr, int* buf = nullptr, NextRows next = {}) {
+                                           double* R = nullptr, int* buf = nullptr, NextRows next = {},
+                                           BoxIO = {}) {
   using C = V3<N, M, WPE, NC>;
   static_assert(!STAGED || NC == 1, "row staging is per component");
   constexpr int NX = NC * N * N, NY = NC * N * M, NZ = NC * M * M;
@@ -291,7 +310,7 @@ __device__ __forceinline__ void v3_forward(const Tab3<N, M>& tb, const Geo& g, c
 template <int N, int M, int WPE, int NC, bool GRAD, bool VAL>
 __device__ __forceinline__ void v3_backward(const Tab3<N, M>& tb, const Geo& g, double* __restrict__ dst,
                                             int X0, int Y0, int Z0, double* A, double* B, int t, int gid,
-                                            double* evb = nullptr) {
+                                            double* evb = nullptr, BoxIO = {}) {
   using C = V3<N, M, WPE, NC>;
   constexpr int NX = NC * N * N, NY = NC * N * M, NZ = NC * M * M;
 #pragma unroll 1
@@ -434,13 +453,29 @@ __device__ __forceinline__ void qp_k(const double (&H)[9], QpK& s) {
 // STG: cp.async double-buffered row staging (NC == 1); needs 2*N^3 extra
 // doubles of shared memory per element (see V3 launch in sdme_abi.cu).
 // TB: Tab3 (plain contractions) or TabEO (even-odd, element_eo.cuh).
+// TMB: TMA element boxes (NC == 3, WPE == 1, even-odd tables): per element two
+// staging boxes of all three components (u / p / next element, mbarrier
+// completion) and an output box added back with bulk tensor reduce-adds.
+template <int N, int M, int WPE, int NC, bool VALS, bool STG, bool TMB>
+struct V3Smem {
+  using C = V3<N, M, WPE, NC, VALS>;
+  static constexpr int BW = BoxW<N>::BW;
+  static constexpr int BOX = 3 * BoxW<N>::CB;  // one box: three 128-B aligned component boxes
+  static constexpr int BOXO = (C::PER + 15) / 16 * 16;
+  static constexpr int PERS =
+      TMB ? (BOXO + 3 * BOX + 2 + 15) / 16 * 16 : C::PER + (STG ? 2 * N * N * N : 0);
+};
+
 template <int N, int M, int WPE, int NC, int EPB, int MINB, int MODE, bool VAL, bool STG = false,
-          class TB = Tab3<N, M>>
+          class TB = Tab3<N, M>, bool TMB = false>
 __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_constant__ TB tb,
                                                                      const __grid_constant__ Geo g, OpArgs args) {
   using C = V3<N, M, WPE, NC, VAL || MODE == MODE_MASS>;
-  constexpr int PERS = C::PER + (STG ? 2 * N * N * N : 0);
-  extern __shared__ double smem[];
+  using SM = V3Smem<N, M, WPE, NC, VAL || MODE == MODE_MASS, STG, TMB>;
+  static_assert(!TMB || (NC == 3 && WPE == 1 && !STG), "TMA boxes: all-component shape");
+  constexpr int PERS = SM::PERS;
+  constexpr int BW = SM::BW;
+  extern __shared__ __align__(128) double smem[];
   const int gid = threadIdx.x / C::T;
   const int t = threadIdx.x % C::T;
   double* A = smem + gid * PERS;
@@ -457,6 +492,31 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
   const double mu_k = args.c_k * g.mu, lam_k = args.c_k * g.lam;
   const double cmr = args.c_m * g.rho;
   const double* first_field = UPASS ? args.u : args.p;
+  // TMB: boxes [buf 0][buf 1][out], then two mbarriers (one per staging box)
+  double* Rbox = A + SM::BOXO;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(Rbox + 3 * SM::BOX);
+  const CUtensorMap* umap = static_cast<const CUtensorMap*>(args.tu);
+  const CUtensorMap* pmap = static_cast<const CUtensorMap*>(args.tp);
+  unsigned ph = 0;
+  auto issue = [&](const CUtensorMap* map, int X0, int Y0, int Z0, int b) {
+    // one lane: the three component boxes of an element into staging box b
+    mbar_expect_tx(bars + b, 3 * N * N * BW * 8);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) tma_load_box(Rbox + b * SM::BOX + c * BoxW<N>::CB, map, X0 & ~1, Y0, Z0, c, bars + b);
+  };
+  if (TMB) {
+    if (t == 0) {
+      mbar_init(bars, 1);
+      mbar_init(bars + 1, 1);
+      mbar_fence_init();
+    }
+    group_sync<WPE>(gid);
+    if (t == 0 && (long long)blockIdx.x * EPB + gid < cnt) {
+      int ei, ej, ek;
+      colour_element(g, args.colour, (long long)blockIdx.x * EPB + gid, ei, ej, ek);
+      issue(UPASS ? umap : pmap, (N - 1) * ei, (N - 1) * ej, (N - 1) * ek, 0);
+    }
+  }
   if (STG && (long long)blockIdx.x * EPB + gid < cnt) {
     int ei, ej, ek;
     colour_element(g, args.colour, (long long)blockIdx.x * EPB + gid, ei, ej, ek);
@@ -472,16 +532,37 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
       colour_element(g, args.colour, idx + stride, ni, nj, nk);
       nxt = NextRows{first_field, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
     }
-    if (!STG && idx + stride < cnt) {  // warm L2 with the next element's rows
+    int nX0 = -1, nY0 = 0, nZ0 = 0;  // TMB: next element of this warp
+    if (TMB && idx + stride < cnt) {
+      int ni, nj, nk;
+      colour_element(g, args.colour, idx + stride, ni, nj, nk);
+      nX0 = (N - 1) * ni, nY0 = (N - 1) * nj, nZ0 = (N - 1) * nk;
+    }
+    if (!STG && !TMB && idx + stride < cnt) {  // warm L2 with the next element's rows
       int ni, nj, nk;
       colour_element(g, args.colour, idx + stride, ni, nj, nk);
       if (UPASS) v3_prefetch<N, C::T>(g, args.u, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk, t);
       if (PPASS) v3_prefetch<N, C::T>(g, args.p, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk, t);
     }
+    BoxIO bx{};
+    bx.shift = X0 & 1;
+    auto box_next = [&](bool to_p) {
+      // TMB: issue the next box into the other buffer, wait for the current one
+      if (!TMB) return;
+      if (t == 0) {
+        if (to_p) issue(pmap, X0, Y0, Z0, buf ^ 1);
+        else if (nX0 >= 0) issue(UPASS ? umap : pmap, nX0, nY0, nZ0, buf ^ 1);
+      }
+      mbar_wait(bars + buf, (ph >> buf) & 1u);
+      ph ^= 1u << buf;
+      bx.in = Rbox + buf * SM::BOX;
+    };
     double Hu[C::QPT][9];
     if (UPASS) {
       const NextRows after_u = MODE == MODE_APPLY ? NextRows{args.p, X0, Y0, Z0} : nxt;
-      v3_forward<N, M, WPE, NC, true, false, STG>(tb, g, args.u, X0, Y0, Z0, A, Bf, t, gid, Rb, &buf, after_u);
+      box_next(MODE == MODE_APPLY);
+      v3_forward<N, M, WPE, NC, true, false, STG>(tb, g, args.u, X0, Y0, Z0, A, Bf, t, gid, Rb, &buf, after_u, bx);
+      if (TMB) buf ^= 1;
 #pragma unroll
       for (int r = 0; r < C::QPT; ++r) {
         const int q = t + r * C::T;
@@ -494,8 +575,11 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
       }
       group_sync<WPE>(gid);
     }
-    if (PPASS)
-      v3_forward<N, M, WPE, NC, GRADP, VAL, STG>(tb, g, args.p, X0, Y0, Z0, A, Bf, t, gid, Rb, &buf, nxt);
+    if (PPASS) {
+      box_next(false);
+      v3_forward<N, M, WPE, NC, GRADP, VAL, STG>(tb, g, args.p, X0, Y0, Z0, A, Bf, t, gid, Rb, &buf, nxt, bx);
+      if (TMB) buf ^= 1;
+    }
 #pragma unroll
     for (int r = 0; r < C::QPT; ++r) {
       const int q = t + r * C::T;
@@ -594,13 +678,19 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
       continue;
     }
     double* evb = args.ev ? args.ev + (((long long)ek * g.ny + ej) * g.nx + ei) * 3 * (N * N * N) : nullptr;
+    if (TMB) {
+      bx.out = Rbox + 2 * SM::BOX;
+      bx.ymap = args.ty;
+      bx.xs = X0 & ~1, bx.Y0 = Y0, bx.Z0 = Z0;
+    }
     if (MODE == MODE_MASS)
-      v3_backward<N, M, WPE, NC, false, true>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb);
+      v3_backward<N, M, WPE, NC, false, true>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb, bx);
     else if (MODE == MODE_FINT)
-      v3_backward<N, M, WPE, NC, true, false>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb);
+      v3_backward<N, M, WPE, NC, true, false>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb, bx);
     else
-      v3_backward<N, M, WPE, NC, true, VAL>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb);
+      v3_backward<N, M, WPE, NC, true, VAL>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb, bx);
   }
+  if (TMB && t == 0) bulk_wait_all();
 }
 
 }  // namespace sdme

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "ctx.cuh"
@@ -87,11 +88,12 @@ void ev_gather(sdme_ctx* c, const OpArgs& a) {
   ++c->launches;
 }
 
-template <int N, int M, class S, int MODE, bool VAL, class TB = Tab3<N, M>>
-void launch_v3(sdme_ctx* c, const TB& tb, OpArgs a) {
+template <int N, int M, class S, int MODE, bool VAL, class TB, bool TMB>
+void launch_v3_k(sdme_ctx* c, const TB& tb, OpArgs a) {
   constexpr bool VALS = VAL || MODE == MODE_MASS;
-  constexpr int smem = (V3<N, M, S::WPE, S::NC, VALS>::PER + (S::STG ? 2 * N * N * N : 0)) * 8 * S::EPB;
-  auto kern = element_v3<N, M, S::WPE, S::NC, S::EPB, S::MINB, MODE, VAL, S::STG, TB>;
+  constexpr int smem = V3Smem<N, M, S::WPE, S::NC, VALS, S::STG, TMB>::PERS * 8 * S::EPB;
+  constexpr int MINB = TMB && S::MINB > 6 ? 6 : S::MINB;  // TMA boxes: 168-register cap (see DESIGN)
+  auto kern = element_v3<N, M, S::WPE, S::NC, S::EPB, MINB, MODE, VAL, S::STG, TB, TMB>;
   static int max_blocks = -1;
   if (max_blocks < 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -127,6 +129,25 @@ void launch_v3(sdme_ctx* c, const TB& tb, OpArgs a) {
     kern<<<grid, S::EPB * S::WPE * 32, smem, c->st>>>(tb, c->geo, a);
     ++c->launches;
   }
+}
+
+// TMA element boxes for the all-component shape (small P) with even-odd
+// tables on colour passes, when every vector of the mode has a tensor map;
+// SDME_VARIANT=11 keeps the per-lane loads and RED (A/B only)
+template <int N, int M, class S, int MODE, bool VAL, class TB = Tab3<N, M>>
+void launch_v3(sdme_ctx* c, const TB& tb, OpArgs a) {
+  constexpr bool tmb_ok = S::NC == 3 && S::WPE == 1 && !S::STG && !std::is_same<TB, Tab3<N, M>>::value &&
+                          MODE != MODE_ENERGY;
+  if constexpr (tmb_ok) {
+    const bool maps = MODE == MODE_SETUP ? a.tu != nullptr
+                                         : (a.ty && (MODE == MODE_PA || MODE == MODE_MASS || a.tu) &&
+                                            (MODE == MODE_FINT || a.tp));
+    if (maps && !c->ev_mode && c->variant != 11) {
+      launch_v3_k<N, M, S, MODE, VAL, TB, true>(c, tb, a);
+      return;
+    }
+  }
+  launch_v3_k<N, M, S, MODE, VAL, TB, false>(c, tb, a);
 }
 
 template <int N, int M, class S, class TB = Tab3<N, M>>

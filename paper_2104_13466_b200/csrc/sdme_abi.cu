@@ -113,15 +113,17 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 }
 
 // Tensor map of one lattice vector for the element box TMA (tma.cuh): 4D
-// (x, y, z, component) FP64, pitched rows (Px), box (RP, n, n, 1) with RP = n
-// rounded up to even (16-byte box rows); elements outside (Lx, Ly, Lz) are
-// zero-filled on load and dropped on reduce.  nullptr if unavailable.
+// (x, y, z, component) FP64, pitched rows (Px), box (BW, n, n, 1) with BW the
+// even width that covers n points from the even x at or below the element's
+// start (n + 1 for odd n, n + 2 for even n; 16-byte box rows); elements outside
+// (Lx, Ly, Lz) are zero-filled on load and dropped on reduce.  nullptr if
+// unavailable.
 void* make_tmap(sdme_ctx* ctx, double* p) {
   if (ctx->gen || getenv("SDME_NO_TMA")) return nullptr;
   auto enc = tmap_encoder();
   if (!enc) return nullptr;
   const Geo& g = ctx->geo;
-  const int n = ctx->n, rp = n + (n & 1);
+  const int n = ctx->n, rp = (n + 2) & ~1;  // BoxW<n>: even width covering n points from an even start
   CUtensorMap m;
   cuuint64_t dims[4] = {(cuuint64_t)g.Lx, (cuuint64_t)g.Ly, (cuuint64_t)g.Lz, 3};
   cuuint64_t strides[3] = {(cuuint64_t)g.Px * 8, (cuuint64_t)g.Px * g.Ly * 8, (cuuint64_t)g.Ns * 8};

@@ -527,14 +527,17 @@ def test_collocated_path_vs_oracle(tag, monkeypatch):
     assert max_rel_err(out["0"], out["10"]) <= 1e-13
 
 
-@pytest.mark.parametrize("tag,P,div", [("SDME_M", 4, (3, 2, 2)), ("LagrangeGLL", 4, (2, 3, 1)),
+@pytest.mark.parametrize("tag,P,div", [("LagrangeGLL", 1, (3, 2, 2)), ("ModalJacobi", 2, (3, 2, 2)),
+                                       ("SDME_H", 3, (3, 2, 1)), ("SDME_K", 3, (2, 3, 2)),
+                                       ("SDME_M", 4, (3, 2, 2)), ("LagrangeGLL", 4, (2, 3, 1)),
                                        ("ModalJacobi", 5, (3, 1, 2)), ("SDME_H", 6, (2, 2, 1)),
                                        ("SDME_M", 7, (1, 2, 1)), ("SDME_K", 8, (2, 1, 1))])
 def test_tma_box_path_vs_oracle(tag, P, div, monkeypatch):
-    """Colour passes of the collocated kernels load each element box with a
-    TMA tensor copy and add the result back with a bulk tensor reduce-add
-    (tma.cuh; pitched lattice rows) for even P; odd P (box starts off a
-    16-byte boundary) keeps the cp.async / RED kernel.  Dirichlet planes on three faces (the
+    """Colour passes load each element box with a TMA tensor copy and add the
+    result back with a bulk tensor reduce-add (tma.cuh; pitched lattice rows):
+    the collocated kernels at even P >= 4, the all-component kernel at P <= 3
+    (boxes from the even x at or below the element start, so odd P shifts the
+    rows by one); odd P >= 5 keeps the cp.async / RED kernel.  Dirichlet planes on three faces (the
     output box zeroes them), odd and even element counts (the pitch slot of
     the last element is dropped at the lattice edge): f_int and K.p + c_m M p
     agree with the oracle to 1e-12, with the per-lane cp.async / RED kernel

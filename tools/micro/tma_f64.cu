@@ -9,14 +9,18 @@
 #include <cstdlib>
 #include <vector>
 
-constexpr int Lx = 9, Px = 10, Ly = 9, Lz = 9, BX = 6, BY = 5, BZ = 5;
+#ifndef BXV
+#define BXV 6
+#define BYV 5
+#endif
+constexpr int Lx = 9, Px = 10, Ly = 9, Lz = 9, BX = BXV, BY = BYV, BZ = BYV;
 constexpr long long Ns = (long long)Px * Ly * Lz;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 __global__ void k_tensor(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, int x0,
                          int y0, int z0) {
-  __shared__ alignas(128) double box[3 * BZ * BY * BX];
+  __shared__ alignas(128) double box[(3 * BZ * BY * BX + 15) / 16 * 16];
   __shared__ alignas(8) unsigned long long bar;
   const int t = threadIdx.x;
   if (t == 0) {
@@ -26,7 +30,7 @@ __global__ void k_tensor(const __grid_constant__ CUtensorMap tin, const __grid_c
   __syncthreads();
   if (t == 0) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)),
-                 "r"((int)sizeof(box)));
+                 "r"((int)(3 * BZ * BY * BX * 8)));
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
         "[%6];" ::"r"(smem_u32(box)),

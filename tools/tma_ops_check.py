@@ -1,5 +1,4 @@
-"""Run f_int / K.p on a small mesh through the colour-pass (TMA) path for one
-order P (argv[1]); prints ok or the native error.  Debug aid."""
+"""Debug aid: each operator separately through the colour-pass path for one P."""
 import os
 import sys
 
@@ -11,13 +10,14 @@ from paper_2104_13466_b200 import BoxMesh, GpuFemProblem, NeoHookean, build_basi
 from paper_2104_13466_b200.basis import BasisKind, gauss_rule  # noqa: E402
 
 P = int(sys.argv[1])
-div = tuple(int(x) for x in sys.argv[2].split(",")) if len(sys.argv) > 2 else (3, 2, 2)
+op = sys.argv[2]
+div = tuple(int(x) for x in sys.argv[3].split(",")) if len(sys.argv) > 3 else (3, 2, 2)
 pb = GpuFemProblem(BoxMesh(div, (1.0, 1.0, 1.0)), build_basis(P, BasisKind("SDME_M" if P > 1 else "LagrangeGLL")),
                    NeoHookean.from_engineering(1e7, 0.3, 1e3), gauss_rule(P + 1), [("xmin", (0, 1, 2))])
 u = 1e-3 * np.random.default_rng(0).uniform(-1, 1, pb.n_free)
 try:
-    f = pb.internal_force(u)
-    y = pb.apply_tangent(u, u, 1.0)
-    print("P", P, "ok", float(np.abs(f).max()), float(np.abs(y).max()))
+    f = {"fint": lambda: pb.internal_force(u), "apply": lambda: pb.apply_tangent(u, u, 0.0),
+         "mass": lambda: pb.mass_apply(u), "applym": lambda: pb.apply_tangent(u, u, 1.0)}[op]()
+    print("P", P, op, div, os.environ.get("SDME_VARIANT"), "ok", float(np.abs(f).max()))
 except Exception as e:  # noqa: BLE001
-    print("P", P, "error", e)
+    print("P", P, op, div, os.environ.get("SDME_VARIANT"), "error", e)
