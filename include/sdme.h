@@ -122,6 +122,13 @@ int sdme_fint(sdme_ctx* ctx, int u, int r);
 /* y = c_k K_T(u) p + c_m M p -- element_tangent(...)@p + mass (femcore.py:130-156,
  * consumer solver.py:149 `a @ p`, Newmark eff = kt + b1 m, dynamics.py:236-237) */
 int sdme_apply(sdme_ctx* ctx, int u, int p, int y, double c_k, double c_m);
+/* n operator applications with host buffers (free order; page-locked for full
+ * overlap): y[k] = (c_k K(u[k]) + c_m M) p[k].  Pipelined: the H2D copies of
+ * pair k+1 and the D2H copy of result k-1 run on two copy streams while pair k
+ * is permuted and applied (box contexts with a permutation).  Replaces a loop
+ * of element_tangent(...) @ p_e assemblies (femcore.py:130-146) over a batch. */
+int sdme_apply_batch(sdme_ctx* ctx, int n, const double* const* u, const double* const* p, double* const* y,
+                     double c_k, double c_m);
 /* y = M a -- mass_full @ a_trial (dynamics.py:198) */
 int sdme_mass(sdme_ctx* ctx, int a, int y);
 /* total strain energy sum_e sum_q w det J psi(F) (femcore.py:374-378, material.py:80);

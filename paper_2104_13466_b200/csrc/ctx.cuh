@@ -99,6 +99,17 @@ struct sdme_ctx {
   bool pa = true;  // SDME_PA=0 disables (the PCG then applies K(u) from scratch)
   // general mesh (sdme_create_mesh): vectors in the reference free order,
   // elements gathered / assembled through index tables (element_gen.cuh)
+  // pipelined batch K.p with host buffers (sdme_apply_batch): copy streams,
+  // double-buffered free-order staging, events
+  struct Batch {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    double* su[2] = {nullptr, nullptr};
+    double* sp[2] = {nullptr, nullptr};
+    double* sy[2] = {nullptr, nullptr};
+    cudaEvent_t ev_h2d[2] = {}, ev_in_free[2] = {}, ev_comp[2] = {}, ev_out_free[2] = {};
+    int u = -1, p = -1, y = -1;  // lattice vectors
+  };
+  Batch* batch = nullptr;
   bool gen = false;
   int* d_dof = nullptr;           // [elem][comp][Q] 2*free + neg, or -1
   long long* d_aptr = nullptr;    // assembly CSR over free DOFs

@@ -442,6 +442,8 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   return SDME_OK;
 }
 
+void batch_free(sdme_ctx* ctx);  // sdme_apply_batch state (below)
+
 // general hexahedral mesh context (element_gen.cuh)
 int sdme_create_mesh(const sdme_mesh_desc* d, sdme_ctx** out) {
   if (!d || !out) return SDME_BAD_ARGUMENT;
@@ -532,6 +534,7 @@ int sdme_create_mesh(const sdme_mesh_desc* d, sdme_ctx** out) {
 int sdme_destroy(sdme_ctx* ctx) {
   if (!ctx) return SDME_OK;
   if (ctx->st) cudaStreamSynchronize(ctx->st);
+  batch_free(ctx);
   for (double* p : ctx->vecs)
     if (p) cudaFree(p);
   for (void* p : ctx->vec_tmaps)
@@ -1084,6 +1087,93 @@ int sdme_time_op(sdme_ctx* ctx, int op, int u, int p, int y, double c_m, int rep
   cudaEventDestroy(e1);
   *ms = (double)t / reps;
   return check_launch(ctx);
+}
+
+// Pipelined batch K.p with host buffers (the e2e path of many operator
+// applications): pair k's H2D copies (copy stream 1) and result k-1's D2H copy
+// (copy stream 2) overlap the permutations and operator of pair k on the
+// context stream.  Free-order staging is double-buffered; events order reuse.
+int batch_setup(sdme_ctx* ctx) {
+  if (ctx->batch) return SDME_OK;
+  auto* b = new sdme_ctx::Batch();
+  ctx->batch = b;
+  CK(cudaStreamCreateWithFlags(&b->h2d, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&b->d2h, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaMalloc(&b->su[i], ctx->n_free * sizeof(double)));
+    CK(cudaMalloc(&b->sp[i], ctx->n_free * sizeof(double)));
+    CK(cudaMalloc(&b->sy[i], ctx->n_free * sizeof(double)));
+    CK(cudaEventCreateWithFlags(&b->ev_h2d[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&b->ev_in_free[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&b->ev_comp[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&b->ev_out_free[i], cudaEventDisableTiming));
+  }
+  int rc = alloc_vec(ctx, &b->u);
+  if (!rc) rc = alloc_vec(ctx, &b->p);
+  if (!rc) rc = alloc_vec(ctx, &b->y);
+  return rc;
+}
+
+void batch_free(sdme_ctx* ctx) {
+  auto* b = ctx->batch;
+  if (!b) return;
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(b->su[i]);
+    cudaFree(b->sp[i]);
+    cudaFree(b->sy[i]);
+    for (cudaEvent_t e : {b->ev_h2d[i], b->ev_in_free[i], b->ev_comp[i], b->ev_out_free[i]})
+      if (e) cudaEventDestroy(e);
+  }
+  if (b->h2d) cudaStreamDestroy(b->h2d);
+  if (b->d2h) cudaStreamDestroy(b->d2h);
+  delete b;
+  ctx->batch = nullptr;
+}
+
+int sdme_apply_batch(sdme_ctx* ctx, int n, const double* const* u, const double* const* p, double* const* y,
+                     double c_k, double c_m) {
+  if (!ctx || n < 0 || (!u && c_k != 0.0) || !p || !y) return SDME_BAD_ARGUMENT;
+  if (!ctx->d_perm) return set_err(ctx, SDME_BAD_ARGUMENT, "batch apply needs a box context with a permutation");
+  int rc = batch_setup(ctx);
+  if (rc) return rc;
+  if ((rc = reset_flag(ctx))) return rc;
+  auto* b = ctx->batch;
+  double* U = vec(ctx, b->u);
+  double* Pv = vec(ctx, b->p);
+  double* Y = vec(ctx, b->y);
+  const size_t bytes = ctx->n_free * sizeof(double);
+  for (int k = 0; k < n; ++k) {
+    const int s = k & 1;
+    // H2D of pair k into staging s (free once the permutations of pair k-2 ran)
+    if (k >= 2) CK(cudaStreamWaitEvent(b->h2d, b->ev_in_free[s], 0));
+    if (c_k != 0.0) CK(cudaMemcpyAsync(b->su[s], u[k], bytes, cudaMemcpyHostToDevice, b->h2d));
+    CK(cudaMemcpyAsync(b->sp[s], p[k], bytes, cudaMemcpyHostToDevice, b->h2d));
+    CK(cudaEventRecord(b->ev_h2d[s], b->h2d));
+    // operator on the context stream
+    CK(cudaStreamWaitEvent(ctx->st, b->ev_h2d[s], 0));
+    if (c_k != 0.0) k_free_to_lattice<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(U, b->su[s], ctx->d_perm, ctx->nvec);
+    k_free_to_lattice<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(Pv, b->sp[s], ctx->d_perm, ctx->nvec);
+    ctx->launches += c_k != 0.0 ? 2 : 1;
+    CK(cudaEventRecord(b->ev_in_free[s], ctx->st));
+    CK(cudaMemsetAsync(Y, 0, ctx->nvec * sizeof(double), ctx->st));
+    if (c_k != 0.0)
+      ctx->ops->element(ctx, MODE_APPLY, U, Pv, Y, c_k, c_m);
+    else
+      ctx->ops->element(ctx, MODE_MASS, nullptr, Pv, Y, 0.0, c_m);
+    if (k >= 2) CK(cudaStreamWaitEvent(ctx->st, b->ev_out_free[s], 0));
+    k_lattice_to_free<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(b->sy[s], Y, ctx->d_perm, ctx->nvec);
+    ++ctx->launches;
+    CK(cudaEventRecord(b->ev_comp[s], ctx->st));
+    // D2H of result k
+    CK(cudaStreamWaitEvent(b->d2h, b->ev_comp[s], 0));
+    CK(cudaMemcpyAsync(y[k], b->sy[s], bytes, cudaMemcpyDeviceToHost, b->d2h));
+    CK(cudaEventRecord(b->ev_out_free[s], b->d2h));
+  }
+  CK(cudaStreamSynchronize(b->d2h));
+  CK(cudaStreamSynchronize(ctx->st));
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  return c_k != 0.0 ? check_flag(ctx) : SDME_OK;
 }
 
 int sdme_host_alloc(size_t bytes, void** ptr) {

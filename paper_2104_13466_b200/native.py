@@ -66,6 +66,8 @@ SIGNATURES = {
     "sdme_vec_reciprocal": [C.c_void_p, C.c_int, C.c_int],
     "sdme_fint": [C.c_void_p, C.c_int, C.c_int],
     "sdme_apply": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double],
+    "sdme_apply_batch": [C.c_void_p, C.c_int, C.POINTER(_dp), C.POINTER(_dp), C.POINTER(_dp), C.c_double,
+                         C.c_double],
     "sdme_mass": [C.c_void_p, C.c_int, C.c_int],
     "sdme_diag": [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int],
     "sdme_pcg": [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, C.c_double, C.c_int,

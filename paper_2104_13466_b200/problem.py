@@ -259,6 +259,27 @@ class GpuFemProblem:
         p = self._scratch("p").set_free(p_free)
         return self.apply_(u, p, self._scratch("y"), 1.0, c_m).free(out)
 
+    def apply_tangent_batch(self, us, ps, c_m: float = 0.0, outs=None) -> list:
+        """[(K_T(u_k) + c_m M) p_k for k]: ``apply_tangent`` over a batch of host
+        pairs, pipelined over PCIe (the H2D copies of pair k+1 and the D2H copy of
+        result k-1 overlap pair k's operator; ``sdme_apply_batch``).  Inputs and
+        ``outs`` should be page-locked (:func:`native.pinned_empty`) for full overlap."""
+        n = len(ps)
+        if len(us) != n:
+            raise ValueError("us and ps must have the same length")
+        if outs is None:
+            outs = [np.empty(self.n_free) for _ in range(n)]
+        arrs = []
+        for a in list(us) + list(ps) + list(outs):
+            if a.shape != (self.n_free,) or a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ValueError(f"batch vectors must be contiguous float64 free vectors of length {self.n_free}")
+            arrs.append(a)
+        U = (native._dp * n)(*[native.dptr(a) for a in us])
+        Pp = (native._dp * n)(*[native.dptr(a) for a in ps])
+        Y = (native._dp * n)(*[native.dptr(a) for a in outs])
+        native.check(self._ctx, native.lib().sdme_apply_batch(self._ctx, n, U, Pp, Y, 1.0, c_m), "apply_batch")
+        return list(outs)
+
     def tangent_diagonal(self, u_free: np.ndarray, c_m: float = 0.0) -> np.ndarray:
         """diag(K_T(u) + c_m M) over free dofs (solver.py:106 on the assembled operator)."""
         u = self._scratch("u").set_free(u_free)

@@ -565,3 +565,23 @@ def test_tma_box_path_vs_oracle(tag, P, div, monkeypatch):
         assert max_rel_err(a, b) <= 1e-13
     assert abs(out["0"][3] - out["11"][3]) <= 1
     assert max_rel_err(out["0"][2], out["11"][2]) <= 1e-9
+
+
+@pytest.mark.parametrize("ev", ["0", "1"])
+def test_apply_batch_matches_single_calls(ev, monkeypatch):
+    """apply_tangent_batch (pipelined H2D / operator / D2H, sdme_apply_batch)
+    returns exactly the results of one apply_tangent call per pair."""
+    monkeypatch.setenv("SDME_EV", ev)
+    from paper_2104_13466_b200.native import pinned_empty
+    pb = gpu_problem("SDME_M", 4, 5, (3, 2, 2), (1.5, 1.0, 1.0), [("xmin", (0, 1, 2))])
+    rng = np.random.default_rng(5)
+    us, ps = [], []
+    for _ in range(5):
+        u, p = pinned_empty(pb.n_free), pinned_empty(pb.n_free)
+        u[:] = 1e-3 * rng.uniform(-1, 1, pb.n_free)
+        p[:] = rng.standard_normal(pb.n_free)
+        us.append(u)
+        ps.append(p)
+    got = pb.apply_tangent_batch(us, ps, c_m=3.0e4)
+    for u, p, y in zip(us, ps, got):
+        assert np.array_equal(y.view(np.int64), pb.apply_tangent(u, p, 3.0e4).view(np.int64))
