@@ -59,7 +59,7 @@ struct ColLay {
   static constexpr int XSPAN = TM ? (N - 1) * (XK + XJ + XA) + 1 : N * SX;
   __device__ static int xo(int k, int j, int a) { return k * XK + j * XJ + a * XA; }
   static constexpr int X = PTS, Y = X + XSPAN, U = Y + N * SY, W = U + N * SU;
-  static constexpr int RP = TM ? N + (N & 1) : N;           // staged row pitch
+  static constexpr int RP = TM ? BoxW<N>::BW : N;           // staged row pitch (TMA box width)
   static constexpr int RB = TM ? (N * N * RP + 15) / 16 * 16 : N * N * N;  // one staging buffer (128-B multiple)
   static constexpr int R = TM ? (W + N * N * N + 15) / 16 * 16 : W + N * N * N;
   static constexpr int O = R + 2 * RB;                      // TM: output box of the reduce-add
@@ -105,10 +105,10 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
       if (t == 0) {
         if (comp + 1 < 3) {
           mbar_expect_tx(bars + nbi, N * N * L::RP * 8);
-          tma_load_box(R + nbi * L::RB, smap, X0, Y0, Z0, comp + 1, bars + nbi);
+          tma_load_box(R + nbi * L::RB, smap, X0 & ~1, Y0, Z0, comp + 1, bars + nbi);
         } else if (nbox.map) {
           mbar_expect_tx(bars + nbi, N * N * L::RP * 8);
-          tma_load_box(R + nbi * L::RB, nbox.map, nbox.X0, nbox.Y0, nbox.Z0, 0, bars + nbi);
+          tma_load_box(R + nbi * L::RB, nbox.map, nbox.X0 & ~1, nbox.Y0, nbox.Z0, 0, bars + nbi);
         }
       }
       mbar_wait(bars + *buf, (*ph >> *buf) & 1u);
@@ -129,8 +129,9 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
     // x stage: item (k, j) -> values at a
     for (int w = t; w < N * N; w += 32 * WPE) {
       double v[N], E[NE], O[NO], o[N];
-      if (TM) {
-        // 16-byte loads of the pitched box row (conflict-free for RP = 6)
+      if (TM && (N & 1)) {
+        // even P: boxes start at the element; 16-byte loads of the pitched
+        // box row (conflict-free for RP = 6)
         const double2* row = reinterpret_cast<const double2*>(R + *buf * L::RB + w * L::RP);
 #pragma unroll
         for (int i = 0; i < L::RP / 2; ++i) {
@@ -138,6 +139,11 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
           v[2 * i] = d.x;
           if (2 * i + 1 < N) v[2 * i + 1] = d.y;
         }
+      } else if (TM) {
+        // odd P: the box starts at the even x at or below the element (shift X0 & 1)
+        const double* row = R + *buf * L::RB + w * L::RP + (X0 & 1);
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] = row[i];
       } else {
         const double* row = R + *buf * N * N * N + w * N;
 #pragma unroll
@@ -304,10 +310,20 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
           for (int i = 0; i < N; ++i)
             if (constrained(g, comp, X0 + i, Y, Z)) acc[i] = 0.0;
         }
-        double2* orow = reinterpret_cast<double2*>(S + L::O + w * L::RP);
+        if constexpr (N & 1) {
+          double2* orow = reinterpret_cast<double2*>(S + L::O + w * L::RP);
 #pragma unroll
-        for (int i = 0; i < L::RP / 2; ++i)
-          orow[i] = make_double2(acc[2 * i], 2 * i + 1 < N ? acc[2 * i + 1] : 0.0);
+          for (int i = 0; i < L::RP / 2; ++i)
+            orow[i] = make_double2(acc[2 * i], 2 * i + 1 < N ? acc[2 * i + 1] : 0.0);
+        } else {
+          // odd P: values at the shift, zeros in the two slots outside the element
+          double* orow = S + L::O + w * L::RP;
+          const int sh = X0 & 1;
+#pragma unroll
+          for (int i = 0; i < N; ++i) orow[sh + i] = acc[i];
+          orow[N + 1] = 0.0;
+          orow[sh ? 0 : N] = 0.0;
+        }
         continue;
       }
       if (evb) {
@@ -325,7 +341,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
     }
     if (TM) fence_proxy_async_smem();
     group_sync<WPE>(0);
-    if (TM && t == 0) tma_reduce_add_box(ymap, S + L::O, X0, Y0, Z0, comp);
+    if (TM && t == 0) tma_reduce_add_box(ymap, S + L::O, X0 & ~1, Y0, Z0, comp);
   }
 }
 
@@ -401,7 +417,7 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
       if (t == 0) {
         unsigned long long* bars = reinterpret_cast<unsigned long long*>(S + L::BAR);
         mbar_expect_tx(bars, N * N * L::RP * 8);
-        tma_load_box(S + L::R, first_map, (N - 1) * ei, (N - 1) * ej, (N - 1) * ek, 0, bars);
+        tma_load_box(S + L::R, first_map, ((N - 1) * ei) & ~1, (N - 1) * ej, (N - 1) * ek, 0, bars);
       }
     } else {
       col_stage<N, 32 * WPE>(g, first_field, 0, (N - 1) * ei, (N - 1) * ej, (N - 1) * ek, S + L::R, t, tab);

@@ -483,13 +483,15 @@ void launch_col_k(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
 }
 
 // TMA box loads / bulk reduce-add (tma.cuh) when every vector of the mode has
-// a tensor map and the colour passes scatter (not E-vector mode), for even P
-// only: element boxes start at x = P i, and an FP64 box whose start is not
-// 16-byte aligned faults (tools/micro/tma_f64.cu).  SDME_VARIANT=11 keeps the
-// cp.async / RED kernel (A/B only).
+// a tensor map and the colour passes scatter (not E-vector mode).  An FP64 box
+// must start 16-byte aligned (tools/micro/tma_f64.cu), so boxes start at the
+// even x at or below the element (odd P: rows shifted by one, box n + 2 wide).
+// SDME_VARIANT=11 keeps the cp.async / RED kernel (A/B only).
+// P = 5 (box pitch 8 doubles: 8-way bank conflicts on the row reads; measured
+// 2.93 vs 2.72 ms) keeps the cp.async kernel; P = 7 (pitch 10) 2.39 vs 2.84 ms.
 template <int N, int MODE, bool VAL, int MIR>
 void launch_col(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
-  if constexpr (N % 2 == 1) {
+  if constexpr ((N & 1) || BoxW<N>::BW % 4 == 2) {
     const bool maps = MODE == MODE_SETUP ? a.tu != nullptr
                                          : (a.ty && (MODE == MODE_PA || a.tu) && (MODE == MODE_FINT || a.tp));
     if (maps && !c->ev_mode && c->variant != 11) {
