@@ -22,6 +22,10 @@
 #define SDME_COL_MINB 11  // resident 1-warp blocks per SM for the P = 4 collocated kernels
 #endif
 
+#ifndef SDME_GEN_MINB
+#define SDME_GEN_MINB 1  // resident blocks per SM asked of the general-mesh P = 4 kernels
+#endif
+
 #ifndef SDME_V5_MINB
 #define SDME_V5_MINB 8
 #endif
@@ -580,7 +584,7 @@ void launch_col_gen(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
   constexpr int WPE = LargeShape<N, N>::WPE;
   constexpr int T = 32 * WPE;
   constexpr int smem = ColLay<N, VAL>::PER * 8;
-  auto kern = element_col<N, WPE, 1, MODE, VAL, MIR, false, true>;
+  auto kern = element_col<N, WPE, (WPE == 1 ? SDME_GEN_MINB : 1), MODE, VAL, MIR, false, true>;
   static int max_blocks = -1;
   if (max_blocks < 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
