@@ -153,11 +153,13 @@ def _sd(m, k, kexp):
     return (xs @ z @ np.diag(ls ** (-0.5 * kexp))).T, ls
 
 
-def _sd_parity(m, k, kexp):
-    """basis1d.py:263-287 (symmetric weights: even/odd blocks)."""
+def _sd_parity(m, k, kexp, with_parity=False):
+    """basis1d.py:263-287 (symmetric weights: even/odd blocks; internal slot i
+    holds mode p = i + 2 of parity (-1)^i, so a block's rows share its parity)."""
     n = m.shape[0]
     if n <= 1:
-        return _sd(m, k, kexp)[0]
+        y = _sd(m, k, kexp)[0]
+        return (y, np.ones(n)) if with_parity else y
     rows = []
     for par in (0, 1):
         idx = list(range(par, n, 2))
@@ -165,9 +167,10 @@ def _sd_parity(m, k, kexp):
         for j in range(len(idx)):
             r = np.zeros(n)
             r[idx] = yb[j]
-            rows.append((lb[j], r))
+            rows.append((lb[j], r, (-1.0) ** par))
     rows.sort(key=lambda t: t[0])
-    return np.array([r for _, r in rows])
+    y = np.array([r for _, r, _ in rows])
+    return (y, np.array([s for _, _, s in rows])) if with_parity else y
 
 
 class Basis:
@@ -177,6 +180,11 @@ class Basis:
         assert tag in TAGS
         self.tag, self.P, self.alpha, self.beta = tag, P, alpha, beta
         self.nodes = None
+        # reflection parity of the internal functions (basis1d.py:85-89, 326-328):
+        # None for the nodal basis (orientation by index reversal) and for
+        # non-symmetric Jacobi weights
+        self.internal_parity = (np.array([(-1.0) ** p for p in range(2, P + 1)])
+                                if tag != "LagrangeGLL" and alpha == beta and P >= 2 else None)
         t = np.eye(P + 1)
         if tag == "LagrangeGLL":  # basis1d.py:317-323
             self.nodes = gll(P + 1)[0]
@@ -185,8 +193,10 @@ class Basis:
             v, d = modal(P, alpha, beta, xq)
             mm = (v * wq) @ v.T
             kk = (d * wq) @ d.T
-            y = (_sd_parity(mm[2:, 2:], kk[2:, 2:], k) if alpha == beta
-                 else _sd(mm[2:, 2:], kk[2:, 2:], k)[0])
+            if alpha == beta:
+                y, self.internal_parity = _sd_parity(mm[2:, 2:], kk[2:, 2:], k, with_parity=True)
+            else:
+                y = _sd(mm[2:, 2:], kk[2:, 2:], k)[0]
             g = {"SDME_M": mm, "SDME_K": kk, "SDME_H": kk + lam * mm}[tag]
             avi = g[:2, 2:] @ y.T
             aii = y @ g[2:, 2:] @ y.T

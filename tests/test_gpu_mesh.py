@@ -103,3 +103,45 @@ def test_newmark_on_general_mesh_vs_reference():
     assert all(abs(a - b) <= 1 for a, b in zip(its, g["pcg_rows"][:, 2]))
     assert max_rel_err(traj.state.u, g["u"]) <= 1e-9
     assert max_rel_err(traj.state.v, g["v"]) <= 1e-8
+
+
+@pytest.mark.parametrize("rot,tag,P", [(1, "SDME_M", 3), (8, "ModalJacobi", 4), (13, "SDME_H", 2),
+                                       (19, "LagrangeGLL", 3), (23, "SDME_K", 4)])
+def test_twisted_meshes_vs_oracle(rot, tag, P):
+    """Other local-axis rotations of the twisted two-hex mesh than the golden
+    cases, against the oracle's general-mesh restatement (pinned to the
+    reference in tests/test_mesh.py): f_int, K.p + c_m M p, the diagonal."""
+    from oracle import basis as ob
+    from oracle import fem as of
+    from oracle.mesh import GeneralMesh, GeneralProblem
+    from paper_2104_13466_b200 import BasisKind, HexMesh, build_basis
+    import itertools
+    rots = []
+    for perm in itertools.permutations(range(3)):
+        for flips in itertools.product((0, 1), repeat=3):
+            m = np.zeros((3, 3))
+            for d in range(3):
+                m[perm[d], d] = -1.0 if flips[d] else 1.0
+            if np.linalg.det(m) > 0:
+                rots.append((perm, flips))
+    bits = ((0, 0, 0), (1, 0, 0), (1, 1, 0), (0, 1, 0), (0, 0, 1), (1, 0, 1), (1, 1, 1), (0, 1, 1))
+    box = HexMesh.box((2, 1, 1), (2.0, 1.0, 1.0))
+    perm, flips = rots[rot]
+    phys = {b: box.elems[1][i] for i, b in enumerate(bits)}
+    e1 = []
+    for b in bits:
+        x = [0, 0, 0]
+        for d in range(3):
+            x[perm[d]] = 1 - b[d] if flips[d] else b[d]
+        e1.append(phys[tuple(x)])
+    coords = box.coords.copy()
+    coords[:, 1] += 0.1 * coords[:, 0] * coords[:, 2]  # non-affine geometry
+    elems = np.array([box.elems[0], e1])
+    pb = GpuMeshProblem(HexMesh(coords, elems), build_basis(P, BasisKind(tag)), MAT)
+    opb = GeneralProblem(GeneralMesh(coords, elems), ob.Basis(tag, P), of.Material(1.0e7, 0.3, 1.0e3), P + 1)
+    rng = np.random.default_rng(rot)
+    u = 2e-3 * rng.uniform(-1, 1, pb.n_free)
+    p = rng.standard_normal(pb.n_free)
+    assert max_rel_err(pb.internal_force(u), opb.internal_force(u)) <= TOL
+    assert max_rel_err(pb.apply_tangent(u, p, 3e4), opb.apply_tangent(u, p, 3e4)) <= TOL
+    assert max_rel_err(pb.tangent_diagonal(u, 3e4), opb.assemble(u, 1.0, 3e4).diagonal()) <= TOL

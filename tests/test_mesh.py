@@ -109,3 +109,35 @@ def test_mesh_errors():
     two = HexMesh.box((2, 1, 1), (2.0, 1.0, 1.0))
     with pytest.raises(MeshError):
         HexMesh(two.coords, two.elems, {"mid": [(1, 4, 10, 7)]})  # interior face
+
+
+# --- the oracle's general-mesh restatement (oracle/mesh.py), pinned to the
+# same reference golden vectors
+
+def oracle_case(g, key):
+    from oracle import basis as ob
+    from oracle import fem as of
+    from oracle.mesh import GeneralMesh, GeneralProblem
+    kind, P = (int(v) for v in g[f"{key}_meta"])
+    dr = {}
+    for t, c in g[f"{key}_dir"]:
+        dr.setdefault(TAGS[int(t)], []).append(int(c))
+    boundary = {str(t): [tuple(q) for q in g[f"{key}_b_{t}"]] for t in g[f"{key}_btags"]}
+    mesh = GeneralMesh(g[f"{key}_coords"], g[f"{key}_elems"], boundary)
+    return GeneralProblem(mesh, ob.Basis(KINDS[kind], P), of.Material(1.0e7, 0.3, 1.0e3), P + 1,
+                          [(t, tuple(c)) for t, c in dr.items()])
+
+
+@pytest.mark.parametrize("case", [c for c in golden_mesh_cases() if c[1] != "m6"], ids=lambda c: c[1])
+def test_oracle_general_mesh_vs_reference(case):
+    from conftest import max_rel_err
+    g, key = case
+    opb = oracle_case(g, key)
+    assert np.array_equal(opb.dmap.gdof, g[f"{key}_gdof"])
+    assert np.array_equal(opb.dmap.gsign, g[f"{key}_gsign"])
+    assert np.array_equal(opb.dmap.free_map, g[f"{key}_free_map"])
+    u, p, cm = g[f"{key}_u"], g[f"{key}_p"], float(g[f"{key}_cm"])
+    assert max_rel_err(opb.internal_force(u), g[f"{key}_fint"]) <= 1e-12
+    assert max_rel_err(opb.apply_tangent(u, p), g[f"{key}_kp"]) <= 1e-12
+    assert max_rel_err(opb.assemble(u, 1.0, cm).diagonal(), g[f"{key}_diag"]) <= 1e-12
+    assert max_rel_err(opb.mass() @ p, g[f"{key}_mp"]) <= 1e-12
