@@ -36,7 +36,11 @@ def run(div, P, m):
 
 
 if __name__ == "__main__":
-    run((4, 4, 4), 4, 6)
-    run((8, 8, 8), 4, 6)
+    if len(sys.argv) > 1:  # e.g. 64 4 5: per-iteration cost at config-2 size
+        n, P, m = (int(a) for a in sys.argv[1:4])
+        run((n, n, n), P, m)
+    else:
+        run((4, 4, 4), 4, 6)
+        run((8, 8, 8), 4, 6)
     run((16, 16, 16), 4, 5)
     run((32, 32, 32), 4, 5)
