@@ -39,6 +39,7 @@ struct Geo {
   double detJ;        // h_x h_y h_z / 8
   double mu, lam, rho;
   int dmask[3];       // Dirichlet face bits per component (xmin,xmax,ymin,ymax,zmin,zmax)
+  int serp;           // 1: odd colour passes run their elements in reverse order
 };
 
 // MODE_SETUP stores K = F^-T and ln J at every quadrature point (OpArgs::qpd);
@@ -97,26 +98,55 @@ __device__ __forceinline__ bool colour_element(const Geo& g, int colour, long lo
     ek = (int)(r / g.ny);
     return true;
   }
+  // colour code: parity bits 0-2, optional z-slab [izlo, izhi) of the
+  // colour's element layers in bits 3-16 / 17-30 (0, 0: all layers)
   const int cx = colour & 1, cy = (colour >> 1) & 1, cz = (colour >> 2) & 1;
   const int nex = (g.nx - cx + 1) >> 1, ney = (g.ny - cy + 1) >> 1, nez = (g.nz - cz + 1) >> 1;
-  if (nex <= 0 || ney <= 0 || nez <= 0) return false;
-  if (idx >= (long long)nex * ney * nez) return false;
+  int izlo = (colour >> 3) & 0x3fff, izhi = (colour >> 17) & 0x3fff;
+  if (izhi == 0) izlo = 0, izhi = nez;
+  if (izhi > nez) izhi = nez;
+  if (nex <= 0 || ney <= 0 || izhi <= izlo) return false;
+  const long long cnt = (long long)nex * ney * (izhi - izlo);
+  if (idx >= cnt) return false;
+  // serpentine pass order: the passes run in Gray-code colour order
+  // (colour_of_pass: consecutive passes are face neighbours) and sweep the mesh
+  // in alternating directions (odd popcount = odd pass), so a pass starts
+  // where the previous one ended and finds their shared faces still in L2
+  if (g.serp && (__popc(colour & 7) & 1)) idx = cnt - 1 - idx;
   const int ix = (int)(idx % nex);
   const long long r = idx / nex;
   const int iy = (int)(r % ney);
-  const int iz = (int)(r / ney);
+  const int iz = izlo + (int)(r / ney);
   ei = 2 * ix + cx;
   ej = 2 * iy + cy;
   ek = 2 * iz + cz;
   return true;
 }
 
+// launch order of the 8 colour passes: Gray code 0 1 3 2 6 7 5 4 (each pass
+// flips one parity bit, i.e. shares faces with the previous one)
+__host__ __device__ constexpr int colour_of_pass(int pass) { return pass ^ (pass >> 1); }
+
 __host__ __device__ inline long long colour_count(const Geo& g, int colour) {
   if (colour < 0) return (long long)g.nx * g.ny * g.nz;
   const int cx = colour & 1, cy = (colour >> 1) & 1, cz = (colour >> 2) & 1;
   const long long nex = (g.nx - cx + 1) >> 1, ney = (g.ny - cy + 1) >> 1, nez = (g.nz - cz + 1) >> 1;
-  if (nex <= 0 || ney <= 0 || nez <= 0) return 0;
-  return nex * ney * nez;
+  long long izlo = (colour >> 3) & 0x3fff, izhi = (colour >> 17) & 0x3fff;
+  if (izhi == 0) izlo = 0, izhi = nez;
+  if (izhi > nez) izhi = nez;
+  if (nex <= 0 || ney <= 0 || izhi <= izlo) return 0;
+  return nex * ney * (izhi - izlo);
+}
+
+// colour code of pass `pass` over z-slab `slab` of `nslab` (element layers
+// split evenly in the colour's own layer index)
+inline int colour_code(const Geo& g, int pass, int slab, int nslab) {
+  const int c = colour_of_pass(pass);
+  if (nslab <= 1) return c;
+  const int nez = (g.nz - ((c >> 2) & 1) + 1) >> 1;
+  const int lo = (int)((long long)nez * slab / nslab), hi = (int)((long long)nez * (slab + 1) / nslab);
+  if (hi <= lo) return -2;  // empty slab
+  return c | (lo << 3) | (hi << 17);
 }
 
 // ---------------------------------------------------------------------------

@@ -124,7 +124,9 @@ void launch_v3_k(sdme_ctx* c, const TB& tb, OpArgs a) {
     else ev_gather<N>(c, a);
     return;
   }
-  for (int col = 0; col < 8; ++col) {
+  for (int sp = 0; sp < 8 * c->nslab; ++sp) {
+    const int col = colour_code(c->geo, sp % 8, sp / 8, c->nslab);
+    if (col == -2) continue;
     const long long cnt = colour_count(c->geo, col);
     if (cnt == 0) continue;
     a.colour = col;
@@ -309,7 +311,9 @@ void launch_v5(sdme_ctx* c, const TabEO<N, M, MIR>& tb, OpArgs a) {
     else ev_gather<N>(c, a);
     return;
   }
-  for (int col = 0; col < 8; ++col) {
+  for (int sp = 0; sp < 8 * c->nslab; ++sp) {
+    const int col = colour_code(c->geo, sp % 8, sp / 8, c->nslab);
+    if (col == -2) continue;
     const long long cnt = colour_count(c->geo, col);
     if (cnt == 0) continue;
     a.colour = col;
@@ -477,7 +481,9 @@ void launch_col_k(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
     else ev_gather<N>(c, a);
     return;
   }
-  for (int col = 0; col < 8; ++col) {
+  for (int sp = 0; sp < 8 * c->nslab; ++sp) {
+    const int col = colour_code(c->geo, sp % 8, sp / 8, c->nslab);
+    if (col == -2) continue;
     const long long cnt = colour_count(c->geo, col);
     if (cnt == 0) continue;
     a.colour = col;
@@ -543,7 +549,9 @@ void diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm) {
     ev_gather<N>(c, a);
     return;
   }
-  for (int col = 0; col < 8; ++col) {
+  for (int sp = 0; sp < 8 * c->nslab; ++sp) {
+    const int col = colour_code(c->geo, sp % 8, sp / 8, c->nslab);
+    if (col == -2) continue;
     const long long cnt = colour_count(c->geo, col);
     if (cnt == 0) continue;
     a.colour = col;

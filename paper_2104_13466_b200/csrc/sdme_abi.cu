@@ -351,6 +351,7 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   sdme_ctx* ctx = new sdme_ctx();
   ctx->ops = ops;
   if (const char* v = getenv("SDME_VARIANT")) ctx->variant = atoi(v);
+  if (const char* v = getenv("SDME_SLABS")) ctx->nslab = std::max(1, std::min(atoi(v), 64));
   if (const char* v = getenv("SDME_PCG_DIRECT")) ctx->pcg_direct = atoi(v) != 0;
   if (const char* v = getenv("SDME_PA")) ctx->pa = atoi(v) != 0;
   ctx->P = d->P;
@@ -377,6 +378,8 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   g.detJ = d->hx * d->hy * d->hz / 8.0;
   g.mu = d->mu; g.lam = d->lambda_lame; g.rho = d->rho0;
   for (int c = 0; c < 3; ++c) g.dmask[c] = d->dirichlet_mask[c];
+  g.serp = 1;
+  if (const char* v = getenv("SDME_SERPENTINE")) g.serp = atoi(v) != 0;
   ctx->h[0] = d->hx; ctx->h[1] = d->hy; ctx->h[2] = d->hz;
   for (int c = 0; c < 3; ++c) ctx->origin[c] = d->origin[c];
   ctx->nvec = 3 * g.Ns;

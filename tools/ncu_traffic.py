@@ -22,7 +22,7 @@ def main(log, out):
         launches[k][r[imet]] = float(r[ival].replace(",", "")) * scale[r[iunit]]
     ids = sorted(launches)
     res = {"source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-                     "--clock-control none, tools/prof_variant.py (config 2: K.p = launches 0-7, mass 8-15, "
+                     "--clock-control none --cache-control none (steady state), tools/prof_variant.py (config 2: K.p = launches 0-7, mass 8-15, "
                      "f_int 16-23); tools/ncu_traffic.py",
            "kernel_kp": names[ids[0]]}
     for j, op in enumerate(("kp", "mass", "fint")):
