@@ -103,11 +103,11 @@ struct sdme_ctx {
   // pipelined batch K.p with host buffers (sdme_apply_batch): copy streams,
   // double-buffered free-order staging, events
   struct Batch {
-    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaStream_t h2d = nullptr, h2d2 = nullptr, d2h = nullptr;  // u / p copies on separate streams
     double* su[2] = {nullptr, nullptr};
     double* sp[2] = {nullptr, nullptr};
     double* sy[2] = {nullptr, nullptr};
-    cudaEvent_t ev_h2d[2] = {}, ev_in_free[2] = {}, ev_comp[2] = {}, ev_out_free[2] = {};
+    cudaEvent_t ev_h2d[2] = {}, ev_h2d2[2] = {}, ev_in_free[2] = {}, ev_comp[2] = {}, ev_out_free[2] = {};
     int u = -1, p = -1, y = -1;  // lattice vectors
   };
   Batch* batch = nullptr;

@@ -1092,6 +1092,8 @@ int sdme_time_op(sdme_ctx* ctx, int op, int u, int p, int y, double c_m, int rep
   return check_launch(ctx);
 }
 
+void batch_free(sdme_ctx* ctx);
+
 // Pipelined batch K.p with host buffers (the e2e path of many operator
 // applications): pair k's H2D copies (copy stream 1) and result k-1's D2H copy
 // (copy stream 2) overlap the permutations and operator of pair k on the
@@ -1100,34 +1102,46 @@ int batch_setup(sdme_ctx* ctx) {
   if (ctx->batch) return SDME_OK;
   auto* b = new sdme_ctx::Batch();
   ctx->batch = b;
-  CK(cudaStreamCreateWithFlags(&b->h2d, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&b->d2h, cudaStreamNonBlocking));
-  for (int i = 0; i < 2; ++i) {
-    CK(cudaMalloc(&b->su[i], ctx->n_free * sizeof(double)));
-    CK(cudaMalloc(&b->sp[i], ctx->n_free * sizeof(double)));
-    CK(cudaMalloc(&b->sy[i], ctx->n_free * sizeof(double)));
-    CK(cudaEventCreateWithFlags(&b->ev_h2d[i], cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&b->ev_in_free[i], cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&b->ev_comp[i], cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&b->ev_out_free[i], cudaEventDisableTiming));
+  bool ok = cudaStreamCreateWithFlags(&b->h2d, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&b->h2d2, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&b->d2h, cudaStreamNonBlocking) == cudaSuccess;
+  for (int i = 0; ok && i < 2; ++i) {
+    ok = cudaMalloc(&b->su[i], ctx->n_free * sizeof(double)) == cudaSuccess &&
+         cudaMalloc(&b->sp[i], ctx->n_free * sizeof(double)) == cudaSuccess &&
+         cudaMalloc(&b->sy[i], ctx->n_free * sizeof(double)) == cudaSuccess;
+    for (cudaEvent_t* e : {&b->ev_h2d[i], &b->ev_h2d2[i], &b->ev_in_free[i], &b->ev_comp[i], &b->ev_out_free[i]})
+      ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
   }
-  int rc = alloc_vec(ctx, &b->u);
+  int rc = ok ? alloc_vec(ctx, &b->u) : SDME_CUDA_ERROR;
   if (!rc) rc = alloc_vec(ctx, &b->p);
   if (!rc) rc = alloc_vec(ctx, &b->y);
-  return rc;
+  if (rc) {  // leave no half-built pipeline behind
+    batch_free(ctx);
+    cudaGetLastError();
+    return set_err(ctx, SDME_CUDA_ERROR, "batch apply: allocation failed");
+  }
+  return SDME_OK;
 }
 
 void batch_free(sdme_ctx* ctx) {
   auto* b = ctx->batch;
   if (!b) return;
+  for (int id : {b->u, b->p, b->y})
+    if (id >= 0 && vec(ctx, id)) {
+      cudaFree(ctx->vecs[id]);
+      ctx->vecs[id] = nullptr;
+      if (ctx->vec_tmaps[id]) cudaFree(ctx->vec_tmaps[id]);
+      ctx->vec_tmaps[id] = nullptr;
+    }
   for (int i = 0; i < 2; ++i) {
     cudaFree(b->su[i]);
     cudaFree(b->sp[i]);
     cudaFree(b->sy[i]);
-    for (cudaEvent_t e : {b->ev_h2d[i], b->ev_in_free[i], b->ev_comp[i], b->ev_out_free[i]})
+    for (cudaEvent_t e : {b->ev_h2d[i], b->ev_h2d2[i], b->ev_in_free[i], b->ev_comp[i], b->ev_out_free[i]})
       if (e) cudaEventDestroy(e);
   }
   if (b->h2d) cudaStreamDestroy(b->h2d);
+  if (b->h2d2) cudaStreamDestroy(b->h2d2);
   if (b->d2h) cudaStreamDestroy(b->d2h);
   delete b;
   ctx->batch = nullptr;
@@ -1148,12 +1162,17 @@ int sdme_apply_batch(sdme_ctx* ctx, int n, const double* const* u, const double*
   for (int k = 0; k < n; ++k) {
     const int s = k & 1;
     // H2D of pair k into staging s (free once the permutations of pair k-2 ran)
-    if (k >= 2) CK(cudaStreamWaitEvent(b->h2d, b->ev_in_free[s], 0));
+    if (k >= 2) {
+      CK(cudaStreamWaitEvent(b->h2d, b->ev_in_free[s], 0));
+      CK(cudaStreamWaitEvent(b->h2d2, b->ev_in_free[s], 0));
+    }
     if (c_k != 0.0) CK(cudaMemcpyAsync(b->su[s], u[k], bytes, cudaMemcpyHostToDevice, b->h2d));
-    CK(cudaMemcpyAsync(b->sp[s], p[k], bytes, cudaMemcpyHostToDevice, b->h2d));
+    CK(cudaMemcpyAsync(b->sp[s], p[k], bytes, cudaMemcpyHostToDevice, b->h2d2));
     CK(cudaEventRecord(b->ev_h2d[s], b->h2d));
+    CK(cudaEventRecord(b->ev_h2d2[s], b->h2d2));
     // operator on the context stream
     CK(cudaStreamWaitEvent(ctx->st, b->ev_h2d[s], 0));
+    CK(cudaStreamWaitEvent(ctx->st, b->ev_h2d2[s], 0));
     if (c_k != 0.0) k_free_to_lattice<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(U, b->su[s], ctx->d_perm, ctx->nvec);
     k_free_to_lattice<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(Pv, b->sp[s], ctx->d_perm, ctx->nvec);
     ctx->launches += c_k != 0.0 ? 2 : 1;
