@@ -585,3 +585,22 @@ def test_apply_batch_matches_single_calls(ev, monkeypatch):
     got = pb.apply_tangent_batch(us, ps, c_m=3.0e4)
     for u, p, y in zip(us, ps, got):
         assert np.array_equal(y.view(np.int64), pb.apply_tangent(u, p, 3.0e4).view(np.int64))
+
+
+@pytest.mark.parametrize("P,div", [(2, (1, 1, 1)), (3, (1, 3, 1)), (4, (1, 1, 3)), (4, (5, 1, 1)), (3, (4, 2, 1)),
+                                   (6, (1, 2, 1)), (8, (1, 1, 1))])
+def test_tma_paths_on_thin_meshes(P, div, monkeypatch):
+    """Single-element rows / columns / layers on the colour-pass TMA paths:
+    boxes at both lattice ends (out-of-tensor slots dropped), every face
+    Dirichlet-constrained for one component, the odd-P row shift at odd x."""
+    monkeypatch.setenv("SDME_EV", "0")
+    L = tuple(0.25 * d for d in div)
+    dr = [("xmin", (0,)), ("xmax", (1,)), ("ymin", (2,)), ("zmax", (0, 1))]
+    opb = of.Problem(of.Mesh(div, L), ob.Basis("SDME_M", P), OMAT, P + 1, dr)
+    pb = gpu_problem("SDME_M", P, P + 1, div, L, dr)
+    rng = np.random.default_rng(P * 7 + sum(div))
+    u = 1e-3 * rng.uniform(-1, 1, opb.n_free)
+    p = rng.standard_normal(opb.n_free)
+    assert max_rel_err(pb.internal_force(u), opb.internal_force(u)) <= TOL
+    assert max_rel_err(pb.apply_tangent(u, p, 2.0e5), opb.apply_tangent(u, p, 2.0e5)) <= TOL
+    assert max_rel_err(pb.mass_apply(p), opb.mass() @ p) <= TOL
