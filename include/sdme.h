@@ -150,6 +150,12 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
  * reciprocal lumped mass vector (0 on Dirichlet points). */
 int sdme_explicit_step(sdme_ctx* ctx, int u, int u_prev, int v, int load, double s_load,
                        int fc, int inv_ml, double dt, int scratch);
+/* n such steps back to back on the device (no host round trip per step): the
+ * contact force (fc >= 0) uses the parameters of the last sdme_contact call,
+ * the load scale of step k is s_load[k]; the inversion flag is checked once
+ * at the end (smallest element / point over the n steps). */
+int sdme_explicit_steps(sdme_ctx* ctx, int n, int u, int u_prev, int v, int load, const double* s_load, int fc,
+                        int inv_ml, double dt, int scratch);
 
 /* penalty contact against a rigid plane on a box side (contact.py:87-128):
  * fc = sum_q warea t_N N_f n, gaps (optional, host) = gap per face point in the

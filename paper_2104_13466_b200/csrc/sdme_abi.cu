@@ -917,6 +917,44 @@ int sdme_explicit_step(sdme_ctx* ctx, int u, int u_prev, int v, int load, double
   return check_launch(ctx);
 }
 
+// n central-difference steps back to back on the context stream (no host
+// round trip per step): per step the contact force at u with the parameters
+// of the last sdme_contact call (if fc >= 0), f_int, and the update with load
+// scale s_load[k] (load >= 0).  The inversion flag is read once at the end;
+// it carries the smallest (element, point) over all n steps, so a caller that
+// needs the first inverted step replays the chunk step by step.
+int sdme_explicit_steps(sdme_ctx* ctx, int n, int u, int u_prev, int v, int load, const double* s_load, int fc,
+                        int inv_ml, double dt, int scratch) {
+  if (!ctx || n < 0) return SDME_BAD_ARGUMENT;
+  double *pu = vec(ctx, u), *pup = vec(ctx, u_prev), *pv = vec(ctx, v), *pm = vec(ctx, inv_ml),
+         *ps = vec(ctx, scratch);
+  const double* pl = load >= 0 ? vec(ctx, load) : nullptr;
+  double* pf = fc >= 0 ? vec(ctx, fc) : nullptr;
+  if (!pu || !pup || !pv || !pm || !ps || (load >= 0 && (!pl || !s_load)) || (fc >= 0 && (!pf || !ctx->c_ready)) ||
+      !(dt > 0.0))
+    return set_err(ctx, SDME_BAD_ARGUMENT, "bad explicit-steps argument");
+  int rc = reset_flag(ctx);
+  if (rc) return rc;
+  for (int k = 0; k < n; ++k) {
+    if (pf) {
+      ContactArgs ca = ctx->c_ca;
+      ca.mode = CONTACT_FORCE;
+      ca.u = pu;
+      ca.fc = pf;
+      CK(cudaMemsetAsync(pf, 0, ctx->nvec * sizeof(double), ctx->st));
+      launch_contact(ctx, ca);
+    }
+    CK(cudaMemsetAsync(ps, 0, ctx->nvec * sizeof(double), ctx->st));
+    ctx->ops->element(ctx, MODE_FINT, pu, nullptr, ps, 1.0, 0.0);
+    k_explicit_step<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(pu, pup, pv, pl, pl ? s_load[k] : 0.0, ps, pf, pm,
+                                                             dt, ctx->nvec);
+    ++ctx->launches;
+  }
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  return check_flag(ctx);
+}
+
 int sdme_contact_points(const sdme_ctx* ctx, int side, int qf, int64_t* n) {
   if (!ctx || ctx->gen || side < 0 || side > 5 || qf < 1 || !n) return SDME_BAD_ARGUMENT;
   const int axis = side / 2;

@@ -308,7 +308,9 @@ __global__ void k_explicit_step(double* __restrict__ u, double* __restrict__ u_p
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     double psi = -fint[i];
-    if (load) psi = fma(s_load, load[i], psi);
+    // the scaled load is rounded before the add (as the host-scaled load of the
+    // per-step path: s_load = 1 there), so chunked and per-step runs agree bitwise
+    if (load) psi = __dadd_rn(psi, __dmul_rn(s_load, load[i]));
     if (fc) psi += fc[i];
     const double ui = u[i], up = u_prev[i];
     const double un = (2.0 * ui - up) + dt2 * psi * inv_ml[i];

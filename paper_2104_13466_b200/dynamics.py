@@ -317,7 +317,8 @@ def explicit_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
     from . import native
 
     lib = native.lib()
-    for step in range(n_steps):
+
+    def one_step(step, t):
         lid = -1
         if load is not None:
             lid = load.at(t).vid
@@ -327,8 +328,57 @@ def explicit_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
             fid = fc.vid
         native.check(pb._ctx, lib.sdme_explicit_step(pb._ctx, u.vid, u_prev.vid, v.vid, lid, 1.0, fid,
                                                      inv_ml.vid, dt, fint.vid), "explicit_step")
-        t += dt
-        if snapshot_stride and (step + 1) % snapshot_stride == 0:
+
+    # Steps run in chunks on the device (sdme_explicit_steps: no host round trip
+    # per step) between the steps that need the host (contact records,
+    # snapshots); a general load callable runs step by step.  An inversion in a
+    # chunk is replayed step by step from the chunk's start, so the error names
+    # the first inverted step's element as the reference does.
+    chunked = load is None or load.scaled
+    saved = [DeviceVector(pb) for _ in range(3)] if chunked else None
+    step = 0
+    while step < n_steps:
+        if not chunked:
+            one_step(step, t)
+            step += 1
+            t += dt
+        else:
+            # the first step of a chunk goes through forces_ (records, contact parameters)
+            one_step(step, t)
+            step += 1
+            t += dt
+            end = n_steps
+            if record_every:
+                end = min(end, (step + record_every - 1) // record_every * record_every)
+            if snapshot_stride:
+                end = min(end, (step + snapshot_stride - 1) // snapshot_stride * snapshot_stride)
+            if snapshot_stride and step % snapshot_stride == 0:
+                traj.times.append(t)
+                traj.snapshots.append(u.free())
+            n = end - step
+            if n > 0:
+                for dst, src in zip(saved, (u, u_prev, v)):
+                    dst.copy_from(src)
+                scales = np.array([float(external_load.scale(t + k * dt)) if load is not None else 0.0
+                                   for k in range(n)])
+                rc = lib.sdme_explicit_steps(pb._ctx, n, u.vid, u_prev.vid, v.vid,
+                                             load.base.vid if load is not None else -1, native.dptr(scales),
+                                             fc.vid if contact is not None else -1, inv_ml.vid, dt, fint.vid)
+                if rc == native.INVERSION:
+                    for dst, src in zip((u, u_prev, v), saved):
+                        dst.copy_from(src)
+                    for k in range(n):  # raises at the first inverted step
+                        one_step(step + k, t + k * dt)
+                native.check(pb._ctx, rc, "explicit_steps")
+                if contact is not None:
+                    contact._serial += n
+                step += n
+                t += n * dt
+                if snapshot_stride and step % snapshot_stride == 0:
+                    traj.times.append(t)
+                    traj.snapshots.append(u.free())
+            continue
+        if snapshot_stride and step % snapshot_stride == 0:
             traj.times.append(t)
             traj.snapshots.append(u.free())
     traj.state = TimeState(t, u.free(), v.free(), a0.free(), u_prev.free())

@@ -74,6 +74,8 @@ SIGNATURES = {
                  C.c_int, C.POINTER(C.c_int), _dp],
     "sdme_explicit_step": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
                            C.c_double, C.c_int],
+    "sdme_explicit_steps": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, C.c_int, C.c_int,
+                            C.c_double, C.c_int],
     "sdme_contact": [C.c_void_p, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, C.c_double, C.c_int,
                      _dp, _dp],
     "sdme_contact_points": [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int64)],

@@ -604,3 +604,27 @@ def test_tma_paths_on_thin_meshes(P, div, monkeypatch):
     assert max_rel_err(pb.internal_force(u), opb.internal_force(u)) <= TOL
     assert max_rel_err(pb.apply_tangent(u, p, 2.0e5), opb.apply_tangent(u, p, 2.0e5)) <= TOL
     assert max_rel_err(pb.mass_apply(p), opb.mass() @ p) <= TOL
+
+
+def test_explicit_chunks_match_per_step_and_report_first_inversion():
+    """explicit_run runs steps in device chunks (sdme_explicit_steps) between
+    host-visible steps; the result equals the step-by-step path bitwise, and an
+    inversion inside a chunk is replayed so the error names the same element
+    and point as the per-step path (the reference raises at the first
+    inverted step, femcore.py:92-93)."""
+    pb = gpu_problem("SDME_M", 3, 4, (3, 2, 2), (0.3, 0.2, 0.2), [("xmin", (0, 1, 2))])
+    v0 = pb.constant_field([0.0, 0.0, 1.0])
+    zero = np.zeros(pb.n_free)
+    a = explicit_run(pb, None, 1e-6, 40, v0=v0)                     # chunked
+    b = explicit_run(pb, lambda t: zero, 1e-6, 40, v0=v0)           # callable load: per step
+    assert np.array_equal(a.state.u.view(np.int64), b.state.u.view(np.int64))
+    assert np.array_equal(a.state.v.view(np.int64), b.state.v.view(np.int64))
+    fast = pb.constant_field([0.0, 0.0, 3.0e3])
+    rng = np.random.default_rng(2)
+    fast = fast * (1.0 + rng.uniform(-1, 1, pb.n_free))  # non-uniform: elements invert after some steps
+    errs = []
+    for load in (None, lambda t: zero):
+        with pytest.raises(ElementInversionError) as ei:
+            explicit_run(pb, load, 1e-5, 400, v0=fast)
+        errs.append((ei.value.elem_id, ei.value.qp))
+    assert errs[0] == errs[1]
