@@ -385,7 +385,8 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
   int buf = 0;
   if (args.skip && *(volatile const int*)args.skip) return;
   constexpr bool UPASS = (MODE == MODE_APPLY || MODE == MODE_FINT || MODE == MODE_SETUP);
-  constexpr bool PPASS = (MODE == MODE_APPLY || MODE == MODE_PA);
+  constexpr bool PPASS = (MODE == MODE_APPLY || MODE == MODE_PA || MODE == MODE_MASS);
+  constexpr bool PGRAD = MODE != MODE_MASS;  // c_m M p alone: values only (B stages), no gradient
   const long long cnt = colour_count(g, args.colour);
   const long long stride = gridDim.x;
   const double mu_k = args.c_k * g.mu, lam_k = args.c_k * g.lam;
@@ -470,13 +471,18 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
       group_sync<WPE>(0);
     }
     if (PPASS)
-      col_forward<N, WPE, MIR, VAL, VALS, TM>(tb, g, args.p + eoff, X0, Y0, Z0, S, t, &buf, nxt, true, pmap, nxb,
+      col_forward<N, WPE, MIR, VAL, VALS, TM>(tb, g, args.p + eoff, X0, Y0, Z0, S, t, &buf, nxt, PGRAD, pmap, nxb,
                                               &ph);
 #pragma unroll
     for (int r = 0; r < QPT; ++r) {
       const int q = t + r * T;
       if (q >= Q) continue;
       const double wdet = GEN ? __ldg(args.geo + eid * (10 * Q) + 9 * Q + q) : S[L::W + q];
+      if (MODE == MODE_MASS) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) S[L::qi(3, i, q)] *= cmr * wdet;
+        continue;
+      }
       QpK s;
       if (MODE == MODE_PA) {
         const double* qd = args.qpd + eid * (kQpSlots * Q) + q;
@@ -575,7 +581,7 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
     group_sync<WPE>(0);
     if (MODE == MODE_SETUP) continue;
     double* evb = args.ev ? args.ev + eid * 3 * Q : nullptr;
-    col_backward<N, WPE, MIR, VAL, VALS, TM>(tb, g, args.y, X0, Y0, Z0, S, t, evb, true,
+    col_backward<N, WPE, MIR, VAL, VALS, TM>(tb, g, args.y, X0, Y0, Z0, S, t, evb, PGRAD,
                                              static_cast<const CUtensorMap*>(args.ty));
   }
   // the reduce-adds have completed before the CTA (and its shared memory) retires

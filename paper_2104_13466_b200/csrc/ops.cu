@@ -363,8 +363,8 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
     // f_int and K.p: collocated sum factorisation (element_col.cuh) unless
     // SDME_VARIANT=10; other modes and non-mirrored tables: component-serial,
     // cp.async-staged rows, even-odd contractions, 11 warps/SM
-    if ((mode == MODE_FINT || mode == MODE_APPLY || mode == MODE_PA || mode == MODE_SETUP) && c->variant != 10 &&
-        c->mir >= 0) {
+    if ((mode == MODE_FINT || mode == MODE_APPLY || mode == MODE_PA || mode == MODE_SETUP || mode == MODE_MASS) &&
+        c->variant != 10 && c->mir >= 0) {
       if (c->mir == 0) col_modes<N, 0>(c, mode, a);
       else col_modes<N, 1>(c, mode, a);
       return;
@@ -373,8 +373,8 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
     return;
   } else if constexpr (N >= 6) {
     if constexpr (N == M) {
-      if ((mode == MODE_FINT || mode == MODE_APPLY || mode == MODE_PA || mode == MODE_SETUP) && c->variant != 10 &&
-          c->mir >= 0) {
+      if ((mode == MODE_FINT || mode == MODE_APPLY || mode == MODE_PA || mode == MODE_SETUP || mode == MODE_MASS) &&
+          c->variant != 10 && c->mir >= 0) {
         if (c->mir == 0) col_modes<N, 0>(c, mode, a);
         else col_modes<N, 1>(c, mode, a);
         return;
@@ -503,7 +503,8 @@ template <int N, int MODE, bool VAL, int MIR>
 void launch_col(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
   if constexpr ((N & 1) || BoxW<N>::BW % 4 == 2) {
     const bool maps = MODE == MODE_SETUP ? a.tu != nullptr
-                                         : (a.ty && (MODE == MODE_PA || a.tu) && (MODE == MODE_FINT || a.tp));
+                                         : (a.ty && (MODE == MODE_PA || MODE == MODE_MASS || a.tu) &&
+                                            (MODE == MODE_FINT || a.tp));
     if (maps && !c->ev_mode && c->variant != 11) {
       launch_col_k<N, MODE, VAL, MIR, true>(c, tb, a);
       return;
@@ -521,6 +522,7 @@ void col_modes(sdme_ctx* c, int mode, OpArgs a) {
   else if (mode == MODE_APPLY && a.c_m != 0.0) launch_col<N, MODE_APPLY, true, MIR>(c, tb, a);
   else if (mode == MODE_APPLY) launch_col<N, MODE_APPLY, false, MIR>(c, tb, a);
   else if (mode == MODE_PA && a.c_m != 0.0) launch_col<N, MODE_PA, true, MIR>(c, tb, a);
+  else if (mode == MODE_MASS) launch_col<N, MODE_MASS, true, MIR>(c, tb, a);
   else launch_col<N, MODE_PA, false, MIR>(c, tb, a);
 }
 
@@ -615,6 +617,7 @@ void gen_modes(sdme_ctx* c, int mode, OpArgs a) {
   else if (mode == MODE_APPLY && a.c_m != 0.0) launch_col_gen<N, MODE_APPLY, true, MIR>(c, tb, a);
   else if (mode == MODE_APPLY) launch_col_gen<N, MODE_APPLY, false, MIR>(c, tb, a);
   else if (mode == MODE_PA && a.c_m != 0.0) launch_col_gen<N, MODE_PA, true, MIR>(c, tb, a);
+  else if (mode == MODE_MASS) launch_col_gen<N, MODE_MASS, true, MIR>(c, tb, a);
   else launch_col_gen<N, MODE_PA, false, MIR>(c, tb, a);
 }
 
@@ -629,16 +632,11 @@ void gen_element_impl(sdme_ctx* c, int mode, const double* u, const double* p, d
   a.geo = c->d_geom;
   a.qpd = c->d_qpd;
   a.ev = c->d_ev;
-  if (mode == MODE_MASS) {
-    // c_m M p: the K.p kernel with c_k = 0 on a zero u (F = I)
-    mode = MODE_APPLY;
-    a.c_k = 0.0;
-    cudaMemsetAsync(c->d_evu, 0, ns * sizeof(double), c->st);
-  } else if (mode == MODE_FINT || mode == MODE_APPLY || mode == MODE_SETUP) {
+  if (mode == MODE_FINT || mode == MODE_APPLY || mode == MODE_SETUP) {
     k_gen_gather<<<gen_grid(ns), 256, 0, c->st>>>(c->d_evu, u, c->d_dof, ns, skip);
     ++c->launches;
   }
-  if (mode == MODE_APPLY || mode == MODE_PA) {
+  if (mode == MODE_APPLY || mode == MODE_PA || mode == MODE_MASS) {
     k_gen_gather<<<gen_grid(ns), 256, 0, c->st>>>(c->d_evp, p, c->d_dof, ns, skip);
     ++c->launches;
   }
