@@ -22,6 +22,10 @@
 #define SDME_COL_MINB 11  // resident 1-warp blocks per SM for the P = 4 collocated kernels
 #endif
 
+#ifndef SDME_TMB_MINB
+#define SDME_TMB_MINB 7  // max resident 2-warp blocks per SM of the TMA all-component kernels
+#endif
+
 #ifndef SDME_GEN_MINB
 #define SDME_GEN_MINB 1  // resident blocks per SM asked of the general-mesh P = 4 kernels
 #endif
@@ -96,7 +100,7 @@ template <int N, int M, class S, int MODE, bool VAL, class TB, bool TMB>
 void launch_v3_k(sdme_ctx* c, const TB& tb, OpArgs a) {
   constexpr bool VALS = VAL || MODE == MODE_MASS;
   constexpr int smem = V3Smem<N, M, S::WPE, S::NC, VALS, S::STG, TMB>::PERS * 8 * S::EPB;
-  constexpr int MINB = TMB && S::MINB > 6 ? 6 : S::MINB;  // TMA boxes: 168-register cap (see DESIGN)
+  constexpr int MINB = TMB && S::MINB > SDME_TMB_MINB ? SDME_TMB_MINB : S::MINB;  // TMA boxes: register cap (see DESIGN)
   auto kern = element_v3<N, M, S::WPE, S::NC, S::EPB, MINB, MODE, VAL, S::STG, TB, TMB>;
   static int max_blocks = -1;
   if (max_blocks < 0) {
