@@ -628,3 +628,22 @@ def test_explicit_chunks_match_per_step_and_report_first_inversion():
             explicit_run(pb, load, 1e-5, 400, v0=fast)
         errs.append((ei.value.elem_id, ei.value.qp))
     assert errs[0] == errs[1]
+
+
+def test_gll_collocation_mass_is_diagonal():
+    """test_femcore.py:111-116: the nodal basis with the (P+1)-point GLL rule
+    (collocation_mass=True, femcore.py:284-288) has an exactly diagonal mass:
+    every probed column of M has one non-zero, on the diagonal, positive; and
+    M p agrees with (M 1) * p to rounding."""
+    from paper_2104_13466_b200 import gll_rule
+    pb = GpuFemProblem(BoxMesh((3, 2, 2), (1.5, 1.0, 1.0)), build_basis(3, BasisKind("LagrangeGLL")), MAT,
+                       gll_rule(4), [("xmin", (0, 1, 2))])
+    rng = np.random.default_rng(4)
+    for j in rng.choice(pb.n_free, 12, replace=False):
+        e = np.zeros(pb.n_free)
+        e[j] = 1.0
+        col = pb.mass_apply(e)
+        assert np.count_nonzero(col) == 1 and col[j] > 0.0
+    d = pb.mass_apply(np.ones(pb.n_free))
+    p = rng.standard_normal(pb.n_free)
+    assert np.abs(pb.mass_apply(p) - d * p).max() <= 1e-14 * np.abs(d * p).max()

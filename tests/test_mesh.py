@@ -141,3 +141,14 @@ def test_oracle_general_mesh_vs_reference(case):
     assert max_rel_err(opb.apply_tangent(u, p), g[f"{key}_kp"]) <= 1e-12
     assert max_rel_err(opb.assemble(u, 1.0, cm).diagonal(), g[f"{key}_diag"]) <= 1e-12
     assert max_rel_err(opb.mass() @ p, g[f"{key}_mp"]) <= 1e-12
+
+
+def test_free_dofs_match_reference_table():
+    """test_meshdof.py:88-92: the 8-hex cube clamped on xmin has 300 / 1944 /
+    6084 / 13872 free DOFs at P = 2 / 4 / 6 / 8 (box path and general path)."""
+    for P, expect in ((2, 300), (4, 1944), (6, 6084), (8, 13872)):
+        _, n_free = reference_free_index(BoxMesh((2, 2, 2), (1.0, 1.0, 1.0)), P, [("xmin", (0, 1, 2))])
+        assert n_free == expect
+        dm = build_mesh_dofmap(HexMesh.box((2, 2, 2), (1.0, 1.0, 1.0)), build_basis(P, BasisKind("SDME_M")),
+                               [("xmin", (0, 1, 2))])
+        assert dm.n_free == expect
