@@ -647,3 +647,49 @@ def test_gll_collocation_mass_is_diagonal():
     d = pb.mass_apply(np.ones(pb.n_free))
     p = rng.standard_normal(pb.n_free)
     assert np.abs(pb.mass_apply(p) - d * p).max() <= 1e-14 * np.abs(d * p).max()
+
+
+def test_pcg_diagonal_operator_converges_in_one_iteration():
+    """test_solver.py:25-31 on the FE operator: the GLL collocation mass is
+    diagonal, so Jacobi-PCG on c_m M converges in one iteration to b / diag."""
+    from paper_2104_13466_b200 import gll_rule
+    pb = GpuFemProblem(BoxMesh((2, 2, 1), (1.0, 1.0, 0.5)), build_basis(3, BasisKind("LagrangeGLL")), MAT,
+                       gll_rule(4), [("xmin", (0, 1, 2))])
+    b = np.random.default_rng(6).standard_normal(pb.n_free)
+    x, st = pcg_gpu(pb, None, b, c_m=2.0, c_k=0.0, precond="diagonal", tol=1e-12)
+    assert st.iterations == 1
+    d = 2.0 * pb.mass_apply(np.ones(pb.n_free))
+    assert np.abs(x - b / d).max() <= 1e-13 * np.abs(b / d).max()
+
+
+def test_pcg_error_monotone_in_a_norm():
+    """test_solver.py:90-105 on the FE operator A = K_T(u) + c_m M: tighter
+    tolerances never need fewer iterations nor give a larger A-norm error."""
+    pb = gpu_problem("SDME_M", 3, 4, (2, 2, 2), (1.0, 1.0, 1.0), [("xmin", (0, 1, 2))])
+    rng = np.random.default_rng(8)
+    u = 1e-3 * rng.uniform(-1, 1, pb.n_free)
+    b = rng.standard_normal(pb.n_free)
+    cm = 1.0e6
+    x_ex, _ = pcg_gpu(pb, u, b, c_m=cm, tol=1e-14, maxit=100000)
+    errs, iters = [], []
+    for tol in (1e-2, 1e-4, 1e-6, 1e-8, 1e-10):
+        x, st = pcg_gpu(pb, u, b, c_m=cm, tol=tol, maxit=100000)
+        e = x - x_ex
+        errs.append(np.sqrt(e @ pb.apply_tangent(u, e, cm)))
+        iters.append(st.iterations)
+    assert all(i2 >= i1 for i1, i2 in zip(iters, iters[1:]))
+    assert all(e2 <= e1 * (1 + 1e-10) for e1, e2 in zip(errs, errs[1:]))
+
+
+def test_mass_spd_and_tangent_at_reference_state():
+    """test_femcore.py:119-125 (p.Mp > 0) and :81-89 (K_T(0) is the linear
+    stiffness: compared with the oracle's dense tangent at u = 0)."""
+    pb = gpu_problem("SDME_H", 3, 4, (2, 1, 2), (1.0, 0.5, 1.0), [("zmin", (0, 1, 2))])
+    opb = of.Problem(of.Mesh((2, 1, 2), (1.0, 0.5, 1.0)), ob.Basis("SDME_H", 3), OMAT, 4, [("zmin", (0, 1, 2))])
+    rng = np.random.default_rng(9)
+    for _ in range(5):
+        p = rng.standard_normal(pb.n_free)
+        assert p @ pb.mass_apply(p) > 0.0
+    p = rng.standard_normal(pb.n_free)
+    zero = np.zeros(pb.n_free)
+    assert max_rel_err(pb.apply_tangent(zero, p), opb.apply_tangent(zero, p)) <= TOL

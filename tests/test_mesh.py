@@ -152,3 +152,14 @@ def test_free_dofs_match_reference_table():
         dm = build_mesh_dofmap(HexMesh.box((2, 2, 2), (1.0, 1.0, 1.0)), build_basis(P, BasisKind("SDME_M")),
                                [("xmin", (0, 1, 2))])
         assert dm.n_free == expect
+
+
+def test_all_dirichlet_empty_system():
+    """test_femcore.py:248-253: every face of a single P = 1 hexahedron
+    clamped leaves no free DOF (box numbering and general numbering)."""
+    tags = ("xmin", "xmax", "ymin", "ymax", "zmin", "zmax")
+    dr = [(t, (0, 1, 2)) for t in tags]
+    _, n_free = reference_free_index(BoxMesh((1, 1, 1), (1.0, 1.0, 1.0)), 1, dr)
+    assert n_free == 0
+    dm = build_mesh_dofmap(HexMesh.box((1, 1, 1), (1.0, 1.0, 1.0)), build_basis(1, BasisKind("ModalJacobi")), dr)
+    assert dm.n_free == 0
