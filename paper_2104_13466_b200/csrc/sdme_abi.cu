@@ -180,7 +180,7 @@ int read_scalars(sdme_ctx* ctx) {
 }
 
 int reset_flag(sdme_ctx* ctx) {
-  CK(cudaMemcpyAsync(ctx->d_flag, &kNoFlag, sizeof(kNoFlag), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemsetAsync(ctx->d_flag, 0xFF, sizeof(kNoFlag), ctx->st));  // = kNoFlag; no pageable H2D (implicit stream sync)
   return SDME_OK;
 }
 
@@ -710,7 +710,7 @@ int sdme_vec_reciprocal(sdme_ctx* ctx, int dst, int src) {
   double* a = ctx ? vec(ctx, dst) : nullptr;
   double* b = ctx ? vec(ctx, src) : nullptr;
   if (!a || !b) return SDME_BAD_ARGUMENT;
-  CK(cudaMemcpyAsync(ctx->d_flag, &kNoFlag, sizeof(kNoFlag), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemsetAsync(ctx->d_flag, 0xFF, sizeof(kNoFlag), ctx->st));  // = kNoFlag; no pageable H2D (implicit stream sync)
   k_invert_diag<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(a, b, ctx->d_free, ctx->nvec, ctx->d_flag);
   ++ctx->launches;
   CK(cudaMemcpyAsync(ctx->h_flag, ctx->d_flag, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->st));
@@ -792,7 +792,7 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
   // diagonal, ||b|| = 0, converged / indefinite / maxit) are read back once
   // and reported in the reference's order (solver.py:102-170).
   if ((rc = reset_flag(ctx))) return rc;
-  CK(cudaMemcpyAsync(ctx->d_dflag, &kNoFlag, sizeof(kNoFlag), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemsetAsync(ctx->d_dflag, 0xFF, sizeof(kNoFlag), ctx->st));  // = kNoFlag
   // K(u) is fixed during the solve: store K = F^-T and ln J at the quadrature
   // points once (MODE_SETUP, flags inverted elements) and iterate with MODE_PA
   const bool pa = c_k != 0.0 && ctx->pa && ensure_qpd(ctx);
