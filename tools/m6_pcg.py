@@ -1,3 +1,5 @@
+"""Debug aid: GPU PCG iterations / solution error against the reference golden on the general-mesh
+cases m5, m6 (tests/golden/meshes.npz).  Run from the repo root on a GPU box."""
 import sys; sys.path.insert(0,'tests'); sys.path.insert(0,'.')
 import numpy as np
 from test_gpu_mesh import gpu_case, golden_mesh_cases
