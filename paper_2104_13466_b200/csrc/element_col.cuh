@@ -47,8 +47,17 @@ struct ColLay {
   using C = V3<N, N, 1, 1, VALS>;
   static constexpr int SQ = TM ? N * N * N : C::Ly::sq;    // point slot stride (no cross-slot accesses)
   static constexpr int SX = N * N;                          // x output, k stride
-  static constexpr int SY = C::Ly::sy;                      // y output, k stride
-  static constexpr int SU = N * N;                          // point values, c stride
+  // odd N >= 7 (P = 6, 8): y-stage output and point values in transposed slabs,
+  // Y(k, b, a) = k N^2 + b + a N and U(c, b, a) = c N + b + a N^2 (bank model,
+  // tools/col_layout_n.py: 882 -> 504 / 1344 -> 1218 wavefronts at N = 7,
+  // 1377 -> 972 / 2160 -> 2025 at N = 9; worse for even N)
+  static constexpr bool TY = N >= 7 && (N & 1);
+  static constexpr int SY = TY ? N * N : C::Ly::sy;         // y output, k stride
+  static constexpr int SU = N * N;                          // point values region per c (size)
+  static constexpr int YB = TY ? 1 : N, YA = TY ? N : 1;
+  static constexpr int UC = TY ? N : SU, UB = TY ? 1 : N, UA = TY ? N * N : 1;
+  __device__ static int yo(int k, int b, int a) { return k * SY + b * YB + a * YA; }
+  __device__ static int uo(int c, int b, int a) { return c * UC + b * UB + a * UA; }
   static constexpr int PTS = (VALS ? 12 : 9) * SQ;
   // x-stage output X(k, j, a) = k XK + j XJ + a XA: TM layout (XK, XJ, XA) =
   // (N, 1, N^2 rounded up to 1 mod 16), bank-conflict free for both the x-stage
@@ -164,18 +173,18 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
       eo_split<N, MIR>(v, E, O);
       eo_fwd<N, Mr::NE, Mr::NO>(tb.B, E, O, o);
 #pragma unroll
-      for (int b = 0; b < N; ++b) S[L::Y + k * L::SY + b * N + a] = o[b];
+      for (int b = 0; b < N; ++b) S[L::Y + L::yo(k, b, a)] = o[b];
     }
     group_sync<WPE>(0);
     // z stage: column (b, a) -> values U at c, and d/dz at the points
     for (int w = t; w < N * N; w += 32 * WPE) {
       double v[N], E[NE], O[NO], u[N];
 #pragma unroll
-      for (int k = 0; k < N; ++k) v[k] = S[L::Y + k * L::SY + w];
+      for (int k = 0; k < N; ++k) v[k] = S[L::Y + L::yo(k, w / N, w % N)];
       eo_split<N, MIR>(v, E, O);
       eo_fwd<N, Mr::NE, Mr::NO>(tb.B, E, O, u);
 #pragma unroll
-      for (int c = 0; c < N; ++c) S[L::U + c * L::SU + w] = u[c];
+      for (int c = 0; c < N; ++c) S[L::U + L::uo(c, w / N, w % N)] = u[c];
       if (VAL) {
 #pragma unroll
         for (int c = 0; c < N; ++c) S[L::qi(3, comp, c * N * N + w)] = u[c];
@@ -195,13 +204,13 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
         const int c = w / N, r = w % N;
         double v[N], pe[PE], po[PO], gx[N], gy[N];
 #pragma unroll
-        for (int a = 0; a < N; ++a) v[a] = S[L::U + c * L::SU + r * N + a];
+        for (int a = 0; a < N; ++a) v[a] = S[L::U + L::uo(c, r, a)];
         eo_split<N, 0>(v, pe, po);
         eo_fwd<N, Mp::NO, Mp::NE>(tb.Dx, po, pe, gx);
 #pragma unroll
         for (int a = 0; a < N; ++a) S[L::qi(0, comp, c * N * N + r * N + a)] = gx[a];
 #pragma unroll
-        for (int b = 0; b < N; ++b) v[b] = S[L::U + c * L::SU + b * N + r];
+        for (int b = 0; b < N; ++b) v[b] = S[L::U + L::uo(c, b, r)];
         eo_split<N, 0>(v, pe, po);
         eo_fwd<N, Mp::NO, Mp::NE>(tb.Dy, po, pe, gy);
 #pragma unroll
@@ -235,7 +244,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
         eo_qsplit<N>(q, qe, qo);
         eo_bwd<N, N, 0, -1, Mp::NO, Mp::NE, false>(tb.bDx, qe, qo, y);
 #pragma unroll
-        for (int a = 0; a < N; ++a) S[L::U + c * L::SU + b * N + a] = y[a];
+        for (int a = 0; a < N; ++a) S[L::U + L::uo(c, b, a)] = y[a];
       }
       group_sync<WPE>(0);
       // y' pencils (c, a): U += D^_y^T F_y
@@ -245,12 +254,12 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
 #pragma unroll
         for (int b = 0; b < N; ++b) {
           q[b] = S[L::qi(1, comp, c * N * N + b * N + a)];
-          y[b] = S[L::U + c * L::SU + b * N + a];
+          y[b] = S[L::U + L::uo(c, b, a)];
         }
         eo_qsplit<N>(q, qe, qo);
         eo_bwd<N, N, 0, -1, Mp::NO, Mp::NE, true>(tb.bDy, qe, qo, y);
 #pragma unroll
-        for (int b = 0; b < N; ++b) S[L::U + c * L::SU + b * N + a] = y[b];
+        for (int b = 0; b < N; ++b) S[L::U + L::uo(c, b, a)] = y[b];
       }
       group_sync<WPE>(0);
     }
@@ -258,7 +267,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
     for (int w = t; w < N * N; w += 32 * WPE) {
       double v[N], q[N], qe[HP], qo[H], h[N];
 #pragma unroll
-      for (int c = 0; c < N; ++c) v[c] = grad ? S[L::U + c * L::SU + w] : 0.0;
+      for (int c = 0; c < N; ++c) v[c] = grad ? S[L::U + L::uo(c, w / N, w % N)] : 0.0;
       if (grad) {
 #pragma unroll
         for (int c = 0; c < N; ++c) q[c] = S[L::qi(2, comp, c * N * N + w)];
@@ -272,7 +281,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
       eo_qsplit<N>(v, qe, qo);
       eo_bwd<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.bB, qe, qo, h);
 #pragma unroll
-      for (int k = 0; k < N; ++k) S[L::Y + k * L::SY + w] = h[k];
+      for (int k = 0; k < N; ++k) S[L::Y + L::yo(k, w / N, w % N)] = h[k];
     }
     group_sync<WPE>(0);
     // y' items (k, a): B^T along y
@@ -280,7 +289,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
       const int k = w / N, a = w % N;
       double v[N], qe[HP], qo[H], h[N];
 #pragma unroll
-      for (int b = 0; b < N; ++b) v[b] = S[L::Y + k * L::SY + b * N + a];
+      for (int b = 0; b < N; ++b) v[b] = S[L::Y + L::yo(k, b, a)];
       eo_qsplit<N>(v, qe, qo);
       eo_bwd<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.bB, qe, qo, h);
 #pragma unroll
