@@ -52,12 +52,21 @@ struct ColLay {
   // tools/col_layout_n.py: 882 -> 504 / 1344 -> 1218 wavefronts at N = 7,
   // 1377 -> 972 / 2160 -> 2025 at N = 9; worse for even N)
   static constexpr bool TY = N >= 7 && (N & 1);
-  static constexpr int SY = TY ? N * N : C::Ly::sy;         // y output, k stride
+  // N = 4 with TMA boxes (P = 3, one element per half-warp): 16 lanes touch a
+  // 4x4 slice of a 4x4x4 array with one coordinate fixed; bank (within a
+  // 16-double row, row = slowest index s) (4 m + f) ^ 5 s makes every
+  // axis-aligned slice hit 16 distinct banks (Y, U and the point slots)
+  static constexpr bool SW = TM && N == 4;
+  static constexpr int SY = TY ? N * N : (SW ? 16 : C::Ly::sy);  // y output, k stride
   static constexpr int SU = N * N;                          // point values region per c (size)
   static constexpr int YB = TY ? 1 : N, YA = TY ? N : 1;
   static constexpr int UC = TY ? N : SU, UB = TY ? 1 : N, UA = TY ? N * N : 1;
-  __device__ static int yo(int k, int b, int a) { return k * SY + b * YB + a * YA; }
-  __device__ static int uo(int c, int b, int a) { return c * UC + b * UB + a * UA; }
+  __device__ static int yo(int k, int b, int a) {
+    return SW ? k * 16 + ((b * 4 + a) ^ (5 * k)) : k * SY + b * YB + a * YA;
+  }
+  __device__ static int uo(int c, int b, int a) {
+    return SW ? c * 16 + ((b * 4 + a) ^ (5 * c)) : c * UC + b * UB + a * UA;
+  }
   static constexpr int PTS = (VALS ? 12 : 9) * SQ;
   // x-stage output X(k, j, a) = k XK + j XJ + a XA: TM layout (XK, XJ, XA) =
   // (N, 1, N^2 rounded up to 1 mod 16), bank-conflict free for both the x-stage
@@ -75,7 +84,13 @@ struct ColLay {
   static constexpr int TAB = R + 2 * RB;                    // !TM: int lattice offsets of the box entries
   static constexpr int BAR = O + RB;                        // TM: two mbarriers
   static constexpr int PER = TM ? BAR + 2 : TAB + (N * N * N + 1) / 2;
-  __device__ static int qi(int d, int comp, int q) { return (d * 3 + comp) * SQ + q; }
+  __device__ static int qi(int d, int comp, int q) { return (d * 3 + comp) * SQ + (SW ? q ^ (5 * (q >> 4)) : q); }
+};
+
+// per-element shared region rounded to 128 B (the SUB = 2 half-warp regions)
+template <int N, bool VALS, bool TM = false>
+struct ColPer {
+  static constexpr int PERP = (ColLay<N, VALS, TM>::PER + 15) / 16 * 16;
 };
 
 // what to stage after the last component of a forward pass (TMA path)
@@ -92,7 +107,7 @@ __device__ __forceinline__ void col_stage(const Geo& g, const double* __restrict
   cp_async_commit();
 }
 
-template <int N, int WPE, int MIR, bool VAL, bool VALS, bool TM = false>
+template <int N, int WPE, int MIR, bool VAL, bool VALS, bool TM = false, int SUB = 1>
 __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g, const double* __restrict__ src,
                                             int X0, int Y0, int Z0, double* S, int t, int* buf, NextRows next,
                                             bool grad, const CUtensorMap* smap = nullptr, NextBox nbox = {},
@@ -125,10 +140,10 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
     } else {
       double* nb = R + (*buf ^ 1) * N * N * N;
       if (comp + 1 < 3) {
-        col_stage<N, 32 * WPE>(g, src, comp + 1, X0, Y0, Z0, nb, t, tab);
+        col_stage<N, 32 * WPE / SUB>(g, src, comp + 1, X0, Y0, Z0, nb, t, tab);
         cp_async_wait<1>();
       } else if (next.field) {
-        col_stage<N, 32 * WPE>(g, next.field, 0, next.X0, next.Y0, next.Z0, nb, t, tab);
+        col_stage<N, 32 * WPE / SUB>(g, next.field, 0, next.X0, next.Y0, next.Z0, nb, t, tab);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
@@ -136,7 +151,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
       group_sync<WPE>(0);
     }
     // x stage: item (k, j) -> values at a
-    for (int w = t; w < N * N; w += 32 * WPE) {
+    for (int w = t; w < N * N; w += 32 * WPE / SUB) {
       double v[N], E[NE], O[NO], o[N];
       if (TM && (N & 1)) {
         // even P: boxes start at the element; 16-byte loads of the pitched
@@ -165,7 +180,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
     }
     group_sync<WPE>(0);
     // y stage: item (k, a) -> values at b
-    for (int w = t; w < N * N; w += 32 * WPE) {
+    for (int w = t; w < N * N; w += 32 * WPE / SUB) {
       const int k = w / N, a = w % N;
       double v[N], E[NE], O[NO], o[N];
 #pragma unroll
@@ -177,7 +192,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
     }
     group_sync<WPE>(0);
     // z stage: column (b, a) -> values U at c, and d/dz at the points
-    for (int w = t; w < N * N; w += 32 * WPE) {
+    for (int w = t; w < N * N; w += 32 * WPE / SUB) {
       double v[N], E[NE], O[NO], u[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) v[k] = S[L::Y + L::yo(k, w / N, w % N)];
@@ -200,7 +215,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
     group_sync<WPE>(0);
     if (grad) {
       // x pencils (c, b) and y pencils (c, a) of the point values
-      for (int w = t; w < N * N; w += 32 * WPE) {
+      for (int w = t; w < N * N; w += 32 * WPE / SUB) {
         const int c = w / N, r = w % N;
         double v[N], pe[PE], po[PO], gx[N], gy[N];
 #pragma unroll
@@ -224,7 +239,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
 
 // backward: per component, the weighted flux slots 0..2 (and the weighted
 // value slot 3 when VAL) -> y += B^T (x) B^T (x) B^T (sum_d D^_d^T F_d [+ V])
-template <int N, int WPE, int MIR, bool VAL, bool VALS, bool TM = false>
+template <int N, int WPE, int MIR, bool VAL, bool VALS, bool TM = false, int SUB = 1>
 __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& g, double* __restrict__ dst, int X0,
                                              int Y0, int Z0, double* S, int t, double* evb, bool grad,
                                              const CUtensorMap* ymap = nullptr) {
@@ -236,7 +251,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
   for (int comp = 0; comp < 3; ++comp) {
     if (grad) {
       // x' pencils (c, b): U = D^_x^T F_x
-      for (int w = t; w < N * N; w += 32 * WPE) {
+      for (int w = t; w < N * N; w += 32 * WPE / SUB) {
         const int c = w / N, b = w % N;
         double q[N], qe[HP], qo[H], y[N];
 #pragma unroll
@@ -248,7 +263,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
       }
       group_sync<WPE>(0);
       // y' pencils (c, a): U += D^_y^T F_y
-      for (int w = t; w < N * N; w += 32 * WPE) {
+      for (int w = t; w < N * N; w += 32 * WPE / SUB) {
         const int c = w / N, a = w % N;
         double q[N], qe[HP], qo[H], y[N];
 #pragma unroll
@@ -264,7 +279,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
       group_sync<WPE>(0);
     }
     // z' columns (b, a): V = U + D^_z^T F_z (+ value term), then B^T along z
-    for (int w = t; w < N * N; w += 32 * WPE) {
+    for (int w = t; w < N * N; w += 32 * WPE / SUB) {
       double v[N], q[N], qe[HP], qo[H], h[N];
 #pragma unroll
       for (int c = 0; c < N; ++c) v[c] = grad ? S[L::U + L::uo(c, w / N, w % N)] : 0.0;
@@ -285,7 +300,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
     }
     group_sync<WPE>(0);
     // y' items (k, a): B^T along y
-    for (int w = t; w < N * N; w += 32 * WPE) {
+    for (int w = t; w < N * N; w += 32 * WPE / SUB) {
       const int k = w / N, a = w % N;
       double v[N], qe[HP], qo[H], h[N];
 #pragma unroll
@@ -302,7 +317,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
       if (t == 0) bulk_wait_read();
       group_sync<WPE>(0);
     }
-    for (int w = t; w < N * N; w += 32 * WPE) {
+    for (int w = t; w < N * N; w += 32 * WPE / SUB) {
       const int k = w / N, j = w % N;
       double v[N], qe[HP], qo[H], acc[N];
 #pragma unroll
@@ -350,7 +365,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
     }
     if (TM) fence_proxy_async_smem();
     group_sync<WPE>(0);
-    if (TM && t == 0) tma_reduce_add_box(ymap, S + L::O, X0 & ~1, Y0, Z0, comp);
+    if (TM && t == 0 && ymap) tma_reduce_add_box(ymap, S + L::O, X0 & ~1, Y0, Z0, comp);
   }
 }
 
@@ -381,23 +396,29 @@ __device__ __forceinline__ void gen_to_phys(double* H, const double J[3][3]) {
   }
 }
 
-template <int N, int WPE, int MINB, int MODE, bool VAL, int MIR, bool TM = false, bool GEN = false>
+// SUB = 2 (TMA boxes, small N): two elements per warp, one per half-warp,
+// each with its own shared region and barriers; the halves run the same
+// number of iterations (a half past the end of the colour repeats the last
+// element without scattering it) so the warp-wide syncs stay uniform
+template <int N, int WPE, int MINB, int MODE, bool VAL, int MIR, bool TM = false, bool GEN = false, int SUB = 1>
 __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_constant__ TabC<N, MIR> tb,
                                                         const __grid_constant__ Geo g, OpArgs args) {
+  static_assert(SUB == 1 || (SUB == 2 && WPE == 1 && TM && !GEN), "half-warp elements: TMA path only");
   constexpr bool VALS = VAL;
   using L = ColLay<N, VALS, TM>;
-  constexpr int T = 32 * WPE;
+  constexpr int T = 32 * WPE / SUB;
   constexpr int Q = N * N * N, QPT = (Q + T - 1) / T;
   extern __shared__ __align__(128) double smem[];
-  double* S = smem;
-  const int t = threadIdx.x;
+  const int t = threadIdx.x % T;
+  double* S = smem + (threadIdx.x / T) * ColPer<N, VALS, TM>::PERP;
+  const long long half = threadIdx.x / T;
   int buf = 0;
   if (args.skip && *(volatile const int*)args.skip) return;
   constexpr bool UPASS = (MODE == MODE_APPLY || MODE == MODE_FINT || MODE == MODE_SETUP);
   constexpr bool PPASS = (MODE == MODE_APPLY || MODE == MODE_PA || MODE == MODE_MASS);
   constexpr bool PGRAD = MODE != MODE_MASS;  // c_m M p alone: values only (B stages), no gradient
   const long long cnt = colour_count(g, args.colour);
-  const long long stride = gridDim.x;
+  const long long stride = (long long)gridDim.x * SUB;
   const double mu_k = args.c_k * g.mu, lam_k = args.c_k * g.lam;
   const double cmr = args.c_m * g.rho;
   const double* first_field = UPASS ? args.u : args.p;
@@ -420,9 +441,10 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
   group_sync<WPE>(0);
   if (GEN && (long long)blockIdx.x < cnt) {
     col_stage<N, 32 * WPE>(g, first_field + (long long)blockIdx.x * 3 * Q, 0, 0, 0, 0, S + L::R, t, tab);
-  } else if ((long long)blockIdx.x < cnt) {
+  } else if ((long long)blockIdx.x * SUB < cnt) {
     int ei, ej, ek;
-    colour_element(g, args.colour, blockIdx.x, ei, ej, ek);
+    colour_element(g, args.colour, SUB == 1 ? (long long)blockIdx.x : min((long long)blockIdx.x * SUB + half, cnt - 1),
+                   ei, ej, ek);
     if (TM) {
       if (t == 0) {
         unsigned long long* bars = reinterpret_cast<unsigned long long*>(S + L::BAR);
@@ -433,7 +455,9 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
       col_stage<N, 32 * WPE>(g, first_field, 0, (N - 1) * ei, (N - 1) * ej, (N - 1) * ek, S + L::R, t, tab);
     }
   }
-  for (long long idx = blockIdx.x; idx < cnt; idx += stride) {
+  for (long long base = (long long)blockIdx.x * SUB; base < cnt; base += stride) {
+    const long long idx = SUB == 1 ? base : min(base + half, cnt - 1);
+    const bool ghost = SUB > 1 && base + half >= cnt;  // repeats idx, scatters nothing
     int X0 = 0, Y0 = 0, Z0 = 0;
     long long eid = idx, eoff = 0;  // GEN: E-vector box offset of this element
     if (GEN) {
@@ -446,12 +470,12 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
     }
     NextRows nxt{nullptr, 0, 0, 0};
     NextBox nxb{nullptr, 0, 0, 0};
-    if (idx + stride < cnt) {
+    if (base + stride < cnt) {
       if (GEN) {
         nxt = NextRows{first_field + (idx + stride) * 3 * Q, 0, 0, 0};
       } else {
         int ni, nj, nk;
-        colour_element(g, args.colour, idx + stride, ni, nj, nk);
+        colour_element(g, args.colour, SUB == 1 ? idx + stride : min(base + stride + half, cnt - 1), ni, nj, nk);
         if (TM) nxb = NextBox{first_map, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
         else nxt = NextRows{first_field, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
       }
@@ -460,7 +484,7 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
     if (UPASS) {
       const NextRows after_u = MODE == MODE_APPLY ? NextRows{args.p + eoff, X0, Y0, Z0} : nxt;
       const NextBox after_ub = MODE == MODE_APPLY ? NextBox{pmap, X0, Y0, Z0} : nxb;
-      col_forward<N, WPE, MIR, false, VALS, TM>(tb, g, args.u + eoff, X0, Y0, Z0, S, t, &buf, after_u, true, umap,
+      col_forward<N, WPE, MIR, false, VALS, TM, SUB>(tb, g, args.u + eoff, X0, Y0, Z0, S, t, &buf, after_u, true, umap,
                                                 after_ub, &ph);
 #pragma unroll
       for (int r = 0; r < QPT; ++r) {
@@ -480,7 +504,7 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
       group_sync<WPE>(0);
     }
     if (PPASS)
-      col_forward<N, WPE, MIR, VAL, VALS, TM>(tb, g, args.p + eoff, X0, Y0, Z0, S, t, &buf, nxt, PGRAD, pmap, nxb,
+      col_forward<N, WPE, MIR, VAL, VALS, TM, SUB>(tb, g, args.p + eoff, X0, Y0, Z0, S, t, &buf, nxt, PGRAD, pmap, nxb,
                                               &ph);
 #pragma unroll
     for (int r = 0; r < QPT; ++r) {
@@ -590,8 +614,8 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
     group_sync<WPE>(0);
     if (MODE == MODE_SETUP) continue;
     double* evb = args.ev ? args.ev + eid * 3 * Q : nullptr;
-    col_backward<N, WPE, MIR, VAL, VALS, TM>(tb, g, args.y, X0, Y0, Z0, S, t, evb, PGRAD,
-                                             static_cast<const CUtensorMap*>(args.ty));
+    col_backward<N, WPE, MIR, VAL, VALS, TM, SUB>(tb, g, args.y, X0, Y0, Z0, S, t, evb, PGRAD,
+                                                  ghost ? nullptr : static_cast<const CUtensorMap*>(args.ty));
   }
   // the reduce-adds have completed before the CTA (and its shared memory) retires
   if (TM && t == 0) bulk_wait_all();

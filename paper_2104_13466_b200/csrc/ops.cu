@@ -335,6 +335,13 @@ void apply_v5(sdme_ctx* c, const TabEO<N, M, MIR>& tb, OpArgs a) {
 template <int N, int MIR>
 void col_modes(sdme_ctx* c, int mode, OpArgs a);
 
+// every vector of the mode has a TMA tensor map (launch_col's box path)
+inline bool col_tma_ok(const sdme_ctx* c, int mode, const OpArgs& a) {
+  if (c->variant == 11) return false;
+  if (mode == MODE_SETUP) return a.tu != nullptr;
+  return a.ty && (mode == MODE_PA || mode == MODE_MASS || a.tu) && (mode == MODE_FINT || a.tp);
+}
+
 template <int N, int M>
 void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, double* y, double ck, double cm) {
   const Tab3<N, M> tb = make_tab3<N, M>(c);
@@ -388,6 +395,16 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
     return;
   } else {
     // small P: all three components per stage (more pencils per warp), even-odd
+    if constexpr (N == M && N == 4) {
+      // P = 3: collocated, one element per half-warp, TMA boxes (swizzled
+      // layout, ColLay::SW): 2.42 -> 1.98 ms per K.p (profiles/variants_r01.txt)
+      if ((mode == MODE_FINT || mode == MODE_APPLY || mode == MODE_PA || mode == MODE_SETUP || mode == MODE_MASS) &&
+          c->variant != 10 && c->mir >= 0 && !c->ev_mode && col_tma_ok(c, mode, a)) {
+        if (c->mir == 0) col_modes<N, 0>(c, mode, a);
+        else col_modes<N, 1>(c, mode, a);
+        return;
+      }
+    }
     element_eo_or_plain<N, M, typename DefaultShape<N, M>::type>(c, mode, tb, a);
   }
 }
@@ -465,8 +482,10 @@ template <int N, int MODE, bool VAL, int MIR, bool TM>
 void launch_col_k(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
   constexpr int WPE = LargeShape<N, N>::WPE;  // one round per stage
   constexpr int T = 32 * WPE;
-  constexpr int smem = ColLay<N, VAL, TM>::PER * 8;
-  auto kern = element_col<N, WPE, (WPE == 1 ? SDME_COL_MINB : 1), MODE, VAL, MIR, TM>;
+  // N * N <= 16 pencils per stage: two elements per warp (TMA path)
+  constexpr int SUB = (TM && WPE == 1 && N * N <= 16) ? 2 : 1;
+  constexpr int smem = SUB * ColPer<N, VAL, TM>::PERP * 8;
+  auto kern = element_col<N, WPE, (WPE == 1 ? SDME_COL_MINB : 1), MODE, VAL, MIR, TM, false, SUB>;
   static int max_blocks = -1;
   if (max_blocks < 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -480,7 +499,8 @@ void launch_col_k(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
     // setup: no scatter, one pass over all elements; E-vector mode: boxes + gather
     a.colour = -1;
     if (MODE != MODE_SETUP) a.ev = c->d_ev;
-    kern<<<(unsigned)std::min<long long>(colour_count(c->geo, -1), max_blocks), T, smem, c->st>>>(tb, c->geo, a);
+    kern<<<(unsigned)std::min<long long>((colour_count(c->geo, -1) + SUB - 1) / SUB, max_blocks), T, smem, c->st>>>(
+        tb, c->geo, a);
     if (MODE == MODE_SETUP || c->ev_no_gather) ++c->launches;
     else ev_gather<N>(c, a);
     return;
@@ -491,7 +511,7 @@ void launch_col_k(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
     const long long cnt = colour_count(c->geo, col);
     if (cnt == 0) continue;
     a.colour = col;
-    kern<<<(unsigned)std::min<long long>(cnt, max_blocks), T, smem, c->st>>>(tb, c->geo, a);
+    kern<<<(unsigned)std::min<long long>((cnt + SUB - 1) / SUB, max_blocks), T, smem, c->st>>>(tb, c->geo, a);
     ++c->launches;
   }
 }
