@@ -85,3 +85,41 @@ def test_library_is_sm100a():
 
     out = subprocess.run(["cuobjdump", "--list-elf", native.LIB_PATH], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
+
+
+def test_p3_swizzled_layout_is_conflict_free():
+    """ColLay::SW (csrc/element_col.cuh, P = 3 with one element per half-warp):
+    address 16 s + ((4 m + f) ^ 5 s) of a 4x4x4 array (s slowest).  It is a
+    bijection, and every pencil access -- 16 lanes over a slice with one
+    coordinate fixed -- is one wavefront in the half-warp 64-bit bank model
+    (tools/bank_model.py); the natural layout 16 s + 4 m + f is not."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from bank_model import wavefronts
+
+    def sw(s, m, f):
+        return 16 * s + ((4 * m + f) ^ (5 * s))
+
+    def natural(s, m, f):
+        return 16 * s + 4 * m + f
+
+    R = range(4)
+    assert sorted(sw(s, m, f) for s in R for m in R for f in R) == list(range(64))
+    # the point slots: qi applies q ^ 5 (q >> 4) to q = 16 s + 4 m + f
+    assert all(sw(s, m, f) == (lambda q: q ^ (5 * (q >> 4)))(16 * s + 4 * m + f) for s in R for m in R for f in R)
+
+    def worst(lay):
+        w = 0
+        for fixed in range(3):
+            for v in R:
+                addrs = []
+                for x in R:
+                    for y in R:
+                        idx = [x, y]
+                        idx.insert(fixed, v)
+                        addrs.append(lay(*idx))
+                w = max(w, wavefronts(addrs))
+        return w
+
+    assert worst(sw) == 1
+    assert worst(natural) > 1
