@@ -47,7 +47,7 @@ struct Lay {
   template <> struct Lay<NN, MM, NCC> { static constexpr int xo = XO, yo = YO, sx = SX, sy = SY, sq = SQ; };
 SDME_LAY(2, 2, 3, 0, 0, 5, 6, 20)
 SDME_LAY(2, 3, 3, 0, 0, 6, 9, 41)
-SDME_LAY(3, 3, 3, 0, 1, 9, 19, 41)
+SDME_LAY(3, 3, 3, 0, 1, 9, 9, 41)
 SDME_LAY(3, 4, 3, 0, 1, 25, 19, 64)
 SDME_LAY(4, 4, 3, 0, 0, 19, 20, 64)
 SDME_LAY(4, 5, 3, 0, 2, 20, 28, 137)
@@ -63,6 +63,17 @@ SDME_LAY(9, 9, 3, 1, 0, 89, 89, 737)
 SDME_LAY(9, 10, 3, 0, 2, 105, 105, 1012)
 SDME_LAY(5, 5, 1, 0, 0, 25, 37, 137)
 #undef SDME_LAY
+// stride of one (comp, s) slab of the Y layout when it is not N * sy: P = 2
+// (y-stage writes over lanes (comp, k, a), z-stage reads over lanes (comp, b, a);
+// bank model 63 -> 45 wavefronts per field pass, 36 ideal)
+template <int N, int M, int NC>
+struct LayYS {
+  static constexpr int v = N * Lay<N, M, NC>::sy;
+};
+template <>
+struct LayYS<3, 3, 3> {
+  static constexpr int v = 41;
+};
 
 template <int N, int M, int WPE, int NC, bool VALS = true>
 struct V3 {
@@ -70,7 +81,7 @@ struct V3 {
   static constexpr int Q = M * M * M;
   static constexpr int XS = NC * N * Ly::sx;     // one X-layout array ([comp][k] rows of sx)
   static constexpr int XO = 2 * XS;
-  static constexpr int YS = N * Ly::sy;          // one (comp, s) slab of the Y layout
+  static constexpr int YS = LayYS<N, M, NC>::v;  // one (comp, s) slab of the Y layout
   static constexpr int YO = 3 * NC * YS;
   static constexpr int GO = (VALS ? 12 : 9) * Ly::sq;  // point slots [d][comp] of sq
   // NC = 3: the x-stage scratch reuses A (free before the points are written);
