@@ -45,6 +45,13 @@ __device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo
         const double* row = R + *buf * N * N * N + (k * N + j) * N;
 #pragma unroll
         for (int i = 0; i < N; ++i) v[i] = row[i];
+      } else if (bx.in && N == 3 && BoxW<N>::BW == 4) {
+        // P = 2 (shift 0): 32-byte box rows, one 16-byte and one 8-byte load
+        const double* row = bx.in + comp * BoxW<N>::CB + (k * N + j) * 4;
+        const double2 d = *reinterpret_cast<const double2*>(row);
+        v[0] = d.x;
+        v[1 % N] = d.y;
+        v[2 % N] = row[2];
       } else if (bx.in) {
         const double* row = bx.in + comp * BoxW<N>::CB + (k * N + j) * BoxW<N>::BW + bx.shift;
 #pragma unroll
@@ -256,6 +263,15 @@ __device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Ge
         // output box row: the element's N values at `shift`, zeros elsewhere
         // (slots outside the element belong to elements of other colours)
         double* orow = bx.out + comp * BoxW<N>::CB + (k * N + j) * BW;
+        if constexpr (N == 3 && BW == 4) {
+          // P = 2 (shift 0): the row as two 16-byte stores, pad slot 0
+          double o[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) o[i] = (chk && constrained(g, comp, X0 + i, Y, Z)) ? 0.0 : acc[i];
+          reinterpret_cast<double2*>(orow)[0] = make_double2(o[0], o[1]);
+          reinterpret_cast<double2*>(orow)[1] = make_double2(o[2], 0.0);
+          continue;
+        }
 #pragma unroll
         for (int i = 0; i < N; ++i) orow[bx.shift + i] = (chk && constrained(g, comp, X0 + i, Y, Z)) ? 0.0 : acc[i];
         if (BW - N == 1) {
