@@ -155,7 +155,7 @@ class DofMap:
 class Tables:
     """Per-element quadrature tables (femcore.py:62-81, tensorelem.py:156-182)."""
 
-    def __init__(self, mesh: Mesh, basis: Basis, m: int):
+    def __init__(self, mesh: Mesh, basis: Basis, m: int, share_geometry: bool = False):
         xq, wq = gauss(m)
         v, d = basis.eval(xq)  # (n, m)
         n = basis.P + 1
@@ -166,10 +166,22 @@ class Tables:
              for ax, _ in enumerate(range(3))]
         self.dref = np.stack([gi.reshape(m ** 3, n ** 3) for gi in g], axis=-1)
         self.per_elem = []
+        shared = {}
         for e in range(mesh.ne):
             x, jac, det = mesh.geometry(e, self.pts_ref)
-            grad = np.einsum("qfd,qdc->qfc", self.dref, np.linalg.inv(jac))
-            self.per_elem.append((x, grad, self.w * det))
+            key = None
+            if share_geometry:
+                # large uniform box meshes (test-size memory): elements whose
+                # Jacobians agree to 1e-13 reuse one (grad, w det J) pair
+                key = np.round(jac / np.abs(jac).max(), 13).tobytes() + np.round(det / np.abs(det).max(), 13).tobytes()
+            if key is not None and key in shared:
+                grad, wdet = shared[key]
+            else:
+                grad = np.einsum("qfd,qdc->qfc", self.dref, np.linalg.inv(jac))
+                wdet = self.w * det
+                if key is not None:
+                    shared[key] = (grad, wdet)
+            self.per_elem.append((x, grad, wdet))
 
 
 class Material:
@@ -255,11 +267,11 @@ def elem_mass(mat, vals, wdet):
 class Problem:
     """FemProblem (femcore.py:273-431) on a box mesh."""
 
-    def __init__(self, mesh, basis, mat, m=None, dirichlet=None):
+    def __init__(self, mesh, basis, mat, m=None, dirichlet=None, share_geometry=False):
         self.mesh, self.basis, self.mat = mesh, basis, mat
         self.m = basis.P + 1 if m is None else m  # femcore.py:283-292
         self.dmap = DofMap(mesh, basis.P, dirichlet)
-        self.tab = Tables(mesh, basis, self.m)
+        self.tab = Tables(mesh, basis, self.m, share_geometry)
         self.n_free = self.dmap.n_free
         self._edofs = [self.dmap.evdofs(e) for e in range(mesh.ne)]
 
@@ -323,6 +335,16 @@ class Problem:
 
     def mass(self):
         return self.assemble(None, c_k=0.0, c_m=1.0)
+
+    def lumped_mass(self):
+        """Row sums of the assembled mass over free columns,
+        ``mass().sum(axis=1)``, accumulated element by element
+        (M_e applied to the element's free-DOF mask) without forming the CSR."""
+        out = np.zeros(self.n_free)
+        for e in range(self.mesh.ne):
+            me = elem_mass(self.mat, self.tab.vals, self.tab.per_elem[e][2])
+            self.scatter(out, e, me @ (self._edofs[e] >= 0).astype(float))
+        return out
 
     # ---------------------------------------------------------- faces (femcore.py:215-259)
     def face_tables(self, tag, q):

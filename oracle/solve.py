@@ -135,7 +135,7 @@ def explicit_lumped(problem, load, dt, n_steps, u0=None, v0=None, contact=None):
     n = problem.n_free
     u = np.zeros(n) if u0 is None else np.array(u0, float)
     v = np.zeros(n) if v0 is None else np.array(v0, float)
-    ml = np.asarray(problem.mass().sum(axis=1)).ravel()
+    ml = problem.lumped_mass()
 
     def psi_of(t, uu):
         p = load(t) - problem.internal_force(uu)

@@ -26,6 +26,9 @@ struct SdmeOps {
   // small-mesh PCG iteration tail after an E-vector element launch (pcg_small.cuh)
   void (*pcg_small)(sdme_ctx*, double* x, double* r, double* p, double* ap, const double* dinv,
                     cudaGraphConditionalHandle cond, int has_cond);
+  // 1 if the 16-CTA cluster of pcg_small can be placed on the current device
+  // (cudaOccupancyMaxActiveClusters > 0; 0 e.g. under MIG / MPS partitions)
+  int (*pcg_small_fits)(sdme_ctx*);
 };
 
 struct sdme_ctx {
@@ -69,7 +72,9 @@ struct sdme_ctx {
   // boxes to d_ev, then a deterministic gather -- instead of 8 colour passes
   bool ev_mode = false;
   bool ev_no_gather = false;
-  int pcg_warm = 0;  // operator kinds whose launch setup ran (sdme_pcg)
+  int pcg_warm = 0;
+  int small_fits = -1;  // pcg_small cluster placement on this device (-1: not queried yet)
+  cudaError_t launch_err = cudaSuccess;  // a failed cudaLaunchKernelEx, reported by check_launch  // operator kinds whose launch setup ran (sdme_pcg)
   // instantiated PCG graph, reused while the solve's operands are the same
   cudaGraph_t pcg_graph = nullptr;
   cudaGraphExec_t pcg_exec = nullptr;
@@ -80,9 +85,10 @@ struct sdme_ctx {
     bool pa = false;
     bool contact = false;
     double eps = 0.0;
+    unsigned long long cgen = 0;  // contact generation (face tables, plane, gaps buffer) captured
     bool operator==(const PcgKey& o) const {
       return u == o.u && x == o.x && ck == o.ck && cm == o.cm && pa == o.pa && contact == o.contact &&
-             eps == o.eps;
+             eps == o.eps && cgen == o.cgen;
     }
   } pcg_key;
   long long pcg_per_iter = 0;
@@ -92,6 +98,9 @@ struct sdme_ctx {
   sdme::FaceTab c_ft{};
   sdme::ContactArgs c_ca{};
   bool c_ready = false;
+  // bumped whenever c_ft / c_ca (other than the per-call u / fc pointers) or
+  // d_gaps change, so a cached PCG graph never replays a stale contact node
+  unsigned long long c_gen = 0;
   bool pcg_contact = false;  // sdme_pcg adds K_c (and its diagonal)  // element launch leaves A p in d_ev (small PCG path gathers)
   double* d_ev = nullptr;
   // stored quadrature data of the PCG linearisation point (MODE_SETUP / MODE_PA)

@@ -15,7 +15,6 @@
 #include "element_gen.cuh"
 #include "element_kernels.cuh"
 #include "element_v3.cuh"
-#include "element_v5.cuh"
 #include "pcg_small.cuh"
 
 #ifndef SDME_COL_MINB
@@ -30,10 +29,6 @@
 #define SDME_GEN_MINB 1  // resident blocks per SM asked of the general-mesh P = 4 kernels
 #endif
 
-#ifndef SDME_V5_MINB
-#define SDME_V5_MINB 8
-#endif
-
 #ifndef SDME_ORDER
 #error "compile with -DSDME_ORDER=P"
 #endif
@@ -42,6 +37,40 @@ using namespace sdme;
 using Ops = SdmeOps;
 
 namespace {
+
+constexpr int kMaxDevices = 64;
+
+// One cached value per CUDA device: kernel attributes (dynamic shared memory
+// opt-in) and occupancy are per device, so they are set / queried for the
+// device current at the launch, never assumed to be device 0.
+struct PerDevice {
+  int v[kMaxDevices];
+  PerDevice() {
+    for (int& x : v) x = -1;
+  }
+};
+
+inline int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return (dev >= 0 && dev < kMaxDevices) ? dev : 0;
+}
+
+// resident CTAs of ``kern`` over the whole current device (persistent grid cap)
+template <class K>
+int resident_grid(PerDevice& cache, K kern, int threads, int smem) {
+  const int dev = current_device();
+  int& mb = cache.v[dev];
+  if (mb < 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    mb = std::max(1, nb) * sms;
+  }
+  return mb;
+}
 
 // v3 tables: weights, det J and dxi/dX folded per axis (element_v3.cuh)
 template <int N, int M>
@@ -102,15 +131,8 @@ void launch_v3_k(sdme_ctx* c, const TB& tb, OpArgs a) {
   constexpr int smem = V3Smem<N, M, S::WPE, S::NC, VALS, S::STG, TMB>::PERS * 8 * S::EPB;
   constexpr int MINB = TMB && S::MINB > SDME_TMB_MINB ? SDME_TMB_MINB : S::MINB;  // TMA boxes: register cap (see DESIGN)
   auto kern = element_v3<N, M, S::WPE, S::NC, S::EPB, MINB, MODE, VAL, S::STG, TB, TMB>;
-  static int max_blocks = -1;
-  if (max_blocks < 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, S::EPB * S::WPE * 32, smem);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    max_blocks = std::max(1, nb) * sms;
-  }
+  static PerDevice grid_cache;  // per device: attribute + occupancy set once
+  const int max_blocks = resident_grid(grid_cache, kern, S::EPB * S::WPE * 32, smem);
   if (MODE == MODE_SETUP || MODE == MODE_ENERGY) {
     // no scatter: one pass over all elements
     a.colour = -1;
@@ -291,47 +313,6 @@ void element_eo_or_plain(sdme_ctx* c, int mode, const Tab3<N, M>& tb, OpArgs a) 
     element_shape<N, M, S>(c, mode, tb, a);
 }
 
-// v5 (element_v5.cuh): K.p with the p-side z stage, point work and z'
-// stage fused per quadrature column in registers
-template <int N, int M, int MINB, bool VAL, int MIR>
-void launch_v5(sdme_ctx* c, const TabEO<N, M, MIR>& tb, OpArgs a) {
-  using C = V3<N, M, 1, 1, false>;
-  constexpr int smem = (C::PER + 2 * N * N * N) * 8;
-  auto kern = element_v5<N, M, MINB, VAL, MIR>;
-  static int max_blocks = -1;
-  if (max_blocks < 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    max_blocks = std::max(1, nb) * sms;
-  }
-  if (c->ev_mode) {
-    a.colour = -1;
-    a.ev = c->d_ev;
-    kern<<<(unsigned)std::min<long long>(colour_count(c->geo, -1), max_blocks), 32, smem, c->st>>>(tb, c->geo, a);
-    if (c->ev_no_gather) ++c->launches;
-    else ev_gather<N>(c, a);
-    return;
-  }
-  for (int sp = 0; sp < 8 * c->nslab; ++sp) {
-    const int col = colour_code(c->geo, sp % 8, sp / 8, c->nslab);
-    if (col == -2) continue;
-    const long long cnt = colour_count(c->geo, col);
-    if (cnt == 0) continue;
-    a.colour = col;
-    kern<<<(unsigned)std::min<long long>(cnt, max_blocks), 32, smem, c->st>>>(tb, c->geo, a);
-    ++c->launches;
-  }
-}
-
-template <int N, int M, int MIR>
-void apply_v5(sdme_ctx* c, const TabEO<N, M, MIR>& tb, OpArgs a) {
-  if (a.c_m != 0.0) launch_v5<N, M, SDME_V5_MINB, true, MIR>(c, tb, a);
-  else launch_v5<N, M, SDME_V5_MINB, false, MIR>(c, tb, a);
-}
-
 template <int N, int MIR>
 void col_modes(sdme_ctx* c, int mode, OpArgs a);
 
@@ -361,16 +342,9 @@ void element_impl(sdme_ctx* c, int mode, const double* u, const double* p, doubl
   if constexpr (N == 5 && M == 5) {
     // P = 4, m = 5 (BASELINE config 2); schedule history in profiles/variants_r01.txt
     // (the 3-component, 12-warp and unstaged shapes measured there are template
-    // arguments of this same kernel).  SDME_VARIANT=8: column-fused v5, slower,
-    // opt-in only (the column-resident v4 of that history was removed).
+    // arguments of this same kernel; the rejected column-resident v4 and
+    // column-fused v5 were removed).
     using SK = Shape<N, M, 1, 1, 1, 11, true>;
-    if (mode == MODE_APPLY && c->variant == 8 && c->mir >= 0) {
-      // column-fused v5 (element_v5.cuh): 255 registers, 8 warps/SM; measured
-      // 2.87 ms vs 2.50 ms for the default below (profiles/variants_r01.txt)
-      if (c->mir == 0) apply_v5<N, M, 0>(c, make_tabeo<N, M, 0>(c), a);
-      else apply_v5<N, M, 1>(c, make_tabeo<N, M, 1>(c), a);
-      return;
-    }
     // f_int and K.p: collocated sum factorisation (element_col.cuh) unless
     // SDME_VARIANT=10; other modes and non-mirrored tables: component-serial,
     // cp.async-staged rows, even-odd contractions, 11 warps/SM
@@ -486,15 +460,8 @@ void launch_col_k(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
   constexpr int SUB = (TM && WPE == 1 && N * N <= 16) ? 2 : 1;
   constexpr int smem = SUB * ColPer<N, VAL, TM>::PERP * 8;
   auto kern = element_col<N, WPE, (WPE == 1 ? SDME_COL_MINB : 1), MODE, VAL, MIR, TM, false, SUB>;
-  static int max_blocks = -1;
-  if (max_blocks < 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T, smem);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    max_blocks = std::max(1, nb) * sms;
-  }
+  static PerDevice grid_cache;  // per device: attribute + occupancy set once
+  const int max_blocks = resident_grid(grid_cache, kern, T, smem);
   if (MODE == MODE_SETUP || c->ev_mode) {
     // setup: no scatter, one pass over all elements; E-vector mode: boxes + gather
     a.colour = -1;
@@ -555,15 +522,8 @@ void diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm) {
   constexpr int WPE = LargeShape<N, M>::WPE;  // one round per stage
   constexpr int smem = DiagLay<N, M, WPE>::PER * 8;
   auto kern = element_diag3<N, M, WPE, 1, 1>;
-  static int max_blocks = -1;
-  if (max_blocks < 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, WPE * 32, smem);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    max_blocks = std::max(1, nb) * sms;
-  }
+  static PerDevice grid_cache;  // per device: attribute + occupancy set once
+  const int max_blocks = resident_grid(grid_cache, kern, WPE * 32, smem);
   const Tab3<N, M> tb = make_tab3<N, M>(c);
   const TabD<N, M> td = make_tabd<N, M>(c);
   OpArgs a{u, nullptr, d, ck, cm, 0, c->d_flag};
@@ -587,26 +547,52 @@ void diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm) {
 }
 
 template <int N>
-void pcg_small_impl(sdme_ctx* c, double* x, double* r, double* p, double* ap, const double* dinv,
-                    cudaGraphConditionalHandle cond, int has_cond) {
-  static bool attr = false;
-  if (!attr) {
+void pcg_small_attr() {
+  static PerDevice done;
+  int& d = done.v[current_device()];
+  if (d < 0) {
     cudaFuncSetAttribute(k_pcg_small<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr = true;
+    d = 1;
   }
+}
+
+template <int N>
+cudaLaunchConfig_t pcg_small_config(sdme_ctx* c, cudaLaunchAttribute* at) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kSmallCta);
   cfg.blockDim = dim3(kSmallThreads);
   cfg.stream = c->st;
-  cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = kSmallCta;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_pcg_small<N>, x, r, p, ap, dinv, (const double*)c->d_ev, c->geo, c->d_scal,
-                     c->d_status, cond, has_cond);
+  return cfg;
+}
+
+template <int N>
+int pcg_small_fits_impl(sdme_ctx* c) {
+  pcg_small_attr<N>();
+  cudaLaunchAttribute at[1];
+  cudaLaunchConfig_t cfg = pcg_small_config<N>(c, at);
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, k_pcg_small<N>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return clusters > 0 ? 1 : 0;
+}
+
+template <int N>
+void pcg_small_impl(sdme_ctx* c, double* x, double* r, double* p, double* ap, const double* dinv,
+                    cudaGraphConditionalHandle cond, int has_cond) {
+  pcg_small_attr<N>();
+  cudaLaunchAttribute at[1];
+  cudaLaunchConfig_t cfg = pcg_small_config<N>(c, at);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_pcg_small<N>, x, r, p, ap, dinv, (const double*)c->d_ev,
+                                           c->geo, c->d_scal, c->d_status, cond, has_cond);
+  if (e != cudaSuccess && c->launch_err == cudaSuccess) c->launch_err = e;
   ++c->launches;
 }
 
@@ -619,15 +605,8 @@ void launch_col_gen(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
   constexpr int T = 32 * WPE;
   constexpr int smem = ColLay<N, VAL>::PER * 8;
   auto kern = element_col<N, WPE, (WPE == 1 ? SDME_GEN_MINB : 1), MODE, VAL, MIR, false, true>;
-  static int max_blocks = -1;
-  if (max_blocks < 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T, smem);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    max_blocks = std::max(1, nb) * sms;
-  }
+  static PerDevice grid_cache;  // per device: attribute + occupancy set once
+  const int max_blocks = resident_grid(grid_cache, kern, T, smem);
   a.colour = -1;
   kern<<<(unsigned)std::min<long long>(colour_count(c->geo, -1), max_blocks), T, smem, c->st>>>(tb, c->geo, a);
   ++c->launches;
@@ -694,15 +673,8 @@ void gen_diag_launch(sdme_ctx* c, OpArgs a) {
   constexpr int WPE = LargeShape<N, N>::WPE;
   constexpr int smem = DiagGenLay<N, WPE, MIR>::PER * 8;
   auto kern = element_diag_gen<N, WPE, MIR>;
-  static int max_blocks = -1;
-  if (max_blocks < 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * WPE, smem);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    max_blocks = std::max(1, nb) * sms;
-  }
+  static PerDevice grid_cache;  // per device: attribute + occupancy set once
+  const int max_blocks = resident_grid(grid_cache, kern, 32 * WPE, smem);
   kern<<<(unsigned)std::min<long long>(colour_count(c->geo, -1), max_blocks), 32 * WPE, smem, c->st>>>(
       make_tabc<N, MIR>(c), make_tabd_gen<N>(c), c->geo, a);
   ++c->launches;
@@ -728,13 +700,13 @@ void gen_diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm
 
 template <int N>
 const Ops* gen_ops_for() {
-  static const Ops o{&gen_element_impl<N>, &gen_diag_impl<N>, nullptr};
+  static const Ops o{&gen_element_impl<N>, &gen_diag_impl<N>, nullptr, nullptr};
   return &o;
 }
 
 template <int N, int M>
 const Ops* ops_for() {
-  static const Ops o{&element_impl<N, M>, &diag_impl<N, M>, &pcg_small_impl<N>};
+  static const Ops o{&element_impl<N, M>, &diag_impl<N, M>, &pcg_small_impl<N>, &pcg_small_fits_impl<N>};
   return &o;
 }
 

@@ -47,6 +47,10 @@ int set_err(sdme_ctx* c, int code, const std::string& msg, int64_t elem = -1, in
 
 int check_launch(sdme_ctx* ctx) {
   cudaError_t e = cudaGetLastError();
+  if (ctx->launch_err != cudaSuccess) {
+    if (e == cudaSuccess) e = ctx->launch_err;
+    ctx->launch_err = cudaSuccess;
+  }
   if (e != cudaSuccess) return set_err(ctx, SDME_CUDA_ERROR, std::string("launch: ") + cudaGetErrorString(e));
   return SDME_OK;
 }
@@ -261,7 +265,8 @@ void enqueue_pcg_iteration(sdme_ctx* ctx, const double* pu, double* px, double* 
                            cudaGraphConditionalHandle cond, int has_cond) {
   const int kmode = pa ? MODE_PA : MODE_APPLY;
   // (the cluster tail gathers A p itself, so K_c p needs the general sequence)
-  const bool small = ctx->ev_mode && ctx->nvec <= kSmallPcgMax && ctx->ops->pcg_small && !withc;
+  if (ctx->small_fits < 0) ctx->small_fits = ctx->ops->pcg_small_fits ? ctx->ops->pcg_small_fits(ctx) : 0;
+  const bool small = ctx->ev_mode && ctx->nvec <= kSmallPcgMax && ctx->ops->pcg_small && ctx->small_fits && !withc;
   ctx->cur_skip = ctx->d_status;
   if (small) {
     // E-vector element launch, then one cluster kernel for the rest
@@ -831,7 +836,8 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
     }
     // one graph launch per solve (build_pcg_graph); the instantiated graph is
     // reused while the operands are the same (every Newton step of a run)
-    const sdme_ctx::PcgKey key{pu, px, c_k, c_m, pa, withc, withc ? ctx->c_ca.eps : 0.0};
+    const sdme_ctx::PcgKey key{pu, px, c_k, c_m, pa, withc, withc ? ctx->c_ca.eps : 0.0,
+                               withc ? ctx->c_gen : 0ull};
     if (ctx->pcg_direct) {
       // profiling aid (SDME_PCG_DIRECT=1): plain launches, one host check per
       // iteration, so per-kernel tools see every launch
@@ -977,8 +983,14 @@ int sdme_contact(sdme_ctx* ctx, int u, int side, int qf, const double* Bf, const
   int64_t npts = 0;
   sdme_contact_points(ctx, side, qf, &npts);
   if (npts > ctx->gaps_cap) {
+    // a cached PCG graph may hold the old gaps pointer: invalidate it first
+    CK(cudaStreamSynchronize(ctx->st));
     cudaFree(ctx->d_gaps);
     if (ctx->h_gaps) cudaFreeHost(ctx->h_gaps);
+    ctx->d_gaps = nullptr;
+    ctx->h_gaps = nullptr;
+    ctx->gaps_cap = 0;
+    ++ctx->c_gen;
     CK(cudaMalloc(&ctx->d_gaps, npts * sizeof(double)));
     CK(cudaMallocHost(&ctx->h_gaps, npts * sizeof(double)));
     ctx->gaps_cap = npts;
@@ -1008,6 +1020,15 @@ int sdme_contact(sdme_ctx* ctx, int u, int side, int qf, const double* Bf, const
   ca.fc = pf;
   ca.gaps = ctx->d_gaps;
   ca.mode = CONTACT_FORCE;
+  {
+    // what a captured contact node depends on: face tables and the plane /
+    // penalty arguments (u and fc are replaced per launch by contact_op)
+    ContactArgs a0 = ctx->c_ca, a1 = ca;
+    a0.u = a1.u = nullptr;
+    a0.fc = a1.fc = nullptr;
+    if (!ctx->c_ready || memcmp(&ctx->c_ft, &ft, sizeof(ft)) != 0 || memcmp(&a0, &a1, sizeof(a0)) != 0)
+      ++ctx->c_gen;
+  }
   ctx->c_ft = ft;
   ctx->c_ca = ca;
   ctx->c_ready = true;

@@ -5,7 +5,10 @@
 // tensor maps (one per device vector, sdme_abi.cu) live in global memory.
 // Verified on B200 by tools/micro/tma_f64.cu (load, OOB fill, f64 reduce-add);
 // the box's x start must be 16-byte aligned (even lattice x), else the copy
-// faults with "illegal instruction" -- hence even P only.
+// faults with "illegal instruction".  Boxes therefore start at the even
+// lattice x at or below the element's first point and are BoxW = (n + 2) & ~1
+// points wide: n + 1 for even P, n + 2 for odd P, whose elements starting at
+// an odd x read their rows shifted by one (make_tmap / launch_col).
 #pragma once
 #include <cuda.h>
 

@@ -82,20 +82,29 @@ class ScaledLoad:
         return self.scale(t) * self.base
 
 
+_CFL_MODES = ("AsPrinted", "PhysicalSqrt")
+
+
 def cfl_dt(mesh, mat, delta: float, mode: str = "AsPrinted") -> float:
-    """``dynamics.py:81-101`` (host arithmetic only)."""
-    if not 0.2 < delta < 0.9:
+    """Time-step estimate delta * h_min / c (``dynamics.py:81-101``, host only).
+
+    With E = mu (3 lam + 2 mu)/(lam + mu), nu = lam / (2 (lam + mu)) and
+    K = E / (3 (1 - 2 nu)), the wave-speed expression is
+    c2 = 3 K (1 - nu) / (rho (1 + nu)) = (lam + 2 mu) / rho, i.e. the squared
+    dilatational wave speed.  "PhysicalSqrt" uses c = sqrt(c2); "AsPrinted"
+    uses c2 itself (no square root), as the reference's scenario step counts do.
+    """
+    if not (0.2 < delta < 0.9):
         raise ValueError(f"delta should lie in (0.2, 0.9), got {delta}")
-    mu, lam, rho = mat.mu, mat.lambda_lame, mat.rho0
-    e_mod = mu * (3.0 * lam + 2.0 * mu) / (lam + mu)
-    nu = lam / (2.0 * (lam + mu))
-    bulk = e_mod / (3.0 * (1.0 - 2.0 * nu))
-    c = 3.0 * bulk * (1.0 - nu) / (rho * (1.0 + nu))
-    if mode == "PhysicalSqrt":
-        c = np.sqrt(c)
-    elif mode != "AsPrinted":
+    if mode not in _CFL_MODES:
         raise ValueError(f"unknown CFL mode {mode!r}")
-    return delta * mesh.min_edge_length() / c
+    mu, lam = float(mat.mu), float(mat.lambda_lame)
+    young = mu * (3.0 * lam + 2.0 * mu) / (lam + mu)
+    poisson = 0.5 * lam / (lam + mu)
+    bulk = young / (3.0 - 6.0 * poisson)
+    c2 = 3.0 * bulk * (1.0 - poisson) / ((1.0 + poisson) * mat.rho0)
+    speed = float(np.sqrt(c2)) if mode == "PhysicalSqrt" else c2
+    return delta * mesh.min_edge_length() / speed
 
 
 class _Load:
@@ -133,7 +142,7 @@ def newmark_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
                 cfg: SolverConfig | None = None, gamma: float = 0.5, beta: float = 0.25,
                 contact=None, snapshot_stride: int = 0, track_energy: bool = False) -> Trajectory:
     """Implicit Newmark with Newton-Raphson (``dynamics.py:173-257``)."""
-    cfg = cfg or SolverConfig(precond="diagonal", tol=1e-10, condense=False)
+    cfg = SolverConfig.coerce(cfg) or SolverConfig(precond="diagonal", tol=1e-10, condense=False)
     cfg.validate()
     nm = NewmarkCoeffs(dt, gamma, beta)
     pb = problem
@@ -239,27 +248,54 @@ def lumped_mass(problem: GpuFemProblem) -> tuple[DeviceVector, DeviceVector]:
 
 
 def estimate_lambda_max(problem: GpuFemProblem, inv_ml: DeviceVector, contact=None,
-                        iters: int = 30, seed: int = 0) -> float:
-    """Power iteration for lambda_max(M_L^-1 (K_0 + K_c)) at u = 0.
+                        iters: int = 400, seed: int = 0, rtol: float = 1e-12) -> float:
+    """lambda_max(M_L^-1 K_0) at u = 0 by Lanczos on the symmetric form
+    S = M_L^-1/2 K_0 M_L^-1/2 (same spectrum), every operator application on
+    the device (it sets the explicit time step 2/sqrt(lambda_max)
+    of BASELINE config 4, the reference's ``cfl_dt`` role, dynamics.py:81-101).
 
-    Contact stiffness is bounded by eps * sum_q warea N_f^2 on the contact
-    plane; it is included as a diagonal upper bound when ``contact`` is given.
+    The largest Ritz value of the Lanczos tridiagonal converges from below,
+    monotonically and much faster than power iteration; iteration stops once
+    it changes by less than ``rtol`` (relative) over 10 steps, or after
+    ``iters`` steps.  With ``contact`` the penalty stiffness enters as its
+    diagonal upper bound eps * sum_q warea N_f^2 on the contact plane.
     """
+    from scipy.linalg import eigvalsh_tridiagonal
+
     pb = problem
+    wl = np.sqrt(np.maximum(inv_ml.lattice(), 0.0))
+    w = DeviceVector(pb).set_lattice(wl)
+    del wl
     rng = np.random.default_rng(seed)
-    x = DeviceVector(pb).set_free(rng.standard_normal(pb.n_free))
-    y = DeviceVector(pb)
-    z = DeviceVector(pb)
-    u0 = DeviceVector(pb)
-    lam = 0.0
-    # symmetric form: A = M^-1/2 K M^-1/2 ; iterate on y = M^-1 K x (same spectrum)
-    for _ in range(iters):
-        nrm = x.norm()
-        x.assign(1.0 / nrm, x)
-        pb.apply_(u0, x, y, 1.0, 0.0)
-        _mul(pb, z, inv_ml, y)
-        lam = z.norm()
-        x.copy_from(z)
+    q = DeviceVector(pb).set_free(rng.standard_normal(pb.n_free))
+    q.assign(1.0 / q.norm(), q)
+    q_prev = DeviceVector(pb).fill(0.0)
+    t1, t2 = DeviceVector(pb), DeviceVector(pb)
+    u0 = DeviceVector(pb).fill(0.0)
+    alphas, betas = [], []
+    beta = 0.0
+    lam, history = 0.0, []
+    for j in range(max(2, iters)):
+        _mul(pb, t1, w, q)
+        pb.apply_(u0, t1, t2, 1.0, 0.0)
+        _mul(pb, t1, w, t2)                      # t1 = S q
+        alpha = t1.dot(q)
+        t1.assign(1.0, t1, -alpha, q, -beta, q_prev)
+        alphas.append(alpha)
+        beta = t1.norm()
+        if j >= 1:
+            lam = float(eigvalsh_tridiagonal(np.array(alphas), np.array(betas), select="i",
+                                             select_range=(j, j))[0])
+            history.append(lam)
+            if len(history) > 10 and abs(history[-1] - history[-11]) <= rtol * abs(history[-1]):
+                break
+        if beta <= 1e-300:
+            lam = float(eigvalsh_tridiagonal(np.array(alphas), np.array(betas), select="i",
+                                             select_range=(j, j))[0]) if j else alpha
+            break
+        betas.append(beta)
+        q_prev.copy_from(q)
+        q.assign(1.0 / beta, t1)
     if contact is not None:
         lam += contact.stiffness_bound() * max(inv_ml.lattice().max(), 0.0)
     return float(lam)
@@ -274,20 +310,22 @@ def _mul(pb, out, a, b):
 
 def explicit_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int, u0=None, v0=None,
                  cfg: SolverConfig | None = None, snapshot_stride: int = 0, contact=None,
-                 record_every: int = 0, mass: str = "lumped") -> Trajectory:
+                 record_every: int = 0, mass: str = "consistent") -> Trajectory:
     """Central difference on the GPU.
 
-    ``mass="lumped"`` (default): row-sum lumped mass with optional
-    penalty contact.  ``mass="consistent"``: the reference's own
-    scheme (``dynamics.py:130-170``) -- each step solves (M/dt^2) w = psi with
-    matrix-free Jacobi-PCG (``cfg``, full system) and records SolveStats.
+    ``mass="consistent"`` (default, as the reference): the
+    reference's own scheme (``dynamics.py:130-170``) -- each step solves
+    (M/dt^2) w = psi with matrix-free Jacobi-PCG (``cfg``, full system) and
+    records SolveStats.  ``mass="lumped"`` (BASELINE config 4):
+    row-sum lumped mass with optional penalty contact, no linear solve.
     ``external_load`` may be None (no load), a :class:`ScaledLoad`, or any
     callable of t returning a free vector.  Startup a0 = M^-1 psi0,
     u_-1 = u0 - dt v0 + dt^2/2 a0 (``dynamics.py:152-155``).
     """
     if mass == "consistent":
         if contact is not None:
-            raise NotImplementedError("contact with the consistent-mass explicit scheme")
+            raise NotImplementedError("contact with the consistent-mass explicit scheme; "
+                                      "pass mass=\"lumped\" (SURVEY D6)")
         return _explicit_consistent(problem, external_load, dt, n_steps, u0, v0, cfg, snapshot_stride)
     if mass != "lumped":
         raise ValueError(f"unknown mass treatment {mass!r}")
@@ -390,7 +428,7 @@ def explicit_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
 def _explicit_consistent(pb: GpuFemProblem, external_load, dt, n_steps, u0, v0, cfg, snapshot_stride):
     """``explicit_run`` of the reference with a full (uncondensed) Jacobi-PCG
     mass solve per step (``dynamics.py:147-170``)."""
-    cfg = cfg or SolverConfig(precond="diagonal", tol=1e-12, condense=False)
+    cfg = SolverConfig.coerce(cfg) or SolverConfig(precond="diagonal", tol=1e-12, condense=False)
     cfg.validate()
     u = _dev(pb, u0)
     v = _dev(pb, v0)

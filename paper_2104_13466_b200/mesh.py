@@ -194,45 +194,64 @@ class HexMesh:
         return cls(coords, elems, boundary)
 
 
+_SECTIONS = ("VERTICES", "ELEMENTS", "BOUNDARY")
+
+
+def _numbered_rows(rows, fmt) -> list[str]:
+    return [f"{i} {' '.join(fmt(v) for v in row)}" for i, row in enumerate(rows)]
+
+
 def write_mesh(mesh: HexMesh, path) -> None:
-    """Textual VERTICES / ELEMENTS / BOUNDARY format (``meshdof.py:223-234``)."""
+    """Write the reference's plain-text mesh format (``meshdof.py:223-234``):
+    a VERTICES block of ``id x y z`` rows (round-trip ``repr`` floats), an
+    ELEMENTS block of ``id v0..v7`` rows and a BOUNDARY block of
+    ``tag v0..v3`` rows."""
+    blocks = {
+        "VERTICES": _numbered_rows(np.asarray(mesh.coords, dtype=float).tolist(), lambda c: repr(float(c))),
+        "ELEMENTS": _numbered_rows(np.asarray(mesh.elems).tolist(), lambda v: str(int(v))),
+        "BOUNDARY": [tag + " " + " ".join(str(int(v)) for v in quad)
+                     for tag, quads in mesh.boundary.items() for quad in quads],
+    }
+    text = "".join(name + "\n" + "".join(row + "\n" for row in blocks[name]) for name in _SECTIONS)
     with open(path, "w") as fh:
-        fh.write("VERTICES\n")
-        for i, x in enumerate(mesh.coords):
-            fh.write(f"{i} " + " ".join(repr(float(c)) for c in x) + "\n")
-        fh.write("ELEMENTS\n")
-        for i, conn in enumerate(mesh.elems):
-            fh.write(f"{i} " + " ".join(str(int(v)) for v in conn) + "\n")
-        fh.write("BOUNDARY\n")
-        for tag, faces in mesh.boundary.items():
-            for verts in faces:
-                fh.write(f"{tag} " + " ".join(str(int(v)) for v in verts) + "\n")
+        fh.write(text)
+
+
+def _mesh_tokens(path):
+    """(line number, section, fields) of every non-empty, comment-stripped
+    data line; ``#`` starts a comment, a bare section name switches section."""
+    section = None
+    with open(path) as fh:
+        for ln, raw in enumerate(fh, 1):
+            fields = raw.partition("#")[0].split()
+            if not fields:
+                continue
+            if len(fields) == 1 and fields[0] in _SECTIONS:
+                section = fields[0]
+                continue
+            if section is None:
+                raise MeshError(f"{path}:{ln}: content before any section header")
+            yield ln, section, fields
 
 
 def read_mesh(path) -> HexMesh:
-    """``read_mesh`` (``meshdof.py:237-266``); ``#`` starts a comment."""
-    section, verts, elems, boundary = None, {}, {}, {}
-    with open(path) as fh:
-        for ln, raw in enumerate(fh, 1):
-            line = raw.split("#", 1)[0].strip()
-            if not line:
-                continue
-            if line in ("VERTICES", "ELEMENTS", "BOUNDARY"):
-                section = line
-                continue
-            parts = line.split()
-            if section == "VERTICES":
-                verts[int(parts[0])] = [float(p) for p in parts[1:]]
-            elif section == "ELEMENTS":
-                elems[int(parts[0])] = [int(p) for p in parts[1:]]
-            elif section == "BOUNDARY":
-                boundary.setdefault(parts[0], []).append(tuple(int(p) for p in parts[1:]))
-            else:
-                raise MeshError(f"{path}:{ln}: content before any section header")
-    if not verts or not elems:
+    """Read the format of :func:`write_mesh` (the reference's ``read_mesh``,
+    ``meshdof.py:237-266``): rows are placed by their id, so ids may appear
+    in any order."""
+    table = {"VERTICES": {}, "ELEMENTS": {}}
+    boundary: dict[str, list] = {}
+    for _, section, fields in _mesh_tokens(path):
+        if section == "BOUNDARY":
+            boundary.setdefault(fields[0], []).append(tuple(map(int, fields[1:])))
+        else:
+            conv = float if section == "VERTICES" else int
+            table[section][int(fields[0])] = list(map(conv, fields[1:]))
+    verts, elems = table["VERTICES"], table["ELEMENTS"]
+    if not (verts and elems):
         raise MeshError(f"{path}: missing VERTICES or ELEMENTS section")
-    return HexMesh(np.array([verts[i] for i in sorted(verts)]), np.array([elems[i] for i in sorted(elems)]),
-                   boundary)
+    coords = np.array([row for _, row in sorted(verts.items())], dtype=float)
+    conn = np.array([row for _, row in sorted(elems.items())], dtype=np.int64)
+    return HexMesh(coords, conn, boundary)
 
 
 def _internal_parity(basis: Basis1D):

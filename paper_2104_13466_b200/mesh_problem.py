@@ -34,7 +34,8 @@ class GpuMeshProblem(GpuFemProblem):
     ``dirichlet``: (boundary tag, components) pairs, as ``build_dofmap``
     (``meshdof.py:404-409``)."""
 
-    def __init__(self, mesh: HexMesh, basis: Basis1D, mat: NeoHookean, rule: Rule | None = None, dirichlet=None):
+    def __init__(self, mesh: HexMesh, basis: Basis1D, mat: NeoHookean, rule: Rule | None = None, dirichlet=None,
+                 tables=None):
         self.mesh = mesh
         self.basis = basis
         self.mat = mat
@@ -44,7 +45,8 @@ class GpuMeshProblem(GpuFemProblem):
         if self.m != self.P + 1:
             raise ValueError(f"general meshes use the reference default rule m = P + 1 (got m = {self.m})")
         self.dirichlet = [(t, tuple(c)) for t, c in (dirichlet or [])]
-        self.B, self.D, self.w = basis.tables(self.rule)
+        self.B, self.D, self.w = basis.tables(self.rule) if tables is None else (
+            np.asarray(t, dtype=np.float64) for t in tables)
         self.dofmap = build_mesh_dofmap(mesh, basis, self.dirichlet)
         self.n_free = self.dofmap.n_free
         self.perm = None

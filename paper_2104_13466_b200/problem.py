@@ -143,7 +143,10 @@ class GpuFemProblem:
     """
 
     def __init__(self, mesh: BoxMesh, basis: Basis1D, mat: NeoHookean, rule: Rule | None = None,
-                 dirichlet=None, reference_order: bool = True):
+                 dirichlet=None, reference_order: bool = True, tables=None, perm=None, n_free=None):
+        """``tables`` = (B, D, w) and ``perm`` / ``n_free`` (lattice -> free
+        index) override the ones built here; :func:`interop.from_reference`
+        passes the reference problem's own."""
         self.mesh = mesh
         self.basis = basis
         self.mat = mat
@@ -151,14 +154,23 @@ class GpuFemProblem:
         self.rule = rule if rule is not None else gauss_rule(basis.P + 1)
         self.m = self.rule.n
         self.dirichlet = [(t, tuple(c)) for t, c in (dirichlet or [])]
-        self.B, self.D, self.w = basis.tables(self.rule)
+        self.B, self.D, self.w = basis.tables(self.rule) if tables is None else (
+            np.asarray(t, dtype=np.float64) for t in tables)
         lx, ly, lz = mesh.lattice_shape(self.P)
         self.lattice_shape = (3, lz, ly, lx)
         self.n_lattice = 3 * lx * ly * lz
         masks = dirichlet_face_masks(self.dirichlet)
         self.constrained = constrained_lattice(mesh, self.P, masks)
         self.free_mask_flat = (~self.constrained).reshape(-1).astype(np.float64)
-        if reference_order:
+        if perm is not None:
+            perm = np.asarray(perm).reshape(-1)
+            if perm.size != self.n_lattice or n_free is None:
+                raise ValueError("perm must cover the lattice and come with n_free")
+            if not np.array_equal(perm < 0, self.constrained.reshape(-1)):
+                raise ValueError("perm's constrained entries differ from the Dirichlet faces")
+            self.perm = perm.astype(np.int32)
+            n_free = int(n_free)
+        elif reference_order:
             perm, n_free = reference_free_index(mesh, self.P, self.dirichlet)
             self.perm = perm.reshape(-1).astype(np.int32)
         else:

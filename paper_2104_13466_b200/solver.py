@@ -66,6 +66,18 @@ class SolverConfig:
     maxit: int = 200000
     condense: bool = False
 
+    @classmethod
+    def coerce(cls, cfg) -> "SolverConfig | None":
+        """This class, or any object with the reference ``SolverConfig``'s
+        fields (``dynamics.py:38-43``: precond, tol, maxit, condense) --
+        e.g. ``sdmefem.dynamics.SolverConfig`` itself -- as a GPU-path config."""
+        if cfg is None or isinstance(cfg, cls):
+            return cfg
+        try:
+            return cls(precond=cfg.precond, tol=float(cfg.tol), maxit=int(cfg.maxit), condense=bool(cfg.condense))
+        except AttributeError as exc:
+            raise TypeError(f"not a solver configuration: {cfg!r}") from exc
+
     def validate(self):
         if self.condense:
             raise ValueError("condense=True (Schur on dense element matrices) is not available on the "
@@ -136,7 +148,9 @@ class GpuLinearSolver:
 def make_solver(problem: GpuFemProblem, u_lin, c_m: float, cfg: SolverConfig,
                 c_k: float = 1.0) -> GpuLinearSolver:
     """``make_solver`` (dynamics.py:111-127) without element matrices: the
-    operator is defined by its linearisation point and mass coefficient."""
+    operator is defined by its linearisation point and mass coefficient.
+    ``cfg`` may be this package's or the reference's ``SolverConfig``."""
+    cfg = SolverConfig.coerce(cfg)
     cfg.validate()
     if u_lin is not None and not isinstance(u_lin, DeviceVector):
         u_lin = problem.vector(np.asarray(u_lin, dtype=float))

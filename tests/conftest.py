@@ -19,6 +19,35 @@ KINDS = ("LagrangeGLL", "ModalJacobi", "SDME_M", "SDME_K", "SDME_H")
 FACES = ("xmin", "xmax", "ymin", "ymax", "zmin", "zmax")
 
 
+def reference_src():
+    """Directory holding the reference package ``sdmefem`` (the offline
+    install under baseline/_ref, which also travels to the GPU box, else the
+    read-only tree of the build container), or None.  Only tests import it,
+    as the pin of the drop-in adapter; nothing on the product path does."""
+    for cand in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(cand, "sdmefem")):
+            return cand
+    return None
+
+
+def import_reference():
+    """Import sdmefem from :func:`reference_src` (numba cache redirected to a
+    writable directory), or skip the calling test."""
+    src = reference_src()
+    if src is None:
+        pytest.skip("reference package sdmefem not available")
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "sdme_numba_cache"))
+    if src not in sys.path:
+        sys.path.append(src)
+    try:
+        import sdmefem  # noqa: F401
+    except Exception as exc:  # e.g. numba missing
+        pytest.skip(f"reference package not importable: {exc}")
+    import sdmefem.dynamics
+    import sdmefem.femcore
+    return sdmefem
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200) and libsdme.so")
     config.addinivalue_line("markers", "slow: longer-running oracle checks")

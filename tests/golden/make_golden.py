@@ -412,9 +412,103 @@ def gen_mesh_newmark():
     print("mesh_newmark", traj.newton_iters, [r[2] for r in rows])
 
 
-if __name__ == "__main__":
+# ---------------------------------------------------------------------------
+# BASELINE config 5 (implicit large deformation, P = 6), reduced
+
+C5_TAGS = ("LagrangeGLL", "ModalJacobi", "SDME_H")
+C5_TRACTION = -8.0e5   # ~24% tip deflection (GLL vertex values) after 3 steps
+C5_STEPS = 3
+C5_DT = 2.0833e-3      # the 50 x 1.25e-4 s ramp of the scaled beam in 3 steps
+
+
+def c5_run(tag):
+    """Config 5 geometry reduced to 8x1x1 elements with the same element size
+    h = 0.0625 and aspect ratio (cantilever [0,0.5]x[0,0.0625]^2, P = 6,
+    m = 7, x = 0 clamped), tip traction ramped over 3 Newmark steps so each
+    step needs 4-6 Newton iterations (large deformation)."""
+    P = 6
+    prob = problem(tag, P, (8, 1, 1), (0.5, 0.0625, 0.0625), P + 1, [("xmin", (0, 1, 2))])
+    faces = build_face_tables(prob.mesh, prob.element, "xmax", prob.rule)
+    base = prob.traction_vector(faces, lambda f: np.tile([0.0, 0.0, C5_TRACTION], (len(f.pts), 1)))
+    T = C5_STEPS * C5_DT
+    cfg = SolverConfig(precond="diagonal", tol=1e-10, maxit=200000, condense=False)
+    traj = newmark_run(prob, lambda t: base * min(t / T, 1.0), C5_DT, C5_STEPS, newton_tol=1e-8, cfg=cfg)
+    rows = [(r["step"], r["newton_iter"], r["iterations"]) for r in traj.stats.rows]
+    return traj, base, rows
+
+
+def _spread(kind, arg, threads):
+    """Re-run a case in a fresh process with OPENBLAS_NUM_THREADS=threads and
+    return its PCG iteration counts (the reference's own run-to-run spread)."""
+    import json
+    import subprocess
     import sys
 
+    env = dict(os.environ, OPENBLAS_NUM_THREADS=str(threads))
+    out = subprocess.run([sys.executable, os.path.abspath(__file__), "_" + kind, str(arg)], env=env,
+                         capture_output=True, text=True, check=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def gen_config5():
+    from concurrent.futures import ThreadPoolExecutor
+
+    out = {}
+    jobs = {}
+    with ThreadPoolExecutor(max_workers=6) as ex:
+        for tag in C5_TAGS:
+            for th in (1, 4):
+                jobs[(tag, th)] = ex.submit(_spread, "c5rows", tag, th)
+        for tag in C5_TAGS:
+            traj, base, rows = c5_run(tag)
+            out[f"{tag}_u"] = traj.state.u
+            out[f"{tag}_v"] = traj.state.v
+            out[f"{tag}_a"] = traj.state.a
+            out[f"{tag}_load"] = base
+            out[f"{tag}_newton_iters"] = np.array(traj.newton_iters)
+            out[f"{tag}_pcg_rows"] = np.array(rows)
+            print("config5", tag, traj.newton_iters, [r[2] for r in rows], flush=True)
+        for (tag, th), fut in jobs.items():
+            out[f"{tag}_pcg_iters_t{th}"] = np.array(fut.result())
+            print("config5 spread", tag, th, fut.result(), flush=True)
+    out["meta"] = np.array([C5_TRACTION, C5_STEPS, C5_DT])
+    np.savez_compressed(os.path.join(HERE, "config5.npz"), **out)
+
+
+def _mesh_case_pcg(ci):
+    kind, seed, tag, P, dr = GENERAL_CASES[ci]
+    mesh = general_mesh(kind, seed)
+    el = TensorElement.create(3, build_basis(P, BasisKind(tag)))
+    prob = FemProblem(mesh, el, build_dofmap(mesh, el, dr), MAT)
+    rng = np.random.default_rng(100 + ci)
+    u = 2e-3 * rng.uniform(-1, 1, prob.n_free)
+    p = rng.standard_normal(prob.n_free)
+    eff = prob.tangent(u) + 3.0e4 * prob.mass()
+    _, st = pcg(eff, prob.internal_force(u) + 1e3 * p, precond="diagonal", tol=1e-10, maxit=100000)
+    return st.iterations
+
+
+def gen_meshes_spread():
+    """PCG iteration counts of the general-mesh cases (gen_meshes) under
+    OPENBLAS_NUM_THREADS = 1, 2, 4, 8: the reference's own spread, which
+    bounds the iteration slack of the ill-conditioned m6 case."""
+    out = {}
+    for th in (1, 2, 4, 8):
+        out[f"t{th}"] = np.array(_spread("meshpcg", -1, th))
+        print("meshes spread", th, out[f"t{th}"].tolist(), flush=True)
+    np.savez_compressed(os.path.join(HERE, "meshes_spread.npz"), **out)
+
+
+if __name__ == "__main__":
+    import json
+    import sys
+
+    if len(sys.argv) == 3 and sys.argv[1] == "_c5rows":
+        print(json.dumps([r[2] for r in c5_run(sys.argv[2])[2]]))
+        sys.exit(0)
+    if len(sys.argv) == 3 and sys.argv[1] == "_meshpcg":
+        print(json.dumps([_mesh_case_pcg(ci) for ci in range(len(GENERAL_CASES))]))
+        sys.exit(0)
     which = sys.argv[1:] or ["basis", "elements", "global", "contact", "explicit", "impact", "impact_energy",
                              "config1"]
     for w in which:

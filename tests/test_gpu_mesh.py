@@ -9,7 +9,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from conftest import max_rel_err
+from conftest import load_golden, max_rel_err
 from paper_2104_13466_b200 import ElementInversionError, GpuMeshProblem, NeoHookean, pcg_gpu
 from test_mesh import case_setup, golden_mesh_cases
 
@@ -46,12 +46,17 @@ def test_pcg_vs_reference(case):
     u, cm = g[f"{key}_u"], float(g[f"{key}_cm"])
     x, st = pcg_gpu(pb, u, g[f"{key}_pcg_b"], c_m=cm, precond="diagonal", tol=1e-10, maxit=100000)
     ref_its = int(g[f"{key}_pcg_iters"])
-    # +-1 (the north_star bar) on every case but m6: SDME_K at P = 6 with
-    # Jacobi needs 1369 iterations, where CG's loss of orthogonality makes the
-    # count depend on last-bit rounding of the operator (measured 1375, x
-    # still within 2e-10); there the bar is 0.5%.
-    slack = 1 if ref_its < 1000 else int(0.005 * ref_its)
-    assert abs(st.iterations - ref_its) <= slack
+    # +-1 (the north_star bar), or the reference's own run-to-run spread when
+    # larger: tests/golden/meshes_spread.npz holds the reference's counts for
+    # every case under OPENBLAS_NUM_THREADS = 1, 2, 4, 8 (make_golden.py
+    # gen_meshes_spread).  Only m6 (SDME_K, P = 6, ~1,370 Jacobi-PCG
+    # iterations, where CG's loss of orthogonality makes the count depend on
+    # last-bit rounding) spreads by more than one iteration (1369..1378).
+    ci = int(key[1:])
+    sp = load_golden("meshes_spread")
+    runs = [ref_its] + [int(sp[k][ci]) for k in sp.files]
+    slack = max(1, max(runs) - min(runs))
+    assert abs(st.iterations - ref_its) <= slack, (st.iterations, runs)
     assert max_rel_err(x, g[f"{key}_pcg_x"]) <= 1e-9
 
 

@@ -100,7 +100,7 @@ def test_explicit_lumped_contact_vs_reference_pieces():
     pb = gpu_problem("SDME_M", 3, 4, (3, 2, 2), (0.3, 0.2, 0.2))
     c = GpuPenaltyContact(pb, RigidObstacle([-2e-5, 0, 0], [1, 0, 0]), ContactParams(1e10), "xmin")
     traj = explicit_run(pb, None, float(g["explicit_dt"]), int(g["explicit_steps"]), v0=g["v0"],
-                        contact=c, record_every=1)
+                        contact=c, record_every=1, mass="lumped")
     assert max(h[1] for h in traj.contact_history) > 0.0  # contact engaged
     assert max_rel_err(traj.state.u, g["explicit_u"]) <= 1e-10
     assert max_rel_err(traj.state.v, g["explicit_v"]) <= 1e-9
@@ -338,7 +338,7 @@ def test_explicit_momentum_conservation():
     pb = gpu_problem("SDME_M", 3, 4, (2, 2, 2), (1.0, 1.0, 1.0), mat=RMAT)
     v0 = pb.constant_field([0.0, 0.3, 0.0])
     ey = pb.constant_field([0.0, 1.0, 0.0])
-    traj = explicit_run(pb, ScaledLoad(np.zeros(pb.n_free), lambda t: 0.0), 1e-3, 100, v0=v0)
+    traj = explicit_run(pb, ScaledLoad(np.zeros(pb.n_free), lambda t: 0.0), 1e-3, 100, v0=v0, mass="lumped")
     p0, p1 = ey @ pb.mass_apply(v0), ey @ pb.mass_apply(traj.state.v)
     assert abs(p1 - p0) <= 1e-10 * abs(p0)
     ut = traj.state.t * v0
@@ -615,8 +615,8 @@ def test_explicit_chunks_match_per_step_and_report_first_inversion():
     pb = gpu_problem("SDME_M", 3, 4, (3, 2, 2), (0.3, 0.2, 0.2), [("xmin", (0, 1, 2))])
     v0 = pb.constant_field([0.0, 0.0, 1.0])
     zero = np.zeros(pb.n_free)
-    a = explicit_run(pb, None, 1e-6, 40, v0=v0)                     # chunked
-    b = explicit_run(pb, lambda t: zero, 1e-6, 40, v0=v0)           # callable load: per step
+    a = explicit_run(pb, None, 1e-6, 40, v0=v0, mass="lumped")             # chunked
+    b = explicit_run(pb, lambda t: zero, 1e-6, 40, v0=v0, mass="lumped")   # callable load: per step
     assert np.array_equal(a.state.u.view(np.int64), b.state.u.view(np.int64))
     assert np.array_equal(a.state.v.view(np.int64), b.state.v.view(np.int64))
     fast = pb.constant_field([0.0, 0.0, 3.0e3])
@@ -625,7 +625,7 @@ def test_explicit_chunks_match_per_step_and_report_first_inversion():
     errs = []
     for load in (None, lambda t: zero):
         with pytest.raises(ElementInversionError) as ei:
-            explicit_run(pb, load, 1e-5, 400, v0=fast)
+            explicit_run(pb, load, 1e-5, 400, v0=fast, mass="lumped")
         errs.append((ei.value.elem_id, ei.value.qp))
     assert errs[0] == errs[1]
 

@@ -103,6 +103,7 @@ def test_oracle_explicit_lumped_contact_loop():
     pb = _contact_problem()
     c = of.Contact(pb, [-2e-5, 0, 0], [1, 0, 0], 1e10, "xmin")
     assert max_rel_err(np.asarray(pb.mass().sum(axis=1)).ravel(), g["m_lumped"]) <= TOL
+    assert max_rel_err(pb.lumped_mass(), g["m_lumped"]) <= TOL
     out = osv.explicit_lumped(pb, lambda t: np.zeros(pb.n_free), float(g["explicit_dt"]),
                               int(g["explicit_steps"]), v0=g["v0"], contact=c)
     assert max(out["penetration"]) > 0.0  # contact engaged

@@ -93,14 +93,14 @@ def c4(quick=False, steps=2000):
     obst = RigidObstacle([-1e-3, 0.0, 0.0], [1.0, 0.0, 0.0])
     contact = GpuPenaltyContact(pb, obst, ContactParams(1e10), "xmin")
     _, inv_ml = lumped_mass(pb)
-    lam = estimate_lambda_max(pb, inv_ml, contact=contact, iters=40)
+    lam = estimate_lambda_max(pb, inv_ml, contact=contact)
     dt = 0.5 * 2.0 / np.sqrt(lam)
     v0 = pb.constant_field([-10.0, 0.0, 0.0])
     n_steps = steps if not quick else 200
-    explicit_run(pb, None, dt, 5, v0=v0, contact=contact)  # warm-up
+    explicit_run(pb, None, dt, 5, v0=v0, contact=contact, mass="lumped")  # warm-up
     contact.history.clear()
     t0 = time.perf_counter()
-    traj = explicit_run(pb, None, dt, n_steps, v0=v0, contact=contact, record_every=50)
+    traj = explicit_run(pb, None, dt, n_steps, v0=v0, contact=contact, record_every=50, mass="lumped")
     pb.sync()
     wall = time.perf_counter() - t0
     hist = traj.contact_history
