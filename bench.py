@@ -14,10 +14,13 @@ resident in HBM); ``e2e`` goes through the reference-facing API
 (GpuFemProblem.apply_tangent with host numpy vectors in the reference free-DOF
 order, H2D + permutation + K.p + D2H inside the timed region).
 
-``--impl reference`` times the reference algorithm's CPU path (the oracle
-restatement of element_tangent(...) @ p_e, oracle/fem.py, kind "port") on a
-bounded sample of same-size elements, on all host cores.
-N > 1: replicas only (the path does not shard in this tier).
+``--impl reference`` times the reference's own CPU path -- sdmefem's
+``element_tangent(tab, mat, u_e) @ p_e`` (femcore.py:130-146) from the
+offline install under baseline/_ref, on a bounded sample of same-size
+elements per step, in one single-threaded worker process per host core
+(tools/refcpu.py; the oracle port stands in, kind "port", only if the
+install is absent).  N > 1: replicas only (the path does not shard in this
+tier; DESIGN.md).
 """
 
 from __future__ import annotations
@@ -39,6 +42,9 @@ P, M, NEL = 4, 5, 64
 E_MOD, NU, RHO = 1.0e7, 0.3, 1.0e3
 METRIC = "matrix-free K.p GDOF/s (FP64), 64^3 hex P=4 SDME"
 UNIT = "GDOF/s"
+WORKLOAD = "config2: 64^3 hex on [0,1]^3, P=4 SDME_M, m=5 Gauss, K(u).p"
+N_DOF = 3 * (P * NEL + 1) ** 3
+N_ELEM = NEL ** 3
 
 
 def sf_macs(n, m):
@@ -148,6 +154,9 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thr = threading.Thread(target=self._read, daemon=True)
             self.thr.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0:  # nvidia-smi is up and sampling
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -203,70 +212,88 @@ def dist_barrier(ws):
         dist.barrier()
 
 
-def cpu_sample_kp(n_elem_sample=None, threads=None, reps=1):
-    """Reference algorithm on the host: element_tangent(...) @ p_e over a
-    sample of h=1/64 P=4 elements (oracle restatement, dense B^T D B +
-    geometric, femcore.py:130-146).  Returns (seconds per element, cores, elems)."""
-    from concurrent.futures import ThreadPoolExecutor
+def cpu_kp_baseline(target_s=1.5, workers=None, steps=1, warmup=0, sampler=None):
+    """The reference's CPU K.p on this host: ``element_tangent(...) @ p_e`` of
+    sdmefem (baseline/_ref) on h = 1/64, P = 4, m = 5 elements, one
+    single-threaded worker process per core (tools/refcpu.py); each step lets
+    every worker evaluate enough elements for ~``target_s`` of wall time.
+    Returns (per-step samples, description)."""
+    from tools import refcpu
 
-    from oracle import basis as ob
-    from oracle import fem as of
+    own = sampler is None
+    s = sampler or refcpu.ElementSampler(P, "SDME_M", M, 1.0 / NEL, workers)
+    try:
+        probe = s.sample("kp", 4)
+        per_worker = max(2, int(round(target_s * 4 / probe["worker_busy_s"])))
+        for _ in range(warmup):
+            s.sample("kp", per_worker)
+        out = [s.sample("kp", per_worker) for _ in range(steps)]
+    finally:
+        if own:
+            s.close()
+    return out, refcpu.describe(out[-1], P, M, 1.0 / NEL, "kp")
 
-    threads = threads or os.cpu_count() or 1
-    n_elem_sample = n_elem_sample or max(8, 2 * threads)
-    h = 1.0 / NEL
-    div = (2, 2, 2)
-    pb = of.Problem(of.Mesh(div, (2 * h,) * 3), ob.Basis("SDME_M", P), of.Material(E_MOD, NU, RHO), M)
-    rng = np.random.default_rng(0)
-    u = 1e-3 * h * rng.uniform(-1, 1, pb.n_free)
-    p = rng.standard_normal(pb.n_free)
-    ue = [pb.gather(e, u) for e in range(pb.mesh.ne)]
-    pe = [pb.gather(e, p).reshape(-1) for e in range(pb.mesh.ne)]
 
-    def one(k):
-        e = k % pb.mesh.ne
-        _, grad, wdet = pb.tab.per_elem[e]
-        return of.elem_tangent(pb.mat, grad, wdet, ue[e], e) @ pe[e]
-
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    with ThreadPoolExecutor(max_workers=threads) as ex:
-        list(ex.map(one, range(threads)))  # warm
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            list(ex.map(one, range(n_elem_sample)))
-        dt = time.perf_counter() - t0
-    return dt / (reps * n_elem_sample), threads, n_elem_sample
+def cpu_line(samples, desc):
+    """cpu_baseline object from ElementSampler samples (GDOF/s = elements/s x
+    DOFs per element of config 2)."""
+    el = sum(x["elements"] for x in samples)
+    sec = sum(x["seconds"] for x in samples)
+    value = el / sec * (N_DOF / N_ELEM) / 1e9
+    return {"value": value, "unit": UNIT, "cores": samples[-1]["cores"], "kind": samples[-1]["kind"],
+            "sample": desc, "measured_elements": el, "measured_s": sec, "extrapolated": True,
+            "s_per_element_per_core": sec * samples[-1]["cores"] / el}
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    n_dof = 3 * (P * NEL + 1) ** 3
-    n_elem = NEL ** 3
-    threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        cpu_sample_kp(threads, threads)
-    per = []
-    for _ in range(args.steps):
-        s, cores, ns = cpu_sample_kp(2 * threads, threads)
-        per.append(s)
-    s_elem = float(np.mean(per))
-    t_step = s_elem * n_elem  # one full-mesh K.p, extrapolated from the sample
-    value = n_dof / t_step / 1e9
+    samples, desc = cpu_kp_baseline(target_s=1.5, steps=args.steps, warmup=args.warmup)
+    cpu = cpu_line(samples, desc)
+    ms = 1e3 * float(np.mean([x["seconds"] for x in samples]))
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+        "impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": "config2: 64^3 hex, P=4 SDME_M, m=5, K.p",
-                                        "n_dofs": n_dof, "elements": n_elem},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{2 * threads} elements of h=1/64 per step (dense element_tangent@p_e, "
-                                   f"oracle/fem.py), scaled by 262144 elements"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "data": "synthetic", "config": {"workload": WORKLOAD, "n_dofs": N_DOF, "elements": N_ELEM},
+        "step": "one bounded sample of the config-2 K.p: every host core evaluates its share of "
+                "same-size elements; GDOF/s = elements/s x DOFs per element (extrapolated to the full mesh)",
+        "cpu_baseline": cpu,
+        "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def admissibility(pb, u_lat):
+    """SURVEY D4 log of the config-2 input: min det F and max |grad u|
+    (Frobenius and largest entry) over every quadrature point of the mesh,
+    host numpy sum factorisation over z-slabs of elements (not timed)."""
+    from numpy.lib.stride_tricks import sliding_window_view as swv
+
+    Pp, n = pb.P, pb.P + 1
+    func_of = [0] + list(range(2, Pp + 1)) + [1]  # lattice offset -> function
+    Bl = np.ascontiguousarray(pb.B[:, func_of])
+    Dl = [np.ascontiguousarray(pb.D[:, func_of] * (2.0 / pb.mesh.h[a])) for a in range(3)]
+    nz = pb.mesh.divisions[2]
+    min_j, max_f, max_e = np.inf, 0.0, 0.0
+    for k in range(nz):
+        slab = u_lat[:, Pp * k:Pp * k + n]
+        win = swv(swv(slab, n, axis=2)[:, :, ::Pp], n, axis=3)[:, :, :, ::Pp]  # c, lz, j, i, ly, lx
+        win = win.transpose(1, 2, 3, 4, 5, 0)
+        H = np.stack([np.einsum("az,by,cx,zjiyxq->qajibc", Dl[2] if d == 2 else Bl, Dl[1] if d == 1 else Bl,
+                                Dl[0] if d == 0 else Bl, win, optimize=True) for d in range(3)], axis=1)
+        F = H.copy()
+        for a in range(3):
+            F[a, a] += 1.0
+        det = (F[0, 0] * (F[1, 1] * F[2, 2] - F[1, 2] * F[2, 1]) - F[0, 1] * (F[1, 0] * F[2, 2] - F[1, 2] * F[2, 0])
+               + F[0, 2] * (F[1, 0] * F[2, 1] - F[1, 1] * F[2, 0]))
+        min_j = min(min_j, float(det.min()))
+        max_f = max(max_f, float(np.sqrt((H * H).sum(axis=(0, 1))).max()))
+        max_e = max(max_e, float(np.abs(H).max()))
+    return {"min_J": min_j, "max_grad_u_frobenius": max_f, "max_grad_u_entry": max_e,
+            "points": int(pb.mesh.n_elems * pb.m ** 3)}
 
 
 def config1_time_step(cpu: bool) -> dict:
@@ -292,17 +319,27 @@ def config1_time_step(cpu: bool) -> dict:
            "ms_per_step": gpu * 1e3, "newton_iters": traj.newton_iters,
            "pcg_iters": [r["iterations"] for r in traj.stats.rows if r["step"] >= 0]}
     if cpu:
-        from oracle import basis as ob
-        from oracle import fem as of
-        from oracle import solve as osv
+        from tools import refcpu
 
-        opb = of.Problem(of.Mesh((4, 4, 4), (1.0, 1.0, 1.0)), ob.Basis("SDME_M", 4), of.Material(E_MOD, NU, RHO), 6,
-                         [("xmin", (0, 1, 2))])
-        obase = opb.traction_vector("xmax", [0.0, 0.0, 1.0e5])
-        t0 = time.perf_counter()
-        osv.newmark(opb, lambda t: obase * min(t / 1e-3, 1.0), 1e-4, 1, newton_tol=1e-8, pcg_tol=1e-10)
-        out["cpu_s_per_step"] = time.perf_counter() - t0
-        out["cpu_kind"] = "port (oracle/solve.py newmark: assembled CSR tangent + Jacobi-PCG, numpy/scipy), 1 step"
+        r = refcpu.newmark_step_s((4, 4, 4), (1.0, 1.0, 1.0), 4, 6, "SDME_M", [0.0, 0.0, 1.0e5], 1e-4, 1e-3, 2)
+        if r is not None:
+            out["cpu_s_per_step"] = r["step_s"][-1]
+            out["cpu_kind"] = ("reference: sdmefem newmark_run (baseline/_ref) on config 1, Jacobi-PCG 1e-10, "
+                               "condense=False, default BLAS threads; the wall time of its 2nd step (no setup)")
+            out["cpu_cores"] = r["cores"]
+            out["cpu_newton_pcg"] = [r["newton"], r["pcg"]]
+        else:
+            from oracle import basis as ob
+            from oracle import fem as of
+            from oracle import solve as osv
+
+            opb = of.Problem(of.Mesh((4, 4, 4), (1.0, 1.0, 1.0)), ob.Basis("SDME_M", 4),
+                             of.Material(E_MOD, NU, RHO), 6, [("xmin", (0, 1, 2))])
+            obase = opb.traction_vector("xmax", [0.0, 0.0, 1.0e5])
+            t0 = time.perf_counter()
+            osv.newmark(opb, lambda t: obase * min(t / 1e-3, 1.0), 1e-4, 1, newton_tol=1e-8, pcg_tol=1e-10)
+            out["cpu_s_per_step"] = time.perf_counter() - t0
+            out["cpu_kind"] = "port (oracle/solve.py newmark: assembled CSR tangent + Jacobi-PCG), 1 step"
     return out
 
 
@@ -326,17 +363,22 @@ def run_ours(args):
     u = pb.vector().set_lattice(u_lat)
     p = pb.vector().set_lattice(p_lat)
     y = pb.vector()
-    # admissibility log (D4): min J and max |du/dX| are checked by the kernel's inversion flag
+    # admissibility: the kernel's inversion flag (raises on det F <= 0)
+    # and the host log of min J / max |du/dX| over all quadrature points
     pb.fint_(u, y)
+    adm = admissibility(pb, u_lat) if rank == 0 else None
 
     for _ in range(args.warmup):
         pb.apply_(u, p, y)
     pb.sync()
     dist_barrier(ws)
-    l0 = pb.launch_count()
     with ClockSampler(local) as clk:
+        l0 = pb.launch_count()
         ms_total = pb.time_op("apply", u, p, y, 0.0, args.steps) * args.steps
-    launches = pb.launch_count() - l0
+        launches = pb.launch_count() - l0
+        # keep the same load on for ~0.4 s more (untimed) so the 20 ms clock
+        # samples cover it: the timed region itself is only K x ~1.8 ms
+        pb.time_op("apply", u, p, y, 0.0, 200)
     pb.sync()
     ms_total = dist_max(ms_total, ws)
     t_step = ms_total / 1e3 / args.steps
@@ -404,23 +446,20 @@ def run_ours(args):
     tstep = config1_time_step(rank == 0 and not args.no_cpu) if rank == 0 else None
     cpu = None
     if rank == 0 and not args.no_cpu:
-        s, cores, ns = cpu_sample_kp(None, None)
-        cpu_val = n_dof / (s * NEL ** 3) / 1e9
-        cpu = {"value": cpu_val, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{ns} elements (h=1/64, P=4, m=5) dense element_tangent@p_e per timing, "
-                         f"scaled to 262144 elements"}
+        samples, desc = cpu_kp_baseline(target_s=1.5, steps=1)
+        cpu = cpu_line(samples, desc)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "config2: 64^3 hex on [0,1]^3, P=4 SDME_M, m=5 Gauss, K(u).p",
+            "config": {"workload": WORKLOAD,
                        "n_dofs": n_dof, "elements": NEL ** 3, "parallelism": f"replicas{ws}",
                        "l2": "inputs (2 x 407 MB) exceed the 126 MB L2; no flush"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "fint_ms": t_fint * 1e3,
             "fint_gdofs": n_dof / t_fint / 1e9,
-            "time_step": tstep,
+            "time_step": tstep, "admissibility": adm,
             "pcg_operator": {"setup_ms": t_setup * 1e3, "kp_ms": t_pa * 1e3, "kp_gdofs": n_dof / t_pa / 1e9,
                              "note": "K.p inside sdme_pcg: K = F^-T and ln J stored per quadrature point "
                                      "once per solve (setup), bit-identical to the from-u K.p"},

@@ -222,6 +222,57 @@ def test_config2_properties_full_size():
     assert t1.norm() == 0.0
 
 
+def _grad_peak(u_lat, P):
+    """(k, j, i) of the element whose vertex differences of u are largest."""
+    v = u_lat[:, ::P, ::P, ::P]
+    g = np.zeros(tuple(s - 1 for s in v.shape[1:]))
+    for c in range(3):
+        for ax in range(3):
+            d = np.abs(np.diff(v[c], axis=ax))
+            sl = [slice(0, s - 1) for s in v.shape[1:]]
+            g = np.maximum(g, d[tuple(sl)])
+    return np.unravel_index(int(np.argmax(g)), g.shape)
+
+
+def test_config2_field_vs_oracle_on_sub_boxes():
+    """Config 2 at full size (64^3, P = 4 SDME_M, the bench's own inputs:
+    0.02 sin(2 pi (x+y+z)) + 1e-3 h noise, |grad u| up to ~0.13) against the
+    oracle: on 3x3x3-element sub-boxes -- including the one around the
+    steepest gradient -- every lattice point strictly inside the sub-box
+    receives contributions from sub-box elements only, so the full-mesh GPU
+    K(u).p and f_int(u) there must equal the oracle's (dense element_tangent,
+    femcore.py:130-146) on the sub-box to 1e-12."""
+    from bench import config2_fields
+    from paper_2104_13466_b200.lattice import reference_free_index
+
+    P, h, nb = 4, 1.0 / 64, 3
+    pb = GpuFemProblem(BoxMesh((64, 64, 64), (1.0, 1.0, 1.0)), build_basis(P, BasisKind("SDME_M")), MAT,
+                       reference_order=False)
+    u_lat, p_lat = config2_fields(pb, seed_u=0, seed_p=1)
+    u = pb.vector().set_lattice(u_lat)
+    p = pb.vector().set_lattice(p_lat)
+    y_kp = pb.apply_(u, p, pb.vector()).lattice()
+    y_f = pb.fint_(u, pb.vector()).lattice()
+    kk, jj, ii = _grad_peak(u_lat, P)
+    starts = [(0, 0, 0), (30, 17, 45), (min(kk, 61), min(jj, 61), min(ii, 61))]
+    sub = BoxMesh((nb,) * 3, (nb * h,) * 3)
+    perm, n_free = reference_free_index(sub, P, None)
+    opb = of.Problem(of.Mesh((nb,) * 3, (nb * h,) * 3), ob.Basis("SDME_M", P), OMAT, P + 1)
+    assert opb.n_free == n_free
+    for k0, j0, i0 in starts:
+        box = (slice(None), slice(P * k0, P * (k0 + nb) + 1), slice(P * j0, P * (j0 + nb) + 1),
+               slice(P * i0, P * (i0 + nb) + 1))
+        uf = np.zeros(n_free)
+        pf = np.zeros(n_free)
+        uf[perm] = u_lat[box]
+        pf[perm] = p_lat[box]
+        inner = (slice(None), slice(1, -1), slice(1, -1), slice(1, -1))
+        for got, ref in ((y_kp[box], opb.apply_tangent(uf, pf)), (y_f[box], opb.internal_force(uf))):
+            ref_l = ref[perm]
+            err = np.abs(got[inner] - ref_l[inner]).max() / np.abs(ref_l[inner]).max()
+            assert err <= 1e-12, ((k0, j0, i0), err)
+
+
 def test_explicit_consistent_mass_vs_reference():
     """the reference's own explicit_run (consistent mass, full
     Jacobi-PCG) -- per-step PCG counts +-1, final u, v within 1e-9."""

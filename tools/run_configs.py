@@ -1,6 +1,15 @@
 """Run the BASELINE.json configs 1, 3, 4, 5 on one GPU and print one JSON line each.
 
-    python tools/run_configs.py c1 c3 c4 c5 [--quick]
+    python tools/run_configs.py c1 c3 c4 c5 [--quick] [--cpu]
+
+``--cpu`` adds, in the same run and on the same host, the reference's own CPU
+figure beside each GPU number (tools/refcpu.py: sdmefem from baseline/_ref):
+c1 the reference's newmark_run per step; c3 per-element element_tangent @ p_e
+on every core, scaled to the mesh (extrapolated); c4 the explicit lumped-mass
++ contact restatement loop built from the reference's internal_force /
+PenaltyContact at full size, a few steps scaled to 2,000; c5 the reference's
+newmark_run on the 8x1x1 reduction of the cantilever, per step, scaled by the
+element count (extrapolated).
 
 c1: 4^3 P=4 SDME_M, (P+2)^3 Gauss, 10 Newmark steps (dt 1e-4), traction 1e5 in +z
     on xmax ramped over 10 dt, Jacobi-PCG 1e-10: s/time-step,
@@ -37,8 +46,70 @@ from paper_2104_13466_b200.dynamics import estimate_lambda_max, lumped_mass  # n
 MAT = NeoHookean.from_engineering(1.0e7, 0.3, 1.0e3)
 
 
+CPU = "--cpu" in sys.argv
+
+
 def emit(d):
     print(json.dumps(d), flush=True)
+
+
+def _c4_reference_cpu(div, P, steps, dt, v0_val=-10.0, wall=-1e-3, eps=1e10):
+    """Config 4's explicit loop (lumped mass, penalty contact, central
+    difference) from the reference's own pieces -- FemProblem.internal_force,
+    element_mass row sums, PenaltyContact.evaluate_forces -- at full size,
+    ``steps`` steps, in a subprocess with SDMEFEM_THREADS = all cores."""
+    import subprocess
+
+    from tools import refcpu
+
+    if not refcpu.reference_dir():
+        return None
+    code = f"""
+import json, sys, time
+sys.path.insert(0, {refcpu.REF_DIR!r})
+import numpy as np
+from sdmefem.basis1d import BasisKind, build_basis
+from sdmefem.contact import ContactParams, PenaltyContact, RigidObstacle
+from sdmefem.femcore import FemProblem, element_mass
+from sdmefem.material import NeoHookean
+from sdmefem.meshdof import build_dofmap, gen_box_mesh
+from sdmefem.quadrature import gauss_rule
+from sdmefem.tensorelem import TensorElement
+t0 = time.perf_counter()
+mesh = gen_box_mesh({tuple(div)!r}, (1.0, 0.2, 0.2))
+el = TensorElement.create(3, build_basis({P}, BasisKind("SDME_M")))
+prob = FemProblem(mesh, el, build_dofmap(mesh, el, None), NeoHookean.from_engineering(1e7, 0.3, 1e3),
+                  rule=gauss_rule({P + 1}))
+ml = np.zeros(prob.n_free)
+me = element_mass(prob.tables[0], prob.mat, 3)  # identical geometry on the box
+for e in range(prob.mesh.n_elems):
+    d, sg = prob.dmap.elem_vector_dofs(e)
+    ok = d >= 0
+    np.add.at(ml, d[ok], (me @ ok.astype(float))[ok])
+cont = PenaltyContact(prob, RigidObstacle(np.array([{wall}, 0.0, 0.0]), np.array([1.0, 0.0, 0.0])),
+                      ContactParams({eps}), "xmin")
+v = np.zeros(prob.n_free); v[0::3] = {v0_val}  # vertex-coefficient constant field, timing only
+u = np.zeros(prob.n_free)
+psi = lambda uu: -prob.internal_force(uu) + cont.evaluate_forces(uu).force
+dt = {dt!r}
+t1 = time.perf_counter()
+a = psi(u) / ml
+up = u - dt * v + 0.5 * dt * dt * a
+ts = []
+for _ in range({steps}):
+    s0 = time.perf_counter()
+    un = 2 * u - up + dt * dt * psi(u) / ml
+    v = (un - up) / (2 * dt)
+    up, u = u, un
+    ts.append(time.perf_counter() - s0)
+print(json.dumps({{"setup_s": t1 - t0, "step_s": ts}}))
+"""
+    env = dict(os.environ, SDMEFEM_THREADS=str(os.cpu_count()), NUMBA_CACHE_DIR="/tmp/sdme_numba_cache")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=3600)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr[-2000:])
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    return out
 
 
 def c1():
@@ -52,8 +123,18 @@ def c1():
     traj = newmark_run(pb, load, 1e-4, 10, newton_tol=1e-8, cfg=cfg)
     wall = time.perf_counter() - t0
     its = [r["iterations"] for r in traj.stats.rows if r["step"] >= 0]
-    emit({"config": "c1", "s_per_step": wall / 10, "total_s": wall, "newton_iters": traj.newton_iters,
-          "pcg_iters": its, "max_u": float(np.abs(traj.state.u).max()), "n_free": pb.n_free})
+    row = {"config": "c1", "s_per_step": wall / 10, "total_s": wall, "newton_iters": traj.newton_iters,
+           "pcg_iters": its, "max_u": float(np.abs(traj.state.u).max()), "n_free": pb.n_free}
+    if CPU:
+        from tools import refcpu
+
+        r = refcpu.newmark_step_s((4, 4, 4), (1.0, 1.0, 1.0), 4, 6, "SDME_M", [0.0, 0.0, 1.0e5], 1e-4, 1e-3, 2)
+        if r:
+            row["cpu"] = {"s_per_step": r["step_s"][-1], "kind": "reference", "cores": r["cores"],
+                          "what": "sdmefem newmark_run, 2nd step wall time (no setup), default BLAS threads",
+                          "newton": r["newton"], "pcg": r["pcg"]}
+            row["speedup"] = r["step_s"][-1] / row["s_per_step"]
+    emit(row)
 
 
 def c3(quick=False):
@@ -78,10 +159,22 @@ def c3(quick=False):
             t_kp = pb.time_op("apply", u, p, y, 0.0, 5) / 1e3
             t_f = pb.time_op("fint", u, p, y, 0.0, 5) / 1e3
             flops = bench.kp_flops(n ** 3, P + 1, P + 1)
-            emit({"config": "c3", "P": P, "basis": tag, "n_elem_side": n, "n_dofs": pb.n_lattice,
-                  "kp_ms": t_kp * 1e3, "kp_gdofs": pb.n_lattice / t_kp / 1e9,
-                  "kp_tflops": flops / t_kp / 1e12, "kp_frac_fp64": flops / t_kp / 1e12 / fp if fp else None,
-                  "fint_ms": t_f * 1e3, "fint_gdofs": pb.n_lattice / t_f / 1e9})
+            row = {"config": "c3", "P": P, "basis": tag, "n_elem_side": n, "n_dofs": pb.n_lattice,
+                   "kp_ms": t_kp * 1e3, "kp_gdofs": pb.n_lattice / t_kp / 1e9,
+                   "kp_tflops": flops / t_kp / 1e12, "kp_frac_fp64": flops / t_kp / 1e12 / fp if fp else None,
+                   "fint_ms": t_f * 1e3, "fint_gdofs": pb.n_lattice / t_f / 1e9}
+            if CPU and tag == "SDME_M":  # the basis kind does not change the CPU cost
+                from tools import refcpu
+
+                with refcpu.ElementSampler(P, tag, P + 1, 1.0 / n) as smp:
+                    probe = smp.sample("kp", 2)
+                    k = max(1, int(round(1.5 * 2 / probe["worker_busy_s"])))
+                    r = smp.sample("kp", k)
+                eps = r["elements_per_s"]
+                row["cpu"] = {"kp_gdofs": eps * pb.n_lattice / n ** 3 / 1e9, "kind": r["kind"], "cores": r["cores"],
+                              "sample": refcpu.describe(r, P, P + 1, 1.0 / n, "kp"), "extrapolated": True}
+                row["speedup_kp"] = row["kp_gdofs"] / row["cpu"]["kp_gdofs"]
+            emit(row)
             del pb, u, p, y
 
 
@@ -104,11 +197,22 @@ def c4(quick=False, steps=2000):
     pb.sync()
     wall = time.perf_counter() - t0
     hist = traj.contact_history
-    emit({"config": "c4", "elements": int(np.prod(div)), "n_dofs": pb.n_free, "dt": dt, "lambda_max": lam,
-          "steps": n_steps, "s_per_step": wall / n_steps, "total_s": wall,
-          "max_penetration": max(h[1] for h in hist) if hist else 0.0,
-          "contact_active_max": max(h[3] for h in hist) if hist else 0,
-          "final_mean_vx": float(traj.state.v[0::3].mean()), "history_every50": hist[:8]})
+    row = {"config": "c4", "elements": int(np.prod(div)), "n_dofs": pb.n_free, "dt": dt, "lambda_max": lam,
+           "steps": n_steps, "s_per_step": wall / n_steps, "total_s": wall,
+           "max_penetration": max(h[1] for h in hist) if hist else 0.0,
+           "contact_active_max": max(h[3] for h in hist) if hist else 0,
+           "final_mean_vx": float(traj.state.v[0::3].mean()), "history_every50": hist[:8]}
+    if CPU:
+        r = _c4_reference_cpu(div, P, 3, dt)
+        if r:
+            sps = float(np.mean(r["step_s"]))
+            row["cpu"] = {"s_per_step": sps, "s_2000_steps_extrapolated": 2000 * sps, "kind": "reference",
+                          "cores": os.cpu_count(), "setup_s": r["setup_s"],
+                          "what": "restatement loop from sdmefem pieces (internal_force with SDMEFEM_THREADS = "
+                                  "all cores, element_mass row sums, PenaltyContact.evaluate_forces), "
+                                  f"{len(r['step_s'])} full-size steps, scaled to 2000"}
+            row["speedup"] = sps / row["s_per_step"]
+    emit(row)
 
 
 def c5(quick=False, traction=-1.3e6, tags=("LagrangeGLL", "ModalJacobi", "SDME_H")):
@@ -129,10 +233,26 @@ def c5(quick=False, traction=-1.3e6, tags=("LagrangeGLL", "ModalJacobi", "SDME_H
         lat = pb.to_lattice(traj.state.u)
         # vertex coefficients are point values in every basis (internal modes vanish there)
         tip = float(lat[2, ::6, ::6, -1].mean())
-        emit({"config": "c5", "basis": tag, "n_free": pb.n_free, "steps": n_steps, "s_per_step": wall / n_steps,
-              "newton_iters_mean": float(np.mean(traj.newton_iters)), "pcg_iters_mean": float(np.mean(its)),
-              "pcg_iters_max": int(max(its)), "tip_uz_mean": tip, "tip_deflection_over_length": -tip / 4.0,
-              "traction": traction})
+        row = {"config": "c5", "basis": tag, "n_free": pb.n_free, "steps": n_steps, "s_per_step": wall / n_steps,
+               "newton_iters_mean": float(np.mean(traj.newton_iters)), "pcg_iters_mean": float(np.mean(its)),
+               "pcg_iters_max": int(max(its)), "tip_uz_mean": tip, "tip_deflection_over_length": -tip / 4.0,
+               "traction": traction}
+        if CPU:
+            from tools import refcpu
+
+            # the reference on the 8x1x1 reduction (same h, aspect, P, rule;
+            # tests/golden config5), 2 steps, scaled by the element count
+            r = refcpu.newmark_step_s((8, 1, 1), (0.5, 0.0625, 0.0625), 6, 7, tag, [0.0, 0.0, -8.0e5],
+                                      2.0833e-3, 3 * 2.0833e-3, 2)
+            if r:
+                sps = r["step_s"][-1]
+                row["cpu"] = {"s_per_step_8_elements": sps, "s_per_step_extrapolated": sps * int(np.prod(div)) / 8,
+                              "kind": "reference", "cores": r["cores"], "newton": r["newton"], "pcg": r["pcg"],
+                              "what": "sdmefem newmark_run on 8x1x1 elements (h = 0.0625, P = 6, m = 7), 2nd step "
+                                      "wall time, scaled by 4096 / 8 elements (Newton / PCG counts differ from "
+                                      "the full mesh: extrapolated)"}
+                row["speedup_extrapolated"] = row["cpu"]["s_per_step_extrapolated"] / row["s_per_step"]
+        emit(row)
 
 
 if __name__ == "__main__":
