@@ -180,6 +180,52 @@ int sdme_contact_diag(sdme_ctx* ctx, int d);
  * preconditioner), the operator of newmark_run with contact (dynamics.py:241) */
 int sdme_pcg_contact(sdme_ctx* ctx, int on);
 
+/* assembled / Schur-condensed solve (the reference's default solver,
+ * SolverConfig(precond="sgs", condense=True), dynamics.py:38-43, 111-127;
+ * condense_elements / CondensedSystem / LinearSolver, solver.py:179-322).
+ * Box-mesh contexts.  The host describes every element's local DOFs in the
+ * reference local order (function-major (p,q,r) r fastest, component fastest,
+ * tensorelem.py:97-129): its lattice address (-1 when Dirichlet) and its role,
+ * the global boundary index 0..nb-1 (the reference's free index, boundary DOFs
+ * first) or -2 for an element-interior DOF (condensed out) or -1
+ * (constrained).  With no -2 roles (condense=False) the CSR is the full free
+ * operator.  Element matrices use the tabulated physical gradients G (nq x nf
+ * x 3), values N (nq x nf) and w det J (nq) of the problem's rule. */
+typedef struct sdme_schur sdme_schur;
+typedef struct {
+  int64_t n_elems;
+  int nd;                 /* 3 (P+1)^3 local DOFs                                  */
+  int nq;                 /* quadrature points per element                         */
+  int64_t nb;             /* size of the (condensed) system                        */
+  const int64_t* addr;    /* n_elems x nd lattice addresses, -1 constrained        */
+  const int32_t* role;    /* n_elems x nd: boundary index, -1 constrained, -2 interior */
+  const int64_t* addr_b;  /* nb lattice addresses of the system's DOFs             */
+  const double* G;        /* nq x nf x 3 physical gradients (reference orders)    */
+  const double* N;        /* nq x nf values                                        */
+  const double* wdet;     /* nq weights x det J                                    */
+  double mu, lambda_lame, rho0;
+} sdme_schur_desc;
+int sdme_schur_create(sdme_ctx* ctx, const sdme_schur_desc* desc, sdme_schur** out);
+int sdme_schur_destroy(sdme_schur* s);
+/* system size, CSR nonzeros, level counts of the forward / backward SGS sweeps */
+int sdme_schur_info(const sdme_schur* s, int64_t* nb, int64_t* nnz, int* fwd_levels, int* bwd_levels);
+/* element matrices of c_k K_T(u) + c_m M (femcore.py:130-156; u ignored when
+ * c_k = 0), per-element condensation (Cholesky of K_ii; SDME_BAD_ARGUMENT
+ * "element interior block is not SPD" as solver.py:284-285 raises ValueError),
+ * deterministic CSR assembly in element order */
+int sdme_schur_factor(sdme_schur* s, int u, double c_k, double c_m);
+/* x = A^-1 b: reduce_rhs, PCG on the (condensed) CSR with precond 0 none,
+ * 1 diagonal, 2 symmetric Gauss-Seidel (solver.py:129-170, same order of
+ * checks and errors as sdme_pcg), interior recovery; b, x lattice vectors */
+int sdme_schur_solve(sdme_schur* s, int b, int x, int precond, double tol, int maxit, int* iters,
+                     double* relres);
+/* host copies of the assembled CSR (rowptr nb+1, cols nnz, vals nnz) and of
+ * element 0's matrix (nd x nd); any pointer may be NULL */
+int sdme_schur_matrix(const sdme_schur* s, int64_t* rowptr, int32_t* cols, double* vals,
+                      double* element_matrix0);
+/* row-major dense lattice -> device address of a lattice point of component c */
+int sdme_lattice_address(const sdme_ctx* ctx, int c, int x, int y, int z, int64_t* addr);
+
 /* page-locked host buffers (fast H2D/D2H for the free-order vector calls) */
 int sdme_host_alloc(size_t bytes, void** ptr);
 int sdme_host_free(void* ptr);

@@ -21,7 +21,11 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsdme.so")
 OBJDIR = os.path.join(HERE, "build_obj")
+# checked build (-DSDME_CHECKED: device bounds / alignment asserts, csrc/check.cuh)
+CHECKED_LIB = os.path.join(HERE, "libsdme_checked.so")
+CHECKED_OBJDIR = os.path.join(HERE, "build_obj_checked")
 ORDERS = range(1, 9)
+ABI_UNITS = ["sdme_abi.cu", "schur.cu"]  # host-side ABI translation units (operator units: ops.cu per order)
 DEPS = sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.cu")) +
               [os.path.join(ROOT, "include", "sdme.h")])
 
@@ -52,30 +56,38 @@ def _compile(args):
     return obj
 
 
-def build(force: bool = False, verbose: bool = True, jobs: int | None = None, only=None, defs=()) -> str:
+def build(force: bool = False, verbose: bool = True, jobs: int | None = None, only=None, defs=(),
+          checked: bool = False) -> str:
     """Compile every translation unit (or, with ``only``, just those orders'
     operator units -- a development shortcut that relinks the other existing
-    objects) and link libsdme.so.  ``defs``: extra -D flags for the operator units."""
-    if not force and up_to_date():
+    objects) and link libsdme.so.  ``defs``: extra -D flags for the operator units.
+    ``checked``: the -DSDME_CHECKED variant, libsdme_checked.so (load it with
+    SDME_LIB=paper_2104_13466_b200/libsdme_checked.so)."""
+    lib, objdir = (CHECKED_LIB, CHECKED_OBJDIR) if checked else (LIB, OBJDIR)
+    if checked:
+        defs = (*defs, "-DSDME_CHECKED")
+    if not force and not checked and up_to_date():
         return LIB
-    os.makedirs(OBJDIR, exist_ok=True)
-    units = [(os.path.join(CSRC, "sdme_abi.cu"), os.path.join(OBJDIR, "sdme_abi.o"), [])]
-    units += [(os.path.join(CSRC, "ops.cu"), os.path.join(OBJDIR, f"ops_p{p}.o"), [f"-DSDME_ORDER={p}", *defs])
+    os.makedirs(objdir, exist_ok=True)
+    units = [(os.path.join(CSRC, u), os.path.join(objdir, u.replace(".cu", ".o")), list(defs if checked else []))
+             for u in ABI_UNITS]
+    units += [(os.path.join(CSRC, "ops.cu"), os.path.join(objdir, f"ops_p{p}.o"), [f"-DSDME_ORDER={p}", *defs])
               for p in ORDERS]
     objs_all = [u[1] for u in units]
     if only is not None:
-        units = [u for u in units[1:] if int(u[1].rsplit("_p", 1)[1][:-2]) in only]
+        units = [u for u in units[len(ABI_UNITS):] if int(u[1].rsplit("_p", 1)[1][:-2]) in only]
     if verbose:
         print(f"nvcc {' '.join(NVCC_FLAGS)} : {len(units)} translation units", flush=True)
     with ThreadPoolExecutor(max_workers=jobs or min(len(units), os.cpu_count() or 4)) as ex:
         list(ex.map(_compile, units))
-    cmd = [nvcc(), *ARCH, "-shared", "-o", LIB + ".tmp", *objs_all]
+    cmd = [nvcc(), *ARCH, "-shared", "-o", lib + ".tmp", *objs_all]
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
     only = [int(a.split("=", 1)[1]) for a in sys.argv if a.startswith("--only=")]
     defs = [a for a in sys.argv if a.startswith("-D")]
-    build(force="--force" in sys.argv or bool(only) or bool(defs), only=only or None, defs=defs)
+    build(force="--force" in sys.argv or bool(only) or bool(defs), only=only or None, defs=defs,
+          checked="--checked" in sys.argv)

@@ -162,6 +162,46 @@ class GpuPenaltyContact:
             self._u = DeviceVector(self.problem)
         return self._u, self._fc
 
+    def face_points(self) -> np.ndarray:
+        """Reference positions of the face quadrature points, (n_points, 3), in
+        the order of the gaps: faces of the side with the first in-plane axis
+        d1 fastest, points (a along d1, b along d2) with b fastest
+        (``build_face_tables``, femcore.py:215-253)."""
+        mesh = self.problem.mesh
+        ax, side = divmod(self.side, 2)
+        d1, d2 = [d for d in range(3) if d != ax]
+        n1, n2 = mesh.divisions[d1], mesh.divisions[d2]
+        t = 0.5 * (1.0 + self.xf)
+        c1 = mesh.origin[d1] + mesh.h[d1] * (np.arange(n1)[:, None] + t[None, :])  # (face i1, a)
+        c2 = mesh.origin[d2] + mesh.h[d2] * (np.arange(n2)[:, None] + t[None, :])  # (face i2, b)
+        qf = self.qf
+        pts = np.empty((n2, n1, qf, qf, 3))
+        pts[..., ax] = mesh.origin[ax] + (mesh.lengths[ax] if side else 0.0)
+        pts[..., d1] = c1[None, :, :, None]
+        pts[..., d2] = c2[:, None, None, :]
+        return pts.reshape(-1, 3)
+
+    def update_active_set(self, u_free: np.ndarray):
+        """``contact.py:98-101``: (active flags, gaps), one array per face."""
+        u, fc = self._scratch()
+        u.set_free(u_free)
+        g = self._gaps(u, fc).reshape(-1, self.qf * self.qf)
+        gaps = [row.copy() for row in g]
+        return [row < 0.0 for row in gaps], gaps
+
+    def pressure_profile(self, u_free: np.ndarray) -> np.ndarray:
+        """``contact.py:186-204``: (in-plane distance from the surface's
+        minimum corner, pressure) rows sorted by the distance."""
+        _, gaps = self.update_active_set(u_free)
+        g = np.concatenate(gaps) if gaps else np.zeros(0)
+        t_n = np.where(g < 0.0, -self.params.eps_n * g, 0.0)
+        pts = self.face_points()
+        nrm = np.asarray(self.obstacle.outward_normal, dtype=float)
+        inplane = pts - np.outer(pts @ nrm, nrm)
+        dist = np.linalg.norm(inplane - inplane.min(axis=0), axis=1)
+        order = np.argsort(dist, kind="stable")
+        return np.column_stack([dist[order], t_n[order]])
+
     def evaluate_forces(self, u_free: np.ndarray) -> ContactForces:
         """``contact.py:103-151`` (force, pressures per face point, gaps, active, settled)."""
         u, fc = self._scratch()

@@ -62,10 +62,14 @@ struct ColLay {
   static constexpr int YB = TY ? 1 : N, YA = TY ? N : 1;
   static constexpr int UC = TY ? N : SU, UB = TY ? 1 : N, UA = TY ? N * N : 1;
   __device__ static int yo(int k, int b, int a) {
-    return SW ? k * 16 + ((b * 4 + a) ^ (5 * k)) : k * SY + b * YB + a * YA;
+    const int o = SW ? k * 16 + ((b * 4 + a) ^ (5 * k)) : k * SY + b * YB + a * YA;
+    SDME_CHECK(k >= 0 && k < N && b >= 0 && b < N && a >= 0 && a < N && o >= 0 && o < N * SY);
+    return o;
   }
   __device__ static int uo(int c, int b, int a) {
-    return SW ? c * 16 + ((b * 4 + a) ^ (5 * c)) : c * UC + b * UB + a * UA;
+    const int o = SW ? c * 16 + ((b * 4 + a) ^ (5 * c)) : c * UC + b * UB + a * UA;
+    SDME_CHECK(c >= 0 && c < N && b >= 0 && b < N && a >= 0 && a < N && o >= 0 && o < N * SU);
+    return o;
   }
   static constexpr int PTS = (VALS ? 12 : 9) * SQ;
   // x-stage output X(k, j, a) = k XK + j XJ + a XA: TM layout (XK, XJ, XA) =
@@ -75,7 +79,10 @@ struct ColLay {
   static constexpr int XK = TM ? N : SX, XJ = TM ? 1 : N;
   static constexpr int XA = TM ? (N * N + 14) / 16 * 16 + 1 : 1;
   static constexpr int XSPAN = TM ? (N - 1) * (XK + XJ + XA) + 1 : N * SX;
-  __device__ static int xo(int k, int j, int a) { return k * XK + j * XJ + a * XA; }
+  __device__ static int xo(int k, int j, int a) {
+    SDME_CHECK(k >= 0 && k < N && j >= 0 && j < N && a >= 0 && a < N);
+    return k * XK + j * XJ + a * XA;
+  }
   static constexpr int X = PTS, Y = X + XSPAN, U = Y + N * SY, W = U + N * SU;
   static constexpr int RP = TM ? BoxW<N>::BW : N;           // staged row pitch (TMA box width)
   static constexpr int RB = TM ? (N * N * RP + 15) / 16 * 16 : N * N * N;  // one staging buffer (128-B multiple)
@@ -84,7 +91,10 @@ struct ColLay {
   static constexpr int TAB = R + 2 * RB;                    // !TM: int lattice offsets of the box entries
   static constexpr int BAR = O + RB;                        // TM: two mbarriers
   static constexpr int PER = TM ? BAR + 2 : TAB + (N * N * N + 1) / 2;
-  __device__ static int qi(int d, int comp, int q) { return (d * 3 + comp) * SQ + (SW ? q ^ (5 * (q >> 4)) : q); }
+  __device__ static int qi(int d, int comp, int q) {
+    SDME_CHECK(d >= 0 && d < (VALS ? 4 : 3) && comp >= 0 && comp < 3 && q >= 0 && q < N * N * N);
+    return (d * 3 + comp) * SQ + (SW ? q ^ (5 * (q >> 4)) : q);
+  }
 };
 
 // per-element shared region rounded to 128 B (the SUB = 2 half-warp regions)
@@ -157,6 +167,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
         // even P: boxes start at the element; 16-byte loads of the pitched
         // box row (conflict-free for RP = 6)
         const double2* row = reinterpret_cast<const double2*>(R + *buf * L::RB + w * L::RP);
+        SDME_CHECK(smem_ok(row, L::RP * 8, 16));
 #pragma unroll
         for (int i = 0; i < L::RP / 2; ++i) {
           const double2 d = row[i];
@@ -336,6 +347,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
         }
         if constexpr (N & 1) {
           double2* orow = reinterpret_cast<double2*>(S + L::O + w * L::RP);
+          SDME_CHECK(smem_ok(orow, L::RP * 8, 16));
 #pragma unroll
           for (int i = 0; i < L::RP / 2; ++i)
             orow[i] = make_double2(acc[2 * i], 2 * i + 1 < N ? acc[2 * i + 1] : 0.0);
@@ -358,6 +370,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
       }
       const int Z = Z0 + k, Y = Y0 + j;
       const bool chk = touches_dirichlet(g, comp, X0, Y0, Z0, N);
+      SDME_CHECK(comp >= 0 && comp < 3 && Z >= 0 && Z < g.Lz && Y >= 0 && Y < g.Ly && X0 >= 0 && X0 + N <= g.Lx);
       double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Px + X0;
 #pragma unroll
       for (int i = 0; i < N; ++i)
@@ -411,6 +424,7 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
   extern __shared__ __align__(128) double smem[];
   const int t = threadIdx.x % T;
   double* S = smem + (threadIdx.x / T) * ColPer<N, VALS, TM>::PERP;
+  SDME_CHECK(smem_ok(S, L::PER * 8, 128));
   const long long half = threadIdx.x / T;
   int buf = 0;
   if (args.skip && *(volatile const int*)args.skip) return;

@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_diag3(const __gr
           continue;
         }
         const int Z = Z0 + k, Y = Y0 + j;
+        SDME_CHECK(Z >= 0 && Z < g.Lz && Y >= 0 && Y < g.Ly && X0 >= 0 && X0 + N <= g.Lx);
         double* row = args.y + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Px + X0;
 #pragma unroll
         for (int i = 0; i < N; ++i)

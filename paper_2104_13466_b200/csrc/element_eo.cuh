@@ -48,6 +48,7 @@ __device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo
       } else if (bx.in && N == 3 && BoxW<N>::BW == 4) {
         // P = 2 (shift 0): 32-byte box rows, one 16-byte and one 8-byte load
         const double* row = bx.in + comp * BoxW<N>::CB + (k * N + j) * 4;
+        SDME_CHECK(smem_ok(row, 24, 16));
         const double2 d = *reinterpret_cast<const double2*>(row);
         v[0] = d.x;
         v[1 % N] = d.y;
@@ -268,6 +269,7 @@ __device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Ge
           double o[N];
 #pragma unroll
           for (int i = 0; i < N; ++i) o[i] = (chk && constrained(g, comp, X0 + i, Y, Z)) ? 0.0 : acc[i];
+          SDME_CHECK(smem_ok(orow, 32, 16));
           reinterpret_cast<double2*>(orow)[0] = make_double2(o[0], o[1]);
           reinterpret_cast<double2*>(orow)[1] = make_double2(o[2], 0.0);
           continue;
@@ -282,6 +284,7 @@ __device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Ge
         }
         continue;
       }
+      SDME_CHECK(comp >= 0 && comp < 3 && Z >= 0 && Z < g.Lz && Y >= 0 && Y < g.Ly && X0 >= 0 && X0 + N <= g.Lx);
       double* row = dst + comp * g.Ns + ((long long)Z * g.Ly + Y) * g.Px + X0;
 #pragma unroll
       for (int i = 0; i < N; ++i)

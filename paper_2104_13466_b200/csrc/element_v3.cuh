@@ -141,6 +141,7 @@ __device__ __forceinline__ void v3_stage_rows(const Geo& g, const double* __rest
   for (int w = t; w < N * N * N; w += T) {
     const int kj = w / N, i = w % N;
     const int k = kj / N, j = kj % N;
+    SDME_CHECK(comp >= 0 && comp < 3 && Z0 + k < g.Lz && Y0 + j < g.Ly && X0 + i < g.Lx && X0 >= 0);
     cp_async8(rows + w, field + comp * g.Ns + ((long long)(Z0 + k) * g.Ly + (Y0 + j)) * g.Px + X0 + i);
   }
   cp_async_commit();
@@ -490,6 +491,7 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
   const int gid = threadIdx.x / C::T;
   const int t = threadIdx.x % C::T;
   double* A = smem + gid * PERS;
+  SDME_CHECK(smem_ok(A, PERS * 8, 8));
   double* Bf = A + C::SA;
   double* Rb = A + C::PER;  // staged rows [2][N^3] (STG)
   int buf = 0;

@@ -1064,6 +1064,14 @@ int sdme_contact(sdme_ctx* ctx, int u, int side, int qf, const double* Bf, const
   return SDME_OK;
 }
 
+int sdme_lattice_address(const sdme_ctx* ctx, int c, int x, int y, int z, int64_t* addr) {
+  if (!ctx || !addr || ctx->gen || c < 0 || c > 2) return SDME_BAD_ARGUMENT;
+  const Geo& g = ctx->geo;
+  if (x < 0 || x >= g.Lx || y < 0 || y >= g.Ly || z < 0 || z >= g.Lz) return SDME_BAD_ARGUMENT;
+  *addr = c * g.Ns + ((int64_t)z * g.Ly + y) * g.Px + x;
+  return SDME_OK;
+}
+
 int sdme_strain_energy(sdme_ctx* ctx, int u, double* out) {
   double* pu = ctx ? vec(ctx, u) : nullptr;
   if (!pu || !out) return SDME_BAD_ARGUMENT;

@@ -12,6 +12,8 @@
 #pragma once
 #include <cuda.h>
 
+#include "check.cuh"
+
 namespace sdme {
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -27,6 +29,7 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned
 }
 
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  SDME_CHECK(smem_ok(bar, 8, 8));
   asm volatile(
       "{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}" ::"r"(
           smem_addr(bar)),
@@ -37,6 +40,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // box load of lattice block (x0, y0, z0) of component c
 __device__ __forceinline__ void tma_load_box(double* dst, const CUtensorMap* map, int x0, int y0, int z0, int c,
                                              unsigned long long* bar) {
+  SDME_CHECK(smem_ok(dst, 128, 128) && smem_ok(bar, 8, 8) && (x0 & 1) == 0);
   asm volatile(
       "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
       "[%6];" ::"r"(smem_addr(dst)),
@@ -47,6 +51,7 @@ __device__ __forceinline__ void tma_load_box(double* dst, const CUtensorMap* map
 // y[box] += src  (bulk tensor reduce-add; elements outside the tensor are dropped)
 __device__ __forceinline__ void tma_reduce_add_box(const CUtensorMap* map, const double* src, int x0, int y0, int z0,
                                                    int c) {
+  SDME_CHECK(smem_ok(src, 128, 128) && (x0 & 1) == 0);
   asm volatile(
       "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
           map),

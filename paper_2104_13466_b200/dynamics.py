@@ -25,7 +25,7 @@ import numpy as np
 from . import native
 from .errors import NewtonDivergenceError
 from .problem import DeviceVector, GpuFemProblem
-from .solver import SolverConfig, StatsLog, pcg_gpu
+from .solver import DriverSolver, SolverConfig, StatsLog, pcg_gpu
 
 __all__ = ["NewmarkCoeffs", "TimeState", "Trajectory", "ScaledLoad", "cfl_dt", "newmark_run",
            "explicit_run", "estimate_lambda_max"]
@@ -167,10 +167,10 @@ def newmark_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
         return settled, active
 
     # a0 = M^-1 psi0 (mass-only PCG, short-circuits for psi0 = 0)
+    solver = DriverSolver(pb, cfg)
     atr.fill(0.0)
     residual(u, atr, 0.0)
-    _, st = pcg_gpu(pb, None, psi, c_m=1.0, precond=cfg.precond, tol=cfg.tol, maxit=cfg.maxit,
-                    c_k=0.0, x=a)
+    _, st = solver.solve(None, 0.0, 1.0, psi, a, slot="mass")
     traj.stats.add(-1, 0, "newmark-init", st)
 
     t = 0.0
@@ -206,11 +206,13 @@ def newmark_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
                     f"(residual {rnorm / psi_ref:.3e} relative)", rnorm)
             # effective operator K_T + b1 M (+ K_c on the active set of this
             # residual, dynamics.py:235-241)
+            if active and cfg.assembled:
+                raise NotImplementedError("implicit contact with the assembled (SGS / Schur) solver; "
+                                          "use precond=\"diagonal\", condense=False")
             if active:
                 lib.sdme_pcg_contact(pb._ctx, 1)
             try:
-                _, st = pcg_gpu(pb, uk, psi, c_m=nm.b1, precond=cfg.precond, tol=cfg.tol,
-                                maxit=cfg.maxit, x=du)
+                _, st = solver.solve(uk, 1.0, nm.b1, psi, du)
             finally:
                 if active:
                     lib.sdme_pcg_contact(pb._ctx, 0)
@@ -444,15 +446,14 @@ def _explicit_consistent(pb: GpuFemProblem, external_load, dt, n_steps, u0, v0, 
             psi.assign(-1.0, fint)
         return psi
 
-    _, st = pcg_gpu(pb, None, residual(0.0), c_m=1.0, precond=cfg.precond, tol=cfg.tol, maxit=cfg.maxit,
-                    c_k=0.0, x=a)
+    solver = DriverSolver(pb, cfg)
+    _, st = solver.solve(None, 0.0, 1.0, residual(0.0), a, slot="mass")
     traj.stats.add(-1, 0, "explicit-init", st)
     up.assign(1.0, u, -dt, v, 0.5 * dt * dt, a)
     t = 0.0
     inv_dt2 = 1.0 / dt ** 2
     for step in range(n_steps):
-        _, st = pcg_gpu(pb, None, residual(t), c_m=inv_dt2, precond=cfg.precond, tol=cfg.tol,
-                        maxit=cfg.maxit, c_k=0.0, x=w)
+        _, st = solver.solve(None, 0.0, inv_dt2, residual(t), w, slot="mhat")
         traj.stats.add(step, 0, "explicit", st)
         un.assign(2.0, u, -1.0, up, 1.0, w)        # (2u - u_prev) + w
         v.assign(1.0, un, -1.0, up)                # (u_next - u_prev) ...

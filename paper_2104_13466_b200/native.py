@@ -19,7 +19,9 @@ import numpy as np
 from .errors import ElementInversionError, NativeError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsdme.so")
+# SDME_LIB: an alternative build of the same library (A/B and sanitizer
+# experiments, e.g. a different register cap); default the in-tree build
+LIB_PATH = os.environ.get("SDME_LIB") or os.path.join(HERE, "libsdme.so")
 
 OK, INVERSION, INDEFINITE, MAXIT, BAD_DIAGONAL, BAD_ARGUMENT, CUDA_ERROR = range(7)
 
@@ -43,6 +45,13 @@ class MeshDesc(C.Structure):
     _fields_ = [("P", C.c_int), ("m", C.c_int), ("n_elems", C.c_int64), ("B", _dp), ("D", _dp), ("w", _dp),
                 ("mu", C.c_double), ("lambda_lame", C.c_double), ("rho0", C.c_double), ("n_free", C.c_int64),
                 ("dof", _i32p), ("asm_ptr", _i64p), ("asm_slot", _i32p), ("geom", _dp)]
+
+
+class SchurDesc(C.Structure):
+    """``sdme_schur_desc`` (include/sdme.h): the assembled / condensed solve."""
+    _fields_ = [("n_elems", C.c_int64), ("nd", C.c_int), ("nq", C.c_int), ("nb", C.c_int64),
+                ("addr", _i64p), ("role", _i32p), ("addr_b", _i64p), ("G", _dp), ("N", _dp), ("wdet", _dp),
+                ("mu", C.c_double), ("lambda_lame", C.c_double), ("rho0", C.c_double)]
 
 
 # name -> argtypes (restype c_int for all)
@@ -84,6 +93,14 @@ SIGNATURES = {
     "sdme_pcg_contact": [C.c_void_p, C.c_int],
     "sdme_strain_energy": [C.c_void_p, C.c_int, C.POINTER(C.c_double)],
     "sdme_time_op": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, _dp],
+    "sdme_schur_create": [C.c_void_p, C.POINTER(SchurDesc), C.POINTER(C.c_void_p)],
+    "sdme_schur_destroy": [C.c_void_p],
+    "sdme_schur_info": [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int),
+                        C.POINTER(C.c_int)],
+    "sdme_schur_factor": [C.c_void_p, C.c_int, C.c_double, C.c_double],
+    "sdme_schur_solve": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.POINTER(C.c_int), _dp],
+    "sdme_schur_matrix": [C.c_void_p, _i64p, _i32p, _dp, _dp],
+    "sdme_lattice_address": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)],
     "sdme_host_alloc": [C.c_size_t, C.POINTER(C.c_void_p)],
     "sdme_host_free": [C.c_void_p],
     "sdme_sync": [C.c_void_p],

@@ -21,9 +21,10 @@ from .errors import PCGError
 from .problem import DeviceVector, GpuFemProblem
 
 __all__ = ["SolveStats", "StatsLog", "PCGError", "SolverConfig", "pcg_gpu", "GpuLinearSolver",
-           "make_solver"]
+           "AssembledLinearSolver", "DriverSolver", "make_solver"]
 
 _PRECOND = {"diagonal": 1, "none": 0, None: 0}
+_ASSEMBLED = ("sgs", "gauss-seidel")  # need the assembled CSR (csrc/schur.cu)
 
 
 @dataclass
@@ -57,9 +58,13 @@ class StatsLog:
 
 @dataclass
 class SolverConfig:
-    """``dynamics.py:38-43``.  The GPU path solves the full (uncondensed)
-    system with the Jacobi preconditioner; ``precond="sgs"`` and
-    ``condense=True`` need the assembled CSR and are rejected."""
+    """``dynamics.py:38-43``.  ``precond`` "diagonal" / "none" with
+    ``condense=False`` is the matrix-free Jacobi-PCG path (any mesh size, SURVEY
+    D3); ``precond="sgs"`` and / or ``condense=True`` select the assembled
+    path, the reference's default solver (:class:`~.schur.SchurSolver`: dense
+    element matrices, Schur condensation, level-scheduled SGS on the device),
+    sized like the reference.  This class defaults to the matrix-free path;
+    ``SolverConfig.reference_default()`` is the reference's own default."""
 
     precond: str = "diagonal"
     tol: float = 1e-12
@@ -78,13 +83,19 @@ class SolverConfig:
         except AttributeError as exc:
             raise TypeError(f"not a solver configuration: {cfg!r}") from exc
 
+    @classmethod
+    def reference_default(cls) -> "SolverConfig":
+        """``sdmefem.dynamics.SolverConfig()``: SGS, Schur condensation, tol 1e-12."""
+        return cls(precond="sgs", tol=1e-12, maxit=200000, condense=True)
+
+    @property
+    def assembled(self) -> bool:
+        """True when the solve needs the assembled operator (SGS or condensation)."""
+        return bool(self.condense) or self.precond in _ASSEMBLED
+
     def validate(self):
-        if self.condense:
-            raise ValueError("condense=True (Schur on dense element matrices) is not available on the "
-                             "matrix-free GPU path; use condense=False")
-        if self.precond not in _PRECOND:
-            raise ValueError(f"preconditioner {self.precond!r} is not available on the GPU path "
-                             "(Jacobi 'diagonal' or 'none')")
+        if self.precond not in _PRECOND and self.precond not in _ASSEMBLED:
+            raise ValueError(f"unknown preconditioner {self.precond!r}")
 
 
 def pcg_gpu(problem: GpuFemProblem, u_lin, b, c_m: float = 0.0, precond: str = "diagonal",
@@ -145,13 +156,65 @@ class GpuLinearSolver:
                        self.c_k, x=x)
 
 
+class AssembledLinearSolver:
+    """``LinearSolver`` (solver.py:302-322) on the assembled / condensed operator
+    c_k K_T(u_lin) + c_m M (:class:`~.schur.SchurSolver`)."""
+
+    def __init__(self, schur, u_lin, c_m: float, c_k: float = 1.0):
+        self.schur = schur
+        self.schur.factor(u_lin, c_k, c_m)
+
+    @property
+    def condensed(self) -> bool:
+        return self.schur.condensed
+
+    def solve(self, rhs, x: DeviceVector | None = None):
+        return self.schur.solve(rhs, x=x)
+
+
 def make_solver(problem: GpuFemProblem, u_lin, c_m: float, cfg: SolverConfig,
-                c_k: float = 1.0) -> GpuLinearSolver:
+                c_k: float = 1.0):
     """``make_solver`` (dynamics.py:111-127) without element matrices: the
     operator is defined by its linearisation point and mass coefficient.
-    ``cfg`` may be this package's or the reference's ``SolverConfig``."""
+    ``cfg`` may be this package's or the reference's ``SolverConfig``; with
+    ``condense=True`` or ``precond="sgs"`` the result is the assembled solver
+    (the reference's default path), else matrix-free Jacobi-PCG."""
     cfg = SolverConfig.coerce(cfg)
     cfg.validate()
+    if cfg.assembled:
+        from .schur import SchurSolver
+
+        sch = SchurSolver(problem, cfg.condense, cfg.precond, cfg.tol, cfg.maxit)
+        return AssembledLinearSolver(sch, u_lin, c_m, c_k)
     if u_lin is not None and not isinstance(u_lin, DeviceVector):
         u_lin = problem.vector(np.asarray(u_lin, dtype=float))
     return GpuLinearSolver(problem, u_lin, c_m, cfg.precond, cfg.tol, cfg.maxit, c_k)
+
+
+class DriverSolver:
+    """The linear solves of one time-integration run (dynamics.py:186-241):
+    matrix-free Jacobi-PCG, or the assembled / condensed solver whose
+    structure (CSR pattern, SGS levels, element tables) is built once per run
+    and refactored per operator."""
+
+    def __init__(self, problem: GpuFemProblem, cfg: SolverConfig):
+        self.pb, self.cfg = problem, cfg
+        self._schur = {}
+
+    def solve(self, u_lin, c_k: float, c_m: float, rhs: DeviceVector, x: DeviceVector, slot: str = "k"):
+        """x = (c_k K_T(u_lin) + c_m M)^-1 rhs; ``slot`` names a cached factorisation
+        reused while (c_k, c_m, u_lin) stay the same object/values."""
+        cfg = self.cfg
+        if not cfg.assembled:
+            return pcg_gpu(self.pb, u_lin, rhs, c_m=c_m, precond=cfg.precond, tol=cfg.tol, maxit=cfg.maxit,
+                           c_k=c_k, x=x)
+        from .schur import SchurSolver
+
+        ent = self._schur.get(slot)
+        key = (c_k, c_m)
+        if ent is None:
+            ent = self._schur[slot] = [SchurSolver(self.pb, cfg.condense, cfg.precond, cfg.tol, cfg.maxit), None]
+        if c_k != 0.0 or ent[1] != key:  # K_T(u) changes every call; mass-only operators factor once
+            ent[0].factor(u_lin, c_k, c_m)
+            ent[1] = key
+        return ent[0].solve(rhs, x=x)

@@ -499,6 +499,87 @@ def gen_meshes_spread():
     np.savez_compressed(os.path.join(HERE, "meshes_spread.npz"), **out)
 
 
+# ---------------------------------------------------------------------------
+# the reference's default solver (SGS, Schur condensation)
+
+SGS_CFGS = (("sgs", True), ("sgs", False), ("diagonal", True), ("none", True))
+
+
+def gen_sgs():
+    """make_solver(problem, element_matrices, cfg).solve(b) (dynamics.py:111-127,
+    solver.py:258-322) on the global cases for SGS / diagonal with and without
+    condensation (tol 1e-10), the condensed Schur CSR of the smallest case,
+    and explicit_run / newmark_run with the reference's default SolverConfig()."""
+    from sdmefem.dynamics import explicit_run, make_solver
+
+    out = {}
+    cases = [("SDME_M", 4, 5, (2, 3, 2), (1.0, 1.5, 1.0), [("xmin", (0, 1, 2))]),
+             ("LagrangeGLL", 3, 5, (3, 2, 2), (1.0, 1.0, 0.5), [("xmin", (0, 1, 2)), ("zmax", (2,))]),
+             ("ModalJacobi", 2, 3, (2, 2, 3), (0.5, 0.5, 1.0), None),
+             ("SDME_H", 3, 4, (2, 2, 2), (1.0, 1.0, 1.0), [("ymin", (1,))])]
+    for ci, (tag, P, m, div, L, dr) in enumerate(cases):
+        prob = problem(tag, P, div, L, m, dr)
+        u = smooth_plus_noise(prob, 0.01, 1e-4, 7 + ci)
+        p = np.random.default_rng(50 + ci).standard_normal(prob.n_free)
+        c_m = 3.0e4
+        eff = [(kt + c_m * mm, d, sg) for (kt, d, sg), (mm, _, _) in zip(prob.tangent_matrices(u),
+                                                                           prob.mass_matrices())]
+        b = prob.internal_force(u) + 1e3 * p
+        for k, (pc, cond) in enumerate(SGS_CFGS):
+            solver = make_solver(prob, eff, SolverConfig(precond=pc, tol=1e-10, maxit=100000, condense=cond))
+            x, st = solver.solve(b)
+            out[f"g{ci}_c{k}_x"] = x
+            out[f"g{ci}_c{k}_iters"] = np.array(st.iterations)
+            out[f"g{ci}_c{k}_tag"] = np.array(st.preconditioner)
+            if ci == 2 and cond:
+                cs = solver.operator.schur.tocsr()
+                cs.sort_indices()
+                out[f"g{ci}_c{k}_schur_indptr"] = cs.indptr
+                out[f"g{ci}_c{k}_schur_indices"] = cs.indices
+                out[f"g{ci}_c{k}_schur_data"] = cs.data
+            print("sgs", ci, pc, cond, st.iterations, st.preconditioner, flush=True)
+    # explicit_run with the reference default SolverConfig() (dynamics.py:130-170)
+    P = 3
+    prob = problem("SDME_M", P, (3, 2, 2), (1.0, 0.5, 0.5), P + 1, [("xmin", (0, 1, 2))])
+    faces = build_face_tables(prob.mesh, prob.element, "xmax", prob.rule)
+    base = prob.traction_vector(faces, lambda f: np.tile([0.0, 0.0, 2.0e4], (len(f.pts), 1)))
+    traj = explicit_run(prob, lambda t: base * min(t / 5e-5, 1.0), 1e-5, 20)
+    out["explicit_u"] = traj.state.u
+    out["explicit_v"] = traj.state.v
+    out["explicit_rows"] = np.array([(r["step"], r["iterations"]) for r in traj.stats.rows])
+    out["explicit_tags"] = np.array([r["preconditioner"] for r in traj.stats.rows])
+    # newmark_run with SolverConfig() on a 2x2x2 SDME_H P = 3 block under a ramped traction
+    prob = problem("SDME_H", 3, (2, 2, 2), (1.0, 1.0, 1.0), 4, [("xmin", (0, 1, 2))])
+    faces = build_face_tables(prob.mesh, prob.element, "xmax", prob.rule)
+    base = prob.traction_vector(faces, lambda f: np.tile([0.0, 1.0e5, -2.0e5], (len(f.pts), 1)))
+    traj = newmark_run(prob, lambda t: base * min(t / 4e-4, 1.0), 1e-4, 4, newton_tol=1e-8)
+    out["newmark_u"] = traj.state.u
+    out["newmark_v"] = traj.state.v
+    out["newmark_load"] = base
+    out["newmark_newton"] = np.array(traj.newton_iters)
+    out["newmark_rows"] = np.array([(r["step"], r["newton_iter"], r["iterations"]) for r in traj.stats.rows])
+    print("sgs explicit", out["explicit_rows"][:4].tolist(), "newmark", traj.newton_iters,
+          out["newmark_rows"][:, 2].tolist(), flush=True)
+    np.savez_compressed(os.path.join(HERE, "sgs.npz"), **out)
+
+
+def gen_config1_default():
+    """BASELINE config 1 with the reference's DEFAULT solver (SolverConfig():
+    SGS + Schur condensation, tol 1e-12), 10 Newmark steps."""
+    P, m = 4, 6
+    prob = problem("SDME_M", P, (4, 4, 4), (1.0, 1.0, 1.0), m, [("xmin", (0, 1, 2))])
+    faces = build_face_tables(prob.mesh, prob.element, "xmax", prob.rule)
+    base = prob.traction_vector(faces, lambda f: np.tile([0.0, 0.0, 1.0e5], (len(f.pts), 1)))
+    t0 = time.perf_counter()
+    traj = newmark_run(prob, lambda t: base * min(t / 1e-3, 1.0), 1e-4, 10, newton_tol=1e-8)
+    wall = time.perf_counter() - t0
+    rows = [(r["step"], r["newton_iter"], r["iterations"]) for r in traj.stats.rows]
+    np.savez_compressed(os.path.join(HERE, "config1_default.npz"), u=traj.state.u, v=traj.state.v,
+                        a=traj.state.a, newton_iters=np.array(traj.newton_iters), pcg_rows=np.array(rows),
+                        tags=np.array([r["preconditioner"] for r in traj.stats.rows]), wall_s=np.array(wall))
+    print("config1_default", wall, "s", traj.newton_iters, [r[2] for r in rows])
+
+
 if __name__ == "__main__":
     import json
     import sys

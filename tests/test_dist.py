@@ -68,4 +68,10 @@ def test_reference_arm_prints_contract_line():
     line = json.loads(r.stdout.strip().splitlines()[-1])
     for k in ("metric", "value", "unit", "impl", "cpu_baseline", "e2e", "higher_is_better"):
         assert k in line
-    assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "port"
+    # the real reference (baseline/_ref) when installed, else the oracle port
+    from tools import refcpu
+
+    want = "reference" if refcpu.reference_dir() else "port"
+    assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == want
+    assert line["config"]["workload"] == __import__("bench").WORKLOAD
+    assert line["cpu_baseline"]["extrapolated"] is True and line["cpu_baseline"]["measured_elements"] > 0

@@ -87,3 +87,39 @@ def test_newmark_with_reference_objects_matches_reference_run():
     rits = [r["iterations"] for r in ref.stats.rows]
     assert len(its) == len(rits) and max(abs(a - b) for a, b in zip(its, rits)) <= 1
     assert max_rel_err(got.state.u, ref.state.u) <= 1e-9
+
+
+def test_contact_helpers_vs_reference():
+    """GpuPenaltyContact.update_active_set / pressure_profile / evaluate_forces
+    (contact.py:98-151, 186-204) on a problem built by from_reference, against
+    the reference's PenaltyContact on the same FemProblem (tilted plane:
+    partially active surface)."""
+    import_reference()
+    from sdmefem.contact import ContactParams as RP
+    from sdmefem.contact import PenaltyContact, RigidObstacle as RO
+    from sdmefem.meshdof import gen_box_mesh
+
+    from paper_2104_13466_b200 import ContactParams, GpuPenaltyContact, RigidObstacle
+
+    prob = _ref("SDME_M", 3, 4, gen_box_mesh((2, 3, 2), (0.3, 0.45, 0.2)))
+    n = np.array([1.0, 0.15, -0.05])
+    n /= np.linalg.norm(n)
+    point = np.array([1e-4, 0.2, 0.1])
+    ref = PenaltyContact(prob, RO(point, n), RP(1e9), "xmin")
+    gp = from_reference(prob)
+    ours = GpuPenaltyContact(gp, RigidObstacle(point, n), ContactParams(1e9), "xmin")
+    u = 1e-4 * np.random.default_rng(3).uniform(-1, 1, prob.n_free)
+    ra, rg = ref.update_active_set(u)
+    oa, og = ours.update_active_set(u)
+    assert len(rg) == len(og)
+    for a, b, fa, fb in zip(rg, og, ra, oa):
+        assert np.abs(a - b).max() <= 1e-15 + 1e-12 * np.abs(a).max()
+        assert np.array_equal(fa, fb)
+    assert 0 < sum(int(a.sum()) for a in ra) < sum(a.size for a in ra)  # partially active
+    rp, op = ref.pressure_profile(u), ours.pressure_profile(u)
+    ko, kr = np.lexsort((op[:, 1], op[:, 0])), np.lexsort((rp[:, 1], rp[:, 0]))
+    assert np.abs(op[ko] - rp[kr]).max() <= 1e-12 * np.abs(rp).max()
+    fr, fo = ref.evaluate_forces(u), ours.evaluate_forces(u)
+    assert max_rel_err(fo.force, fr.force) <= 1e-12
+    p = np.random.default_rng(4).standard_normal(prob.n_free)
+    assert max_rel_err(fo.stiffness @ p, fr.stiffness @ p) <= 1e-12

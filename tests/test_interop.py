@@ -64,16 +64,21 @@ def test_general_mesh_is_not_a_box():
     assert box_layout(Mesh(3, coords, np.array(box.elems), {})) is None
 
 
-def test_reference_solver_config_is_accepted_and_unsupported_modes_rejected():
+def test_reference_solver_config_is_accepted():
+    """The reference's SolverConfig objects are accepted as they are; its
+    default (SGS + Schur condensation) selects the assembled solver
+    (csrc/schur.cu), diagonal / none without condensation the matrix-free
+    one; unknown preconditioners are rejected like solver.py:122."""
     sd = import_reference()
     from sdmefem.dynamics import SolverConfig as RefCfg
 
     cfg = SolverConfig.coerce(RefCfg(precond="diagonal", tol=1e-10, maxit=500, condense=False))
-    assert cfg == SolverConfig(precond="diagonal", tol=1e-10, maxit=500, condense=False)
-    with pytest.raises(ValueError, match="condense"):
-        make_solver(None, None, 0.0, RefCfg())  # the reference default: sgs + Schur
+    assert cfg == SolverConfig(precond="diagonal", tol=1e-10, maxit=500, condense=False) and not cfg.assembled
+    ref_default = SolverConfig.coerce(RefCfg())
+    assert ref_default == SolverConfig.reference_default() and ref_default.assembled
+    assert SolverConfig(precond="sgs", condense=False).assembled
     with pytest.raises(ValueError, match="preconditioner"):
-        make_solver(None, None, 0.0, SolverConfig(precond="sgs", condense=False))
+        make_solver(None, None, 0.0, SolverConfig(precond="ilu", condense=False))
     with pytest.raises(TypeError):
         SolverConfig.coerce(object())
 
