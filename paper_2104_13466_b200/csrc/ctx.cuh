@@ -73,7 +73,13 @@ struct sdme_ctx {
   bool ev_mode = false;
   bool ev_no_gather = false;
   int pcg_warm = 0;
-  int small_fits = -1;  // pcg_small cluster placement on this device (-1: not queried yet)
+  int small_fits = -1;
+  // programmatic dependent launch of the TMA colour passes (SDME_PDL=0 disables);
+  // pdl_first: the next operator's first pass may overlap the zeroing of y
+  // (k_zero_pdl); capturing: inside a graph capture (PDL off)
+  bool pdl = true;
+  bool pdl_first = false;
+  bool capturing = false;  // pcg_small cluster placement on this device (-1: not queried yet)
   cudaError_t launch_err = cudaSuccess;  // a failed cudaLaunchKernelEx, reported by check_launch  // operator kinds whose launch setup ran (sdme_pcg)
   // instantiated PCG graph, reused while the solve's operands are the same
   cudaGraph_t pcg_graph = nullptr;

@@ -253,7 +253,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
 template <int N, int WPE, int MIR, bool VAL, bool VALS, bool TM = false, int SUB = 1>
 __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& g, double* __restrict__ dst, int X0,
                                              int Y0, int Z0, double* S, int t, double* evb, bool grad,
-                                             const CUtensorMap* ymap = nullptr) {
+                                             const CUtensorMap* ymap = nullptr, bool* waited = nullptr) {
   using L = ColLay<N, VALS, TM>;
   using Mr = Mir<N, MIR>;
   using Mp = Mir<N, 0>;
@@ -378,7 +378,15 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& 
     }
     if (TM) fence_proxy_async_smem();
     group_sync<WPE>(0);
-    if (TM && t == 0 && ymap) tma_reduce_add_box(ymap, S + L::O, X0 & ~1, Y0, Z0, comp);
+    if (TM && t == 0 && ymap) {
+      // first write to y of this CTA: the previous launch on the stream (a
+      // colour pass, or the zeroing of y) has completed (PDL, tma.cuh)
+      if (waited && !*waited) {
+        pdl_wait();
+        *waited = true;
+      }
+      tma_reduce_add_box(ymap, S + L::O, X0 & ~1, Y0, Z0, comp);
+    }
   }
 }
 
@@ -428,6 +436,8 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
   const long long half = threadIdx.x / T;
   int buf = 0;
   if (args.skip && *(volatile const int*)args.skip) return;
+  bool waited = false;  // TM colour passes: griddepcontrol.wait done (thread 0)
+  if (TM) pdl_launch_dependents();
   constexpr bool UPASS = (MODE == MODE_APPLY || MODE == MODE_FINT || MODE == MODE_SETUP);
   constexpr bool PPASS = (MODE == MODE_APPLY || MODE == MODE_PA || MODE == MODE_MASS);
   constexpr bool PGRAD = MODE != MODE_MASS;  // c_m M p alone: values only (B stages), no gradient
@@ -629,7 +639,8 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
     if (MODE == MODE_SETUP) continue;
     double* evb = args.ev ? args.ev + eid * 3 * Q : nullptr;
     col_backward<N, WPE, MIR, VAL, VALS, TM, SUB>(tb, g, args.y, X0, Y0, Z0, S, t, evb, PGRAD,
-                                                  ghost ? nullptr : static_cast<const CUtensorMap*>(args.ty));
+                                                  ghost ? nullptr : static_cast<const CUtensorMap*>(args.ty),
+                                                  &waited);
   }
   // the reduce-adds have completed before the CTA (and its shared memory) retires
   if (TM && t == 0) bulk_wait_all();

@@ -472,15 +472,40 @@ void launch_col_k(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
     else ev_gather<N>(c, a);
     return;
   }
+  // TMA passes: programmatic dependent launch -- pass k+1 starts its u / p
+  // forward work while pass k drains (each CTA waits before its first
+  // reduce-add into y); the first pass too when the launch before it is the
+  // PDL-triggering zeroing of y (c->pdl_first).  Not inside graph capture
+  // (the PCG graph's passes follow kernels that write p).
+  bool pdl = TM && c->pdl && !c->capturing;
+  bool first = true;
   for (int sp = 0; sp < 8 * c->nslab; ++sp) {
     const int col = colour_code(c->geo, sp % 8, sp / 8, c->nslab);
     if (col == -2) continue;
     const long long cnt = colour_count(c->geo, col);
     if (cnt == 0) continue;
     a.colour = col;
-    kern<<<(unsigned)std::min<long long>((cnt + SUB - 1) / SUB, max_blocks), T, smem, c->st>>>(tb, c->geo, a);
+    const unsigned grid = (unsigned)std::min<long long>((cnt + SUB - 1) / SUB, max_blocks);
+    if (pdl && (!first || c->pdl_first)) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(T);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = c->st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tb, c->geo, a);
+      if (e != cudaSuccess && c->launch_err == cudaSuccess) c->launch_err = e;
+    } else {
+      kern<<<grid, T, smem, c->st>>>(tb, c->geo, a);
+    }
+    first = false;
     ++c->launches;
   }
+  c->pdl_first = false;
 }
 
 // TMA box loads / bulk reduce-add (tma.cuh) when every vector of the mode has

@@ -207,8 +207,21 @@ int check_flag(sdme_ctx* ctx) {
 }
 
 // y = A p  with A = c_k K(u) + c_m M (y zeroed first)
-int apply_raw(sdme_ctx* ctx, const double* u, const double* p, double* y, double ck, double cm) {
+// y = 0 before an operator's colour passes: a PDL-triggering kernel, so the
+// first pass overlaps it (box contexts with tensor maps, outside captures)
+int zero_output(sdme_ctx* ctx, double* y) {
+  if (ctx->pdl && !ctx->capturing && !ctx->ev_mode && !ctx->gen && sdme_tmap_of(ctx, y)) {
+    k_zero_pdl<<<148 * 4, 256, 0, ctx->st>>>(y, ctx->nvec);
+    ++ctx->launches;
+    ctx->pdl_first = true;
+    return SDME_OK;
+  }
   CK(cudaMemsetAsync(y, 0, ctx->nvec * sizeof(double), ctx->st));
+  return SDME_OK;
+}
+
+int apply_raw(sdme_ctx* ctx, const double* u, const double* p, double* y, double ck, double cm) {
+  if (int rc = zero_output(ctx, y)) return rc;
   if (ck != 0.0)
     ctx->ops->element(ctx, MODE_APPLY, u, p, y, ck, cm);
   else
@@ -318,7 +331,9 @@ int build_pcg_graph(sdme_ctx* ctx, const double* pu, double* px, double* r, doub
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   const long long l0 = ctx->launches;
   CK(cudaStreamBeginCaptureToGraph(ctx->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  ctx->capturing = true;  // plain launches inside the graph (no PDL edges)
   enqueue_pcg_iteration(ctx, pu, px, r, p, ap, dinv, c_k, c_m, pa, withc, cond, 1);
+  ctx->capturing = false;
   const cudaError_t ce = cudaStreamEndCapture(ctx->st, &body);
   const long long per_iter = ctx->launches - l0;
   ctx->launches = l0;
@@ -359,6 +374,7 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   if (const char* v = getenv("SDME_SLABS")) ctx->nslab = std::max(1, std::min(atoi(v), 64));
   if (const char* v = getenv("SDME_PCG_DIRECT")) ctx->pcg_direct = atoi(v) != 0;
   if (const char* v = getenv("SDME_PA")) ctx->pa = atoi(v) != 0;
+  if (const char* v = getenv("SDME_PDL")) ctx->pdl = atoi(v) != 0;
   ctx->P = d->P;
   ctx->m = d->m;
   ctx->n = d->P + 1;
@@ -476,6 +492,7 @@ int sdme_create_mesh(const sdme_mesh_desc* d, sdme_ctx** out) {
   ctx->gen = true;
   if (const char* v = getenv("SDME_PCG_DIRECT")) ctx->pcg_direct = atoi(v) != 0;
   if (const char* v = getenv("SDME_PA")) ctx->pa = atoi(v) != 0;
+  if (const char* v = getenv("SDME_PDL")) ctx->pdl = atoi(v) != 0;
   const int P = d->P, n = P + 1, m = d->m;
   ctx->P = P;
   ctx->m = m;
@@ -732,7 +749,7 @@ int sdme_fint(sdme_ctx* ctx, int u, int r) {
   if (!pu || !pr) return SDME_BAD_ARGUMENT;
   int rc = reset_flag(ctx);
   if (rc) return rc;
-  CK(cudaMemsetAsync(pr, 0, ctx->nvec * sizeof(double), ctx->st));
+  if ((rc = zero_output(ctx, pr))) return rc;
   ctx->ops->element(ctx, MODE_FINT, pu, nullptr, pr, 1.0, 0.0);
   rc = check_launch(ctx);
   if (rc) return rc;
@@ -1129,7 +1146,7 @@ int sdme_time_op(sdme_ctx* ctx, int op, int u, int p, int y, double c_m, int rep
     switch (op) {
       case 0: apply_raw(ctx, pu, pp, py, 1.0, c_m); break;
       case 1:
-        cudaMemsetAsync(py, 0, ctx->nvec * sizeof(double), ctx->st);
+        zero_output(ctx, py);
         ctx->ops->element(ctx, MODE_FINT, pu, nullptr, py, 1.0, 0.0);
         break;
       case 2: apply_raw(ctx, nullptr, pp, py, 0.0, 1.0); break;
@@ -1143,7 +1160,7 @@ int sdme_time_op(sdme_ctx* ctx, int op, int u, int p, int y, double c_m, int rep
         break;
       case 5:  // K.p (+ c_m M p) from the stored quadrature data (PCG operator)
         if (!ctx->d_qpd) return SDME_BAD_ARGUMENT;
-        cudaMemsetAsync(py, 0, ctx->nvec * sizeof(double), ctx->st);
+        zero_output(ctx, py);
         ctx->ops->element(ctx, MODE_PA, pu, pp, py, 1.0, c_m);
         break;
       default: return SDME_BAD_ARGUMENT;

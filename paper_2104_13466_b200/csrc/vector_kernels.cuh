@@ -247,6 +247,15 @@ __global__ void k_zero(double* __restrict__ y, long long n, const int* status) {
     y[i] = 0.0;
 }
 
+// y = 0, letting the next launch (the first colour pass of an operator, PDL)
+// start at once; that pass waits for this grid before writing y
+__global__ void k_zero_pdl(double* __restrict__ y, long long n) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = 0.0;
+}
+
 // x = value on free points, 0 on constrained
 __global__ void k_fill_masked(double* __restrict__ x, const unsigned char* __restrict__ freemask, double value,
                               long long n) {

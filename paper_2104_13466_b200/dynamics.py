@@ -142,7 +142,7 @@ def newmark_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
                 cfg: SolverConfig | None = None, gamma: float = 0.5, beta: float = 0.25,
                 contact=None, snapshot_stride: int = 0, track_energy: bool = False) -> Trajectory:
     """Implicit Newmark with Newton-Raphson (``dynamics.py:173-257``)."""
-    cfg = SolverConfig.coerce(cfg) or SolverConfig(precond="diagonal", tol=1e-10, condense=False)
+    cfg = SolverConfig.coerce(cfg) or SolverConfig()  # the reference's default: SGS + Schur
     cfg.validate()
     nm = NewmarkCoeffs(dt, gamma, beta)
     pb = problem
@@ -430,7 +430,7 @@ def explicit_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
 def _explicit_consistent(pb: GpuFemProblem, external_load, dt, n_steps, u0, v0, cfg, snapshot_stride):
     """``explicit_run`` of the reference with a full (uncondensed) Jacobi-PCG
     mass solve per step (``dynamics.py:147-170``)."""
-    cfg = SolverConfig.coerce(cfg) or SolverConfig(precond="diagonal", tol=1e-12, condense=False)
+    cfg = SolverConfig.coerce(cfg) or SolverConfig()  # the reference's default: SGS + Schur
     cfg.validate()
     u = _dev(pb, u0)
     v = _dev(pb, v0)

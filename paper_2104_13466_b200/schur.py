@@ -35,6 +35,20 @@ __all__ = ["SchurSolver", "schur_tables"]
 _PREC = {"none": 0, None: 0, "diagonal": 1, "sgs": 2, "gauss-seidel": 2}
 
 
+def _device_memory():
+    """(free, total) bytes of the current device (cudaMemGetInfo via the runtime)."""
+    try:
+        import ctypes.util
+
+        rt = C.CDLL(ctypes.util.find_library("cudart") or "libcudart.so")
+    except OSError:
+        return float("inf"), float("inf")
+    f, t = C.c_size_t(0), C.c_size_t(0)
+    if rt.cudaMemGetInfo(C.byref(f), C.byref(t)) != 0:
+        return float("inf"), float("inf")
+    return float(f.value), float(t.value)
+
+
 def schur_tables(pb: GpuFemProblem):
     """(G, N, wdet) of the problem's rule in the reference orders: points
     (a, b, c) with c fastest and a along x (tensorelem.py:156-182), local
@@ -133,6 +147,12 @@ class SchurSolver:
         if nb and (addr_b < 0).any():
             raise AssertionError("system DOF without a lattice point")
         G, N, wdet = schur_tables(pb)
+        need = 8 * ne * ((3 * nf) ** 2 + G.shape[0] * 3 * nf) * 1.5
+        free_b, total_b = _device_memory()
+        if need > 0.8 * free_b:
+            raise MemoryError(f"the assembled solver needs ~{need / 2**30:.1f} GiB of element matrices "
+                              f"({ne} elements of {3 * nf} DOFs; {free_b / 2**30:.1f} GiB free): use the "
+                              "matrix-free path, SolverConfig(precond=\"diagonal\", condense=False)")
         self._keep = [np.ascontiguousarray(addr.reshape(ne, -1)), np.ascontiguousarray(role.reshape(ne, -1),
                                                                                         dtype=np.int32),
                       np.ascontiguousarray(addr_b), G, N, wdet]

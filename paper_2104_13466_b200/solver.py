@@ -63,13 +63,15 @@ class SolverConfig:
     D3); ``precond="sgs"`` and / or ``condense=True`` select the assembled
     path, the reference's default solver (:class:`~.schur.SchurSolver`: dense
     element matrices, Schur condensation, level-scheduled SGS on the device),
-    sized like the reference.  This class defaults to the matrix-free path;
-    ``SolverConfig.reference_default()`` is the reference's own default."""
+    sized like the reference.  The defaults are the reference's (SGS with
+    Schur condensation, tol 1e-12), so ``SolverConfig()`` and drivers called
+    without ``cfg`` behave as the reference does; pass ``precond="diagonal",
+    condense=False`` for the matrix-free path on large meshes."""
 
-    precond: str = "diagonal"
+    precond: str = "sgs"
     tol: float = 1e-12
     maxit: int = 200000
-    condense: bool = False
+    condense: bool = True
 
     @classmethod
     def coerce(cls, cfg) -> "SolverConfig | None":
@@ -87,6 +89,11 @@ class SolverConfig:
     def reference_default(cls) -> "SolverConfig":
         """``sdmefem.dynamics.SolverConfig()``: SGS, Schur condensation, tol 1e-12."""
         return cls(precond="sgs", tol=1e-12, maxit=200000, condense=True)
+
+    @classmethod
+    def matrix_free(cls, tol: float = 1e-10, maxit: int = 200000) -> "SolverConfig":
+        """Jacobi-PCG on the matrix-free operator: any mesh size."""
+        return cls(precond="diagonal", tol=tol, maxit=maxit, condense=False)
 
     @property
     def assembled(self) -> bool:
