@@ -391,14 +391,17 @@ def run_ours(args):
     fp64_peak = peaks.get("fp64_tflops")
     achieved = flops / t_step / 1e12
     traffic = None
-    try:  # DRAM bytes of one K.p (8 colour launches) from the committed ncu capture
-        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")))
-        traffic = tr["kp"]["traffic_bytes"]
-    except Exception:
-        pass
+    traffic_src = None
+    for name in ("ncu_traffic_r02.json", "ncu_traffic_r01.json"):  # DRAM bytes of one K.p (8 colour launches)
+        try:
+            traffic = json.load(open(os.path.join(ROOT, "profiles", name)))["kp"]["traffic_bytes"]
+            traffic_src = "profiles/" + name
+            break
+        except Exception:
+            pass
     roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": achieved / fp64_peak if fp64_peak else None, "traffic": traffic,
-            "traffic_note": "dram read+write bytes per K.p (8 launches), profiles/ncu_traffic_r01.json; "
+            "traffic_note": f"dram read+write bytes per K.p (8 launches), {traffic_src}; "
                             "algorithmic bytes = algorithmic_bytes_per_step",
             "peak_source": "profiles/fp64_peak.json (measured DFMA chain on this pool's B200: the pipe the "
                            "kernels use; the FP64 tensor-core DMMA peak, profiles/dmma_peak.json, is 1.09x "

@@ -10,7 +10,10 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_launch.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --cache-control none -c 24 --csv --log-file gpurun_out/traffic.csv python tools/prof_variant.py > gpurun_out/ncu_traffic.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --cache-control none -k regex:element_col -c 24 --csv --log-file gpurun_out/traffic.csv python tools/prof_variant.py > gpurun_out/ncu_traffic.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:element_col -c 1 -o gpurun_out/kp -f python tools/prof_apply.py > gpurun_out/ncu_full.log 2>&1
-timeout 1500 python tools/run_configs.py c1 c3 c4 c5 > gpurun_out/configs.jsonl 2> gpurun_out/configs.err
+timeout 1500 python tools/run_configs.py c1 c3 c4 c5 --cpu > gpurun_out/configs.jsonl 2> gpurun_out/configs.err
 timeout 600 python tools/gen_mesh_bench.py 32 48 > gpurun_out/gen_mesh.jsonl 2> gpurun_out/gen_mesh.err
+# checked build (device bounds / alignment asserts; compute-sanitizer is closed on this pool)
+SDME_LIB=paper_2104_13466_b200/libsdme_checked.so timeout 900 python tools/sanitize_cases.py > gpurun_out/checked_cases.log 2>&1; echo "exit $?" >> gpurun_out/checked_cases.log
+SDME_LIB=paper_2104_13466_b200/libsdme_checked.so timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/checked_pytest.log 2>&1; echo "exit $?" >> gpurun_out/checked_pytest.log
