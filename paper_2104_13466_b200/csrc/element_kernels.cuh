@@ -113,10 +113,22 @@ __device__ __forceinline__ bool colour_element(const Geo& g, int colour, long lo
   // in alternating directions (odd popcount = odd pass), so a pass starts
   // where the previous one ended and finds their shared faces still in L2
   if (g.serp && (__popc(colour & 7) & 1)) idx = cnt - 1 - idx;
-  const int ix = (int)(idx % nex);
-  const long long r = idx / nex;
-  const int iy = (int)(r % ney);
-  const int iz = izlo + (int)(r / ney);
+  int ix, iy, iz;
+  if (cnt <= 0x7fffffffLL) {
+    // 32-bit unsigned division (a 64-bit divide is a ~70-instruction
+    // subroutine, and this runs twice per element: current and next)
+    const unsigned id = (unsigned)idx, ux = (unsigned)nex, uy = (unsigned)ney;
+    const unsigned r = id / ux;
+    ix = (int)(id - r * ux);
+    const unsigned q = r / uy;
+    iy = (int)(r - q * uy);
+    iz = izlo + (int)q;
+  } else {
+    ix = (int)(idx % nex);
+    const long long r = idx / nex;
+    iy = (int)(r % ney);
+    iz = izlo + (int)(r / ney);
+  }
   ei = 2 * ix + cx;
   ej = 2 * iy + cy;
   ek = 2 * iz + cz;
