@@ -83,6 +83,13 @@ typedef struct {
   const int64_t* asm_ptr;   /* n_free + 1: CSR of element-vector slots per free DOF  */
   const int32_t* asm_slot;  /* asm_ptr[n_free]: 2*slot + (sign < 0), element order  */
   const double* geom;    /* n_elems x 10 x m^3: J^-1[d][c] (slot 3d + c), w det J    */
+  /* optional locality layout (NULL = identity): the element rows of dof / geom
+   * and the slots of asm_slot refer to STORAGE positions; elem_id[s] is the
+   * reference element id stored at position s (inversion errors report it),
+   * asm_rows[r] the free DOF of CSR row r.  Summation order per DOF is still
+   * the reference's element order, so results do not depend on the layout. */
+  const int32_t* elem_id;
+  const int32_t* asm_rows;
 } sdme_mesh_desc;
 
 /* lifecycle ------------------------------------------------------------- */

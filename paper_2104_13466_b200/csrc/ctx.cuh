@@ -131,6 +131,8 @@ struct sdme_ctx {
   long long* d_aptr = nullptr;    // assembly CSR over free DOFs
   int* d_aslot = nullptr;
   double* d_geom = nullptr;       // [elem][10][Q] J^-1, w det J
+  int* d_elem_id = nullptr;       // storage position -> reference element id (nullptr: identity)
+  int* d_asm_rows = nullptr;      // assembly CSR row -> free DOF (nullptr: identity)
   double* d_evu = nullptr;        // gathered element boxes of u and p
   double* d_evp = nullptr;
 };

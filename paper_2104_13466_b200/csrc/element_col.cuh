@@ -552,7 +552,8 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
         qp_k(Hu[r], s);
         if (!(s.det > 0.0)) {
           const int a = q % N, b = (q / N) % N, c = q / (N * N);
-          atomicMin(args.inv_flag, (unsigned long long)eid * Q + (unsigned long long)((a * N + b) * N + c));
+          const long long ref = (GEN && args.elem_id) ? (long long)__ldg(args.elem_id + eid) : eid;
+          atomicMin(args.inv_flag, (unsigned long long)ref * Q + (unsigned long long)((a * N + b) * N + c));
         }
       }
       if (MODE == MODE_SETUP) {

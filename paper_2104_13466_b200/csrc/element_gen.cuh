@@ -34,16 +34,18 @@ static __global__ void __launch_bounds__(256) k_gen_gather(double* __restrict__ 
 }
 
 // y[f] += sum_k sign_k ev[slot_k] over the CSR entries of f (increasing element);
-// unsigned for a diagonal (sign_k^2 = 1)
+// unsigned for a diagonal (sign_k^2 = 1).  CSR row r belongs to DOF rows[r]
+// (rows: the locality order of the rows, nullptr = identity)
 static __global__ void __launch_bounds__(256) k_gen_assemble(double* __restrict__ y, const double* __restrict__ ev,
                                                       const long long* __restrict__ ptr,
                                                       const int* __restrict__ slot, long long n, const int* skip,
-                                                      bool diagonal = false) {
+                                                      bool diagonal = false, const int* __restrict__ rows = nullptr) {
   if (skip && *(volatile const int*)skip) return;
-  for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < n;
-       f += (long long)gridDim.x * blockDim.x) {
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (long long)gridDim.x * blockDim.x) {
+    const long long f = rows ? __ldg(rows + r) : r;
     double s = 0.0;
-    for (long long k = __ldg(ptr + f), e = __ldg(ptr + f + 1); k < e; ++k) {
+    for (long long k = __ldg(ptr + r), e = __ldg(ptr + r + 1); k < e; ++k) {
       const int sl = __ldg(slot + k);
       const double v = __ldg(ev + (sl >> 1));
       s += ((sl & 1) && !diagonal) ? -v : v;
@@ -111,7 +113,8 @@ __global__ void __launch_bounds__(32 * WPE, 1) element_diag_gen(const __grid_con
         qp_state(H, g.mu, g.lam, st);
         if (!(st.detF > 0.0)) {
           const int a = q % N, b = (q / N) % N, c = q / (N * N);
-          atomicMin(args.inv_flag, (unsigned long long)eid * Q + (unsigned long long)((a * N + b) * N + c));
+          const long long ref = args.elem_id ? __ldg(args.elem_id + eid) : eid;
+          atomicMin(args.inv_flag, (unsigned long long)ref * Q + (unsigned long long)((a * N + b) * N + c));
         }
         const double cc = g.mu - g.lam * st.lnJ;
 #pragma unroll

@@ -68,6 +68,7 @@ struct OpArgs {
   // general meshes (element_gen.cuh): per element and point J^-1 (9 slots) and
   // w det J ([elem][10][Q]); u / p are then E-vector boxes [elem][comp][Q]
   const double* geo = nullptr;
+  const int* elem_id = nullptr;  // general meshes: reference element id of a storage position (nullptr: same)
 };
 
 __device__ __forceinline__ bool constrained(const Geo& g, int comp, int X, int Y, int Z) {

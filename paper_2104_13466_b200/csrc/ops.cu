@@ -26,7 +26,14 @@
 #endif
 
 #ifndef SDME_GEN_MINB
-#define SDME_GEN_MINB 1  // resident blocks per SM asked of the general-mesh P = 4 kernels
+// resident blocks per SM asked of the general-mesh P = 4 kernels: K.p from u
+// at the 168-register cap of 11-12 warps (12.5 -> 13.5 GDOF/s at 32^3,
+// tools/gen_mesh_bench.py); f_int and the stored-data operator unconstrained
+// (188 registers; the PA operator is 5% slower at the cap)
+#define SDME_GEN_MINB 1
+#endif
+#ifndef SDME_GEN_APPLY_MINB
+#define SDME_GEN_APPLY_MINB 11
 #endif
 
 #ifndef SDME_ORDER
@@ -629,7 +636,8 @@ void launch_col_gen(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
   constexpr int WPE = LargeShape<N, N>::WPE;
   constexpr int T = 32 * WPE;
   constexpr int smem = ColLay<N, VAL>::PER * 8;
-  auto kern = element_col<N, WPE, (WPE == 1 ? SDME_GEN_MINB : 1), MODE, VAL, MIR, false, true>;
+  constexpr int MINB = WPE != 1 ? 1 : (MODE == MODE_APPLY ? SDME_GEN_APPLY_MINB : SDME_GEN_MINB);
+  auto kern = element_col<N, WPE, MINB, MODE, VAL, MIR, false, true>;
   static PerDevice grid_cache;  // per device: attribute + occupancy set once
   const int max_blocks = resident_grid(grid_cache, kern, T, smem);
   a.colour = -1;
@@ -658,6 +666,7 @@ void gen_element_impl(sdme_ctx* c, int mode, const double* u, const double* p, d
   const int* skip = c->cur_skip;
   OpArgs a{c->d_evu, c->d_evp, y, ck, cm, -1, c->d_flag, skip};
   a.geo = c->d_geom;
+  a.elem_id = c->d_elem_id;
   a.qpd = c->d_qpd;
   a.ev = c->d_ev;
   if (mode == MODE_FINT || mode == MODE_APPLY || mode == MODE_SETUP) {
@@ -671,7 +680,8 @@ void gen_element_impl(sdme_ctx* c, int mode, const double* u, const double* p, d
   if (c->mir == 0) gen_modes<N, 0>(c, mode, a);
   else gen_modes<N, 1>(c, mode, a);
   if (mode != MODE_SETUP) {
-    k_gen_assemble<<<gen_grid(c->nvec), 256, 0, c->st>>>(y, c->d_ev, c->d_aptr, c->d_aslot, c->nvec, skip);
+    k_gen_assemble<<<gen_grid(c->nvec), 256, 0, c->st>>>(y, c->d_ev, c->d_aptr, c->d_aslot, c->nvec, skip, false,
+                                                         c->d_asm_rows);
     ++c->launches;
   }
 }
@@ -711,6 +721,7 @@ void gen_diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm
   const long long ns = (long long)c->geo.nx * 3 * Q;
   OpArgs a{c->d_evu, nullptr, d, ck, cm, -1, c->d_flag};
   a.geo = c->d_geom;
+  a.elem_id = c->d_elem_id;
   a.ev = c->d_ev;
   if (ck != 0.0) {
     k_gen_gather<<<gen_grid(ns), 256, 0, c->st>>>(c->d_evu, u, c->d_dof, ns, nullptr);
@@ -719,7 +730,7 @@ void gen_diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm
   if (c->mir == 0) gen_diag_launch<N, 0>(c, a);
   else gen_diag_launch<N, 1>(c, a);
   k_gen_assemble<<<gen_grid(c->nvec), 256, 0, c->st>>>(d, c->d_ev, c->d_aptr, c->d_aslot, c->nvec, nullptr,
-                                                       true);
+                                                       true, c->d_asm_rows);
   ++c->launches;
 }
 

@@ -551,6 +551,12 @@ int sdme_create_mesh(const sdme_mesh_desc* d, sdme_ctx** out) {
        cudaMemcpy(ctx->d_aslot, d->asm_slot, nnz * sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
        cudaMemcpy(ctx->d_geom, d->geom, d->n_elems * 10 * g.Ns * sizeof(double), cudaMemcpyHostToDevice) ==
            cudaSuccess;
+  if (ok && d->elem_id)
+    ok = cudaMalloc(&ctx->d_elem_id, d->n_elems * sizeof(int)) == cudaSuccess &&
+         cudaMemcpy(ctx->d_elem_id, d->elem_id, d->n_elems * sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess;
+  if (ok && d->asm_rows)
+    ok = cudaMalloc(&ctx->d_asm_rows, d->n_free * sizeof(int)) == cudaSuccess &&
+         cudaMemcpy(ctx->d_asm_rows, d->asm_rows, d->n_free * sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess;
   if (!ok) return fail(SDME_CUDA_ERROR);
   *out = ctx;
   return SDME_OK;
@@ -569,6 +575,8 @@ int sdme_destroy(sdme_ctx* ctx) {
   cudaFree(ctx->d_dof);
   cudaFree(ctx->d_aptr);
   cudaFree(ctx->d_aslot);
+  cudaFree(ctx->d_elem_id);
+  cudaFree(ctx->d_asm_rows);
   cudaFree(ctx->d_geom);
   cudaFree(ctx->d_evu);
   cudaFree(ctx->d_evp);

@@ -459,3 +459,45 @@ def kernel_tables(dm: MeshDofMap):
     if slot.size and slot.max() >= 2 ** 31:
         raise MeshError("mesh too large for 32-bit element-vector slots")
     return dof.reshape(ne, 3, n, n, n), ptr, slot.astype(np.int32)
+
+
+def locality_order(mesh: HexMesh, dm: MeshDofMap, ptr: np.ndarray, slot: np.ndarray, n_box: int):
+    """Storage order of the element boxes and of the assembly rows for memory
+    locality (pure data placement: the per-DOF summation order, i.e. the
+    reference's element order, is unchanged, so results are bit-identical).
+
+    Elements are stored along a Morton (Z-order) curve of their centroids, so
+    the boxes a DOF gathers from lie close together; the assembly CSR rows are
+    visited in the order of their first stored element.  Returns (perm, rows,
+    ptr2, slot2): storage position -> element id, CSR row -> free DOF, and the
+    CSR re-laid in that row order with slots pointing into the permuted boxes
+    (``n_box`` = doubles per element box)."""
+    cent = mesh.coords[mesh.elems].mean(axis=1)
+    lo, hi = cent.min(axis=0), cent.max(axis=0)
+    q = np.floor((cent - lo) / np.maximum(hi - lo, 1e-300) * 1023.0).astype(np.int64)
+
+    def spread(v):  # 10 bits -> every third bit
+        v = (v | (v << 16)) & 0x030000FF
+        v = (v | (v << 8)) & 0x0300F00F
+        v = (v | (v << 4)) & 0x030C30C3
+        return (v | (v << 2)) & 0x09249249
+
+    code = spread(q[:, 0]) | (spread(q[:, 1]) << 1) | (spread(q[:, 2]) << 2)
+    perm = np.argsort(code, kind="stable")
+    pos = np.empty_like(perm)
+    pos[perm] = np.arange(len(perm))
+    s = slot.astype(np.int64)
+    flat = s >> 1
+    e, j = flat // n_box, flat % n_box
+    s2 = ((pos[e] * n_box + j) << 1) | (s & 1)
+    n_free = len(ptr) - 1
+    counts = np.diff(ptr)
+    first = np.full(n_free, np.iinfo(np.int64).max)
+    row_of = np.repeat(np.arange(n_free), counts)
+    np.minimum.at(first, row_of, pos[e])
+    rows = np.argsort(first, kind="stable")
+    ptr2 = np.zeros(n_free + 1, dtype=np.int64)
+    np.cumsum(counts[rows], out=ptr2[1:])
+    lens = counts[rows]
+    take = np.repeat(ptr[rows] - ptr2[:-1], lens) + np.arange(ptr2[-1])
+    return perm.astype(np.int32), rows.astype(np.int32), ptr2, s2[take].astype(np.int32)

@@ -22,7 +22,8 @@ import numpy as np
 
 from . import native
 from .basis import Basis1D, Rule, gauss_rule
-from .mesh import HexMesh, FACE_TABLE, MeshError, build_mesh_dofmap, element_tables, kernel_tables, _jacobians
+from .mesh import (HexMesh, FACE_TABLE, MeshError, build_mesh_dofmap, element_tables, kernel_tables, _jacobians,
+                   locality_order)
 from .problem import GpuFemProblem, NeoHookean
 
 __all__ = ["GpuMeshProblem"]
@@ -35,7 +36,7 @@ class GpuMeshProblem(GpuFemProblem):
     (``meshdof.py:404-409``)."""
 
     def __init__(self, mesh: HexMesh, basis: Basis1D, mat: NeoHookean, rule: Rule | None = None, dirichlet=None,
-                 tables=None):
+                 tables=None, locality: bool = True):
         self.mesh = mesh
         self.basis = basis
         self.mat = mat
@@ -53,6 +54,13 @@ class GpuMeshProblem(GpuFemProblem):
         self.n_lattice = self.n_free
         geom = element_tables(mesh, self.rule)
         dof, ptr, slot = kernel_tables(self.dofmap)
+        order = rows = None
+        if locality:
+            # element boxes along a Morton curve, assembly rows in box order
+            # (placement only: per-DOF sums keep the reference element order)
+            n_box = 3 * (self.P + 1) ** 3
+            order, rows, ptr, slot = locality_order(mesh, self.dofmap, ptr, slot, n_box)
+            dof, geom = dof[order], geom[order]
         d = native.MeshDesc()
         d.P, d.m, d.n_elems = self.P, self.m, mesh.n_elems
         self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (self.B, self.D, self.w)]
@@ -61,6 +69,10 @@ class GpuMeshProblem(GpuFemProblem):
         d.n_free = self.n_free
         tabs = [np.ascontiguousarray(dof, dtype=np.int32), np.ascontiguousarray(ptr, dtype=np.int64),
                 np.ascontiguousarray(slot, dtype=np.int32), np.ascontiguousarray(geom, dtype=np.float64)]
+        if order is not None:
+            tabs += [np.ascontiguousarray(order, dtype=np.int32), np.ascontiguousarray(rows, dtype=np.int32)]
+            d.elem_id = tabs[4].ctypes.data_as(C.POINTER(C.c_int32))
+            d.asm_rows = tabs[5].ctypes.data_as(C.POINTER(C.c_int32))
         d.dof = tabs[0].ctypes.data_as(C.POINTER(C.c_int32))
         d.asm_ptr = tabs[1].ctypes.data_as(C.POINTER(C.c_int64))
         d.asm_slot = tabs[2].ctypes.data_as(C.POINTER(C.c_int32))

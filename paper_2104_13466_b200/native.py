@@ -44,7 +44,8 @@ class MeshDesc(C.Structure):
     """``sdme_mesh_desc`` (include/sdme.h): general hexahedral mesh context."""
     _fields_ = [("P", C.c_int), ("m", C.c_int), ("n_elems", C.c_int64), ("B", _dp), ("D", _dp), ("w", _dp),
                 ("mu", C.c_double), ("lambda_lame", C.c_double), ("rho0", C.c_double), ("n_free", C.c_int64),
-                ("dof", _i32p), ("asm_ptr", _i64p), ("asm_slot", _i32p), ("geom", _dp)]
+                ("dof", _i32p), ("asm_ptr", _i64p), ("asm_slot", _i32p), ("geom", _dp),
+                ("elem_id", _i32p), ("asm_rows", _i32p)]
 
 
 class SchurDesc(C.Structure):

@@ -84,6 +84,28 @@ def test_inversion_reports_element():
     assert 0 <= ei.value.elem_id < pb.mesh.n_elems
 
 
+def test_locality_layout_is_bit_identical_and_reports_reference_elements():
+    """The Morton-ordered storage of element boxes / assembly rows
+    (mesh.locality_order) only moves data: f_int, K.p, the diagonal and a PCG
+    solve are bit-identical to the unpermuted layout, and an inversion names
+    the same (reference-order) element and point."""
+    g, key, pb = gpu_case(golden_mesh_cases()[3])
+    mesh, basis, dr = case_setup(g, key)
+    plain = GpuMeshProblem(mesh, basis, MAT, dirichlet=dr, locality=False)
+    u, p, cm = g[f"{key}_u"], g[f"{key}_p"], float(g[f"{key}_cm"])
+    for a, b in ((pb.internal_force(u), plain.internal_force(u)), (pb.apply_tangent(u, p, cm), plain.apply_tangent(u, p, cm)),
+                 (pb.tangent_diagonal(u, cm), plain.tangent_diagonal(u, cm)),
+                 (pcg_gpu(pb, u, p, c_m=cm, tol=1e-10)[0], pcg_gpu(plain, u, p, c_m=cm, tol=1e-10)[0])):
+        assert np.array_equal(a.view(np.int64), b.view(np.int64))
+    big = 5.0 * np.random.default_rng(0).uniform(-1, 1, pb.n_free)
+    errs = []
+    for q in (pb, plain):
+        with pytest.raises(ElementInversionError) as ei:
+            q.internal_force(big)
+        errs.append((ei.value.elem_id, ei.value.qp))
+    assert errs[0] == errs[1]
+
+
 def test_newmark_on_general_mesh_vs_reference():
     """newmark_run (dynamics.py:173-257) on a renumbered, rotated, perturbed
     mesh with a traction on xmax: the load vector (femcore.py:215-259,

@@ -66,7 +66,8 @@ def main():
     for n in sizes:
         t0 = time.perf_counter()
         mesh = general_box(n)
-        pb = GpuMeshProblem(mesh, basis, MAT, dirichlet=[("xmin", (0, 1, 2))])
+        pb = GpuMeshProblem(mesh, basis, MAT, dirichlet=[("xmin", (0, 1, 2))],
+                            locality=os.environ.get("GEN_LOCALITY", "1") == "1")
         setup_s = time.perf_counter() - t0
         rng = np.random.default_rng(0)
         u = pb.vector(1e-3 / n * rng.uniform(-1, 1, pb.n_free))
