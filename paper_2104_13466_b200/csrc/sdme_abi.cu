@@ -371,7 +371,10 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   sdme_ctx* ctx = new sdme_ctx();
   ctx->ops = ops;
   if (const char* v = getenv("SDME_VARIANT")) ctx->variant = atoi(v);
-  if (const char* v = getenv("SDME_SLABS")) ctx->nslab = std::max(1, std::min(atoi(v), 64));
+  if (const char* v = getenv("SDME_SLABS")) {
+    ctx->nslab = std::max(1, std::min(atoi(v), 64));
+    ctx->nslab_env = true;
+  }
   if (const char* v = getenv("SDME_PCG_DIRECT")) ctx->pcg_direct = atoi(v) != 0;
   if (const char* v = getenv("SDME_PA")) ctx->pa = atoi(v) != 0;
   if (const char* v = getenv("SDME_PDL")) ctx->pdl = atoi(v) != 0;

@@ -14,7 +14,7 @@ u = pb.vector().set_lattice(u_lat)
 p = pb.vector().set_lattice(p_lat)
 y = pb.vector()
 out = {}
-for op in ("apply", "fint", "mass", "setup", "apply_pa"):
+for op in ("apply", "fint", "mass", "setup", "apply_pa", "diag"):
     pb.time_op(op, u, p, y, 1e3 if op == "mass" else 0.0, 2)
     out[op] = round(pb.time_op(op, u, p, y, 1e3 if op == "mass" else 0.0, 10), 4)
 print(os.environ.get("SDME_VARIANT", "0"), out)
