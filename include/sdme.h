@@ -142,6 +142,13 @@ int sdme_mass(sdme_ctx* ctx, int a, int y);
  * fixed-order reduction */
 int sdme_strain_energy(sdme_ctx* ctx, int u, double* out);
 
+/* one Newton iterate of newmark_run (dynamics.py:213-226) with one host
+ * synchronisation: [uk += du if du >= 0]; atr = b1 (uk - u) - b2 v - b3 a;
+ * psi = s_load * load - f_int(uk) - M atr (load may be -1); *norm = ||psi||;
+ * tmp is scratch.  SDME_INVERSION as sdme_fint. */
+int sdme_newmark_residual(sdme_ctx* ctx, int uk, int du, int u, int v, int a, int load, double s_load, double b1,
+                          double b2, double b3, int atr, int tmp, int psi, double* norm);
+
 /* d = diag(c_k K_T(u) + c_m M) on free points -- a.diagonal() (solver.py:106) */
 int sdme_diag(sdme_ctx* ctx, int u, double c_k, double c_m, int d);
 

@@ -786,6 +786,52 @@ int sdme_mass(sdme_ctx* ctx, int a, int y) {
   return apply_raw(ctx, nullptr, pa, py, 0.0, 1.0);
 }
 
+// One Newton iterate's residual of newmark_run (dynamics.py:213-226) as one
+// enqueued sequence with a single host synchronisation: [uk += du]; tmp = uk -
+// u; atr = b1 tmp - b2 v - b3 a; tmp = f_int(uk); psi = M atr; psi = s load -
+// tmp - psi; ||psi||.  The same kernels in the same order as the separate
+// calls, so results are bit-identical to them.
+int sdme_newmark_residual(sdme_ctx* ctx, int uk, int du, int u, int v, int a, int load, double s_load, double b1,
+                          double b2, double b3, int atr, int tmp, int psi, double* norm) {
+  if (!ctx || !norm) return SDME_BAD_ARGUMENT;
+  double *puk = vec(ctx, uk), *pu = vec(ctx, u), *pv = vec(ctx, v), *pa = vec(ctx, a);
+  double *patr = vec(ctx, atr), *ptmp = vec(ctx, tmp), *ppsi = vec(ctx, psi);
+  double* pdu = du >= 0 ? vec(ctx, du) : nullptr;
+  double* pl = load >= 0 ? vec(ctx, load) : nullptr;
+  if (!puk || !pu || !pv || !pa || !patr || !ptmp || !ppsi || (du >= 0 && !pdu) || (load >= 0 && !pl))
+    return SDME_BAD_ARGUMENT;
+  const int grid = grid_for(ctx->nvec);
+  auto lincomb = [&](double* y, std::initializer_list<std::pair<double, const double*>> terms) {
+    LinComb lc{};
+    lc.nt = 0;
+    for (auto& t : terms) {
+      lc.c[lc.nt] = t.first;
+      lc.x[lc.nt] = t.second;
+      ++lc.nt;
+    }
+    k_lincomb<<<grid, 256, 0, ctx->st>>>(lc, y, ctx->nvec);
+    ++ctx->launches;
+  };
+  if (pdu) lincomb(puk, {{1.0, puk}, {1.0, pdu}});
+  lincomb(ptmp, {{1.0, puk}, {-1.0, pu}});
+  lincomb(patr, {{b1, ptmp}, {-b2, pv}, {-b3, pa}});
+  int rc = reset_flag(ctx);
+  if (rc) return rc;
+  if ((rc = zero_output(ctx, ptmp))) return rc;
+  ctx->ops->element(ctx, MODE_FINT, puk, nullptr, ptmp, 1.0, 0.0);
+  if ((rc = apply_raw(ctx, nullptr, patr, ppsi, 0.0, 1.0))) return rc;
+  if (pl)
+    lincomb(ppsi, {{s_load, pl}, {-1.0, ptmp}, {-1.0, ppsi}});
+  else
+    lincomb(ppsi, {{-1.0, ptmp}, {-1.0, ppsi}});
+  if ((rc = dot_into(ctx, ppsi, ppsi, S_SCRATCH))) return rc;
+  CK(cudaMemcpyAsync(ctx->h_flag, ctx->d_flag, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->st));
+  if ((rc = read_scalars(ctx)) || (rc = check_launch(ctx))) return rc;
+  if ((rc = flag_error(ctx, ctx->h_flag[0]))) return rc;
+  *norm = std::sqrt(ctx->h_scal[S_SCRATCH]);
+  return SDME_OK;
+}
+
 int sdme_diag(sdme_ctx* ctx, int u, double c_k, double c_m, int d) {
   double* pu = ctx ? vec(ctx, u) : nullptr;
   double* pd = ctx ? vec(ctx, d) : nullptr;

@@ -130,6 +130,22 @@ class _Load:
         return self.vec
 
 
+def _fused_residual(pb, lib, uk, du, u, v, a, load, t_next, nm, atr, tmp, psi) -> float:
+    """``residual`` + ``psi.norm()`` of one Newton iterate without contact, as
+    one native call (``sdme_newmark_residual``; bit-identical to the separate calls)."""
+    import ctypes as C
+
+    if load.scaled:
+        lid, s = load.base.vid, float(load.fn.scale(t_next))
+    else:
+        lid, s = load.at(t_next).vid, 1.0
+    out = C.c_double(0.0)
+    native.check(pb._ctx, lib.sdme_newmark_residual(pb._ctx, uk.vid, du.vid if du is not None else -1, u.vid, v.vid,
+                                                    a.vid, lid, s, nm.b1, nm.b2, nm.b3, atr.vid, tmp.vid, psi.vid,
+                                                    C.byref(out)), "newmark residual")
+    return out.value
+
+
 def _dev(problem, x) -> DeviceVector:
     v = DeviceVector(problem)
     if x is not None:
@@ -188,12 +204,21 @@ def newmark_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
         uk.copy_from(u)
         psi_ref = None
         n_newton = 0
+        pending = False  # uk += du folded into the next fused residual
         for k in range(newton_maxit):
-            # a_trial = b1 (uk - u) - b2 v - b3 a  (difference first, as dynamics.py:219)
-            tmp.assign(1.0, uk, -1.0, u)
-            atr.assign(nm.b1, tmp, -nm.b2, v, -nm.b3, a)
-            contact_ok, active = residual(uk, atr, t_next)
-            rnorm = psi.norm()
+            if contact is None:
+                # one enqueued sequence + one host sync (sdme_newmark_residual):
+                # [uk += du]; a_trial = b1 (uk - u) - b2 v - b3 a; psi = P - f_int - M a_trial
+                rnorm = _fused_residual(pb, lib, uk, du if pending else None, u, v, a, load, t_next, nm,
+                                        atr, tmp, psi)
+                pending = False
+                contact_ok, active = True, False
+            else:
+                # a_trial = b1 (uk - u) - b2 v - b3 a  (difference first, as dynamics.py:219)
+                tmp.assign(1.0, uk, -1.0, u)
+                atr.assign(nm.b1, tmp, -nm.b2, v, -nm.b3, a)
+                contact_ok, active = residual(uk, atr, t_next)
+                rnorm = psi.norm()
             if psi_ref is None:
                 psi_ref = rnorm
             if psi_ref == 0.0:
@@ -217,8 +242,13 @@ def newmark_run(problem: GpuFemProblem, external_load, dt: float, n_steps: int,
                 if active:
                     lib.sdme_pcg_contact(pb._ctx, 0)
             traj.stats.add(step, k, "newmark", st)
-            uk.assign(1.0, uk, 1.0, du)
+            if contact is None:
+                pending = True
+            else:
+                uk.assign(1.0, uk, 1.0, du)
             n_newton += 1
+        if pending:  # Newton stopped by the iteration cap right after a solve
+            uk.assign(1.0, uk, 1.0, du)
         traj.newton_iters.append(n_newton)
         # a_next = b1(uk-u) - b2 v - b3 a ; v += dt((1-g) a + g a_next) ; u = uk
         tmp.assign(1.0, uk, -1.0, u)

@@ -80,6 +80,8 @@ SIGNATURES = {
                          C.c_double],
     "sdme_mass": [C.c_void_p, C.c_int, C.c_int],
     "sdme_diag": [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int],
+    "sdme_newmark_residual": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                              C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, _dp],
     "sdme_pcg": [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, C.c_double, C.c_int,
                  C.c_int, C.POINTER(C.c_int), _dp],
     "sdme_explicit_step": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,

@@ -14,12 +14,12 @@ load = ScaledLoad(base, lambda t: min(t / 1e-3, 1.0))
 cfg = SolverConfig(precond="diagonal", tol=1e-10, condense=False)
 newmark_run(pb, load, 1e-4, 1, cfg=cfg)
 acc = {}
-orig_pcg = dyn.pcg_gpu
+orig_pcg = sol.pcg_gpu
 def timed(name, fn):
     def w(*a, **k):
         t = time.perf_counter(); r = fn(*a, **k); acc[name] = acc.get(name, 0) + time.perf_counter() - t; return r
     return w
-dyn.pcg_gpu = timed("pcg", orig_pcg)
+sol.pcg_gpu = timed("pcg", orig_pcg)
 from paper_2104_13466_b200 import problem as prb
 GpuFemProblem.fint_ = timed("fint", GpuFemProblem.fint_)
 GpuFemProblem.mass_ = timed("mass", GpuFemProblem.mass_)
