@@ -14,11 +14,16 @@
 #include "element_eo.cuh"
 #include "element_gen.cuh"
 #include "element_kernels.cuh"
+#include "element_q5.cuh"
 #include "element_v3.cuh"
 #include "pcg_small.cuh"
 
 #ifndef SDME_COL_MINB
 #define SDME_COL_MINB 11  // resident 1-warp blocks per SM for the P = 4 collocated kernels
+#endif
+
+#ifndef SDME_Q5_MINB
+#define SDME_Q5_MINB 3  // resident 4-warp quintet blocks per SM of the P = 4 kernel (168 registers)
 #endif
 
 #ifndef SDME_TMB_MINB
@@ -520,6 +525,55 @@ void launch_col_k(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
   c->pdl_first = false;
 }
 
+// P = 4 with tensor maps: five elements per 4-warp CTA (element_q5.cuh);
+// SDME_VARIANT=12 keeps the warp-per-element kernel (A/B only)
+template <int MODE, bool VAL, int MIR>
+void launch_q5(sdme_ctx* c, const TabC<5, MIR>& tb, OpArgs a) {
+  using L = Q5Lay<MODE, VAL>;
+  constexpr int T = 128, smem = L::PER * 8;
+  constexpr int MINB = (227 * 1024) / (smem + 1024) < SDME_Q5_MINB ? (227 * 1024) / (smem + 1024) : SDME_Q5_MINB;
+  auto kern = element_q5<MINB, MODE, VAL, MIR>;
+  static PerDevice grid_cache;
+  const int max_blocks = resident_grid(grid_cache, kern, T, smem);
+  if (MODE == MODE_SETUP) {
+    a.colour = -1;
+    const long long nq = (colour_count(c->geo, -1) + L::E - 1) / L::E;
+    kern<<<(unsigned)std::min<long long>(nq, max_blocks), T, smem, c->st>>>(tb, c->geo, a);
+    ++c->launches;
+    return;
+  }
+  bool pdl = c->pdl && !c->capturing;
+  bool first = true;
+  const int nslab = c->nslab_env ? c->nslab : ((MODE == MODE_APPLY || MODE == MODE_MASS) ? 8 : 1);
+  for (int sp = 0; sp < 8 * nslab; ++sp) {
+    const int col = colour_code(c->geo, sp % 8, sp / 8, nslab);
+    if (col == -2) continue;
+    const long long cnt = colour_count(c->geo, col);
+    if (cnt == 0) continue;
+    a.colour = col;
+    const unsigned grid = (unsigned)std::min<long long>((cnt + L::E - 1) / L::E, max_blocks);
+    if (pdl && (!first || c->pdl_first)) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(T);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = c->st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tb, c->geo, a);
+      if (e != cudaSuccess && c->launch_err == cudaSuccess) c->launch_err = e;
+    } else {
+      kern<<<grid, T, smem, c->st>>>(tb, c->geo, a);
+    }
+    first = false;
+    ++c->launches;
+  }
+  c->pdl_first = false;
+}
+
 // TMA box loads / bulk reduce-add (tma.cuh) when every vector of the mode has
 // a tensor map and the colour passes scatter (not E-vector mode).  An FP64 box
 // must start 16-byte aligned (tools/micro/tma_f64.cu), so boxes start at the
@@ -534,6 +588,12 @@ void launch_col(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
                                          : (a.ty && (MODE == MODE_PA || MODE == MODE_MASS || a.tu) &&
                                             (MODE == MODE_FINT || a.tp));
     if (maps && !c->ev_mode && c->variant != 11) {
+      if constexpr (N == 5) {
+        if (c->variant != 12) {
+          launch_q5<MODE, VAL, MIR>(c, tb, a);
+          return;
+        }
+      }
       launch_col_k<N, MODE, VAL, MIR, true>(c, tb, a);
       return;
     }
