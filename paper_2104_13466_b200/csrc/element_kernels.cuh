@@ -69,6 +69,13 @@ struct OpArgs {
   // w det J ([elem][10][Q]); u / p are then E-vector boxes [elem][comp][Q]
   const double* geo = nullptr;
   const int* elem_id = nullptr;  // general meshes: reference element id of a storage position (nullptr: same)
+  // always 0; a value the compiler cannot fold.  Kernels add zero * (loop
+  // counter) to the address of their 1D tables inside a loop so that the
+  // table reads stay constant-bank loads (LDCU) in the loop body: hoisted,
+  // the ~100 table doubles overflow the uniform register file and ptxas
+  // shuffles them through vector registers (R2UR / MOV.SPILL, 18% of the
+  // K.p kernel's instructions, ncu) and local memory
+  int zero = 0;
 };
 
 __device__ __forceinline__ bool constrained(const Geo& g, int comp, int X, int Y, int Z) {

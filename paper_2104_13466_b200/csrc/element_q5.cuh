@@ -55,6 +55,13 @@ struct Q5Lay {
   __device__ static int vslot(int comp) { return (VB + comp) * EQ; }
 };
 
+// the tables again, through an offset (always 0) that varies with the loop:
+// their reads stay LDCU in the loop body (OpArgs::zero)
+template <class T>
+__device__ __forceinline__ const T& reload_tab(const T& tb, int off) {
+  return *reinterpret_cast<const T*>(reinterpret_cast<const char*>(&tb) + off);
+}
+
 // which element coordinates a lane 0..4 stages next (coordinate set of the
 // quintet table) and from which tensor map; map == nullptr: nothing
 struct Q5Next {
@@ -67,7 +74,7 @@ struct Q5Next {
 // points.  Three CTA barriers per component (the derivative stage needs none
 // after it: the next component does not touch U before its own two barriers).
 template <int MODE, int MIR, bool VAL, bool WITHVAL, bool VALS>
-__device__ __forceinline__ void q5_forward(const TabC<5, MIR>& tb, double* S, int t, bool act, int o_row, int o5,
+__device__ __forceinline__ void q5_forward(const TabC<5, MIR>& tb0, int zoff, double* S, int t, bool act, int o_row, int o5,
                                            int o_y, int o_z, int* buf, unsigned* ph, const CUtensorMap* smap,
                                            int cset, Q5Next nxt, bool grad, bool first) {
   constexpr int N = 5;
@@ -81,6 +88,7 @@ __device__ __forceinline__ void q5_forward(const TabC<5, MIR>& tb, double* S, in
   const int* coord = reinterpret_cast<const int*>(S + L::COORD);
 #pragma unroll 1
   for (int comp = 0; comp < 3; ++comp) {
+    const TabC<5, MIR>& tb = reload_tab(tb0, zoff * (comp + 1));
     const int nbi = *buf ^ 1;
     if (t < L::E) {
       // lane e stages element e's next box (this field's next component, or
@@ -178,7 +186,7 @@ __device__ __forceinline__ void q5_forward(const TabC<5, MIR>& tb, double* S, in
 // slot) -> B^T (x) B^T (x) B^T (sum_d D^_d^T F_d [+ V]) as an output box per
 // element, added to y by lanes 0..4 (bulk tensor reduce-add)
 template <int MODE, int MIR, bool VAL, bool VALS>
-__device__ __forceinline__ void q5_backward(const TabC<5, MIR>& tb, const Geo& g, double* S, int t, bool act,
+__device__ __forceinline__ void q5_backward(const TabC<5, MIR>& tb0, int zoff, const Geo& g, double* S, int t, bool act,
                                             int o_row, int o5, int o_y, int o_z, int obuf, int cset, bool grad,
                                             const CUtensorMap* ymap, bool* waited) {
   constexpr int N = 5;
@@ -190,6 +198,7 @@ __device__ __forceinline__ void q5_backward(const TabC<5, MIR>& tb, const Geo& g
   double* O = S + L::R + obuf * L::E * L::RB;
 #pragma unroll 1
   for (int comp = 0; comp < 3; ++comp) {
+    const TabC<5, MIR>& tb = reload_tab(tb0, zoff * (comp + 1));
     if (grad) {
       // x' pencils (e; c, b): U = D^_x^T F_x
       if (act) {
@@ -303,6 +312,7 @@ __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ 
   constexpr bool PGRAD = MODE != MODE_MASS;
   extern __shared__ __align__(128) double S[];
   const int t = threadIdx.x;
+  const int zoff = args.zero;
   if (args.skip && *(volatile const int*)args.skip) return;
   pdl_launch_dependents();
   SDME_CHECK(smem_ok(S, L::PER * 8, 128));
@@ -356,7 +366,7 @@ __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ 
     double Hu[QPT][9];
     if (UPASS) {
       const Q5Next after_u = MODE == MODE_APPLY ? Q5Next{pmap, cur} : after_last;
-      q5_forward<MODE, MIR, VAL, false, VAL>(tb, S, t, act, o_row, o5, o_y, o_z, &buf, &ph, umap, cur, after_u, true,
+      q5_forward<MODE, MIR, VAL, false, VAL>(tb, zoff, S, t, act, o_row, o5, o_y, o_z, &buf, &ph, umap, cur, after_u, true,
                                               true);
 #pragma unroll
       for (int r = 0; r < QPT; ++r) {
@@ -370,7 +380,7 @@ __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ 
       }
     }
     if (PPASS)
-      q5_forward<MODE, MIR, VAL, VAL, VAL>(tb, S, t, act, o_row, o5, o_y, o_z, &buf, &ph, pmap, cur, after_last,
+      q5_forward<MODE, MIR, VAL, VAL, VAL>(tb, zoff, S, t, act, o_row, o5, o_y, o_z, &buf, &ph, pmap, cur, after_last,
                                             PGRAD, !UPASS);
 #pragma unroll
     for (int r = 0; r < QPT; ++r) {
@@ -458,7 +468,7 @@ __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ 
       continue;
     }
     __syncthreads();
-    q5_backward<MODE, MIR, VAL, VAL>(tb, g, S, t, act, o_row, o5, o_y, o_z, buf ^ 1, cur, PGRAD, ymap, &waited);
+    q5_backward<MODE, MIR, VAL, VAL>(tb, zoff, g, S, t, act, o_row, o5, o_y, o_z, buf ^ 1, cur, PGRAD, ymap, &waited);
   }
   // the reduce-adds have completed before the CTA (and its shared memory) retires
   if (t < L::E) bulk_wait_all();
