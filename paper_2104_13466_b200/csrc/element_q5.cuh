@@ -62,6 +62,32 @@ __device__ __forceinline__ const T& reload_tab(const T& tb, int off) {
   return *reinterpret_cast<const T*>(reinterpret_cast<const char*>(&tb) + off);
 }
 
+// y = T^T q of a B-type (F = +1) or D-type (F = -1) operator read from its
+// *forward* tables: make_tabc stores the backward tables as their exact
+// transposes (bwd E[e][a] = fwd S[a][e], O[o][a] = T[a][o]), so this is
+// eo_bwd bit for bit with half as many distinct table constants
+template <int N, int M, int MIR, int F, int WE, int WO, bool ACC>
+__device__ __forceinline__ void eo_bwd_t(const EoFwd<M, WE, WO>& t, const double (&qe)[Half<M>::HP],
+                                         const double (&qo)[Half<M>::H > 0 ? Half<M>::H : 1], double (&y)[N]) {
+  constexpr int H = Half<M>::H, HP = Half<M>::HP;
+  double YE[WE > 0 ? WE : 1], YO[WO > 0 ? WO : 1];
+#pragma unroll
+  for (int e = 0; e < WE; ++e) {
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < HP; ++a) s = fma(t.S[a][e], qe[a], s);
+    YE[e] = s;
+  }
+#pragma unroll
+  for (int o = 0; o < WO; ++o) {
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < H; ++a) s = fma(t.T[a][o], qo[a], s);
+    YO[o] = s;
+  }
+  eo_recon<N, MIR, F, WE, WO, ACC>(YE, YO, y);
+}
+
 // which element coordinates a lane 0..4 stages next (coordinate set of the
 // quintet table) and from which tensor map; map == nullptr: nothing
 struct Q5Next {
@@ -73,7 +99,7 @@ struct Q5Next {
 // derivative fused into the z stage, then the x and y derivatives at the
 // points.  Three CTA barriers per component (the derivative stage needs none
 // after it: the next component does not touch U before its own two barriers).
-template <int MODE, int MIR, bool VAL, bool WITHVAL, bool VALS>
+template <int MODE, int MIR, bool VAL, bool WITHVAL, bool VALS, bool ISO>
 __device__ __forceinline__ void q5_forward(const TabC<5, MIR>& tb0, int zoff, double* S, int t, bool act, int o_row, int o5,
                                            int o_y, int o_z, int* buf, unsigned* ph, const CUtensorMap* smap,
                                            int cset, Q5Next nxt, bool grad, bool first) {
@@ -88,7 +114,9 @@ __device__ __forceinline__ void q5_forward(const TabC<5, MIR>& tb0, int zoff, do
   const int* coord = reinterpret_cast<const int*>(S + L::COORD);
 #pragma unroll 1
   for (int comp = 0; comp < 3; ++comp) {
-    const TabC<5, MIR>& tb = reload_tab(tb0, zoff * (comp + 1));
+    const TabC<5, MIR>& tb = reload_tab(tb0, ISO ? 0 : zoff * (comp + 1));
+    const auto& tDy = ISO ? tb.Dx : tb.Dy;
+    const auto& tDz = ISO ? tb.Dx : tb.Dz;
     const int nbi = *buf ^ 1;
     if (t < L::E) {
       // lane e stages element e's next box (this field's next component, or
@@ -154,7 +182,7 @@ __device__ __forceinline__ void q5_forward(const TabC<5, MIR>& tb0, int zoff, do
       if (grad) {
         double pe[PE], po[PO], gz[N];
         eo_split<N, 0>(u, pe, po);
-        eo_fwd<N, Mp::NO, Mp::NE>(tb.Dz, po, pe, gz);
+        eo_fwd<N, Mp::NO, Mp::NE>(tDz, po, pe, gz);
 #pragma unroll
         for (int c = 0; c < N; ++c) S[L::slot(2, comp) + o_z + 25 * c] = gz[c];
       }
@@ -173,7 +201,7 @@ __device__ __forceinline__ void q5_forward(const TabC<5, MIR>& tb0, int zoff, do
 #pragma unroll
       for (int b = 0; b < N; ++b) v[b] = S[L::U + o_y + 5 * b];
       eo_split<N, 0>(v, pe, po);
-      eo_fwd<N, Mp::NO, Mp::NE>(tb.Dy, po, pe, gd);
+      eo_fwd<N, Mp::NO, Mp::NE>(tDy, po, pe, gd);
 #pragma unroll
       for (int b = 0; b < N; ++b) S[L::slot(1, comp) + o_y + 5 * b] = gd[b];
     }
@@ -185,7 +213,7 @@ __device__ __forceinline__ void q5_forward(const TabC<5, MIR>& tb0, int zoff, do
 // backward pass: per component the weighted flux slots (and the weighted value
 // slot) -> B^T (x) B^T (x) B^T (sum_d D^_d^T F_d [+ V]) as an output box per
 // element, added to y by lanes 0..4 (bulk tensor reduce-add)
-template <int MODE, int MIR, bool VAL, bool VALS>
+template <int MODE, int MIR, bool VAL, bool VALS, bool ISO>
 __device__ __forceinline__ void q5_backward(const TabC<5, MIR>& tb0, int zoff, const Geo& g, double* S, int t, bool act,
                                             int o_row, int o5, int o_y, int o_z, int obuf, int cset, bool grad,
                                             const CUtensorMap* ymap, bool* waited) {
@@ -198,7 +226,9 @@ __device__ __forceinline__ void q5_backward(const TabC<5, MIR>& tb0, int zoff, c
   double* O = S + L::R + obuf * L::E * L::RB;
 #pragma unroll 1
   for (int comp = 0; comp < 3; ++comp) {
-    const TabC<5, MIR>& tb = reload_tab(tb0, zoff * (comp + 1));
+    const TabC<5, MIR>& tb = reload_tab(tb0, ISO ? 0 : zoff * (comp + 1));
+    const auto& tDy = ISO ? tb.Dx : tb.Dy;
+    const auto& tDz = ISO ? tb.Dx : tb.Dz;
     if (grad) {
       // x' pencils (e; c, b): U = D^_x^T F_x
       if (act) {
@@ -206,7 +236,7 @@ __device__ __forceinline__ void q5_backward(const TabC<5, MIR>& tb0, int zoff, c
 #pragma unroll
         for (int a = 0; a < N; ++a) q[a] = S[L::slot(0, comp) + o5 + a];
         eo_qsplit<N>(q, qe, qo);
-        eo_bwd<N, N, 0, -1, Mp::NO, Mp::NE, false>(tb.bDx, qe, qo, y);
+        eo_bwd_t<N, N, 0, -1, Mp::NO, Mp::NE, false>(tb.Dx, qe, qo, y);
 #pragma unroll
         for (int a = 0; a < N; ++a) S[L::U + o5 + a] = y[a];
       }
@@ -220,7 +250,7 @@ __device__ __forceinline__ void q5_backward(const TabC<5, MIR>& tb0, int zoff, c
           y[b] = S[L::U + o_y + 5 * b];
         }
         eo_qsplit<N>(q, qe, qo);
-        eo_bwd<N, N, 0, -1, Mp::NO, Mp::NE, true>(tb.bDy, qe, qo, y);
+        eo_bwd_t<N, N, 0, -1, Mp::NO, Mp::NE, true>(tDy, qe, qo, y);
 #pragma unroll
         for (int b = 0; b < N; ++b) S[L::U + o_y + 5 * b] = y[b];
       }
@@ -235,14 +265,14 @@ __device__ __forceinline__ void q5_backward(const TabC<5, MIR>& tb0, int zoff, c
 #pragma unroll
         for (int c = 0; c < N; ++c) q[c] = S[L::slot(2, comp) + o_z + 25 * c];
         eo_qsplit<N>(q, qe, qo);
-        eo_bwd<N, N, 0, -1, Mp::NO, Mp::NE, true>(tb.bDz, qe, qo, v);
+        eo_bwd_t<N, N, 0, -1, Mp::NO, Mp::NE, true>(tDz, qe, qo, v);
       }
       if (VAL) {
 #pragma unroll
         for (int c = 0; c < N; ++c) v[c] += S[L::vslot(comp) + o_z + 25 * c];
       }
       eo_qsplit<N>(v, qe, qo);
-      eo_bwd<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.bB, qe, qo, h);
+      eo_bwd_t<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.B, qe, qo, h);
 #pragma unroll
       for (int k = 0; k < N; ++k) S[L::Y + o_z + 25 * k] = h[k];
     }
@@ -253,7 +283,7 @@ __device__ __forceinline__ void q5_backward(const TabC<5, MIR>& tb0, int zoff, c
 #pragma unroll
       for (int b = 0; b < N; ++b) v[b] = S[L::Y + o_y + 5 * b];
       eo_qsplit<N>(v, qe, qo);
-      eo_bwd<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.bB, qe, qo, h);
+      eo_bwd_t<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.B, qe, qo, h);
 #pragma unroll
       for (int j = 0; j < N; ++j) S[L::X + o_y + 5 * j] = h[j];
     }
@@ -267,7 +297,7 @@ __device__ __forceinline__ void q5_backward(const TabC<5, MIR>& tb0, int zoff, c
 #pragma unroll
       for (int a = 0; a < N; ++a) v[a] = S[L::X + o5 + a];
       eo_qsplit<N>(v, qe, qo);
-      eo_bwd<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.bB, qe, qo, acc);
+      eo_bwd_t<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.B, qe, qo, acc);
       if (g.dmask[comp]) {
         const int e = t / 25, w = t - 25 * e;
         const int* cc = coord + (cset * L::E + e) * 4;
@@ -301,7 +331,7 @@ __device__ __forceinline__ void q5_backward(const TabC<5, MIR>& tb0, int zoff, c
   }
 }
 
-template <int MINB, int MODE, bool VAL, int MIR>
+template <int MINB, int MODE, bool VAL, int MIR, bool ISO>
 __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ TabC<5, MIR> tb,
                                                         const __grid_constant__ Geo g, OpArgs args) {
   constexpr int N = 5, Q = 125, T = 128;
@@ -366,7 +396,7 @@ __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ 
     double Hu[QPT][9];
     if (UPASS) {
       const Q5Next after_u = MODE == MODE_APPLY ? Q5Next{pmap, cur} : after_last;
-      q5_forward<MODE, MIR, VAL, false, VAL>(tb, zoff, S, t, act, o_row, o5, o_y, o_z, &buf, &ph, umap, cur, after_u, true,
+      q5_forward<MODE, MIR, VAL, false, VAL, ISO>(tb, zoff, S, t, act, o_row, o5, o_y, o_z, &buf, &ph, umap, cur, after_u, true,
                                               true);
 #pragma unroll
       for (int r = 0; r < QPT; ++r) {
@@ -380,7 +410,7 @@ __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ 
       }
     }
     if (PPASS)
-      q5_forward<MODE, MIR, VAL, VAL, VAL>(tb, zoff, S, t, act, o_row, o5, o_y, o_z, &buf, &ph, pmap, cur, after_last,
+      q5_forward<MODE, MIR, VAL, VAL, VAL, ISO>(tb, zoff, S, t, act, o_row, o5, o_y, o_z, &buf, &ph, pmap, cur, after_last,
                                             PGRAD, !UPASS);
 #pragma unroll
     for (int r = 0; r < QPT; ++r) {
@@ -468,7 +498,7 @@ __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ 
       continue;
     }
     __syncthreads();
-    q5_backward<MODE, MIR, VAL, VAL>(tb, zoff, g, S, t, act, o_row, o5, o_y, o_z, buf ^ 1, cur, PGRAD, ymap, &waited);
+    q5_backward<MODE, MIR, VAL, VAL, ISO>(tb, zoff, g, S, t, act, o_row, o5, o_y, o_z, buf ^ 1, cur, PGRAD, ymap, &waited);
   }
   // the reduce-adds have completed before the CTA (and its shared memory) retires
   if (t < L::E) bulk_wait_all();

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -268,6 +269,15 @@ struct EoBuild {
   }
 };
 
+// backward tables of a square (M = N) operator as the transposed forward ones
+template <int M, int WS, int WT>
+void eo_transpose(EoBwd<M, WS, WT>& b, const EoFwd<M, WS, WT>& f) {
+  for (int e = 0; e < (WS > 0 ? WS : 1); ++e)
+    for (int a = 0; a < Half<M>::HP; ++a) b.E[e][a] = f.S[a][e];
+  for (int o = 0; o < (WT > 0 ? WT : 1); ++o)
+    for (int a = 0; a < (Half<M>::H > 0 ? Half<M>::H : 1); ++a) b.O[o][a] = f.T[a][o];
+}
+
 // Even-odd tables (eo.cuh) from the lattice-order 1D tables, with the same
 // folding of weights, det J and 2/h as make_tab3.
 template <int N, int M, int MIR>
@@ -452,13 +462,17 @@ TabC<N, MIR> make_tabc(const sdme_ctx* c) {
     }
   TabC<N, MIR> t;
   EoBuild<N, N, MIR>::fwd(t.B, Bv, 1);
-  EoBuild<N, N, MIR>::bwd(t.bB, Bv, 1);
   EoBuild<N, N, 0>::fwd(t.Dx, Dh[0], -1);
   EoBuild<N, N, 0>::fwd(t.Dy, Dh[1], -1);
   EoBuild<N, N, 0>::fwd(t.Dz, Dh[2], -1);
-  EoBuild<N, N, 0>::bwd(t.bDx, Dh[0], -1);
-  EoBuild<N, N, 0>::bwd(t.bDy, Dh[1], -1);
-  EoBuild<N, N, 0>::bwd(t.bDz, Dh[2], -1);
+  // The backward tables are the forward ones transposed, entry for entry
+  // (by the mirror symmetry EoBuild::bwd gives the same numbers up to the
+  // last bit): kernels that read the forward tables in their backward pass
+  // (element_q5: half the table constants) then match the others bit for bit.
+  eo_transpose(t.bB, t.B);
+  eo_transpose(t.bDx, t.Dx);
+  eo_transpose(t.bDy, t.Dy);
+  eo_transpose(t.bDz, t.Dz);
   for (int q = 0; q < N; ++q) t.wq[q] = c->w[q];
   t.detJ = g.detJ;
   return t;
@@ -527,12 +541,12 @@ void launch_col_k(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
 
 // P = 4 with tensor maps: five elements per 4-warp CTA (element_q5.cuh);
 // SDME_VARIANT=12 keeps the warp-per-element kernel (A/B only)
-template <int MODE, bool VAL, int MIR>
-void launch_q5(sdme_ctx* c, const TabC<5, MIR>& tb, OpArgs a) {
+template <int MODE, bool VAL, int MIR, bool ISO>
+void launch_q5_iso(sdme_ctx* c, const TabC<5, MIR>& tb, OpArgs a) {
   using L = Q5Lay<MODE, VAL>;
   constexpr int T = 128, smem = L::PER * 8;
   constexpr int MINB = (227 * 1024) / (smem + 1024) < SDME_Q5_MINB ? (227 * 1024) / (smem + 1024) : SDME_Q5_MINB;
-  auto kern = element_q5<MINB, MODE, VAL, MIR>;
+  auto kern = element_q5<MINB, MODE, VAL, MIR, ISO>;
   static PerDevice grid_cache;
   const int max_blocks = resident_grid(grid_cache, kern, T, smem);
   if (MODE == MODE_SETUP) {
@@ -572,6 +586,21 @@ void launch_q5(sdme_ctx* c, const TabC<5, MIR>& tb, OpArgs a) {
     ++c->launches;
   }
   c->pdl_first = false;
+}
+
+// Cubic elements (hx = hy = hz: one derivative table for the three axes) keep
+// all 25 table constants in uniform registers for the whole kernel; otherwise
+// the 49 constants are re-read from the constant bank per component loop
+// (OpArgs::zero).  SDME_Q5_ISO=0 forces the general instance (A/B).
+template <int MODE, bool VAL, int MIR>
+void launch_q5(sdme_ctx* c, const TabC<5, MIR>& tb, OpArgs a) {
+  static const bool iso_ok = [] {
+    const char* e = getenv("SDME_Q5_ISO");
+    return !(e && e[0] == '0');
+  }();
+  const Geo& g = c->geo;
+  if (iso_ok && g.s[0] == g.s[1] && g.s[1] == g.s[2]) launch_q5_iso<MODE, VAL, MIR, true>(c, tb, a);
+  else launch_q5_iso<MODE, VAL, MIR, false>(c, tb, a);
 }
 
 // TMA box loads / bulk reduce-add (tma.cuh) when every vector of the mode has
