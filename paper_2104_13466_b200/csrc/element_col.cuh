@@ -118,10 +118,10 @@ __device__ __forceinline__ void col_stage(const Geo& g, const double* __restrict
 }
 
 template <int N, int WPE, int MIR, bool VAL, bool VALS, bool TM = false, int SUB = 1>
-__device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g, const double* __restrict__ src,
-                                            int X0, int Y0, int Z0, double* S, int t, int* buf, NextRows next,
-                                            bool grad, const CUtensorMap* smap = nullptr, NextBox nbox = {},
-                                            unsigned* ph = nullptr) {
+__device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb0, int zoff, const Geo& g,
+                                            const double* __restrict__ src, int X0, int Y0, int Z0, double* S, int t,
+                                            int* buf, NextRows next, bool grad, const CUtensorMap* smap = nullptr,
+                                            NextBox nbox = {}, unsigned* ph = nullptr) {
   using L = ColLay<N, VALS, TM>;
   using Mr = Mir<N, MIR>;
   using Mp = Mir<N, 0>;
@@ -131,6 +131,8 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
   const int* tab = reinterpret_cast<const int*>(S + L::TAB);
 #pragma unroll 1
   for (int comp = 0; comp < 3; ++comp) {
+    // tables re-read from the constant bank per component (OpArgs::zero)
+    const TabC<N, MIR>& tb = reload_tab(tb0, N >= SDME_COL_RELOAD_MIN_N ? zoff * (comp + 1) : 0);
     if (TM) {
       // one lane issues the next box (this field's next component, or the
       // next field / element), then every lane waits for the current box
@@ -251,15 +253,17 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb, const Geo& g
 // backward: per component, the weighted flux slots 0..2 (and the weighted
 // value slot 3 when VAL) -> y += B^T (x) B^T (x) B^T (sum_d D^_d^T F_d [+ V])
 template <int N, int WPE, int MIR, bool VAL, bool VALS, bool TM = false, int SUB = 1>
-__device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb, const Geo& g, double* __restrict__ dst, int X0,
-                                             int Y0, int Z0, double* S, int t, double* evb, bool grad,
-                                             const CUtensorMap* ymap = nullptr, bool* waited = nullptr) {
+__device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb0, int zoff, const Geo& g,
+                                             double* __restrict__ dst, int X0, int Y0, int Z0, double* S, int t,
+                                             double* evb, bool grad, const CUtensorMap* ymap = nullptr,
+                                             bool* waited = nullptr) {
   using L = ColLay<N, VALS, TM>;
   using Mr = Mir<N, MIR>;
   using Mp = Mir<N, 0>;
   constexpr int HP = Half<N>::HP, H = Half<N>::H > 0 ? Half<N>::H : 1;
 #pragma unroll 1
   for (int comp = 0; comp < 3; ++comp) {
+    const TabC<N, MIR>& tb = reload_tab(tb0, N >= SDME_COL_RELOAD_MIN_N ? zoff * (comp + 1) : 0);
     if (grad) {
       // x' pencils (c, b): U = D^_x^T F_x
       for (int w = t; w < N * N; w += 32 * WPE / SUB) {
@@ -508,7 +512,7 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
     if (UPASS) {
       const NextRows after_u = MODE == MODE_APPLY ? NextRows{args.p + eoff, X0, Y0, Z0} : nxt;
       const NextBox after_ub = MODE == MODE_APPLY ? NextBox{pmap, X0, Y0, Z0} : nxb;
-      col_forward<N, WPE, MIR, false, VALS, TM, SUB>(tb, g, args.u + eoff, X0, Y0, Z0, S, t, &buf, after_u, true, umap,
+      col_forward<N, WPE, MIR, false, VALS, TM, SUB>(tb, args.zero, g, args.u + eoff, X0, Y0, Z0, S, t, &buf, after_u, true, umap,
                                                 after_ub, &ph);
 #pragma unroll
       for (int r = 0; r < QPT; ++r) {
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
       group_sync<WPE>(0);
     }
     if (PPASS)
-      col_forward<N, WPE, MIR, VAL, VALS, TM, SUB>(tb, g, args.p + eoff, X0, Y0, Z0, S, t, &buf, nxt, PGRAD, pmap, nxb,
+      col_forward<N, WPE, MIR, VAL, VALS, TM, SUB>(tb, args.zero, g, args.p + eoff, X0, Y0, Z0, S, t, &buf, nxt, PGRAD, pmap, nxb,
                                               &ph);
 #pragma unroll
     for (int r = 0; r < QPT; ++r) {
@@ -639,7 +643,7 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
     group_sync<WPE>(0);
     if (MODE == MODE_SETUP) continue;
     double* evb = args.ev ? args.ev + eid * 3 * Q : nullptr;
-    col_backward<N, WPE, MIR, VAL, VALS, TM, SUB>(tb, g, args.y, X0, Y0, Z0, S, t, evb, PGRAD,
+    col_backward<N, WPE, MIR, VAL, VALS, TM, SUB>(tb, args.zero, g, args.y, X0, Y0, Z0, S, t, evb, PGRAD,
                                                   ghost ? nullptr : static_cast<const CUtensorMap*>(args.ty),
                                                   &waited);
   }

@@ -55,12 +55,14 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_diag3(const __gr
   const long long stride = (long long)gridDim.x * EPB;
   const bool stiff = args.c_k != 0.0;
   const double cmr = args.c_m * g.rho;
+  int zit = 0;  // table re-reads (OpArgs::zero)
   for (long long idx = (long long)blockIdx.x * EPB + gid; idx < cnt; idx += stride) {
+    const int zv = args.zero * (++zit);
     int ei, ej, ek;
     colour_element(g, args.colour, idx, ei, ej, ek);
     const int X0 = (N - 1) * ei, Y0 = (N - 1) * ej, Z0 = (N - 1) * ek;
     const long long eid = ((long long)ek * g.ny + ej) * g.nx + ei;
-    if (stiff) v3_forward<N, M, WPE, 1, true, false>(tb, g, args.u, X0, Y0, Z0, A, Bf, t, gid);
+    if (stiff) v3_forward<N, M, WPE, 1, true, false>(tb, zv, g, args.u, X0, Y0, Z0, A, Bf, t, gid);
     // point coefficients: slot comp * 6 + pair, slot 18 mass
     for (int q = t; q < C::Q; q += C::T) {
       double coef[3][6];

@@ -10,7 +10,7 @@
 namespace sdme {
 
 template <int N, int M, int WPE, int NC, bool GRAD, bool VAL, bool STAGED = false, int MIR>
-__device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo& g, const double* __restrict__ src,
+__device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb0, int zv, const Geo& g, const double* __restrict__ src,
                                            int X0, int Y0, int Z0, double* A, double* B, int t, int gid,
                                            double* R = nullptr, int* buf = nullptr, NextRows next = {},
                                            BoxIO bx = {}) {
@@ -21,6 +21,8 @@ __device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo
   double* const P = A;
 #pragma unroll 1
   for (int c0 = 0; c0 < 3; c0 += NC) {
+    // tables re-read from the constant bank per element / component group (OpArgs::zero)
+    const auto& tb = reload_tab(tb0, N >= SDME_V3_RELOAD_MIN_N ? zv * (c0 + 1) : 0);
     double* const X = (NC == 3) ? A : B + C::YO;
     if (STAGED) {
       double* nb = R + (*buf ^ 1) * N * N * N;
@@ -146,7 +148,7 @@ __device__ __forceinline__ void v3_forward(const TabEO<N, M, MIR>& tb, const Geo
 }
 
 template <int N, int M, int WPE, int NC, bool GRAD, bool VAL, int MIR>
-__device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Geo& g, double* __restrict__ dst,
+__device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb0, int zv, const Geo& g, double* __restrict__ dst,
                                             int X0, int Y0, int Z0, double* A, double* B, int t, int gid,
                                             double* evb = nullptr, BoxIO bx = {}) {
   using C = V3<N, M, WPE, NC>;
@@ -155,6 +157,8 @@ __device__ __forceinline__ void v3_backward(const TabEO<N, M, MIR>& tb, const Ge
   constexpr int BW = BoxW<N>::BW;
 #pragma unroll 1
   for (int c0 = 0; c0 < 3; c0 += NC) {
+    // tables re-read from the constant bank per element / component group (OpArgs::zero)
+    const auto& tb = reload_tab(tb0, N >= SDME_V3_RELOAD_MIN_N ? zv * (c0 + 1) : 0);
     double* const X = (NC == 3) ? A : B + C::YO;
     // z' stage: item (comp, b, a), contract over c
     for (int w = t; w < NC * M * M; w += C::T) {

@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(32 * WPE, 1) element_diag_gen(const __grid_con
   for (long long eid = blockIdx.x; eid < cnt; eid += gridDim.x) {
     if (stiff) {
       col_stage<N, T>(g, args.u + eid * 3 * Q, 0, 0, 0, 0, S + L::R + buf * Q, t, tab);
-      col_forward<N, WPE, MIR, false, false>(tb, g, args.u + eid * 3 * Q, 0, 0, 0, S, t, &buf,
+      col_forward<N, WPE, MIR, false, false>(tb, args.zero, g, args.u + eid * 3 * Q, 0, 0, 0, S, t, &buf,
                                              NextRows{nullptr, 0, 0, 0}, true);
     }
     for (int q = t; q < Q; q += T) {

@@ -78,6 +78,26 @@ struct OpArgs {
   int zero = 0;
 };
 
+// Orders from which the kernels re-read their tables (measured, tools/run_configs.py
+// c3, tools/op_times.py): the collocated kernels at P >= 4 (P = 6 K.p
+// 2.10 -> 2.02 ms, P = 8 2.16 -> 1.98 ms; P = 3: 1.97 -> 2.03 ms, so not
+// below); the all-component v3 kernels never (P = 2 K.p 3.66 -> 3.74 ms,
+// diagonal at P = 4 4.98 -> 5.30 ms, config 1 unchanged: few multiply-adds
+// per table constant there)
+#ifndef SDME_COL_RELOAD_MIN_N
+#define SDME_COL_RELOAD_MIN_N 5
+#endif
+#ifndef SDME_V3_RELOAD_MIN_N
+#define SDME_V3_RELOAD_MIN_N 99
+#endif
+
+// the tables again, through an offset (always 0) that varies with the loop:
+// their reads stay LDCU in the loop body (OpArgs::zero)
+template <class T>
+__device__ __forceinline__ const T& reload_tab(const T& tb, int off) {
+  return *reinterpret_cast<const T*>(reinterpret_cast<const char*>(&tb) + off);
+}
+
 __device__ __forceinline__ bool constrained(const Geo& g, int comp, int X, int Y, int Z) {
   const int m = g.dmask[comp];
   return ((m & 1) && X == 0) || ((m & 2) && X == g.Lx - 1) || ((m & 4) && Y == 0) ||

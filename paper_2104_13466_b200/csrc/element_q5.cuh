@@ -55,13 +55,6 @@ struct Q5Lay {
   __device__ static int vslot(int comp) { return (VB + comp) * EQ; }
 };
 
-// the tables again, through an offset (always 0) that varies with the loop:
-// their reads stay LDCU in the loop body (OpArgs::zero)
-template <class T>
-__device__ __forceinline__ const T& reload_tab(const T& tb, int off) {
-  return *reinterpret_cast<const T*>(reinterpret_cast<const char*>(&tb) + off);
-}
-
 // y = T^T q of a B-type (F = +1) or D-type (F = -1) operator read from its
 // *forward* tables: make_tabc stores the backward tables as their exact
 // transposes (bwd E[e][a] = fwd S[a][e], O[o][a] = T[a][o]), so this is

@@ -187,7 +187,7 @@ __device__ __forceinline__ void v3_prefetch(const Geo& g, const double* __restri
 // component's rows -- or `next` after the last one -- are staged while this
 // component computes, so global latency is off the critical path.
 template <int N, int M, int WPE, int NC, bool GRAD, bool VAL, bool STAGED = false>
-__device__ __forceinline__ void v3_forward(const Tab3<N, M>& tb, const Geo& g, const double* __restrict__ src,
+__device__ __forceinline__ void v3_forward(const Tab3<N, M>& tb0, int zv, const Geo& g, const double* __restrict__ src,
                                            int X0, int Y0, int Z0, double* A, double* B, int t, int gid,
                                            double* R = nullptr, int* buf = nullptr, NextRows next = {},
                                            BoxIO = {}) {
@@ -197,6 +197,8 @@ __device__ __forceinline__ void v3_forward(const Tab3<N, M>& tb, const Geo& g, c
   double* const P = A;  // points buffer (all components)
 #pragma unroll 1
   for (int c0 = 0; c0 < 3; c0 += NC) {
+    // tables re-read from the constant bank per element / component group (OpArgs::zero)
+    const auto& tb = reload_tab(tb0, N >= SDME_V3_RELOAD_MIN_N ? zv * (c0 + 1) : 0);
     double* const X = (NC == 3) ? A : B + C::YO;  // x-stage scratch (see V3::SB)
     if (STAGED) {
       double* nb = R + (*buf ^ 1) * N * N * N;
@@ -320,13 +322,15 @@ __device__ __forceinline__ void v3_forward(const Tab3<N, M>& tb, const Geo& g, c
 // evb != nullptr (E-vector mode): the element's box goes to evb[comp][k][j][i]
 // instead of being scattered with RED into the lattice.
 template <int N, int M, int WPE, int NC, bool GRAD, bool VAL>
-__device__ __forceinline__ void v3_backward(const Tab3<N, M>& tb, const Geo& g, double* __restrict__ dst,
+__device__ __forceinline__ void v3_backward(const Tab3<N, M>& tb0, int zv, const Geo& g, double* __restrict__ dst,
                                             int X0, int Y0, int Z0, double* A, double* B, int t, int gid,
                                             double* evb = nullptr, BoxIO = {}) {
   using C = V3<N, M, WPE, NC>;
   constexpr int NX = NC * N * N, NY = NC * N * M, NZ = NC * M * M;
 #pragma unroll 1
   for (int c0 = 0; c0 < 3; c0 += NC) {
+    // tables re-read from the constant bank per element / component group (OpArgs::zero)
+    const auto& tb = reload_tab(tb0, N >= SDME_V3_RELOAD_MIN_N ? zv * (c0 + 1) : 0);
     double* const X = (NC == 3) ? A : B + C::YO;
 #pragma unroll
     for (int r = 0; r < (NZ + C::T - 1) / C::T; ++r) {
@@ -535,7 +539,9 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
     colour_element(g, args.colour, (long long)blockIdx.x * EPB + gid, ei, ej, ek);
     v3_stage_rows<N, C::T>(g, first_field, 0, (N - 1) * ei, (N - 1) * ej, (N - 1) * ek, Rb, t);
   }
+  int zit = 0;  // loop-variant multiplier of args.zero (table re-reads, OpArgs::zero)
   for (long long idx = (long long)blockIdx.x * EPB + gid; idx < cnt; idx += stride) {
+    const int zv = args.zero * (++zit);
     int ei, ej, ek;
     colour_element(g, args.colour, idx, ei, ej, ek);
     const int X0 = (N - 1) * ei, Y0 = (N - 1) * ej, Z0 = (N - 1) * ek;
@@ -574,7 +580,7 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
     if (UPASS) {
       const NextRows after_u = MODE == MODE_APPLY ? NextRows{args.p, X0, Y0, Z0} : nxt;
       box_next(MODE == MODE_APPLY);
-      v3_forward<N, M, WPE, NC, true, false, STG>(tb, g, args.u, X0, Y0, Z0, A, Bf, t, gid, Rb, &buf, after_u, bx);
+      v3_forward<N, M, WPE, NC, true, false, STG>(tb, zv, g, args.u, X0, Y0, Z0, A, Bf, t, gid, Rb, &buf, after_u, bx);
       if (TMB) buf ^= 1;
 #pragma unroll
       for (int r = 0; r < C::QPT; ++r) {
@@ -590,7 +596,7 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
     }
     if (PPASS) {
       box_next(false);
-      v3_forward<N, M, WPE, NC, GRADP, VAL, STG>(tb, g, args.p, X0, Y0, Z0, A, Bf, t, gid, Rb, &buf, nxt, bx);
+      v3_forward<N, M, WPE, NC, GRADP, VAL, STG>(tb, zv, g, args.p, X0, Y0, Z0, A, Bf, t, gid, Rb, &buf, nxt, bx);
       if (TMB) buf ^= 1;
     }
 #pragma unroll
@@ -697,11 +703,11 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_v3(const __grid_
       bx.xs = X0 & ~1, bx.Y0 = Y0, bx.Z0 = Z0;
     }
     if (MODE == MODE_MASS)
-      v3_backward<N, M, WPE, NC, false, true>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb, bx);
+      v3_backward<N, M, WPE, NC, false, true>(tb, zv, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb, bx);
     else if (MODE == MODE_FINT)
-      v3_backward<N, M, WPE, NC, true, false>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb, bx);
+      v3_backward<N, M, WPE, NC, true, false>(tb, zv, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb, bx);
     else
-      v3_backward<N, M, WPE, NC, true, VAL>(tb, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb, bx);
+      v3_backward<N, M, WPE, NC, true, VAL>(tb, zv, g, args.y, X0, Y0, Z0, A, Bf, t, gid, evb, bx);
   }
   if (TMB && t == 0) bulk_wait_all();
 }

@@ -465,14 +465,21 @@ TabC<N, MIR> make_tabc(const sdme_ctx* c) {
   EoBuild<N, N, 0>::fwd(t.Dx, Dh[0], -1);
   EoBuild<N, N, 0>::fwd(t.Dy, Dh[1], -1);
   EoBuild<N, N, 0>::fwd(t.Dz, Dh[2], -1);
-  // The backward tables are the forward ones transposed, entry for entry
-  // (by the mirror symmetry EoBuild::bwd gives the same numbers up to the
-  // last bit): kernels that read the forward tables in their backward pass
-  // (element_q5: half the table constants) then match the others bit for bit.
-  eo_transpose(t.bB, t.B);
-  eo_transpose(t.bDx, t.Dx);
-  eo_transpose(t.bDy, t.Dy);
-  eo_transpose(t.bDz, t.Dz);
+  EoBuild<N, N, MIR>::bwd(t.bB, Bv, 1);
+  EoBuild<N, N, 0>::bwd(t.bDx, Dh[0], -1);
+  EoBuild<N, N, 0>::bwd(t.bDy, Dh[1], -1);
+  EoBuild<N, N, 0>::bwd(t.bDz, Dh[2], -1);
+  if (N == 5) {
+    // P = 4: the backward tables are the forward ones transposed, entry for
+    // entry (by the mirror symmetry EoBuild::bwd gives the same numbers up to
+    // the last bit).  The quintet kernel (element_q5) reads the forward tables
+    // in its backward pass -- half the table constants -- and so matches
+    // element_col<5> bit for bit.  Other orders keep the EoBuild::bwd bits.
+    eo_transpose(t.bB, t.B);
+    eo_transpose(t.bDx, t.Dx);
+    eo_transpose(t.bDy, t.Dy);
+    eo_transpose(t.bDz, t.Dz);
+  }
   for (int q = 0; q < N; ++q) t.wq[q] = c->w[q];
   t.detJ = g.detJ;
   return t;
