@@ -42,6 +42,7 @@ struct sdme_ctx {
   std::vector<double*> vecs;
   std::vector<void*> vec_tmaps;  // device CUtensorMap per vector (element box TMA), parallel to vecs
   int* d_perm = nullptr;
+  int* d_iperm = nullptr;          // free index -> pitched lattice index (gather form of lattice -> free)
   int64_t n_free = 0;
   unsigned char* d_free = nullptr;  // 1 on free lattice dofs
   double* d_fbuf = nullptr;         // staging for free-order vectors

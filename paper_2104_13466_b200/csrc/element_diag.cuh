@@ -15,6 +15,10 @@
 #pragma once
 #include "element_v3.cuh"
 
+#ifndef SDME_DIAG_RELOAD
+#define SDME_DIAG_RELOAD 1
+#endif
+
 namespace sdme {
 
 template <int N, int M>
@@ -39,7 +43,7 @@ struct DiagLay {
 
 template <int N, int M, int WPE, int EPB, int MINB>
 __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_diag3(const __grid_constant__ Tab3<N, M> tb,
-                                                                        const __grid_constant__ TabD<N, M> td,
+                                                                        const __grid_constant__ TabD<N, M> td0,
                                                                         const __grid_constant__ Geo g, OpArgs args) {
   using C = V3<N, M, WPE, 1, true>;
   using L = DiagLay<N, M, WPE>;
@@ -112,7 +116,11 @@ __global__ void __launch_bounds__(EPB * WPE * 32, MINB) element_diag3(const __gr
       for (int r = 0; r < NR; ++r)
 #pragma unroll
         for (int i = 0; i < N; ++i) acc[r][i] = 0.0;
-#pragma unroll 1
+      // the six chains unrolled: their table choice (tx, ty, tz) is then a
+      // compile-time offset (rolled, every multiply-add took an indexed LDC.64
+      // for its table entry: 100 of the kernel's 452 DFMA sites)
+      const TabD<N, M>& td = reload_tab(td0, SDME_DIAG_RELOAD ? zv * (comp + 1) : 0);
+#pragma unroll
       for (int tt = 0; tt < 6; ++tt) {
         if (!stiff && tt != 2) continue;  // mass only: the (z, z) chain carries it
         const int d = pair_d(tt), e = pair_e(tt);

@@ -464,6 +464,9 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
     if (cudaMemcpy(ctx->d_perm, pp.data(), ctx->nvec * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
       return fail(SDME_CUDA_ERROR);
     if (cudaMalloc(&ctx->d_fbuf, d->n_free * sizeof(double)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+    if (cudaMalloc(&ctx->d_iperm, d->n_free * sizeof(int)) != cudaSuccess) return fail(SDME_CUDA_ERROR);
+    k_invert_perm<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(ctx->d_iperm, ctx->d_perm, ctx->nvec);
+    if (cudaStreamSynchronize(ctx->st) != cudaSuccess) return fail(SDME_CUDA_ERROR);
   }
   *out = ctx;
   return SDME_OK;
@@ -574,6 +577,7 @@ int sdme_destroy(sdme_ctx* ctx) {
   for (void* p : ctx->vec_tmaps)
     if (p) cudaFree(p);
   cudaFree(ctx->d_perm);
+  cudaFree(ctx->d_iperm);
   cudaFree(ctx->d_free);
   cudaFree(ctx->d_dof);
   cudaFree(ctx->d_aptr);
@@ -678,7 +682,7 @@ int sdme_vec_download_free(sdme_ctx* ctx, int id, double* host) {
   if (ctx && ctx->gen) return sdme_vec_download(ctx, id, host);
   double* p = ctx ? vec(ctx, id) : nullptr;
   if (!p || !host || !ctx->d_perm) return set_err(ctx, SDME_BAD_ARGUMENT, "no permutation / bad vector");
-  k_lattice_to_free<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(ctx->d_fbuf, p, ctx->d_perm, ctx->nvec);
+  k_lattice_to_free<<<grid_for(ctx->n_free), 256, 0, ctx->st>>>(ctx->d_fbuf, p, ctx->d_iperm, ctx->n_free);
   ++ctx->launches;
   CK(cudaMemcpyAsync(host, ctx->d_fbuf, ctx->n_free * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
@@ -1324,7 +1328,7 @@ int sdme_apply_batch(sdme_ctx* ctx, int n, const double* const* u, const double*
     else
       ctx->ops->element(ctx, MODE_MASS, nullptr, Pv, Y, 0.0, c_m);
     if (k >= 2) CK(cudaStreamWaitEvent(ctx->st, b->ev_out_free[s], 0));
-    k_lattice_to_free<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(b->sy[s], Y, ctx->d_perm, ctx->nvec);
+    k_lattice_to_free<<<grid_for(ctx->n_free), 256, 0, ctx->st>>>(b->sy[s], Y, ctx->d_iperm, ctx->n_free);
     ++ctx->launches;
     CK(cudaEventRecord(b->ev_comp[s], ctx->st));
     // D2H of result k
