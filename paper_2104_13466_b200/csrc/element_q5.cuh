@@ -92,12 +92,11 @@ struct Q5Next {
 // derivative fused into the z stage, then the x and y derivatives at the
 // points.  Three CTA barriers per component (the derivative stage needs none
 // after it: the next component does not touch U before its own two barriers).
-template <int MODE, int MIR, bool VAL, bool WITHVAL, bool VALS, bool ISO>
+template <class L, int MIR, bool WITHVAL, bool ISO>
 __device__ __forceinline__ void q5_forward(const TabC<5, MIR>& tb0, int zoff, double* S, int t, bool act, int o_row, int o5,
                                            int o_y, int o_z, int* buf, unsigned* ph, const CUtensorMap* smap,
                                            int cset, Q5Next nxt, bool grad, bool first) {
   constexpr int N = 5;
-  using L = Q5Lay<MODE, VALS>;
   using Mr = Mir<N, MIR>;
   using Mp = Mir<N, 0>;
   constexpr int NE = Mr::NE > 0 ? Mr::NE : 1, NO = Mr::NO > 0 ? Mr::NO : 1;
@@ -389,7 +388,7 @@ __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ 
     double Hu[QPT][9];
     if (UPASS) {
       const Q5Next after_u = MODE == MODE_APPLY ? Q5Next{pmap, cur} : after_last;
-      q5_forward<MODE, MIR, VAL, false, VAL, ISO>(tb, zoff, S, t, act, o_row, o5, o_y, o_z, &buf, &ph, umap, cur, after_u, true,
+      q5_forward<L, MIR, false, ISO>(tb, zoff, S, t, act, o_row, o5, o_y, o_z, &buf, &ph, umap, cur, after_u, true,
                                               true);
 #pragma unroll
       for (int r = 0; r < QPT; ++r) {
@@ -403,7 +402,7 @@ __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ 
       }
     }
     if (PPASS)
-      q5_forward<MODE, MIR, VAL, VAL, VAL, ISO>(tb, zoff, S, t, act, o_row, o5, o_y, o_z, &buf, &ph, pmap, cur, after_last,
+      q5_forward<L, MIR, VAL, ISO>(tb, zoff, S, t, act, o_row, o5, o_y, o_z, &buf, &ph, pmap, cur, after_last,
                                             PGRAD, !UPASS);
 #pragma unroll
     for (int r = 0; r < QPT; ++r) {

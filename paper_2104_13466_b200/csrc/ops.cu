@@ -16,6 +16,7 @@
 #include "element_gen.cuh"
 #include "element_kernels.cuh"
 #include "element_q5.cuh"
+#include "element_q5d.cuh"
 #include "element_v3.cuh"
 #include "pcg_small.cuh"
 
@@ -650,8 +651,50 @@ void col_modes(sdme_ctx* c, int mode, OpArgs a) {
   else launch_col<N, MODE_PA, false, MIR>(c, tb, a);
 }
 
+// P = 4, m = 5 with tensor maps: the diagonal on the quintet schedule
+// (element_q5d.cuh); SDME_VARIANT=13 keeps element_diag3 (A/B only)
+template <int MIR, bool ISO>
+void launch_q5_diag(sdme_ctx* c, const double* u, double* d, double ck, double cm, const void* tu, const void* td_map) {
+  using L = Q5DLay;
+  constexpr int T = 128, smem = L::PER * 8;
+  auto kern = element_q5_diag<2, MIR, ISO>;
+  static PerDevice grid_cache;
+  const int max_blocks = resident_grid(grid_cache, kern, T, smem);
+  const TabC<5, MIR> tb = make_tabc<5, MIR>(c);
+  const TabD<5, 5> td = make_tabd<5, 5>(c);
+  OpArgs a{u, nullptr, d, ck, cm, 0, c->d_flag};
+  a.tu = tu;
+  a.ty = td_map;
+  for (int sp = 0; sp < 8; ++sp) {
+    const int col = colour_code(c->geo, sp, 0, 1);
+    if (col == -2) continue;
+    const long long cnt = colour_count(c->geo, col);
+    if (cnt == 0) continue;
+    a.colour = col;
+    const unsigned grid = (unsigned)std::min<long long>((cnt + L::E - 1) / L::E, max_blocks);
+    kern<<<grid, T, smem, c->st>>>(tb, td, c->geo, a);
+    ++c->launches;
+  }
+}
+
 template <int N, int M>
 void diag_impl(sdme_ctx* c, const double* u, double* d, double ck, double cm) {
+  if constexpr (N == 5 && M == 5) {
+    const void* tu = sdme_tmap_of(c, u);
+    const void* tdm = sdme_tmap_of(c, d);
+    if (ck != 0.0 && tu && tdm && !c->ev_mode && c->mir >= 0 && c->variant != 13 && c->variant != 11) {
+      const Geo& g = c->geo;
+      const bool iso = g.s[0] == g.s[1] && g.s[1] == g.s[2];
+      if (c->mir == 0) {
+        if (iso) launch_q5_diag<0, true>(c, u, d, ck, cm, tu, tdm);
+        else launch_q5_diag<0, false>(c, u, d, ck, cm, tu, tdm);
+      } else {
+        if (iso) launch_q5_diag<1, true>(c, u, d, ck, cm, tu, tdm);
+        else launch_q5_diag<1, false>(c, u, d, ck, cm, tu, tdm);
+      }
+      return;
+    }
+  }
   constexpr int WPE = LargeShape<N, M>::WPE;  // one round per stage
   constexpr int smem = DiagLay<N, M, WPE>::PER * 8;
   auto kern = element_diag3<N, M, WPE, 1, 1>;
