@@ -7,21 +7,30 @@
 //        coef[comp][(d, e)](c, b, a)  Tz^{tz}[c][k]  Ty^{ty}[b][j]  Tx^{tx}[a][i]
 //
 // with the squared tables T^0 = w B.B, T^1 = w B.D, T^2 = w D.D of TabD
-// (element_diag.cuh; t. = how many of d, e lie along the axis) and the 18 point
-// coefficients of element_diag3 (same arithmetic).  Schedule per quintet:
+// (element_diag.cuh; t. = how many of d, e lie along the axis).  The point
+// coefficient is the (i d, i e) entry of the tangent moduli; with K = F^-T,
+//   coef[i][(d, e)] = c_k m_de (mu delta_de + (lam + mu - lam ln J) K_id K_ie),
+// m_de = 1 (d = e) or 2: element_diag3's expression (lam FC_d FC_e + cc (fcf
+// C^-1_de + FC_e FC_d) + S_de, FC = F C^-1, fcf = FC . F_i) reduces to it since
+// F C^-1 = F^-T, fcf = 1 and the C^-1 terms of cc and S cancel (dP of
+// material.py:84-105 applied to the one-row gradient e_i (x) g).  So a point
+// stores K (9 values, over grad u) and kappa = c_k (lam + mu - lam ln J).
+// Schedule per quintet:
 //   * grad u at the points by q5_forward (collocated, element_q5.cuh) into
 //     point slots 0..8;
-//   * point stage: the thread's points t + 128 r -> 18 coefficients written
-//     over the 18 slots (each thread rewrites only the points it read);
-//   * per component: six z' stages (column threads, one per pair) ping-pong
-//     two stage arrays, the y' stage of each pair accumulates its output into
-//     three register groups by x table (tx = 0: (y,y), (z,z), (y,z); 1: (x,y),
-//     (x,z); 2: (x,x)), then one x' stage contracts the three groups into the
-//     rows of the output box: 6 + 6 + 1 stage passes instead of 18.
-// Shared memory: 18 slots x 625 doubles + three stage arrays + the output boxes
-// = 112 KB, two CTAs per SM.  The two TMA staging buffers of the forward pass
-// alias slots 9..11, which only hold coefficients after the forward pass; so
-// the first box of a quintet is fetched at its start, not prefetched.
+//   * point stage: the thread's points t + 128 r -> K in place, kappa;
+//   * per component i: the column threads load K_i. and kappa of their five
+//     points once, then six z' stages (one per pair, coefficients formed in
+//     registers) ping-pong two stage arrays, the y' stage of each pair
+//     accumulates its output into three register groups by x table (tx = 0:
+//     (y,y), (z,z), (y,z); 1: (x,y), (x,z); 2: (x,x)), then one x' stage
+//     contracts the three groups into the rows of the output box: 6 + 6 + 1
+//     stage passes instead of 18.
+// Shared memory: 9 slots x 625 doubles + three stage arrays + the output boxes
+// + kappa = 73 KB, three CTAs per SM.  The two TMA staging buffers of the
+// forward pass are the output boxes and the kappa array (idle until the point
+// stage), so the first box of a quintet is fetched at its start, after the
+// previous quintet's reduce-adds have read the output boxes.
 // Lane orders and array layouts are those of element_q5.cuh (conflict-free).
 #pragma once
 #include "element_diag.cuh"
@@ -31,19 +40,19 @@ namespace sdme {
 
 struct Q5DLay {
   static constexpr int N = 5, E = 5, Q = 125, EQ = E * Q;
-  static constexpr int NSLOT = 18;
-  static constexpr int X = NSLOT * EQ, Y = X + EQ, U = Y + EQ, W = U + EQ;  // W unused (weights sit in TabD)
+  static constexpr int NSLOT = 9;
+  static constexpr int X = NSLOT * EQ, Y = X + EQ, U = Y + EQ;
   static constexpr int RP = BoxW<N>::BW, RB = BoxW<N>::CB;
-  static constexpr int R = (9 * EQ + 15) / 16 * 16;  // staging [2][e][RB] over slots 9..11
-  static constexpr int O = (U + EQ + 15) / 16 * 16;  // output boxes [e][RB]
-  static constexpr int BAR = O + E * RB;
+  static constexpr int O = (U + EQ + 15) / 16 * 16;  // output boxes [e][RB] = staging buffer 0
+  static constexpr int KP = O + E * RB;              // kappa [e][q] (+ pad) = staging buffer 1
+  static constexpr int R = O;                        // staging [2][e][RB]
+  static constexpr int BAR = R + 2 * E * RB;
   static constexpr int COORD = BAR + 2;              // int [e][4]: X0, Y0, Z0, ghost
   static constexpr int PER = COORD + (E * 4 + 1) / 2;
   static constexpr unsigned BOXBYTES = N * N * RP * 8;
-  static_assert(R + 2 * E * RB <= 12 * EQ, "staging buffers must stay inside slots 9..11");
-  __device__ static int slot(int d, int comp) { return (d * 3 + comp) * EQ; }  // grad u (forward pass)
+  static_assert(EQ <= E * RB, "kappa must fit the second staging buffer");
+  __device__ static int slot(int d, int comp) { return (d * 3 + comp) * EQ; }  // grad u, then K[comp][d]
   __device__ static int vslot(int) { return 0; }                               // (no value slots)
-  __device__ static int cslot(int comp, int tt) { return (comp * 6 + tt) * EQ; }
 };
 
 template <int MINB, int MIR, bool ISO>
@@ -80,11 +89,12 @@ __global__ void __launch_bounds__(128, MINB) element_q5_diag(const __grid_consta
   __syncthreads();
   for (long long qd = blockIdx.x; qd < nq; qd += gridDim.x) {
     // this quintet's elements and their first boxes (the staging buffers were
-    // coefficient slots of the previous quintet: generic writes before the
-    // async-proxy writes of the box loads)
+    // the output boxes and kappa of the previous quintet: its reduce-adds have
+    // read the boxes, generic writes precede the async-proxy box loads)
     fence_proxy_async_smem();
     __syncthreads();
     if (t < L::E) {
+      bulk_wait_read();
       const long long idx = qd * L::E + t;
       int ei, ej, ek;
       colour_element(g, args.colour, idx < cnt ? idx : cnt - 1, ei, ej, ek);
@@ -96,45 +106,44 @@ __global__ void __launch_bounds__(128, MINB) element_q5_diag(const __grid_consta
     __syncthreads();  // coord visible
     q5_forward<L, MIR, false, ISO>(tb, zoff, S, t, act, o_row, o5, o_y, o_z, &buf, &ph, umap, 0, Q5Next{nullptr, 0},
                                    true, false);
-    // point stage: grad u -> the 18 pair coefficients (element_diag3's arithmetic)
+    // point stage: grad u -> K = F^-T in place, kappa = c_k (lam + mu - lam ln J)
+    const double lm = args.c_k * (g.lam + g.mu), cl = args.c_k * g.lam, cmu = args.c_k * g.mu;
 #pragma unroll 1
     for (int r = 0; r < QPT; ++r) {
       const int pid = t + r * T;
       if (pid >= L::EQ) continue;
-      const int e = pid / Q, q = pid - e * Q;
-      double H[3][3];
+      double H[9];
 #pragma unroll
       for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int d = 0; d < 3; ++d) H[i][d] = S[L::slot(d, i) + pid];
-      QpState st;
-      qp_state(H, g.mu, g.lam, st);
-      if (!(st.detF > 0.0)) {
+        for (int d = 0; d < 3; ++d) H[i * 3 + d] = S[L::slot(d, i) + pid];
+      QpK st;
+      qp_k(H, st);
+      if (!(st.det > 0.0)) {
+        const int e = pid / Q, q = pid - e * Q;
         const int* cc = coord + e * 4;
         const long long eid = ((long long)(cc[2] / (N - 1)) * g.ny + cc[1] / (N - 1)) * g.nx + cc[0] / (N - 1);
         const int a = q % N, b = (q / N) % N, c = q / (N * N);
         atomicMin(args.inv_flag, (unsigned long long)eid * Q + (unsigned long long)((a * N + b) * N + c));
       }
-      const double cc2 = g.mu - g.lam * st.lnJ;
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        double FC[3];
+      for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int d = 0; d < 3; ++d)
-          FC[d] = st.F[i][0] * st.Ci[0][d] + st.F[i][1] * st.Ci[1][d] + st.F[i][2] * st.Ci[2][d];
-        const double fcf = FC[0] * st.F[i][0] + FC[1] * st.F[i][1] + FC[2] * st.F[i][2];
-#pragma unroll
-        for (int tt = 0; tt < 6; ++tt) {
-          const int d = pair_d(tt), e2 = pair_e(tt);
-          const double Ade = g.lam * FC[d] * FC[e2] + cc2 * (fcf * st.Ci[d][e2] + FC[e2] * FC[d]);
-          S[L::cslot(i, tt) + pid] = args.c_k * (d == e2 ? 1.0 : 2.0) * (Ade + st.S[d][e2]);
-        }
-      }
+        for (int d = 0; d < 3; ++d) S[L::slot(d, i) + pid] = st.K[i][d];
+      S[L::KP + pid] = fma(-cl, st.lnJ, lm);
     }
     __syncthreads();
 #pragma unroll 1
     for (int comp = 0; comp < 3; ++comp) {
       const TabD<5, 5>& td = reload_tab(td0, zoff * (comp + 1));
+      // K[comp][.] and kappa at the column thread's five points
+      double Kc[3][N], kp[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) Kc[d][c] = S[L::slot(d, comp) + o_z + 25 * c];
+        kp[c] = S[L::KP + o_z + 25 * c];
+      }
       double XG[3][N];  // y' outputs of this thread's item (e; k, a), grouped by x table
 #pragma unroll
       for (int gq = 0; gq < 3; ++gq)
@@ -150,7 +159,8 @@ __global__ void __launch_bounds__(128, MINB) element_q5_diag(const __grid_consta
         if (act) {
           double cf[N];
 #pragma unroll
-          for (int c = 0; c < N; ++c) cf[c] = S[L::cslot(comp, tt) + o_z + 25 * c];
+          for (int c = 0; c < N; ++c)
+            cf[c] = d == e2 ? fma(kp[c] * Kc[d][c], Kc[e2][c], cmu) : 2.0 * (kp[c] * Kc[d][c] * Kc[e2][c]);
 #pragma unroll
           for (int k = 0; k < N; ++k) {
             double h = 0.0;

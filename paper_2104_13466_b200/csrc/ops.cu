@@ -657,7 +657,7 @@ template <int MIR, bool ISO>
 void launch_q5_diag(sdme_ctx* c, const double* u, double* d, double ck, double cm, const void* tu, const void* td_map) {
   using L = Q5DLay;
   constexpr int T = 128, smem = L::PER * 8;
-  auto kern = element_q5_diag<2, MIR, ISO>;
+  auto kern = element_q5_diag<3, MIR, ISO>;
   static PerDevice grid_cache;
   const int max_blocks = resident_grid(grid_cache, kern, T, smem);
   const TabC<5, MIR> tb = make_tabc<5, MIR>(c);
