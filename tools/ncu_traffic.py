@@ -1,6 +1,8 @@
 """Turn an `ncu --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,
 dram__bytes_write.sum` log of tools/prof_variant.py into profiles/ncu_traffic_*.json
-(K.p = launches 0-7, mass 8-15, f_int 16-23).  Run here, no GPU."""
+(the launches of K.p, mass and f_int are grouped by kernel name, in order of
+first appearance: with the z-slab schedule K.p and mass are 64 launches each,
+f_int 8).  Run here, no GPU."""
 import csv
 import json
 import sys
@@ -22,11 +24,16 @@ def main(log, out):
         launches[k][r[imet]] = float(r[ival].replace(",", "")) * scale[r[iunit]]
     ids = sorted(launches)
     res = {"source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-                     "--clock-control none --cache-control none (steady state), tools/prof_variant.py (config 2: K.p = launches 0-7, mass 8-15, "
-                     "f_int 16-23); tools/ncu_traffic.py",
+                     "--clock-control none --cache-control none (steady state), tools/prof_variant.py (config 2: K.p, mass, f_int; launches grouped by "
+                     "kernel name); tools/ncu_traffic.py",
            "kernel_kp": names[ids[0]]}
+    order = []
+    for k in ids:
+        if names[k] not in order:
+            order.append(names[k])
     for j, op in enumerate(("kp", "mass", "fint")):
-        sel = ids[8 * j:8 * j + 8]
+        sel = [k for k in ids if names[k] == order[j]]
+        res["kernel_" + op] = order[j]
         rd = sum(launches[k]["dram__bytes_read.sum"] for k in sel)
         wr = sum(launches[k]["dram__bytes_write.sum"] for k in sel)
         res[op] = {"launches": len(sel), "time_ms_sum": sum(launches[k]["gpu__time_duration.sum"] for k in sel),
