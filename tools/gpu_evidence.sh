@@ -22,6 +22,11 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 # one colour pass of 32,768 elements (SDME_SLABS=1: the default z-slab schedule splits it in 8)
 SDME_SLABS=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:element_q5 -s 8 -c 1 -o gpurun_out/kp -f python tools/prof_apply.py > gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:element_q5 -c 17 -o gpurun_out/pcg_ops -f python tools/prof_pcg_ops.py > gpurun_out/ncu_pcg_ops.log 2>&1
+# summaries on the box; the reports themselves are too large to bring back (64 MiB cap)
+python tools/ncu_summary.py gpurun_out/kp.ncu-rep > gpurun_out/ncu_kp_summary.txt 2>&1
+python tools/ncu_sass_ops.py gpurun_out/kp.ncu-rep > gpurun_out/ncu_kp_sassops.txt 2>&1
+python tools/ncu_summary.py gpurun_out/pcg_ops.ncu-rep > gpurun_out/ncu_pcg_ops_summary.txt 2>&1
+rm -f gpurun_out/pcg_ops.ncu-rep gpurun_out/kp.ncu-rep
 timeout 2400 python tools/run_configs.py c1 c3 c4 c5 --cpu > gpurun_out/configs.jsonl 2> gpurun_out/configs.err
 timeout 600 python tools/gen_mesh_bench.py 32 48 > gpurun_out/gen_mesh.jsonl 2> gpurun_out/gen_mesh.err
 # checked build (device bounds / alignment asserts; compute-sanitizer is closed on this pool)
