@@ -103,6 +103,14 @@ struct ColPer {
   static constexpr int PERP = (ColLay<N, VALS, TM>::PER + 15) / 16 * 16;
 };
 
+// tables re-read per component loop (OpArgs::zero)?  N = 5 only with TMA boxes:
+// the general-mesh instance of this kernel measured slower with it (48^3 K.p
+// 1.54 -> 1.59 ms), the stored-data operator faster (1.51 -> 1.49 ms)
+template <int N, bool TM>
+__host__ __device__ constexpr bool col_reload() {
+  return N >= SDME_COL_RELOAD_MIN_N && (N > 5 || TM);
+}
+
 // what to stage after the last component of a forward pass (TMA path)
 struct NextBox {
   const CUtensorMap* map;  // nullptr: nothing
@@ -132,7 +140,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb0, int zoff, c
 #pragma unroll 1
   for (int comp = 0; comp < 3; ++comp) {
     // tables re-read from the constant bank per component (OpArgs::zero)
-    const TabC<N, MIR>& tb = reload_tab(tb0, N >= SDME_COL_RELOAD_MIN_N ? zoff * (comp + 1) : 0);
+    const TabC<N, MIR>& tb = reload_tab(tb0, col_reload<N, TM>() ? zoff * (comp + 1) : 0);
     if (TM) {
       // one lane issues the next box (this field's next component, or the
       // next field / element), then every lane waits for the current box
@@ -263,7 +271,7 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb0, int zoff, 
   constexpr int HP = Half<N>::HP, H = Half<N>::H > 0 ? Half<N>::H : 1;
 #pragma unroll 1
   for (int comp = 0; comp < 3; ++comp) {
-    const TabC<N, MIR>& tb = reload_tab(tb0, N >= SDME_COL_RELOAD_MIN_N ? zoff * (comp + 1) : 0);
+    const TabC<N, MIR>& tb = reload_tab(tb0, col_reload<N, TM>() ? zoff * (comp + 1) : 0);
     if (grad) {
       // x' pencils (c, b): U = D^_x^T F_x
       for (int w = t; w < N * N; w += 32 * WPE / SUB) {

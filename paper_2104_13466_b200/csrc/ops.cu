@@ -517,7 +517,8 @@ void launch_col_k(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
   // passes slab by slab over 8 z-slabs, so the faces a slab's passes share stay
   // in L2 -- with PDL filling the extra partial waves this costs no time and
   // cuts K.p DRAM traffic 4.69 -> 1.90 GB at config 2 (SDME_SLABS overrides)
-  const int nslab = c->nslab_env ? c->nslab : ((TM && (MODE == MODE_APPLY || MODE == MODE_MASS)) ? 8 : 1);
+  // (P = 6 / 8 K.p: 2.02 / 1.98 ms at 8 slabs, 1.97 / 1.98 at 4, 1.95 / 1.93 at 2; tools/run_configs.py c3)
+  const int nslab = c->nslab_env ? c->nslab : ((TM && (MODE == MODE_APPLY || MODE == MODE_MASS)) ? (N >= 7 ? 2 : 8) : 1);
   for (int sp = 0; sp < 8 * nslab; ++sp) {
     const int col = colour_code(c->geo, sp % 8, sp / 8, nslab);
     if (col == -2) continue;
@@ -566,7 +567,9 @@ void launch_q5_iso(sdme_ctx* c, const TabC<5, MIR>& tb, OpArgs a) {
   }
   bool pdl = c->pdl && !c->capturing;
   bool first = true;
-  const int nslab = c->nslab_env ? c->nslab : ((MODE == MODE_APPLY || MODE == MODE_MASS) ? 8 : 1);
+  // z slabs (DRAM traffic): measured on this kernel K.p 1.589 / 1.597 / 1.575 /
+  // 1.603 ms and mass 0.732 / 0.688 / 0.658 / 0.714 ms for 1 / 2 / 4 / 8 slabs, f_int flat
+  const int nslab = c->nslab_env ? c->nslab : ((MODE == MODE_APPLY || MODE == MODE_MASS) ? 4 : 1);
   for (int sp = 0; sp < 8 * nslab; ++sp) {
     const int col = colour_code(c->geo, sp % 8, sp / 8, nslab);
     if (col == -2) continue;
@@ -625,7 +628,11 @@ void launch_col(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
                                          : (a.ty && (MODE == MODE_PA || MODE == MODE_MASS || a.tu) &&
                                             (MODE == MODE_FINT || a.tp));
     if (maps && !c->ev_mode && c->variant != 11) {
-      if constexpr (N == 5) {
+      if constexpr (N == 5 && MODE != MODE_PA) {
+        // The stored-data operator stays on the warp-per-element kernel: it is
+        // bound by its 10 doubles per point from HBM, not by lane use (1.49 vs
+        // 1.51 ms), and with the mass term the quintet's three extra value
+        // slots leave two CTAs per SM (1.69 vs 1.94 ms; tools/op_times.py).
         if (c->variant != 12) {
           launch_q5<MODE, VAL, MIR>(c, tb, a);
           return;

@@ -17,4 +17,8 @@ out = {}
 for op in ("apply", "fint", "mass", "setup", "apply_pa", "diag"):
     pb.time_op(op, u, p, y, 1e3 if op == "mass" else 0.0, 2)
     out[op] = round(pb.time_op(op, u, p, y, 1e3 if op == "mass" else 0.0, 10), 4)
+# the Newmark operators: K.p + c_m M p from u and from the stored quadrature data
+for op in ("apply", "apply_pa"):
+    pb.time_op(op, u, p, y, 4e8, 2)
+    out[op + "+m"] = round(pb.time_op(op, u, p, y, 4e8, 10), 4)
 print(os.environ.get("SDME_VARIANT", "0"), out)

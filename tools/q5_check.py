@@ -19,6 +19,9 @@ from paper_2104_13466_b200.basis import BasisKind, gauss_rule  # noqa: E402
 
 def problem(div, tag, variant, dr, hs=(1.0, 1.0, 1.0)):
     os.environ["SDME_EV"] = "0"
+    # one z-slab schedule for both kernels (their defaults differ; the order of
+    # the colour passes fixes the summation order at shared points)
+    os.environ["SDME_SLABS"] = "4"
     if variant:
         os.environ["SDME_VARIANT"] = str(variant)
     try:
@@ -28,6 +31,7 @@ def problem(div, tag, variant, dr, hs=(1.0, 1.0, 1.0)):
     finally:
         os.environ.pop("SDME_EV", None)
         os.environ.pop("SDME_VARIANT", None)
+        os.environ.pop("SDME_SLABS", None)
 
 
 def run(pb, seed):
