@@ -17,11 +17,11 @@ timeout 300 python tools/op_times.py > gpurun_out/op_times.log 2>&1
 timeout 300 python tools/pcg_iter_time.py 64 4 5 > gpurun_out/pcg_iter.log 2>&1
 timeout 300 python tools/q5_check.py > gpurun_out/q5_check.log 2>&1
 timeout 300 python tools/q5d_check.py > gpurun_out/q5d_check.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_launch.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_launch.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --cache-control none -k regex:element_q5 -c 160 --csv --log-file gpurun_out/traffic.csv python tools/prof_variant.py > gpurun_out/ncu_traffic.log 2>&1
 # one colour pass of 32,768 elements (SDME_SLABS=1: the default z-slab schedule splits it in 8)
 SDME_SLABS=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:element_q5 -s 8 -c 1 -o gpurun_out/kp -f python tools/prof_apply.py > gpurun_out/ncu_full.log 2>&1
-timeout 900 ncu --set full --clock-control none -k regex:element_q5 -c 17 -o gpurun_out/pcg_ops -f python tools/prof_pcg_ops.py > gpurun_out/ncu_pcg_ops.log 2>&1
+timeout 900 ncu --set full --clock-control none -k "regex:element_q5|element_col" -c 17 -o gpurun_out/pcg_ops -f python tools/prof_pcg_ops.py > gpurun_out/ncu_pcg_ops.log 2>&1
 # summaries on the box; the reports themselves are too large to bring back (64 MiB cap)
 python tools/ncu_summary.py gpurun_out/kp.ncu-rep > gpurun_out/ncu_kp_summary.txt 2>&1
 python tools/ncu_sass_ops.py gpurun_out/kp.ncu-rep > gpurun_out/ncu_kp_sassops.txt 2>&1
