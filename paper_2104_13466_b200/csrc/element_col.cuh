@@ -125,7 +125,7 @@ __device__ __forceinline__ void col_stage(const Geo& g, const double* __restrict
   cp_async_commit();
 }
 
-template <int N, int WPE, int MIR, bool VAL, bool VALS, bool TM = false, int SUB = 1>
+template <int N, int WPE, int MIR, bool VAL, bool VALS, bool TM = false, int SUB = 1, bool ISO = false>
 __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb0, int zoff, const Geo& g,
                                             const double* __restrict__ src, int X0, int Y0, int Z0, double* S, int t,
                                             int* buf, NextRows next, bool grad, const CUtensorMap* smap = nullptr,
@@ -140,7 +140,10 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb0, int zoff, c
 #pragma unroll 1
   for (int comp = 0; comp < 3; ++comp) {
     // tables re-read from the constant bank per component (OpArgs::zero)
-    const TabC<N, MIR>& tb = reload_tab(tb0, col_reload<N, TM>() ? zoff * (comp + 1) : 0);
+    const TabC<N, MIR>& tb = reload_tab(tb0, (col_reload<N, TM>() && !ISO) ? zoff * (comp + 1) : 0);
+    // cubic elements (ISO): one derivative table for the three axes
+    const auto& tDy = ISO ? tb.Dx : tb.Dy;
+    const auto& tDz = ISO ? tb.Dx : tb.Dz;
     if (TM) {
       // one lane issues the next box (this field's next component, or the
       // next field / element), then every lane waits for the current box
@@ -228,7 +231,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb0, int zoff, c
       if (grad) {
         double pe[PE], po[PO], gz[N];
         eo_split<N, 0>(u, pe, po);
-        eo_fwd<N, Mp::NO, Mp::NE>(tb.Dz, po, pe, gz);
+        eo_fwd<N, Mp::NO, Mp::NE>(tDz, po, pe, gz);
 #pragma unroll
         for (int c = 0; c < N; ++c) S[L::qi(2, comp, c * N * N + w)] = gz[c];
       }
@@ -248,7 +251,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb0, int zoff, c
 #pragma unroll
         for (int b = 0; b < N; ++b) v[b] = S[L::U + L::uo(c, b, r)];
         eo_split<N, 0>(v, pe, po);
-        eo_fwd<N, Mp::NO, Mp::NE>(tb.Dy, po, pe, gy);
+        eo_fwd<N, Mp::NO, Mp::NE>(tDy, po, pe, gy);
 #pragma unroll
         for (int b = 0; b < N; ++b) S[L::qi(1, comp, c * N * N + b * N + r)] = gy[b];
       }
@@ -260,7 +263,7 @@ __device__ __forceinline__ void col_forward(const TabC<N, MIR>& tb0, int zoff, c
 
 // backward: per component, the weighted flux slots 0..2 (and the weighted
 // value slot 3 when VAL) -> y += B^T (x) B^T (x) B^T (sum_d D^_d^T F_d [+ V])
-template <int N, int WPE, int MIR, bool VAL, bool VALS, bool TM = false, int SUB = 1>
+template <int N, int WPE, int MIR, bool VAL, bool VALS, bool TM = false, int SUB = 1, bool ISO = false>
 __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb0, int zoff, const Geo& g,
                                              double* __restrict__ dst, int X0, int Y0, int Z0, double* S, int t,
                                              double* evb, bool grad, const CUtensorMap* ymap = nullptr,
@@ -269,9 +272,14 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb0, int zoff, 
   using Mr = Mir<N, MIR>;
   using Mp = Mir<N, 0>;
   constexpr int HP = Half<N>::HP, H = Half<N>::H > 0 ? Half<N>::H : 1;
+  // N <= 5: the forward tables serve the backward pass (make_tabc stores the
+  // backward ones as their exact transposes there): half the table constants
+  constexpr bool FT = N <= 5;
 #pragma unroll 1
   for (int comp = 0; comp < 3; ++comp) {
-    const TabC<N, MIR>& tb = reload_tab(tb0, col_reload<N, TM>() ? zoff * (comp + 1) : 0);
+    const TabC<N, MIR>& tb = reload_tab(tb0, (col_reload<N, TM>() && !ISO) ? zoff * (comp + 1) : 0);
+    const auto& tDy = ISO ? tb.Dx : tb.Dy;
+    const auto& tDz = ISO ? tb.Dx : tb.Dz;
     if (grad) {
       // x' pencils (c, b): U = D^_x^T F_x
       for (int w = t; w < N * N; w += 32 * WPE / SUB) {
@@ -280,7 +288,8 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb0, int zoff, 
 #pragma unroll
         for (int a = 0; a < N; ++a) q[a] = S[L::qi(0, comp, c * N * N + b * N + a)];
         eo_qsplit<N>(q, qe, qo);
-        eo_bwd<N, N, 0, -1, Mp::NO, Mp::NE, false>(tb.bDx, qe, qo, y);
+        if (FT) eo_bwd_t<N, N, 0, -1, Mp::NO, Mp::NE, false>(tb.Dx, qe, qo, y);
+        else eo_bwd<N, N, 0, -1, Mp::NO, Mp::NE, false>(tb.bDx, qe, qo, y);
 #pragma unroll
         for (int a = 0; a < N; ++a) S[L::U + L::uo(c, b, a)] = y[a];
       }
@@ -295,7 +304,8 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb0, int zoff, 
           y[b] = S[L::U + L::uo(c, b, a)];
         }
         eo_qsplit<N>(q, qe, qo);
-        eo_bwd<N, N, 0, -1, Mp::NO, Mp::NE, true>(tb.bDy, qe, qo, y);
+        if (FT) eo_bwd_t<N, N, 0, -1, Mp::NO, Mp::NE, true>(tDy, qe, qo, y);
+        else eo_bwd<N, N, 0, -1, Mp::NO, Mp::NE, true>(tb.bDy, qe, qo, y);
 #pragma unroll
         for (int b = 0; b < N; ++b) S[L::U + L::uo(c, b, a)] = y[b];
       }
@@ -310,14 +320,16 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb0, int zoff, 
 #pragma unroll
         for (int c = 0; c < N; ++c) q[c] = S[L::qi(2, comp, c * N * N + w)];
         eo_qsplit<N>(q, qe, qo);
-        eo_bwd<N, N, 0, -1, Mp::NO, Mp::NE, true>(tb.bDz, qe, qo, v);
+        if (FT) eo_bwd_t<N, N, 0, -1, Mp::NO, Mp::NE, true>(tDz, qe, qo, v);
+        else eo_bwd<N, N, 0, -1, Mp::NO, Mp::NE, true>(tb.bDz, qe, qo, v);
       }
       if (VAL) {
 #pragma unroll
         for (int c = 0; c < N; ++c) v[c] += S[L::qi(3, comp, c * N * N + w)];
       }
       eo_qsplit<N>(v, qe, qo);
-      eo_bwd<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.bB, qe, qo, h);
+      if (FT) eo_bwd_t<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.B, qe, qo, h);
+      else eo_bwd<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.bB, qe, qo, h);
 #pragma unroll
       for (int k = 0; k < N; ++k) S[L::Y + L::yo(k, w / N, w % N)] = h[k];
     }
@@ -329,7 +341,8 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb0, int zoff, 
 #pragma unroll
       for (int b = 0; b < N; ++b) v[b] = S[L::Y + L::yo(k, b, a)];
       eo_qsplit<N>(v, qe, qo);
-      eo_bwd<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.bB, qe, qo, h);
+      if (FT) eo_bwd_t<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.B, qe, qo, h);
+      else eo_bwd<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.bB, qe, qo, h);
 #pragma unroll
       for (int j = 0; j < N; ++j) S[L::X + L::xo(k, j, a)] = h[j];
     }
@@ -346,7 +359,8 @@ __device__ __forceinline__ void col_backward(const TabC<N, MIR>& tb0, int zoff, 
 #pragma unroll
       for (int a = 0; a < N; ++a) v[a] = S[L::X + L::xo(k, j, a)];
       eo_qsplit<N>(v, qe, qo);
-      eo_bwd<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.bB, qe, qo, acc);
+      if (FT) eo_bwd_t<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.B, qe, qo, acc);
+      else eo_bwd<N, N, MIR, 1, Mr::NE, Mr::NO, false>(tb.bB, qe, qo, acc);
       if (TM) {
         // row of the output box; constrained points and the pitch slot get 0
         // (the reduce-add of +0.0 outside the element touches only points no
@@ -433,7 +447,8 @@ __device__ __forceinline__ void gen_to_phys(double* H, const double J[3][3]) {
 // each with its own shared region and barriers; the halves run the same
 // number of iterations (a half past the end of the colour repeats the last
 // element without scattering it) so the warp-wide syncs stay uniform
-template <int N, int WPE, int MINB, int MODE, bool VAL, int MIR, bool TM = false, bool GEN = false, int SUB = 1>
+template <int N, int WPE, int MINB, int MODE, bool VAL, int MIR, bool TM = false, bool GEN = false, int SUB = 1,
+          bool ISO = false>
 __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_constant__ TabC<N, MIR> tb,
                                                         const __grid_constant__ Geo g, OpArgs args) {
   static_assert(SUB == 1 || (SUB == 2 && WPE == 1 && TM && !GEN), "half-warp elements: TMA path only");
@@ -520,7 +535,7 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
     if (UPASS) {
       const NextRows after_u = MODE == MODE_APPLY ? NextRows{args.p + eoff, X0, Y0, Z0} : nxt;
       const NextBox after_ub = MODE == MODE_APPLY ? NextBox{pmap, X0, Y0, Z0} : nxb;
-      col_forward<N, WPE, MIR, false, VALS, TM, SUB>(tb, args.zero, g, args.u + eoff, X0, Y0, Z0, S, t, &buf, after_u, true, umap,
+      col_forward<N, WPE, MIR, false, VALS, TM, SUB, ISO>(tb, args.zero, g, args.u + eoff, X0, Y0, Z0, S, t, &buf, after_u, true, umap,
                                                 after_ub, &ph);
 #pragma unroll
       for (int r = 0; r < QPT; ++r) {
@@ -540,7 +555,7 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
       group_sync<WPE>(0);
     }
     if (PPASS)
-      col_forward<N, WPE, MIR, VAL, VALS, TM, SUB>(tb, args.zero, g, args.p + eoff, X0, Y0, Z0, S, t, &buf, nxt, PGRAD, pmap, nxb,
+      col_forward<N, WPE, MIR, VAL, VALS, TM, SUB, ISO>(tb, args.zero, g, args.p + eoff, X0, Y0, Z0, S, t, &buf, nxt, PGRAD, pmap, nxb,
                                               &ph);
 #pragma unroll
     for (int r = 0; r < QPT; ++r) {
@@ -651,7 +666,7 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
     group_sync<WPE>(0);
     if (MODE == MODE_SETUP) continue;
     double* evb = args.ev ? args.ev + eid * 3 * Q : nullptr;
-    col_backward<N, WPE, MIR, VAL, VALS, TM, SUB>(tb, args.zero, g, args.y, X0, Y0, Z0, S, t, evb, PGRAD,
+    col_backward<N, WPE, MIR, VAL, VALS, TM, SUB, ISO>(tb, args.zero, g, args.y, X0, Y0, Z0, S, t, evb, PGRAD,
                                                   ghost ? nullptr : static_cast<const CUtensorMap*>(args.ty),
                                                   &waited);
   }

@@ -55,32 +55,6 @@ struct Q5Lay {
   __device__ static int vslot(int comp) { return (VB + comp) * EQ; }
 };
 
-// y = T^T q of a B-type (F = +1) or D-type (F = -1) operator read from its
-// *forward* tables: make_tabc stores the backward tables as their exact
-// transposes (bwd E[e][a] = fwd S[a][e], O[o][a] = T[a][o]), so this is
-// eo_bwd bit for bit with half as many distinct table constants
-template <int N, int M, int MIR, int F, int WE, int WO, bool ACC>
-__device__ __forceinline__ void eo_bwd_t(const EoFwd<M, WE, WO>& t, const double (&qe)[Half<M>::HP],
-                                         const double (&qo)[Half<M>::H > 0 ? Half<M>::H : 1], double (&y)[N]) {
-  constexpr int H = Half<M>::H, HP = Half<M>::HP;
-  double YE[WE > 0 ? WE : 1], YO[WO > 0 ? WO : 1];
-#pragma unroll
-  for (int e = 0; e < WE; ++e) {
-    double s = 0.0;
-#pragma unroll
-    for (int a = 0; a < HP; ++a) s = fma(t.S[a][e], qe[a], s);
-    YE[e] = s;
-  }
-#pragma unroll
-  for (int o = 0; o < WO; ++o) {
-    double s = 0.0;
-#pragma unroll
-    for (int a = 0; a < H; ++a) s = fma(t.T[a][o], qo[a], s);
-    YO[o] = s;
-  }
-  eo_recon<N, MIR, F, WE, WO, ACC>(YE, YO, y);
-}
-
 // which element coordinates a lane 0..4 stages next (coordinate set of the
 // quintet table) and from which tensor map; map == nullptr: nothing
 struct Q5Next {

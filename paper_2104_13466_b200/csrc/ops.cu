@@ -470,12 +470,13 @@ TabC<N, MIR> make_tabc(const sdme_ctx* c) {
   EoBuild<N, N, 0>::bwd(t.bDx, Dh[0], -1);
   EoBuild<N, N, 0>::bwd(t.bDy, Dh[1], -1);
   EoBuild<N, N, 0>::bwd(t.bDz, Dh[2], -1);
-  if (N == 5) {
-    // P = 4: the backward tables are the forward ones transposed, entry for
+  if (N <= 5) {
+    // P <= 4: the backward tables are the forward ones transposed, entry for
     // entry (by the mirror symmetry EoBuild::bwd gives the same numbers up to
     // the last bit).  The quintet kernel (element_q5) reads the forward tables
     // in its backward pass -- half the table constants -- and so matches
-    // element_col<5> bit for bit.  Other orders keep the EoBuild::bwd bits.
+    // element_col<5> bit for bit; element_col itself does so for N <= 5.
+    // Higher orders keep the EoBuild::bwd bits.
     eo_transpose(t.bB, t.B);
     eo_transpose(t.bDx, t.Dx);
     eo_transpose(t.bDy, t.Dy);
@@ -486,14 +487,14 @@ TabC<N, MIR> make_tabc(const sdme_ctx* c) {
   return t;
 }
 
-template <int N, int MODE, bool VAL, int MIR, bool TM>
+template <int N, int MODE, bool VAL, int MIR, bool TM, bool ISO = false>
 void launch_col_k(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
   constexpr int WPE = LargeShape<N, N>::WPE;  // one round per stage
   constexpr int T = 32 * WPE;
   // N * N <= 16 pencils per stage: two elements per warp (TMA path)
   constexpr int SUB = (TM && WPE == 1 && N * N <= 16) ? 2 : 1;
   constexpr int smem = SUB * ColPer<N, VAL, TM>::PERP * 8;
-  auto kern = element_col<N, WPE, (WPE == 1 ? SDME_COL_MINB : 1), MODE, VAL, MIR, TM, false, SUB>;
+  auto kern = element_col<N, WPE, (WPE == 1 ? SDME_COL_MINB : 1), MODE, VAL, MIR, TM, false, SUB, ISO>;
   static PerDevice grid_cache;  // per device: attribute + occupancy set once
   const int max_blocks = resident_grid(grid_cache, kern, T, smem);
   if (MODE == MODE_SETUP || c->ev_mode) {
@@ -546,6 +547,15 @@ void launch_col_k(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
     ++c->launches;
   }
   c->pdl_first = false;
+}
+
+// SDME_Q5_ISO=0: never the one-derivative-table (ISO) instances (A/B)
+inline bool q5_iso_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SDME_Q5_ISO");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 // P = 4 with tensor maps: five elements per 4-warp CTA (element_q5.cuh);
@@ -606,12 +616,8 @@ void launch_q5_iso(sdme_ctx* c, const TabC<5, MIR>& tb, OpArgs a) {
 // (OpArgs::zero).  SDME_Q5_ISO=0 forces the general instance (A/B).
 template <int MODE, bool VAL, int MIR>
 void launch_q5(sdme_ctx* c, const TabC<5, MIR>& tb, OpArgs a) {
-  static const bool iso_ok = [] {
-    const char* e = getenv("SDME_Q5_ISO");
-    return !(e && e[0] == '0');
-  }();
   const Geo& g = c->geo;
-  if (iso_ok && g.s[0] == g.s[1] && g.s[1] == g.s[2]) launch_q5_iso<MODE, VAL, MIR, true>(c, tb, a);
+  if (q5_iso_enabled() && g.s[0] == g.s[1] && g.s[1] == g.s[2]) launch_q5_iso<MODE, VAL, MIR, true>(c, tb, a);
   else launch_q5_iso<MODE, VAL, MIR, false>(c, tb, a);
 }
 
@@ -636,6 +642,16 @@ void launch_col(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
         // slots leave two CTAs per SM (1.69 vs 1.94 ms; tools/op_times.py).
         if (c->variant != 12) {
           launch_q5<MODE, VAL, MIR>(c, tb, a);
+          return;
+        }
+      }
+      if constexpr (N <= 5) {
+        // cubic elements: one derivative table (ISO instance; with the forward
+        // tables also serving the backward pass, 16 / 25 table constants at
+        // P = 3 / 4 -- they stay in uniform registers for the whole kernel)
+        const Geo& g = c->geo;
+        if (q5_iso_enabled() && g.s[0] == g.s[1] && g.s[1] == g.s[2]) {
+          launch_col_k<N, MODE, VAL, MIR, true, true>(c, tb, a);
           return;
         }
       }
