@@ -447,6 +447,11 @@ __device__ __forceinline__ void gen_to_phys(double* H, const double J[3][3]) {
 // each with its own shared region and barriers; the halves run the same
 // number of iterations (a half past the end of the colour repeats the last
 // element without scattering it) so the warp-wide syncs stay uniform
+// SDME_COL_PA_PREF: L2 prefetch of the stored point data (MODE_PA) per element
+#ifndef SDME_COL_PA_PREF
+#define SDME_COL_PA_PREF 1
+#endif
+
 template <int N, int WPE, int MINB, int MODE, bool VAL, int MIR, bool TM = false, bool GEN = false, int SUB = 1,
           bool ISO = false>
 __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_constant__ TabC<N, MIR> tb,
@@ -521,12 +526,15 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
     }
     NextRows nxt{nullptr, 0, 0, 0};
     NextBox nxb{nullptr, 0, 0, 0};
+    long long next_eid = -1;
     if (base + stride < cnt) {
       if (GEN) {
         nxt = NextRows{first_field + (idx + stride) * 3 * Q, 0, 0, 0};
+        next_eid = idx + stride;
       } else {
         int ni, nj, nk;
         colour_element(g, args.colour, SUB == 1 ? idx + stride : min(base + stride + half, cnt - 1), ni, nj, nk);
+        next_eid = ((long long)nk * g.ny + nj) * g.nx + ni;
         if (TM) nxb = NextBox{first_map, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
         else nxt = NextRows{first_field, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
       }
@@ -553,6 +561,21 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
         }
       }
       group_sync<WPE>(0);
+    }
+    if (MODE == MODE_PA && SDME_COL_PA_PREF) {
+      // the element's stored point data (K, ln J: 80 Q bytes, 16-byte aligned)
+      // on its way into L2 while the forward pass of p runs (2: the next
+      // element's, a whole element ahead)
+      constexpr int LPE = (kQpSlots * Q * 8 + 127) / 128 + 1;
+      const bool first_it = base == (long long)blockIdx.x * SUB;
+      if (SDME_COL_PA_PREF == 1 || first_it) {
+        const char* bp = reinterpret_cast<const char*>(args.qpd + eid * (kQpSlots * Q));
+        for (int l = t; l < LPE; l += T) prefetch_l2(bp + (l * 128 < kQpSlots * Q * 8 - 8 ? l * 128 : kQpSlots * Q * 8 - 8));
+      }
+      if (SDME_COL_PA_PREF == 2 && next_eid >= 0) {
+        const char* bp = reinterpret_cast<const char*>(args.qpd + next_eid * (kQpSlots * Q));
+        for (int l = t; l < LPE; l += T) prefetch_l2(bp + (l * 128 < kQpSlots * Q * 8 - 8 ? l * 128 : kQpSlots * Q * 8 - 8));
+      }
     }
     if (PPASS)
       col_forward<N, WPE, MIR, VAL, VALS, TM, SUB, ISO>(tb, args.zero, g, args.p + eoff, X0, Y0, Z0, S, t, &buf, nxt, PGRAD, pmap, nxb,

@@ -297,6 +297,18 @@ __device__ __forceinline__ void q5_backward(const TabC<5, MIR>& tb0, int zoff, c
   }
 }
 
+// Stored-data operator (MODE_PA): the point data K, ln J (10 doubles per point,
+// [elem][slot][q]) is on its way while the forward pass of p runs, not fetched
+// at the point stage where its HBM latency would sit between two CTA barriers.
+// SDME_PA_PREF (measured at config 2, K.p / K.p + c_m M in ms; 0: 1.52 / 1.96):
+//   1  loads into registers before the forward pass           1.63 / 1.51
+//   2  L2 prefetch of the quintet's lines before the pass     1.48 / 1.85
+//   3  1 + L2 prefetch of the next quintet a round ahead      1.35 / 1.49  (default)
+//   4  3 with the register loads at the point stage           1.38 / 1.56
+#ifndef SDME_PA_PREF
+#define SDME_PA_PREF 3
+#endif
+
 template <int MINB, int MODE, bool VAL, int MIR, bool ISO>
 __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ TabC<5, MIR> tb,
                                                         const __grid_constant__ Geo g, OpArgs args) {
@@ -348,6 +360,7 @@ __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ 
     mbar_expect_tx(bars, L::BOXBYTES);
     tma_load_box(S + L::R + t * L::RB, first_map, cc[0], cc[1], cc[2], 0, bars);
   }
+  if (MODE == MODE_PA && SDME_PA_PREF) __syncthreads();  // coordinates of the first quintet
   int cur = 0;
   for (long long qd = blockIdx.x; qd < nq; qd += gridDim.x, cur ^= 1) {
     const bool has_next = qd + gridDim.x < nq;
@@ -375,9 +388,42 @@ __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ 
         }
       }
     }
+    constexpr bool KREG = MODE == MODE_PA && (SDME_PA_PREF == 1 || SDME_PA_PREF == 3 || SDME_PA_PREF == 4);
+    double Kq[KREG ? QPT : 1][kQpSlots];
+    auto load_kq = [&]() {
+#pragma unroll
+      for (int r = 0; r < QPT; ++r) {
+        const int pid = t + r * T;
+        if (pid < L::EQ) {
+          const int e = pid / Q, q = pid - e * Q;
+          const int* cc = coord + (cur * L::E + e) * 4;
+          const long long eid = ((long long)(cc[2] / (N - 1)) * g.ny + cc[1] / (N - 1)) * g.nx + cc[0] / (N - 1);
+          const double* qp = args.qpd + eid * (kQpSlots * Q) + q;
+#pragma unroll
+          for (int k = 0; k < kQpSlots; ++k) Kq[KREG ? r : 0][k] = __ldg(qp + k * Q);
+        }
+      }
+    };
+    // L2 prefetch of the point data of coordinate set `set` (an element's 10,000
+    // bytes start 16-byte aligned: 80 lines cover them)
+    auto prefetch_set = [&](int set) {
+      constexpr int LPE = (kQpSlots * Q * 8 + 127) / 128 + 1;
+      for (int l = t; l < L::E * LPE; l += T) {
+        const int e = l / LPE, j = l - e * LPE;
+        const int* cc = coord + (set * L::E + e) * 4;
+        const long long eid = ((long long)(cc[2] / (N - 1)) * g.ny + cc[1] / (N - 1)) * g.nx + cc[0] / (N - 1);
+        const char* base = reinterpret_cast<const char*>(args.qpd + eid * (kQpSlots * Q));
+        const int off = j * 128 < kQpSlots * Q * 8 - 8 ? j * 128 : kQpSlots * Q * 8 - 8;
+        prefetch_l2(base + off);
+      }
+    };
+    if (MODE == MODE_PA && (SDME_PA_PREF == 1 || SDME_PA_PREF == 3)) load_kq();
+    if (MODE == MODE_PA && (SDME_PA_PREF == 2 || (SDME_PA_PREF >= 3 && qd == blockIdx.x))) prefetch_set(cur);
     if (PPASS)
       q5_forward<L, MIR, VAL, ISO>(tb, zoff, S, t, act, o_row, o5, o_y, o_z, &buf, &ph, pmap, cur, after_last,
                                             PGRAD, !UPASS);
+    if (MODE == MODE_PA && SDME_PA_PREF >= 3 && has_next) prefetch_set(cur ^ 1);
+    if (MODE == MODE_PA && SDME_PA_PREF == 4) load_kq();
 #pragma unroll
     for (int r = 0; r < QPT; ++r) {
       const int pid = t + r * T;
@@ -390,12 +436,18 @@ __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ 
         continue;
       }
       long long eid = 0;
-      if (MODE == MODE_PA || MODE == MODE_SETUP) {
+      if ((MODE == MODE_PA && !KREG) || MODE == MODE_SETUP) {
         const int* cc = coord + (cur * L::E + e) * 4;
         eid = ((long long)(cc[2] / (N - 1)) * g.ny + cc[1] / (N - 1)) * g.nx + cc[0] / (N - 1);
       }
       QpK s;
-      if (MODE == MODE_PA) {
+      if (KREG) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) s.K[i][d] = Kq[KREG ? r : 0][i * 3 + d];
+        s.lnJ = Kq[KREG ? r : 0][9];
+      } else if (MODE == MODE_PA) {
         const double* qd = args.qpd + eid * (kQpSlots * Q) + q;
 #pragma unroll
         for (int i = 0; i < 3; ++i)

@@ -635,11 +635,13 @@ void launch_col(sdme_ctx* c, const TabC<N, MIR>& tb, OpArgs a) {
                                          : (a.ty && (MODE == MODE_PA || MODE == MODE_MASS || a.tu) &&
                                             (MODE == MODE_FINT || a.tp));
     if (maps && !c->ev_mode && c->variant != 11) {
-      if constexpr (N == 5 && MODE != MODE_PA) {
-        // The stored-data operator stays on the warp-per-element kernel: it is
-        // bound by its 10 doubles per point from HBM, not by lane use (1.49 vs
-        // 1.51 ms), and with the mass term the quintet's three extra value
-        // slots leave two CTAs per SM (1.69 vs 1.94 ms; tools/op_times.py).
+      if constexpr (N == 5) {
+        // The stored-data operator too (round 2): with its point data (K, ln J)
+        // prefetched into L2 one quintet ahead and loaded into registers before
+        // the forward pass of p (element_q5.cuh, SDME_PA_PREF) it runs at 1.35 ms
+        // against 1.50 ms for the warp-per-element kernel without prefetch
+        // (1.38 with its own L2 prefetch), and with the mass term, two CTAs
+        // per SM, at 1.49 against 1.67 (1.54) ms (tools/op_times.py).
         if (c->variant != 12) {
           launch_q5<MODE, VAL, MIR>(c, tb, a);
           return;

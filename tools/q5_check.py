@@ -49,6 +49,11 @@ def run(pb, seed):
     return out
 
 
+# variants to compare (argv: A B; default the quintet kernel against SDME_VARIANT=12;
+# "14 12": the stored-data operator on the quintet kernel against the warp-per-element one)
+VA, VB = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (0, 12)
+
+
 def main():
     bad = 0
     cases = [((3, 2, 2), "SDME_M", (("xmin", (0, 1, 2)),)),
@@ -61,8 +66,8 @@ def main():
     cases = [c + ((1.0, 1.0, 1.0),) for c in cases] + [((7, 6, 5), "SDME_M", cases[1][2], (1.0, 0.75, 1.5)),
                                                         ((3, 2, 2), "LagrangeGLL", cases[0][2], (2.0, 1.0, 1.0))]
     for div, tag, dr, hs in cases:
-        a = run(problem(div, tag, 0, dr, hs), 1)
-        b = run(problem(div, tag, 12, dr, hs), 1)
+        a = run(problem(div, tag, VA, dr, hs), 1)
+        b = run(problem(div, tag, VB, dr, hs), 1)
         for k in a:
             same = np.array_equal(a[k], b[k])
             rel = float(np.abs(a[k] - b[k]).max() / max(np.abs(b[k]).max(), 1e-300))
