@@ -29,6 +29,7 @@ enum {
   S_STOPREL,   // relative residual at stop
   S_MAXIT,
   S_SCRATCH,   // generic dot result
+  S_ITERB,     // number of the iteration in flight (fused sequence: written by k_pcg_update2, read by k_pcg_p2)
   S_COUNT
 };
 

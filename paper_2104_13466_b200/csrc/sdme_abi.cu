@@ -270,6 +270,35 @@ bool ensure_qpd(sdme_ctx* ctx) {
   return true;
 }
 
+// SDME_PCG_CHAIN bit mask (A/B): 1 fused vector kernels (k_pcg_update2 / k_pcg_p2),
+// 2 the vector kernels as programmatic dependents, 4 the first colour pass
+// overlaps the zeroing of A p.  The colour passes always carry PDL edges (in
+// the captured graph too: config 5 SDME_H 0.090 -> 0.073 s per step, one
+// iteration at 32^3 385 -> 339 us).  Measured (one iteration at 64^3 / 32^3 /
+// 16^3 in us, config 5 SDME_H in s per step): 0: 2511 / 339 / 96.0, 0.0730;
+// 1: 2522 / 337 / 93.6, 0.0715; 3: 2562 / 342 / 93.4, 0.0778 (dependents
+// spinning in griddepcontrol.wait take issue slots from the HBM-bound kernel
+// they wait for); 5: 2515 / 333 / 93.7, 0.0720 (default); 7: 2559 / 339 / 93.5, 0.0775.
+// Read per context (sdme_ctx::chain_mode).
+
+// launch as a programmatic dependent of the previous kernel on the stream
+template <class... KArgs, class... Args>
+void launch_chain(sdme_ctx* ctx, void (*kern)(KArgs...), int grid, int block, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = ctx->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cfg.numAttrs = (ctx->chain_mode & 2) ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess && ctx->launch_err == cudaSuccess) ctx->launch_err = e;
+}
+
 // One PCG iteration on ctx->st: E-vector element launch + one cluster kernel
 // (small meshes) or the 7-kernel sequence.  Every kernel returns at once when
 // the status word is set; the last one clears the graph's loop condition.
@@ -291,6 +320,46 @@ void enqueue_pcg_iteration(sdme_ctx* ctx, const double* pu, double* px, double* 
     ctx->ev_no_gather = false;
     ctx->ops->pcg_small(ctx, px, r, p, ap, dinv, cond, has_cond);
   } else {
+    if (ctx->pdl) {
+      // fused sequence, every kernel a programmatic dependent of its predecessor
+      // (vector_kernels.cuh); the first colour pass of a TMA operator overlaps
+      // the zeroing of A p like the passes overlap one another
+      const bool tm_first = (ctx->chain_mode & 4) && !ctx->ev_mode && !ctx->gen && sdme_tmap_of(ctx, ap);
+      launch_chain(ctx, k_zero_chain, grid_for(ctx->nvec), 256, ap, ctx->nvec, (const int*)ctx->d_status);
+      const bool cap = ctx->capturing;
+      ctx->capturing = false;  // PDL edges between the passes, inside a capture too
+      ctx->pdl_first = tm_first;
+      if (c_k != 0.0)
+        ctx->ops->element(ctx, kmode, pu, p, ap, c_k, c_m);
+      else
+        ctx->ops->element(ctx, MODE_MASS, nullptr, p, ap, 0.0, c_m);
+      ctx->pdl_first = false;
+      ctx->capturing = cap;
+      if (withc) contact_op(ctx, CONTACT_APPLY, p, ap, ctx->d_status);
+      if (!(ctx->chain_mode & 1)) {
+        launch_chain(ctx, k_pcg_pap_chain, kRedBlocks, kRedThreads, (const double*)p, (const double*)ap, ctx->nvec,
+                     ctx->d_partial, (const int*)ctx->d_status);
+        k_pcg_alpha<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, ctx->d_status);
+        k_pcg_update<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(px, r, p, ap, dinv, ctx->d_scal, ctx->nvec,
+                                                              ctx->d_partial, ctx->d_status);
+        k_pcg_check<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, ctx->d_status);
+        k_pcg_p<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, r, dinv, ctx->d_scal, ctx->nvec, ctx->d_status, cond,
+                                                           has_cond);
+        ctx->launches += 6;
+        ctx->cur_skip = nullptr;
+        return;
+      }
+      double* part2 = ctx->d_partial + 2 * kRedBlocks;
+      launch_chain(ctx, k_pcg_pap_chain, kRedBlocks, kRedThreads, (const double*)p, (const double*)ap, ctx->nvec,
+                   ctx->d_partial, (const int*)ctx->d_status);
+      launch_chain(ctx, k_pcg_update2, kRedBlocks, kRedThreads, px, r, (const double*)p, (const double*)ap,
+                   (const double*)dinv, ctx->d_scal, ctx->nvec, (const double*)ctx->d_partial, part2, ctx->d_status);
+      launch_chain(ctx, k_pcg_p2, grid_for(ctx->nvec), kRedThreads, p, (const double*)r, (const double*)dinv,
+                   ctx->d_scal, ctx->nvec, (const double*)part2, ctx->d_status, cond, has_cond);
+      ctx->launches += 4;
+      ctx->cur_skip = nullptr;
+      return;
+    }
     k_zero<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(ap, ctx->nvec, ctx->d_status);
     if (c_k != 0.0)
       ctx->ops->element(ctx, kmode, pu, p, ap, c_k, c_m);
@@ -331,7 +400,9 @@ int build_pcg_graph(sdme_ctx* ctx, const double* pu, double* px, double* r, doub
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   const long long l0 = ctx->launches;
   CK(cudaStreamBeginCaptureToGraph(ctx->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  ctx->capturing = true;  // plain launches inside the graph (no PDL edges)
+  // plain launches inside the graph for the 7-kernel sequence; the fused
+  // sequence adds its own PDL edges, captured as such
+  ctx->capturing = true;
   enqueue_pcg_iteration(ctx, pu, px, r, p, ap, dinv, c_k, c_m, pa, withc, cond, 1);
   ctx->capturing = false;
   const cudaError_t ce = cudaStreamEndCapture(ctx->st, &body);
@@ -371,6 +442,7 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   sdme_ctx* ctx = new sdme_ctx();
   ctx->ops = ops;
   if (const char* v = getenv("SDME_VARIANT")) ctx->variant = atoi(v);
+  if (const char* v = getenv("SDME_PCG_CHAIN")) ctx->chain_mode = atoi(v);
   if (const char* v = getenv("SDME_SLABS")) {
     ctx->nslab = std::max(1, std::min(atoi(v), 64));
     ctx->nslab_env = true;

@@ -239,6 +239,156 @@ __global__ void k_pcg_p(double* __restrict__ p, const double* __restrict__ r, co
     p[i] = fma(beta, p[i], dinv[i] * r[i]);
 }
 
+// ---- fused sequence (default for the large-mesh iteration): k_zero_chain ->
+// colour passes -> k_pcg_pap_chain -> k_pcg_update2 -> k_pcg_p2.  The scalar
+// steps (alpha / indefinite test; convergence test / beta) are evaluated by
+// every block from the same partials in the same order (bit-identical to
+// k_pcg_alpha / k_pcg_check), block 0 records the state.  No kernel both
+// reads and writes a state slot: S_ITER is written by k_pcg_p2 and read by
+// k_pcg_update2, S_ITERB the other way round; the two partial arrays are
+// distinct.  A block that starts after block 0 has set the status word
+// returns at once: it would have returned (indefinite: every block sees
+// p.Ap <= 0) or only skips the update of p, which a stopped solve no longer
+// uses.  Each kernel may be launched as a programmatic dependent of its
+// predecessor (PDL; SDME_PCG_CHAIN bit 2, off by default -- measured slower):
+// it waits for the predecessor's completion FIRST, then lets its own
+// dependent start, so everything upstream of a running kernel has completed.
+// Without the launch attribute the two instructions are no-ops.
+__device__ __forceinline__ void chain_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// sums of NV interleaved partial arrays in the order of k_pcg_alpha /
+// k_pcg_check, valid in every thread
+template <int NV>
+__device__ __forceinline__ void block_sum_all(const double* partial, double (&res)[NV]) {
+  __shared__ double bc[NV];
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+  for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] += partial[NV * i + k];
+  }
+  double out[NV];
+  block_sum<NV>(acc, out);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) bc[k] = out[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) res[k] = bc[k];
+  __syncthreads();  // block_sum's scratch is free for the caller's own reduction
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_pcg_pap_chain(const double* __restrict__ p,
+                                                               const double* __restrict__ ap, long long n,
+                                                               double* partial, const int* status) {
+  chain_enter();
+  if (pcg_done(status)) return;
+  double acc[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    acc[0] = fma(p[i], ap[i], acc[0]);
+  double out[1];
+  block_sum<1>(acc, out);
+  if (threadIdx.x == 0) partial[blockIdx.x] = out[0];
+}
+
+// k_pcg_alpha + k_pcg_update: pap partials in, (r.r, r.z) partials out (partial2)
+__global__ void __launch_bounds__(kRedThreads) k_pcg_update2(double* __restrict__ x, double* __restrict__ r,
+                                                             const double* __restrict__ p,
+                                                             const double* __restrict__ ap,
+                                                             const double* __restrict__ dinv, double* s, long long n,
+                                                             const double* partial, double* partial2, int* status) {
+  chain_enter();
+  if (pcg_done(status)) return;
+  double papv[1];
+  block_sum_all<1>(partial, papv);
+  const double pap = papv[0];
+  const long long k = (long long)s[S_ITER] + 1;
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  if (!(pap > 0.0)) {
+    if (lead) {
+      s[S_PAP] = pap;
+      s[S_ITER] = (double)k;
+      s[S_STOPREL] = s[S_RELPREV];
+      *status = PCG_INDEFINITE;
+    }
+    return;
+  }
+  const double alpha = s[S_RZ0 + ((k - 1) & 1)] / pap;
+  if (lead) {
+    s[S_PAP] = pap;
+    s[S_ALPHA] = alpha;
+    s[S_ITERB] = (double)k;
+  }
+  double acc[2] = {0.0, 0.0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, ap[i], r[i]);
+    r[i] = ri;
+    acc[0] = fma(ri, ri, acc[0]);
+    acc[1] = fma(ri, dinv[i] * ri, acc[1]);
+  }
+  double out[2];
+  block_sum<2>(acc, out);
+  if (threadIdx.x == 0) {
+    partial2[blockIdx.x * 2 + 0] = out[0];
+    partial2[blockIdx.x * 2 + 1] = out[1];
+  }
+}
+
+// k_pcg_check + k_pcg_p; ends the graph's while loop when it stops the solve
+__global__ void __launch_bounds__(kRedThreads) k_pcg_p2(double* __restrict__ p, const double* __restrict__ r,
+                                                        const double* __restrict__ dinv, double* s, long long n,
+                                                        const double* partial2, int* status,
+                                                        cudaGraphConditionalHandle cond, int has_cond) {
+  chain_enter();
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  if (pcg_done(status)) {
+    if (lead) set_cond(cond, has_cond);
+    return;
+  }
+  double rr[2];
+  block_sum_all<2>(partial2, rr);
+  const long long k = (long long)s[S_ITERB];
+  const double rel = sqrt(rr[0]) / s[S_NB];
+  const bool conv = rel <= s[S_TOL];
+  const bool maxed = !conv && (double)k >= s[S_MAXIT];
+  if (conv || maxed) {
+    if (lead) {
+      s[S_ITER] = (double)k;
+      s[S_STOPREL] = rel;
+      *status = conv ? PCG_CONVERGED : PCG_MAXIT;
+      set_cond(cond, has_cond);
+    }
+    return;
+  }
+  const double beta = rr[1] / s[S_RZ0 + ((k - 1) & 1)];
+  if (lead) {
+    s[S_ITER] = (double)k;
+    s[S_RELPREV] = rel;
+    s[S_BETA] = beta;
+    s[S_RZ0 + (k & 1)] = rr[1];
+  }
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], dinv[i] * r[i]);
+}
+
+// y = 0 unless stopped, as a link of the chain
+__global__ void k_zero_chain(double* __restrict__ y, long long n, const int* status) {
+  chain_enter();
+  if (pcg_done(status)) return;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = 0.0;
+}
+
 // y = 0 unless stopped (graph-friendly memset)
 __global__ void k_zero(double* __restrict__ y, long long n, const int* status) {
   if (pcg_done(status)) return;

@@ -440,6 +440,39 @@ def test_pcg_operator_from_stored_quadrature_data_is_bit_identical(tag, P, m, mo
     assert np.array_equal(res["0"][0], res["1"][0])
 
 
+@pytest.mark.parametrize("tag,P,m,div", [("SDME_M", 4, 5, (7, 6, 5)), ("SDME_H", 6, 7, (4, 3, 3)),
+                                         ("LagrangeGLL", 3, 4, (6, 5, 4))])
+def test_pcg_iteration_sequences_are_bit_identical(tag, P, m, div, monkeypatch):
+    """The default PCG iteration on the TMA colour-pass path -- stored point data
+    prefetched (P = 4: on the quintet kernel), colour passes linked by
+    programmatic dependent launches inside the captured graph, alpha / beta
+    evaluated inside the fused update kernels -- against the plain sequence
+    (SDME_PCG_CHAIN=0, SDME_PDL=0: seven kernels per iteration, no PDL edges)
+    on the warp-per-element kernel (SDME_VARIANT=12), and against plain
+    launches without a graph (SDME_PCG_DIRECT=1): same iterates, bit for bit."""
+    monkeypatch.setenv("SDME_EV", "0")
+    rng = np.random.default_rng(5)
+    res = []
+    for env in ({}, {"SDME_PCG_CHAIN": "0", "SDME_PDL": "0", "SDME_VARIANT": "12"}, {"SDME_PCG_DIRECT": "1"},
+                {"SDME_PCG_CHAIN": "7"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        pb = gpu_problem(tag, P, m, div, tuple(d / 8 for d in div), [("xmin", (0, 1, 2)), ("ymax", (1,))])
+        for k in env:
+            monkeypatch.delenv(k)
+        if not res:
+            u = 1e-3 / 8 * rng.uniform(-1, 1, pb.n_free)
+            b = rng.standard_normal(pb.n_free)
+        x, st = pcg_gpu(pb, u, b, c_m=4.0e8, precond="diagonal", tol=1e-10, maxit=2000)
+        x0, st0 = pcg_gpu(pb, u, b, c_m=0.0, precond="diagonal", tol=1e-6, maxit=20000)
+        res.append((x, st.iterations, x0, st0.iterations))
+    assert res[0][1] > 5 and res[0][3] > 5
+    for r in res[1:]:
+        assert r[1] == res[0][1] and r[3] == res[0][3]
+        assert np.array_equal(r[0], res[0][0])
+        assert np.array_equal(r[2], res[0][2])
+
+
 # ------------------------------------------------------------------------------
 # Implicit penalty contact (SURVEY F3): contact stiffness operator and
 # newmark_run(contact=...) against the reference.
