@@ -469,7 +469,9 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
   int buf = 0;
   if (args.skip && *(volatile const int*)args.skip) return;
   bool waited = false;  // TM colour passes: griddepcontrol.wait done (thread 0)
-  if (TM) pdl_launch_dependents();
+  // TM: the next colour pass; E-vector mode: the cluster tail of a small-mesh
+  // PCG iteration (pcg_small.cuh); a no-op without a programmatic dependent
+  pdl_launch_dependents();
   constexpr bool UPASS = (MODE == MODE_APPLY || MODE == MODE_FINT || MODE == MODE_SETUP);
   constexpr bool PPASS = (MODE == MODE_APPLY || MODE == MODE_PA || MODE == MODE_MASS);
   constexpr bool PGRAD = MODE != MODE_MASS;  // c_m M p alone: values only (B stages), no gradient

@@ -768,15 +768,18 @@ cudaLaunchConfig_t pcg_small_config(sdme_ctx* c, cudaLaunchAttribute* at) {
   at[0].val.clusterDim.x = kSmallCta;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  // + programmatic dependent of the E-vector element kernel before it (SDME_PDL=0: plain)
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = c->pdl ? 2 : 1;
   return cfg;
 }
 
 template <int N>
 int pcg_small_fits_impl(sdme_ctx* c) {
   pcg_small_attr<N>();
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   cudaLaunchConfig_t cfg = pcg_small_config<N>(c, at);
   int clusters = 0;
   if (cudaOccupancyMaxActiveClusters(&clusters, k_pcg_small<N>, &cfg) != cudaSuccess) {
@@ -790,7 +793,7 @@ template <int N>
 void pcg_small_impl(sdme_ctx* c, double* x, double* r, double* p, double* ap, const double* dinv,
                     cudaGraphConditionalHandle cond, int has_cond) {
   pcg_small_attr<N>();
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   cudaLaunchConfig_t cfg = pcg_small_config<N>(c, at);
   const cudaError_t e = cudaLaunchKernelEx(&cfg, k_pcg_small<N>, x, r, p, ap, dinv, (const double*)c->d_ev,
                                            c->geo, c->d_scal, c->d_status, cond, has_cond);

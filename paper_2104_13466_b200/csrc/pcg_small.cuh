@@ -78,6 +78,9 @@ __global__ void __launch_bounds__(kSmallThreads)
     if (lead) set_cond(cond, has_cond);
     return;
   }
+  // launched as a programmatic dependent of the element kernel (which wrote
+  // the E-vector): everything above overlapped it
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const long long n = 3 * g.Ns;
   const long long i0 = (long long)cl.block_rank() * kSmallThreads + threadIdx.x;
   constexpr long long stride = (long long)kSmallCta * kSmallThreads;
