@@ -447,6 +447,16 @@ __device__ __forceinline__ void gen_to_phys(double* H, const double J[3][3]) {
 // each with its own shared region and barriers; the halves run the same
 // number of iterations (a half past the end of the colour repeats the last
 // element without scattering it) so the warp-wide syncs stay uniform
+// SDME_COL_BOX_PREF: L2 prefetch (cp.async.bulk.prefetch.tensor) of the next
+// element's u / p boxes (TMA path).  Measured slower (P = 3 K.p 1.937 -> 1.997 ms,
+// P = 6 1.949 -> 1.964): off.
+#ifndef SDME_COL_BOX_PREF
+#define SDME_COL_BOX_PREF 0
+#endif
+// SDME_GEN_GEO_PREF: L2 prefetch of a general-mesh element's J^-1 table
+#ifndef SDME_GEN_GEO_PREF
+#define SDME_GEN_GEO_PREF 1
+#endif
 // SDME_COL_PA_PREF: L2 prefetch of the stored point data (MODE_PA) per element
 #ifndef SDME_COL_PA_PREF
 #define SDME_COL_PA_PREF 1
@@ -537,9 +547,27 @@ __global__ void __launch_bounds__(32 * WPE, MINB) element_col(const __grid_const
         int ni, nj, nk;
         colour_element(g, args.colour, SUB == 1 ? idx + stride : min(base + stride + half, cnt - 1), ni, nj, nk);
         next_eid = ((long long)nk * g.ny + nj) * g.nx + ni;
-        if (TM) nxb = NextBox{first_map, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
+        if (TM) {
+          nxb = NextBox{first_map, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
+          if (SDME_COL_BOX_PREF && t == 0) {
+            // the next element's input boxes on their way into L2 an element
+            // ahead of their TMA loads
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              if (UPASS) tma_prefetch_box(umap, nxb.X0 & ~1, nxb.Y0, nxb.Z0, c);
+              if (PPASS) tma_prefetch_box(pmap, nxb.X0 & ~1, nxb.Y0, nxb.Z0, c);
+            }
+          }
+        }
         else nxt = NextRows{first_field, (N - 1) * ni, (N - 1) * nj, (N - 1) * nk};
       }
+    }
+    if (GEN && SDME_GEN_GEO_PREF && MODE != MODE_MASS) {
+      // general meshes: the element's J^-1 and w det J (10 Q doubles, read at the
+      // points) on their way into L2 while the forward pass runs
+      constexpr int LG = (10 * Q * 8 + 127) / 128 + 1;
+      const char* bp = reinterpret_cast<const char*>(args.geo + eid * (10 * Q));
+      for (int l = t; l < LG; l += T) prefetch_l2(bp + (l * 128 < 10 * Q * 8 - 8 ? l * 128 : 10 * Q * 8 - 8));
     }
     double Hu[QPT][9];
     if (UPASS) {

@@ -305,6 +305,13 @@ __device__ __forceinline__ void q5_backward(const TabC<5, MIR>& tb0, int zoff, c
 //   2  L2 prefetch of the quintet's lines before the pass     1.48 / 1.85
 //   3  1 + L2 prefetch of the next quintet a round ahead      1.35 / 1.49  (default)
 //   4  3 with the register loads at the point stage           1.38 / 1.56
+// SDME_Q5_BOX_PREF: L2 prefetch (cp.async.bulk.prefetch.tensor) of the next
+// quintet's u / p boxes.  Measured slower (K.p 1.606 -> 1.639 ms, f_int 1.105 ->
+// 1.128: the double-buffered box loads already hide their latency and the 30
+// extra bulk operations per quintet cost more than they save): off.
+#ifndef SDME_Q5_BOX_PREF
+#define SDME_Q5_BOX_PREF 0
+#endif
 #ifndef SDME_PA_PREF
 #define SDME_PA_PREF 3
 #endif
@@ -370,6 +377,15 @@ __global__ void __launch_bounds__(128, MINB) element_q5(const __grid_constant__ 
       colour_element(g, args.colour, idx < cnt ? idx : cnt - 1, ei, ej, ek);
       int* cc = coord + ((cur ^ 1) * L::E + t) * 4;
       cc[0] = (N - 1) * ei, cc[1] = (N - 1) * ej, cc[2] = (N - 1) * ek, cc[3] = idx >= cnt;
+      if (SDME_Q5_BOX_PREF) {
+        // the next quintet's input boxes on their way into L2 a round ahead of
+        // their TMA loads (which then complete at L2 latency)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (UPASS) tma_prefetch_box(umap, cc[0], cc[1], cc[2], c);
+          if (PPASS) tma_prefetch_box(pmap, cc[0], cc[1], cc[2], c);
+        }
+      }
     }
     const Q5Next after_last{has_next ? first_map : nullptr, cur ^ 1};
     double Hu[QPT][9];

@@ -580,7 +580,9 @@ void launch_q5_iso(sdme_ctx* c, const TabC<5, MIR>& tb, OpArgs a) {
   // z slabs (DRAM traffic): measured on this kernel K.p 1.589 / 1.597 / 1.575 /
   // 1.603 ms and mass 0.732 / 0.688 / 0.658 / 0.714 ms for 1 / 2 / 4 / 8 slabs, f_int flat
   // K.p keeps 8: 1.7% slower than 4 but 1.89 instead of 3.18 GB of DRAM traffic per call
-  const int nslab = c->nslab_env ? c->nslab : (MODE == MODE_APPLY ? 8 : (MODE == MODE_MASS ? 4 : 1));
+  // f_int: 1.108 / 1.125 / 1.107 / 1.132 ms for 1 / 2 / 4 / 8 slabs; 4 for its DRAM traffic (3.2 GB at 1)
+  const int nslab = c->nslab_env ? c->nslab
+                                 : (MODE == MODE_APPLY ? 8 : ((MODE == MODE_MASS || MODE == MODE_FINT) ? 4 : 1));
   for (int sp = 0; sp < 8 * nslab; ++sp) {
     const int col = colour_code(c->geo, sp % 8, sp / 8, nslab);
     if (col == -2) continue;

@@ -48,6 +48,13 @@ __device__ __forceinline__ void tma_load_box(double* dst, const CUtensorMap* map
       : "memory");
 }
 
+// the same box on its way into L2 (no shared-memory destination, no barrier)
+__device__ __forceinline__ void tma_prefetch_box(const CUtensorMap* map, int x0, int y0, int z0, int c) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(map), "r"(x0),
+               "r"(y0), "r"(z0), "r"(c)
+               : "memory");
+}
+
 // y[box] += src  (bulk tensor reduce-add; elements outside the tensor are dropped)
 __device__ __forceinline__ void tma_reduce_add_box(const CUtensorMap* map, const double* src, int x0, int y0, int z0,
                                                    int c) {
