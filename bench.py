@@ -392,7 +392,7 @@ def run_ours(args):
     achieved = flops / t_step / 1e12
     traffic = None
     traffic_src = None
-    for name in ("ncu_traffic_r02.json", "ncu_traffic_r01.json"):  # DRAM bytes of one K.p (8 colour launches)
+    for name in ("ncu_traffic_r02.json", "ncu_traffic_r01.json"):  # DRAM bytes of one K.p (its 64 colour-pass launches)
         try:
             traffic = json.load(open(os.path.join(ROOT, "profiles", name)))["kp"]["traffic_bytes"]
             traffic_src = "profiles/" + name
@@ -401,7 +401,7 @@ def run_ours(args):
             pass
     roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": achieved / fp64_peak if fp64_peak else None, "traffic": traffic,
-            "traffic_note": f"dram read+write bytes per K.p (8 launches), {traffic_src}; "
+            "traffic_note": f"dram read+write bytes per K.p (its 64 launches: 8 colour passes x 8 z-slabs), {traffic_src}; "
                             "algorithmic bytes = algorithmic_bytes_per_step",
             "peak_source": "profiles/fp64_peak.json (measured DFMA chain on this pool's B200: the pipe the "
                            "kernels use; the FP64 tensor-core DMMA peak, profiles/dmma_peak.json, is 1.09x "
