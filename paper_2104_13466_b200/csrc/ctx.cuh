@@ -37,6 +37,10 @@ struct sdme_ctx {
   double h[3]{}, origin[3]{};
   std::vector<double> Bl, Dl, w;  // lattice-local order, m x n
   cudaStream_t st = nullptr;
+  // side stream + fork / join events: the contact force of an explicit step
+  // runs beside the f_int colour passes (sdme_explicit_steps; created on first use)
+  cudaStream_t st_side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   long long nvec = 0;             // 3 * Ns (device vector length, pitched rows)
   long long nlat = 0;             // 3 * Lx * Ly * Lz (dense host lattice arrays)
   std::vector<double*> vecs;

@@ -674,6 +674,9 @@ int sdme_destroy(sdme_ctx* ctx) {
   cudaFree(ctx->d_status);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_gaps) cudaFreeHost(ctx->h_gaps);
+  if (ctx->st_side) cudaStreamDestroy(ctx->st_side);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->st) cudaStreamDestroy(ctx->st);
   delete ctx;
   return SDME_OK;
@@ -1091,17 +1094,42 @@ int sdme_explicit_steps(sdme_ctx* ctx, int n, int u, int u_prev, int v, int load
     return set_err(ctx, SDME_BAD_ARGUMENT, "bad explicit-steps argument");
   int rc = reset_flag(ctx);
   if (rc) return rc;
+  // The contact force (4 small face-colour launches, ~8 us each) and f_int
+  // (8 colour passes) of a step both read u and write different vectors:
+  // the contact runs on a side stream beside the passes and joins before the
+  // update (config 4: 0.123 -> 0.10 ms per step).  SDME_CONTACT_SIDE=0: in line.
+  static const bool side_on = [] {
+    const char* e = getenv("SDME_CONTACT_SIDE");
+    return !(e && e[0] == '0');
+  }();
+  const bool side = pf && side_on;
+  if (side && !ctx->st_side) {
+    CK(cudaStreamCreateWithFlags(&ctx->st_side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  }
   for (int k = 0; k < n; ++k) {
     if (pf) {
       ContactArgs ca = ctx->c_ca;
       ca.mode = CONTACT_FORCE;
       ca.u = pu;
       ca.fc = pf;
-      CK(cudaMemsetAsync(pf, 0, ctx->nvec * sizeof(double), ctx->st));
+      cudaStream_t main = ctx->st;
+      if (side) {
+        CK(cudaEventRecord(ctx->ev_fork, main));
+        CK(cudaStreamWaitEvent(ctx->st_side, ctx->ev_fork, 0));
+        ctx->st = ctx->st_side;  // launch_contact launches on ctx->st
+      }
+      const cudaError_t me = cudaMemsetAsync(pf, 0, ctx->nvec * sizeof(double), ctx->st);
       launch_contact(ctx, ca);
+      ctx->st = main;
+      if (me != cudaSuccess) return set_err(ctx, SDME_CUDA_ERROR, cudaGetErrorString(me));
+      if (side) CK(cudaEventRecord(ctx->ev_join, ctx->st_side));
     }
-    CK(cudaMemsetAsync(ps, 0, ctx->nvec * sizeof(double), ctx->st));
+    if ((rc = zero_output(ctx, ps))) return rc;  // PDL primary of the first colour pass
     ctx->ops->element(ctx, MODE_FINT, pu, nullptr, ps, 1.0, 0.0);
+    ctx->pdl_first = false;
+    if (side) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_join, 0));
     k_explicit_step<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(pu, pup, pv, pl, pl ? s_load[k] : 0.0, ps, pf, pm,
                                                              dt, ctx->nvec);
     ++ctx->launches;
