@@ -68,7 +68,7 @@ struct sdme_ctx {
   std::string err_msg;
   int64_t launches = 0;
   int variant = 0;  // schedule variant (SDME_VARIANT env), tuning only
-  int chain_mode = 5;  // PCG iteration sequence (SDME_PCG_CHAIN env bit mask, sdme_abi.cu)
+  int chain_mode = -1;  // PCG iteration sequence (SDME_PCG_CHAIN env bit mask; -1: by size, sdme_abi.cu)
   int nslab = 1;    // colour passes per z-slab (SDME_SLABS env): 8 * nslab launches per operator
   bool nslab_env = false;  // SDME_SLABS given: it overrides the per-mode default of the TMA passes
   int mir = -1;     // mirror structure of the 1D tables: 0 nodal, 1 modal/SDME, -1 none (no even-odd)

@@ -279,7 +279,13 @@ bool ensure_qpd(sdme_ctx* ctx) {
 // 1: 2522 / 337 / 93.6, 0.0715; 3: 2562 / 342 / 93.4, 0.0778 (dependents
 // spinning in griddepcontrol.wait take issue slots from the HBM-bound kernel
 // they wait for); 5: 2515 / 333 / 93.7, 0.0720 (default); 7: 2559 / 339 / 93.5, 0.0775.
-// Read per context (sdme_ctx::chain_mode).
+// Bit 8 (with bit 1): k_pcg_p2 also zeroes A p for the next iteration (no zeroing launch;
+// the first pass then follows k_pcg_p2 plainly): 64^3 / 32^3 / 16^3 2475 / 332 / 89.0 us and
+// config-5 size 152.4 us per iteration against 2455 / 336 / 95.9 and 159.4 for mode 5 --
+// so 9 up to 2^24 vector entries and 5 above (chain_mode_of).  Read per context.
+inline int chain_mode_of(const sdme_ctx* c) {
+  return c->chain_mode >= 0 ? c->chain_mode : (c->nvec <= (1LL << 24) ? 9 : 5);
+}
 
 // launch as a programmatic dependent of the previous kernel on the stream
 template <class... KArgs, class... Args>
@@ -294,7 +300,7 @@ void launch_chain(sdme_ctx* ctx, void (*kern)(KArgs...), int grid, int block, Ar
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cfg.numAttrs = (ctx->chain_mode & 2) ? 1 : 0;
+  cfg.numAttrs = (chain_mode_of(ctx) & 2) ? 1 : 0;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
   if (e != cudaSuccess && ctx->launch_err == cudaSuccess) ctx->launch_err = e;
 }
@@ -324,8 +330,12 @@ void enqueue_pcg_iteration(sdme_ctx* ctx, const double* pu, double* px, double* 
       // fused sequence, every kernel a programmatic dependent of its predecessor
       // (vector_kernels.cuh); the first colour pass of a TMA operator overlaps
       // the zeroing of A p like the passes overlap one another
-      const bool tm_first = (ctx->chain_mode & 4) && !ctx->ev_mode && !ctx->gen && sdme_tmap_of(ctx, ap);
-      launch_chain(ctx, k_zero_chain, grid_for(ctx->nvec), 256, ap, ctx->nvec, (const int*)ctx->d_status);
+      // bit 8 (with the fused kernels): k_pcg_p2 zeroes A p for the next
+      // iteration, sdme_pcg once before the first
+      const bool p2_zeroes = (chain_mode_of(ctx) & 9) == 9;
+      const bool tm_first = (chain_mode_of(ctx) & 4) && !p2_zeroes && !ctx->ev_mode && !ctx->gen && sdme_tmap_of(ctx, ap);
+      if (!p2_zeroes)
+        launch_chain(ctx, k_zero_chain, grid_for(ctx->nvec), 256, ap, ctx->nvec, (const int*)ctx->d_status);
       const bool cap = ctx->capturing;
       ctx->capturing = false;  // PDL edges between the passes, inside a capture too
       ctx->pdl_first = tm_first;
@@ -336,7 +346,7 @@ void enqueue_pcg_iteration(sdme_ctx* ctx, const double* pu, double* px, double* 
       ctx->pdl_first = false;
       ctx->capturing = cap;
       if (withc) contact_op(ctx, CONTACT_APPLY, p, ap, ctx->d_status);
-      if (!(ctx->chain_mode & 1)) {
+      if (!(chain_mode_of(ctx) & 1)) {
         launch_chain(ctx, k_pcg_pap_chain, kRedBlocks, kRedThreads, (const double*)p, (const double*)ap, ctx->nvec,
                      ctx->d_partial, (const int*)ctx->d_status);
         k_pcg_alpha<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, ctx->d_status);
@@ -355,8 +365,9 @@ void enqueue_pcg_iteration(sdme_ctx* ctx, const double* pu, double* px, double* 
       launch_chain(ctx, k_pcg_update2, kRedBlocks, kRedThreads, px, r, (const double*)p, (const double*)ap,
                    (const double*)dinv, ctx->d_scal, ctx->nvec, (const double*)ctx->d_partial, part2, ctx->d_status);
       launch_chain(ctx, k_pcg_p2, grid_for(ctx->nvec), kRedThreads, p, (const double*)r, (const double*)dinv,
-                   ctx->d_scal, ctx->nvec, (const double*)part2, ctx->d_status, cond, has_cond);
-      ctx->launches += 4;
+                   ctx->d_scal, ctx->nvec, (const double*)part2, ctx->d_status, cond, has_cond,
+                   p2_zeroes ? ap : (double*)nullptr);
+      ctx->launches += p2_zeroes ? 3 : 4;
       ctx->cur_skip = nullptr;
       return;
     }
@@ -987,6 +998,9 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
       if ((rc = check_launch(ctx))) return rc;
       ctx->pcg_warm |= 1 << kind;
     }
+    // large-mesh sequence with k_pcg_p2 zeroing A p for the next iteration:
+    // the first iteration's zero (after the warm-up pass above may have used ap)
+    if (ctx->pdl && (chain_mode_of(ctx) & 9) == 9) CK(cudaMemsetAsync(ap, 0, ctx->nvec * sizeof(double), ctx->st));
     // one graph launch per solve (build_pcg_graph); the instantiated graph is
     // reused while the operands are the same (every Newton step of a run)
     const sdme_ctx::PcgKey key{pu, px, c_k, c_m, pa, withc, withc ? ctx->c_ca.eps : 0.0,

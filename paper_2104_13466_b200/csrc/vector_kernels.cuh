@@ -346,7 +346,8 @@ __global__ void __launch_bounds__(kRedThreads) k_pcg_update2(double* __restrict_
 __global__ void __launch_bounds__(kRedThreads) k_pcg_p2(double* __restrict__ p, const double* __restrict__ r,
                                                         const double* __restrict__ dinv, double* s, long long n,
                                                         const double* partial2, int* status,
-                                                        cudaGraphConditionalHandle cond, int has_cond) {
+                                                        cudaGraphConditionalHandle cond, int has_cond,
+                                                        double* __restrict__ zero_ap) {
   chain_enter();
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   if (pcg_done(status)) {
@@ -374,6 +375,16 @@ __global__ void __launch_bounds__(kRedThreads) k_pcg_p2(double* __restrict__ p, 
     s[S_RELPREV] = rel;
     s[S_BETA] = beta;
     s[S_RZ0 + (k & 1)] = rr[1];
+  }
+  // zero_ap: A p of the next iteration starts from 0 (k_pcg_update2 has read
+  // this iteration's) -- one launch less per iteration than a separate zeroing
+  if (zero_ap) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+      p[i] = fma(beta, p[i], dinv[i] * r[i]);
+      zero_ap[i] = 0.0;
+    }
+    return;
   }
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)

@@ -446,7 +446,9 @@ def test_pcg_iteration_sequences_are_bit_identical(tag, P, m, div, monkeypatch):
     """The default PCG iteration on the TMA colour-pass path -- stored point data
     prefetched (P = 4: on the quintet kernel), colour passes linked by
     programmatic dependent launches inside the captured graph, alpha / beta
-    evaluated inside the fused update kernels -- against the plain sequence
+    evaluated inside the fused update kernels, A p zeroed by the p update (the
+    default below 2^24 vector entries, SDME_PCG_CHAIN=9) or by its own launch
+    overlapping the first pass (5) -- against the plain sequence
     (SDME_PCG_CHAIN=0, SDME_PDL=0: seven kernels per iteration, no PDL edges)
     on the warp-per-element kernel (SDME_VARIANT=12), and against plain
     launches without a graph (SDME_PCG_DIRECT=1): same iterates, bit for bit."""
@@ -454,7 +456,7 @@ def test_pcg_iteration_sequences_are_bit_identical(tag, P, m, div, monkeypatch):
     rng = np.random.default_rng(5)
     res = []
     for env in ({}, {"SDME_PCG_CHAIN": "0", "SDME_PDL": "0", "SDME_VARIANT": "12"}, {"SDME_PCG_DIRECT": "1"},
-                {"SDME_PCG_CHAIN": "7"}):
+                {"SDME_PCG_CHAIN": "7"}, {"SDME_PCG_CHAIN": "5"}, {"SDME_PCG_CHAIN": "9", "SDME_PCG_DIRECT": "1"}):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         pb = gpu_problem(tag, P, m, div, tuple(d / 8 for d in div), [("xmin", (0, 1, 2)), ("ymax", (1,))])
