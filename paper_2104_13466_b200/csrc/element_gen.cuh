@@ -33,6 +33,25 @@ static __global__ void __launch_bounds__(256) k_gen_gather(double* __restrict__ 
   }
 }
 
+// two fields through one read of the index table (K.p from u: u and p)
+static __global__ void __launch_bounds__(256) k_gen_gather2(double* __restrict__ eva, const double* __restrict__ xa,
+                                                     double* __restrict__ evb, const double* __restrict__ xb,
+                                                     const int* __restrict__ dof, long long n, const int* skip) {
+  if (skip && *(volatile const int*)skip) return;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int d = __ldg(dof + i);
+    double va = 0.0, vb = 0.0;
+    if (d >= 0) {
+      va = __ldg(xa + (d >> 1));
+      vb = __ldg(xb + (d >> 1));
+      if (d & 1) va = -va, vb = -vb;
+    }
+    eva[i] = va;
+    evb[i] = vb;
+  }
+}
+
 // y[f] += sum_k sign_k ev[slot_k] over the CSR entries of f (increasing element);
 // unsigned for a diagonal (sign_k^2 = 1).  CSR row r belongs to DOF rows[r]
 // (rows: the locality order of the rows, nullptr = identity)

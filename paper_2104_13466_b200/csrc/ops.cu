@@ -844,11 +844,13 @@ void gen_element_impl(sdme_ctx* c, int mode, const double* u, const double* p, d
   a.elem_id = c->d_elem_id;
   a.qpd = c->d_qpd;
   a.ev = c->d_ev;
-  if (mode == MODE_FINT || mode == MODE_APPLY || mode == MODE_SETUP) {
+  if (mode == MODE_APPLY) {
+    k_gen_gather2<<<gen_grid(ns), 256, 0, c->st>>>(c->d_evu, u, c->d_evp, p, c->d_dof, ns, skip);
+    ++c->launches;
+  } else if (mode == MODE_FINT || mode == MODE_SETUP) {
     k_gen_gather<<<gen_grid(ns), 256, 0, c->st>>>(c->d_evu, u, c->d_dof, ns, skip);
     ++c->launches;
-  }
-  if (mode == MODE_APPLY || mode == MODE_PA || mode == MODE_MASS) {
+  } else if (mode == MODE_PA || mode == MODE_MASS) {
     k_gen_gather<<<gen_grid(ns), 256, 0, c->st>>>(c->d_evp, p, c->d_dof, ns, skip);
     ++c->launches;
   }
