@@ -20,8 +20,14 @@
 
 namespace sdme {
 
-constexpr int kSmallCta = 16;  // non-portable cluster size (attribute set at launch)
-constexpr int kSmallThreads = 1024;
+#ifndef SDME_SMALL_CTA
+#define SDME_SMALL_CTA 16
+#endif
+#ifndef SDME_SMALL_THREADS
+#define SDME_SMALL_THREADS 1024
+#endif
+constexpr int kSmallCta = SDME_SMALL_CTA;  // non-portable cluster size above 8 (attribute set at launch)
+constexpr int kSmallThreads = SDME_SMALL_THREADS;
 constexpr long long kSmallPcgMax = 1LL << 18;  // lattice entries (3 Ns) for this path
 
 // Cluster-wide sum of NV values: warp trees -> CTA tree (warp 0) -> the
@@ -42,7 +48,7 @@ __device__ __forceinline__ void cluster_sum(cooperative_groups::cluster_group& c
   if (wid == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      const double s = warp_sum(red[k][lane]);
+      const double s = warp_sum(lane < kSmallThreads / 32 ? red[k][lane] : 0.0);
       if (lane == 0) part[k] = s;
     }
   }
