@@ -68,6 +68,7 @@ struct sdme_ctx {
   std::string err_msg;
   int64_t launches = 0;
   int variant = 0;  // schedule variant (SDME_VARIANT env), tuning only
+  bool pcg_start = true;  // start of a solve as two fused launches (SDME_PCG_START=0: nine separate ones)
   int chain_mode = -1;  // PCG iteration sequence (SDME_PCG_CHAIN env bit mask; -1: by size, sdme_abi.cu)
   int nslab = 1;    // colour passes per z-slab (SDME_SLABS env): 8 * nslab launches per operator
   bool nslab_env = false;  // SDME_SLABS given: it overrides the per-mode default of the TMA passes

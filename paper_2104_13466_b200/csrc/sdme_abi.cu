@@ -454,6 +454,7 @@ int sdme_create(const sdme_desc* d, sdme_ctx** out) {
   ctx->ops = ops;
   if (const char* v = getenv("SDME_VARIANT")) ctx->variant = atoi(v);
   if (const char* v = getenv("SDME_PCG_CHAIN")) ctx->chain_mode = atoi(v);
+  if (const char* v = getenv("SDME_PCG_START")) ctx->pcg_start = atoi(v) != 0;
   if (const char* v = getenv("SDME_SLABS")) {
     ctx->nslab = std::max(1, std::min(atoi(v), 64));
     ctx->nslab_env = true;
@@ -967,24 +968,37 @@ int sdme_pcg(sdme_ctx* ctx, int u_lin, double c_k, double c_m, int b, int x, dou
   const bool pa = c_k != 0.0 && ctx->pa && ensure_qpd(ctx);
   const bool withc = c_k != 0.0 && ctx->pcg_contact && ctx->c_ready;
   if (pa) ctx->ops->element(ctx, MODE_SETUP, pu, nullptr, nullptr, 1.0, 0.0);
+  // SDME_PCG_START=0: the start of the solve as separate launches (A/B, bit-identical)
+  const bool fused_start = ctx->pcg_start;
   if (precond == 1) {
     CK(cudaMemsetAsync(ap, 0, ctx->nvec * sizeof(double), ctx->st));
     ctx->ops->diag(ctx, pu, ap, c_k, c_m);
     if (withc) contact_op(ctx, CONTACT_DIAG, nullptr, ap, nullptr);
-    k_invert_diag<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(dinv, ap, ctx->d_free, ctx->nvec, ctx->d_dflag);
-  } else {
-    k_fill_masked<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(dinv, ctx->d_free, 1.0, ctx->nvec);
   }
-  ++ctx->launches;
-  // ||b||, scalar state and status word on the device; r = b ; p = z = dinv r ; rz = r.z
-  if ((rc = dot_into(ctx, pb, pb, S_SCRATCH))) return rc;
-  k_pcg_init<<<1, 32, 0, ctx->st>>>(ctx->d_scal, tol, (double)maxit, ctx->d_status, ctx->d_flag);
-  ++ctx->launches;
-  CK(cudaMemsetAsync(px, 0, ctx->nvec * sizeof(double), ctx->st));
-  CK(cudaMemcpyAsync(r, pb, ctx->nvec * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
-  k_mul<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, dinv, r, ctx->nvec);
-  ++ctx->launches;
-  if ((rc = dot_into(ctx, r, p, S_RZ0))) return rc;
+  if (fused_start) {
+    // dinv, ||b||, x = 0, r = b, p = z = dinv r, rz = r.z, scalar state and status: two launches
+    k_pcg_start<<<kRedBlocks, kRedThreads, 0, ctx->st>>>(dinv, precond == 1 ? ap : nullptr, ctx->d_free, pb, px, r,
+                                                         p, ctx->nvec, ctx->d_partial, ctx->d_dflag);
+    k_pcg_start_finish<<<1, kRedThreads, 0, ctx->st>>>(ctx->d_partial, ctx->d_scal, tol, (double)maxit,
+                                                       ctx->d_status, ctx->d_flag);
+    ctx->launches += 2;
+    if ((rc = check_launch(ctx))) return rc;
+  } else {
+    if (precond == 1)
+      k_invert_diag<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(dinv, ap, ctx->d_free, ctx->nvec, ctx->d_dflag);
+    else
+      k_fill_masked<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(dinv, ctx->d_free, 1.0, ctx->nvec);
+    ++ctx->launches;
+    // ||b||, scalar state and status word on the device; r = b ; p = z = dinv r ; rz = r.z
+    if ((rc = dot_into(ctx, pb, pb, S_SCRATCH))) return rc;
+    k_pcg_init<<<1, 32, 0, ctx->st>>>(ctx->d_scal, tol, (double)maxit, ctx->d_status, ctx->d_flag);
+    ++ctx->launches;
+    CK(cudaMemsetAsync(px, 0, ctx->nvec * sizeof(double), ctx->st));
+    CK(cudaMemcpyAsync(r, pb, ctx->nvec * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
+    k_mul<<<grid_for(ctx->nvec), 256, 0, ctx->st>>>(p, dinv, r, ctx->nvec);
+    ++ctx->launches;
+    if ((rc = dot_into(ctx, r, p, S_RZ0))) return rc;
+  }
   if (maxit > 0) {
     // warm the operator's one-time launch setup (function attributes,
     // occupancy queries) outside the capture, once per operator kind

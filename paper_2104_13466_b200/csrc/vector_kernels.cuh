@@ -239,6 +239,76 @@ __global__ void k_pcg_p(double* __restrict__ p, const double* __restrict__ r, co
     p[i] = fma(beta, p[i], dinv[i] * r[i]);
 }
 
+// ---- start of a solve in two launches instead of nine (invert the diagonal,
+// ||b||^2, state, x = 0, r = b, p = dinv r, r.p): the same arithmetic per
+// entry and the same partial sums (grid kRedBlocks x kRedThreads, fma order
+// of k_dots, k_finish's tree), so the solve is bit-identical to the separate
+// launches (SDME_PCG_START=0).  d: the assembled diagonal (nullptr: no
+// preconditioner, dinv = 1 on free entries).
+__global__ void __launch_bounds__(kRedThreads) k_pcg_start(double* __restrict__ dinv, const double* d,
+                                                           const unsigned char* __restrict__ freemask,
+                                                           const double* __restrict__ b, double* __restrict__ x,
+                                                           double* __restrict__ r, double* __restrict__ p,
+                                                           long long n, double* partial, unsigned long long* bad) {
+  double acc[2] = {0.0, 0.0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double dv = 0.0;
+    if (freemask[i]) {
+      if (d) {
+        const double v = d[i];
+        if (!(v > 0.0)) atomicMin(bad, (unsigned long long)i);
+        dv = 1.0 / v;
+      } else {
+        dv = 1.0;
+      }
+    }
+    dinv[i] = dv;
+    const double bi = b[i];
+    const double pi = dv * bi;
+    x[i] = 0.0;
+    r[i] = bi;
+    p[i] = pi;
+    acc[0] = fma(bi, bi, acc[0]);
+    acc[1] = fma(bi, pi, acc[1]);
+  }
+  double out[2];
+  block_sum<2>(acc, out);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x * 2 + 0] = out[0];
+    partial[blockIdx.x * 2 + 1] = out[1];
+  }
+}
+
+// ||b||^2 -> S_SCRATCH, r.z -> S_RZ0, then k_pcg_init's state and status
+__global__ void __launch_bounds__(kRedThreads) k_pcg_start_finish(const double* partial, double* s, double tol,
+                                                                  double maxit, int* status,
+                                                                  const unsigned long long* flags) {
+  double acc[2] = {0.0, 0.0};
+  for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) {
+    acc[0] += partial[i * 2 + 0];
+    acc[1] += partial[i * 2 + 1];
+  }
+  double out[2];
+  block_sum<2>(acc, out);
+  if (threadIdx.x == 0) {
+    s[S_SCRATCH] = out[0];
+    s[S_RZ0] = out[1];
+    if (flags[0] != ~0ull || flags[1] != ~0ull) {
+      *status = PCG_STOPPED;
+      return;
+    }
+    const double nb = sqrt(out[0]);
+    s[S_NB] = nb;
+    s[S_TOL] = tol;
+    s[S_RELPREV] = 1.0;
+    s[S_ITER] = 0.0;
+    s[S_STOPREL] = 0.0;
+    s[S_MAXIT] = maxit;
+    *status = nb == 0.0 ? PCG_CONVERGED : PCG_RUNNING;
+  }
+}
+
 // ---- fused sequence (default for the large-mesh iteration): k_zero_chain ->
 // colour passes -> k_pcg_pap_chain -> k_pcg_update2 -> k_pcg_p2.  The scalar
 // steps (alpha / indefinite test; convergence test / beta) are evaluated by

@@ -448,15 +448,17 @@ def test_pcg_iteration_sequences_are_bit_identical(tag, P, m, div, monkeypatch):
     programmatic dependent launches inside the captured graph, alpha / beta
     evaluated inside the fused update kernels, A p zeroed by the p update (the
     default below 2^24 vector entries, SDME_PCG_CHAIN=9) or by its own launch
-    overlapping the first pass (5) -- against the plain sequence
+    overlapping the first pass (5), the start of the solve fused into two
+    launches (SDME_PCG_START=0: separate ones) -- against the plain sequence
     (SDME_PCG_CHAIN=0, SDME_PDL=0: seven kernels per iteration, no PDL edges)
     on the warp-per-element kernel (SDME_VARIANT=12), and against plain
     launches without a graph (SDME_PCG_DIRECT=1): same iterates, bit for bit."""
     monkeypatch.setenv("SDME_EV", "0")
     rng = np.random.default_rng(5)
     res = []
-    for env in ({}, {"SDME_PCG_CHAIN": "0", "SDME_PDL": "0", "SDME_VARIANT": "12"}, {"SDME_PCG_DIRECT": "1"},
-                {"SDME_PCG_CHAIN": "7"}, {"SDME_PCG_CHAIN": "5"}, {"SDME_PCG_CHAIN": "9", "SDME_PCG_DIRECT": "1"}):
+    for env in ({}, {"SDME_PCG_CHAIN": "0", "SDME_PDL": "0", "SDME_VARIANT": "12", "SDME_PCG_START": "0"},
+                {"SDME_PCG_DIRECT": "1"},
+                {"SDME_PCG_CHAIN": "7"}, {"SDME_PCG_CHAIN": "5"}, {"SDME_PCG_CHAIN": "9", "SDME_PCG_DIRECT": "1"}, {"SDME_PCG_START": "0"}):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         pb = gpu_problem(tag, P, m, div, tuple(d / 8 for d in div), [("xmin", (0, 1, 2)), ("ymax", (1,))])
